@@ -1,0 +1,401 @@
+"""Benchmark: decoded frames/s of the LightBeam first-pass decoder on B200 (BASELINE.json).
+
+Workload (config 2 of BASELINE.json, the largest single-GPU config without an LLM):
+256 synthetic B2T'25-shaped utterances per GPU (T=500 x 41 classes, N(0,2) fp32 logits),
+beam 64, 100k-word lexicon (+10% homophones), ~1M-n-gram 4-gram LM, no LLM fusion
+(fixed-point n-gram stub on the final pass: `DeviceNgramScorer(model, omega/phi)`, the device
+twin of `StubScorer(ngram_model, scale=omega/phi)`).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+One step = the whole decode of the batch from logits resident in HBM: fp64 log-softmax
+prologue (K1) -> persistent frame loop (K2) -> closure (K3) -> final n-gram fusion.  Timed
+with CUDA events on the decode stream, L2 flushed (256 MiB write) between steps outside the
+timed events.  `e2e` times the public API (`decode_batch_raw`) from host numpy logits to
+DecodeResult objects (H2D, kernels, D2H, n-best assembly).  `--impl reference` times the CPU
+restatement of the reference (oracle/, the reference itself is Python and does not travel to
+the GPU box) on a bounded sample with all host cores.  Multi-GPU: one process per GPU, trials
+sharded (weak scaling), no collective on the data path; the barrier and the max-over-ranks of
+the device time use torch.distributed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FRAME_MS = 80.0  # B2T'25 frame duration
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--trials", type=int, default=256, help="utterances per GPU")
+    ap.add_argument("--frames", type=int, default=500)
+    ap.add_argument("--beam", type=int, default=64)
+    ap.add_argument("--words", type=int, default=100_000)
+    ap.add_argument("--ngrams", type=str, default="500000,250000,150000")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs(args, rank):
+    from paper_2603_14002_b200 import PROFILES, synth
+
+    n2, n3, n4 = (int(x) for x in args.ngrams.split(","))
+    world = synth.make_world(n_words=args.words, n2=n2, n3=n3, n4=n4, seed=12345)
+    cfg = PROFILES["b2t25"].replace(beam_size=args.beam)
+    raws = synth.make_logits(args.trials, args.frames, 41, base_seed=1000 + rank * args.trials)
+    return world, cfg, raws
+
+
+def workload_desc(args, world):
+    return {
+        "workload": (f"BASELINE config 2: {args.trials} utterances/GPU x {args.frames} frames x 41 "
+                     f"classes, beam {args.beam}, {args.words}-word lexicon "
+                     f"({world.table.num_states} states), {len(world.model.probs)}-entry 4-gram, "
+                     "no LLM fusion (fixed-point n-gram stub, final pass only), b2t25 profile"),
+        "trials_per_gpu": args.trials,
+        "frames": args.frames,
+        "beam": args.beam,
+        "vocab": 41,
+        "lexicon_words": args.words,
+        "ngrams": len(world.model.probs),
+        "l2": "flushed between timed steps (256 MiB write, outside the timed events)",
+    }
+
+
+# --------------------------------------------------------------------------- CPU baseline
+_CPU = {}
+
+
+def _cpu_worker(i):
+    from oracle import lightbeam_oracle as O
+    from paper_2603_14002_b200 import StubScorer
+
+    w, cfg, raws = _CPU["world"], _CPU["cfg"], _CPU["raws"]
+    d = O.log_softmax_scaled(raws[i % len(raws)], cfg.acoustic_scale)
+    sc = StubScorer(ngram_model=w.model, scale=cfg.ngram_weight / cfg.llm_weight)
+    t0 = time.perf_counter()
+    O.decode(d, cfg, w.table, w.model, sc, final_llm_only=True)
+    return d.shape[0], time.perf_counter() - t0
+
+
+def cpu_baseline(world, cfg, raws, budget_s):
+    """The oracle port (numpy/Python restatement of the reference decode) on all host cores:
+    a fork pool of os.cpu_count() workers decoding trials of the same workload for ~budget_s."""
+    import multiprocessing as mp
+
+    _CPU.update(world=world, cfg=cfg, raws=raws)
+    cores = os.cpu_count() or 1
+    # probe one trial to size the sample
+    frames0, dt0 = _cpu_worker(0)
+    per_core = max(1, int(budget_s / max(dt0, 1e-3)))
+    n = max(cores, min(per_core * cores, 4 * len(raws)))
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        out = pool.map(_cpu_worker, range(n), chunksize=1)
+    wall = time.perf_counter() - t0
+    frames = sum(f for f, _ in out)
+    return {"value": frames / wall, "unit": "frames/s", "cores": cores, "kind": "port",
+            "sample": f"{n} of the workload's utterances (T={raws.shape[1]}), oracle/ restatement "
+                      f"of lightbeam.decoder.decode, fork pool x{cores}, {wall:.1f} s wall",
+            "single_core_frames_per_s": frames0 / dt0}
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- GPU run
+def algorithmic_bytes(stats, V=41, VP=44):
+    """SURVEY.md §8(d) per-frame bytes, from the run's own counters:
+    logit/log-prob row (8 B x V fp64 as the kernel reads it) + lexicon rows gathered for the
+    mask (4 B x V per beam entering the frame) + n-gram probes (one 32-B record each)
+    + word-history node writes (20 B) + completion CSR reads (8 B per boundary beam)."""
+    return (8 * V * stats["frames"] + 4 * V * stats["beams_in"] + 32 * stats["ngram_probes"]
+            + 20 * stats["history_nodes"] + 8 * stats["boundary_beams"])
+
+
+def run_ours(args):
+    import torch
+
+    world_n, rank, local = dist_env()
+    if world_n > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    from paper_2603_14002_b200 import DeviceNgramScorer, decode_batch_raw
+    from paper_2603_14002_b200.decoder import device_model, run_search
+
+    t_setup = time.perf_counter()
+    world, cfg, raws = make_inputs(args, rank)
+    scale = cfg.ngram_weight / cfg.llm_weight
+    scorer = DeviceNgramScorer(world.model, scale)
+    torch.cuda.set_device(dev)
+    dm = device_model(world.table, world.model, dev)
+    setup_s = time.perf_counter() - t_setup
+    B, T = raws.shape[0], raws.shape[1]
+    frames = np.full(B, T, dtype=np.int32)
+    x_dev = torch.from_numpy(raws).to(f"cuda:{dev}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    batch = dm.batch(cfg, B, T)
+
+    def step():
+        batch.load_logits(None, frames, on_device_ptr=x_dev.data_ptr())
+        run_search(batch, cfg, scorer, world.model, final_llm_only=True)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        batch.mark_begin()
+        step()
+        batch.mark_end()
+    if world_n > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    batch.clear_stats()
+    ms_steps, launches = [], 0
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            batch.mark_begin()
+            step()
+            ms, nl = batch.mark_end()
+            ms_steps.append(ms)
+            launches += nl
+        torch.cuda.synchronize()
+    stats = batch.stats()
+    total_ms = float(sum(ms_steps))
+    if world_n > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    frames_per_step = float(frames.sum()) * world_n
+    value = frames_per_step / (ms_per_step / 1e3)
+
+    # dominant kernel (K2) duration and its roofline, timed alone on the same stream
+    flush.zero_()
+    batch.load_logits(None, frames, on_device_ptr=x_dev.data_ptr())
+    batch.reset()
+    batch.clear_stats()
+    torch.cuda.synchronize()
+    batch.mark_begin()
+    batch.run(0, T, 0, scale)
+    k_ms, _ = batch.mark_end()
+    kstats = batch.stats()
+    alg = algorithmic_bytes(kstats)
+    peaks = {}
+    pp = ROOT / "MEASURED_PEAKS.json"
+    if pp.exists():
+        peaks = json.loads(pp.read_text())
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg / (k_ms / 1e3) / 1e9
+
+    # correctness spot check of this very run against the oracle (2 utterances)
+    check = None
+    if rank == 0:
+        from oracle import lightbeam_oracle as O
+        from paper_2603_14002_b200 import StubScorer
+
+        res = decode_batch_raw((raws[:2], frames[:2]), cfg, world.table, world.model, scorer,
+                               final_llm_only=True, device=dev)
+        ok = 0
+        for i in range(2):
+            want = O.decode(O.log_softmax_scaled(raws[i], cfg.acoustic_scale), cfg, world.table,
+                            world.model, StubScorer(ngram_model=world.model, scale=scale),
+                            final_llm_only=True)
+            ok += int(res[i].text == want.text and abs(res[i].score - want.score) <= 1e-9 * abs(want.score))
+        check = f"{ok}/2 utterances match the oracle (text, score)"
+
+    # e2e through the public API from host logits
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(2):
+            decode_batch_raw((raws, frames), cfg, world.table, world.model, scorer,
+                             final_llm_only=True, device=dev)
+        torch.cuda.synchronize()
+        if world_n > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(1, min(args.steps, 3))
+        for _ in range(n_e2e):
+            res = decode_batch_raw((raws, frames), cfg, world.table, world.model, scorer,
+                                   final_llm_only=True, device=dev)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        if world_n > 1:
+            t = torch.tensor([e2e_s], device=f"cuda:{dev}", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        ne, nw = batch_entry_sizes(batch)
+        h2d = raws.nbytes + frames.nbytes
+        d2h = ne * (4 + 4 + 8 + 8 + 4) + nw * 4 + B * (4 + 4 + 4) + B * cfg.beam_size * 8 + 16 * B
+        e2e = {"value": frames_per_step / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "api": "paper_2603_14002_b200.decode_batch_raw(host fp32 logits) -> DecodeResult list"}
+
+    cpu = None
+    if rank == 0 and world_n == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(world, cfg, raws[: min(64, B)], args.cpu_seconds)
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "decoded frames/s (BASELINE config 2, beam 64, 1 x B200 per rank)",
+            "value": value,
+            "unit": "frames/s",
+            "n_gpus": world_n,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded N(0,2) logits, synthetic lexicon and 4-gram LM)",
+            "config": dict(workload_desc(args, world), parallelism=f"dp{world_n} (utterance sharding, no collective)"),
+            "rtf": (ms_per_step / 1e3) / (frames_per_step * FRAME_MS / 1e3),
+            "trials_per_s": B * world_n / (ms_per_step / 1e3),
+            "frame_latency_us": (ms_per_step * 1e3) / T,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "frames_kernel (K2)", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel_ms": k_ms, "algorithmic_bytes": alg,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pp.exists() else "fallback 6650 GB/s"},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "counters": stats,
+            "setup_s": setup_s,
+            "parity_check": check,
+        }
+        print(json.dumps(line))
+    if world_n > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def batch_entry_sizes(batch):
+    import ctypes as C
+
+    from paper_2603_14002_b200 import _native as N
+
+    ne, nw = C.c_int64(), C.c_int64()
+    N.check(N.lib().lb_batch_gather_entries(batch.h, C.byref(ne), C.byref(nw)))
+    return ne.value, nw.value
+
+
+def run_reference(args):
+    world_n, rank, _ = dist_env()
+    if rank != 0:
+        return
+    world, cfg, raws = make_inputs(args, rank)
+    vals = []
+    cpu = None
+    for _ in range(max(1, args.warmup and 0)):
+        pass
+    budget = max(2.0, args.cpu_seconds / max(1, args.steps))
+    for _ in range(args.steps):
+        cpu = cpu_baseline(world, cfg, raws[: min(64, len(raws))], budget)
+        vals.append(cpu["value"])
+    value = statistics.median(vals)
+    cpu["value"] = value
+    line = {
+        "impl": "reference",
+        "metric": "decoded frames/s (BASELINE config 2, beam 64, 1 x B200 per rank)",
+        "value": value,
+        "unit": "frames/s",
+        "n_gpus": world_n,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded N(0,2) logits, synthetic lexicon and 4-gram LM)",
+        "config": dict(workload_desc(args, world), parallelism="host cores (fork pool)"),
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,215 @@
+/*
+ * lightbeam_b200.h -- C ABI of the B200-native LightBeam first-pass decoder.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * `lightbeam.decoder.decode(d, config, tt, lm, scorer, final_llm_only)`
+ * (/root/reference/pkg/src/lightbeam/decoder.py:408-460).  The reference is pure Python, so its
+ * "FFI" is the Python call itself; a maintainer binds these entry points with ctypes
+ * (see INTEGRATION.md).  All functions are extern "C", take plain pointers and sizes, return
+ * an int status (LB_OK = 0, negative = API/CUDA error; lb_last_error() has the message), and
+ * never throw.  Handles are not thread-safe; one host thread drives one batch.
+ *
+ * Reference interface replaced by each entry point:
+ *   lb_model_create      build_transition_table / load_table (lexicon.py:149-209,236-277) and
+ *                        load_arpa (ngram.py:90-174) results uploaded as device images:
+ *                        dense (S,V) int32 table + completion CSR, hashed 4-gram records.
+ *   lb_batch_create      init_beams (decoder.py:177-179) for B utterances at once.
+ *   lb_batch_set_logits  scale_log_softmax (logits.py:119-130) fused on upload (kernel K1).
+ *   lb_batch_set_logprobs  the LogProbMatrix argument of decode (decoder.py:408) in fp64.
+ *   lb_batch_run         the frame loop of decode (decoder.py:426-430): step (238-326) with
+ *                        valid_mask (lexicon.py:124-137) and apply_ngram (decoder.py:182-235);
+ *                        optionally the interval/final fusion of a device n-gram scorer.
+ *   lb_batch_close       _close_utterance (decoder.py:375-405).
+ *   lb_batch_gather_entries  the text gathering of apply_llm (decoder.py:338-345) as word-id
+ *                        sequences per ortho entry.
+ *   lb_batch_apply_scores  the fusion part of apply_llm (decoder.py:354-371).
+ *   lb_batch_device_ngram_fusion  apply_llm with StubScorer(ngram_model=...) semantics
+ *                        (scorer.py:121-139) evaluated on the device.
+ *   lb_batch_results     ranking + n-best of decode (decoder.py:433-460), assembled on the host.
+ */
+#ifndef LIGHTBEAM_B200_H
+#define LIGHTBEAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LB_OK 0
+#define LB_ERR_ARG -1
+#define LB_ERR_CUDA -2
+#define LB_ERR_CAPACITY -3
+#define LB_ERR_STATE -4
+
+/* per-trial status codes (lb_batch_status) */
+#define LB_TRIAL_OK 0
+#define LB_TRIAL_EMPTY_CANDIDATES 1 /* "all candidates pruned at frame t"  decoder.py:267-268 */
+#define LB_TRIAL_EMPTY_MERGE 2      /* "all hypotheses pruned at frame t"  decoder.py:314-315 */
+#define LB_TRIAL_EMPTY_CLOSE 3      /* "no hypothesis survived ... closure" decoder.py:394-395 */
+#define LB_TRIAL_HISTORY_FULL 4     /* device word-history arena exhausted (capacity error) */
+
+#define LB_PUNCT_NONE 0
+#define LB_PUNCT_PERIOD 1
+#define LB_PUNCT_QUESTION 2
+#define LB_PUNCT_EXCLAIM 3
+
+typedef struct lb_model lb_model;
+typedef struct lb_batch lb_batch;
+
+/* DecodeConfig (config.py:14-62), field for field. */
+typedef struct {
+  double acoustic_scale;
+  double beam_prune_threshold;
+  double homophone_prune_threshold;
+  double token_insertion_bonus;
+  double word_boundary_bonus;
+  double ngram_weight;
+  double llm_weight;
+  int32_t beam_size;
+  int32_t ortho_beams;
+  int32_t llm_rescore_interval;
+  int32_t llm_chunk_size;
+} lb_config;
+
+/* TransitionTable image (host pointers, copied during lb_model_create). */
+typedef struct {
+  const int32_t* table; /* [num_states * vocab_size], row-major */
+  int32_t num_states;
+  int32_t vocab_size; /* <= 64 */
+  int32_t sink, blank_id, space_id;
+  const int32_t* comp_offsets; /* [num_states + 1] */
+  const int32_t* comp_surface; /* [n_comp] distinct surfaces per completion state */
+  const int32_t* comp_lmword;  /* [n_comp] LM word id each surface is scored as, -1 = OOV kill */
+  int32_t n_comp;
+  const char* surface_blob;    /* utf-8 surfaces, concatenated */
+  const int64_t* surface_offsets; /* [n_surfaces + 1] */
+  int32_t n_surfaces;
+} lb_table_desc;
+
+/* NGramModel image. */
+typedef struct {
+  int32_t order; /* 1..4 */
+  int64_t n_grams;
+  const uint32_t* words;   /* [n_grams * 4], 0xFFFFFFFF pads */
+  const double* probs;     /* [n_grams], quiet-NaN 0x7FF8DEAD00000000 = no probability */
+  const double* backoffs;  /* [n_grams], 0.0 if absent */
+  uint32_t bos_id;         /* id of "<s>" (initial history) */
+  int32_t eos_word;        /* LM id "</s>" is scored as, -1 = kill */
+} lb_ngram_desc;
+
+/* Counters a run accumulates (summed over trials and frames). */
+typedef struct {
+  uint64_t frames;        /* frames stepped */
+  uint64_t beams_in;      /* sum over frames of K_t entering the frame */
+  uint64_t beams_out;     /* sum of K_{t+1} */
+  uint64_t ngram_calls;   /* score_word evaluations */
+  uint64_t ngram_probes;  /* hash-slot reads */
+  uint64_t boundary_beams;
+  uint64_t history_nodes;
+  uint64_t fallback_selects; /* frames that needed the radix fallback */
+} lb_stats;
+
+const char* lb_last_error(void);
+int lb_device_count(int32_t* out);
+
+int lb_model_create(const lb_table_desc* table, const lb_ngram_desc* ngram, int32_t device,
+                    lb_model** out);
+int lb_model_destroy(lb_model* m);
+/* bytes of device memory held by the model images */
+int lb_model_footprint(const lb_model* m, int64_t* bytes);
+
+/* stream: a cudaStream_t (NULL = legacy default stream). */
+int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32_t max_frames,
+                    void* stream, lb_batch** out);
+int lb_batch_destroy(lb_batch* b);
+
+/* Inputs.  `x` is [n_trials, max_frames, vocab_size] row-major; frames[i] <= max_frames.
+ * `on_device` != 0: x is a device pointer (stream-ordered), else a host pointer (pinned or
+ * pageable) copied inside the call.  set_logits runs the fp64 log-softmax prologue. */
+int lb_batch_set_logits(lb_batch* b, int32_t n_trials, const float* x, const int32_t* frames,
+                        int32_t on_device);
+int lb_batch_set_logprobs(lb_batch* b, int32_t n_trials, const double* d, const int32_t* frames,
+                          int32_t on_device);
+/* Copy the device log-prob matrix back: out is [n_trials, max_frames, vocab_size]. */
+int lb_batch_get_logprobs(lb_batch* b, double* out_host);
+
+/* Reset every trial to the root hypothesis (init_beams). */
+int lb_batch_reset(lb_batch* b);
+
+/* Advance every live trial over frames [t_begin, t_end) (clipped to its own length).
+ * fusion_mode 0: no interval fusion inside the kernel (the caller performs events).
+ * fusion_mode 1: interval events of a device n-gram scorer with scale `scorer_scale` happen
+ *               inside the kernel (t > 0, t % r == 0).  */
+int lb_batch_run(lb_batch* b, int32_t t_begin, int32_t t_end, int32_t fusion_mode,
+                 double scorer_scale);
+
+/* End-of-utterance closure for every live trial. */
+int lb_batch_close(lb_batch* b);
+
+/* apply_llm with StubScorer(ngram_model=model, scale) semantics on the device.
+ * final != 0 also appends "</s>" and sets punctuation "." (scorer.py:136-139).
+ * only trials with frames > min_frames take part (interval events skip finished trials). */
+int lb_batch_device_ngram_fusion(lb_batch* b, int32_t final, double scale, int32_t min_frames);
+
+/* Word-history gather for host scorers.  Fills, per trial, the ortho entries of every beam
+ * in beam order and their word-id (surface id) sequences.
+ *   entry_count[n_trials]          number of entries per trial
+ *   entry_offsets[n_trials + 1]    prefix sums of entry_count (first-entry index per trial)
+ * then lb_batch_copy_entries copies the flat arrays (sizes from lb_batch_entry_totals). */
+int lb_batch_gather_entries(lb_batch* b, int64_t* n_entries, int64_t* n_words);
+int lb_batch_copy_entries(lb_batch* b, int32_t* entry_trial, int32_t* entry_beam,
+                          int64_t* word_offsets /* [n_entries+1] */, int32_t* words,
+                          double* totals, int32_t* puncts);
+
+/* Host scores for every gathered entry, in gather order.  has_text[i] == 0 marks the empty
+ * history (gets total 0.0 and no punctuation).  final != 0 stores puncts.  Only trials with
+ * frames > min_frames are updated. */
+int lb_batch_apply_scores(lb_batch* b, const double* scores, const int32_t* puncts,
+                          const uint8_t* has_text, int32_t final, int32_t min_frames);
+
+/* Per-trial status and failing frame. */
+int lb_batch_status(lb_batch* b, int32_t* status, int32_t* fail_frame);
+int lb_batch_stats(lb_batch* b, lb_stats* out);
+int lb_batch_clear_stats(lb_batch* b);
+
+/* Debug/parity: copy the current beams of trial `trial` (scores, hashes, prefixes, last). */
+int lb_batch_dump_beams(lb_batch* b, int32_t trial, int32_t* k, double* scores, uint64_t* h1,
+                        uint64_t* h2, int32_t* prefix, int32_t* last);
+
+/* Per-frame beam dump for parity bisection (off by default): after lb_batch_enable_dump(b, 1)
+ * every lb_batch_run records the post-merge beams of each frame. */
+int lb_batch_enable_dump(lb_batch* b, int32_t on);
+int lb_batch_dump_frame(lb_batch* b, int32_t trial, int32_t t, int32_t* k, double* scores,
+                        uint64_t* h1, uint64_t* h2, int32_t* prefix, int32_t* last);
+
+/* Results (decoder.py:433-460).  Two-step: lb_batch_results_size gives the byte size of the
+ * text blob and the total n-best count; lb_batch_results fills caller buffers:
+ *   best_text_off/best_text_len/best_score [n_trials]
+ *   nbest_count [n_trials], nbest_text_off/nbest_text_len/nbest_score [total nbest]
+ * Texts are utf-8 "w1 w2 ...<punct>" in `blob`. */
+int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest);
+int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* best_text_len,
+                     double* best_score, int32_t* nbest_count, int64_t* nbest_text_off,
+                     int32_t* nbest_text_len, double* nbest_score);
+
+/* Device-side timing of everything enqueued between mark_begin and mark_end (CUDA events on
+ * the batch stream); also the number of kernels this library launched in between. */
+int lb_batch_mark_begin(lb_batch* b);
+int lb_batch_mark_end(lb_batch* b, float* ms, int64_t* launches);
+int lb_batch_sync(lb_batch* b);
+
+/* Standalone acoustic prologue (logits.py:119-130) on device `device`: host in/out. */
+int lb_log_softmax_host(const float* x, int64_t rows, int32_t cols, double alpha,
+                        double* out, int32_t device);
+
+/* Host n-gram scorer parity helper: device score_word for (history ids, word). */
+int lb_model_score_words(lb_model* m, int32_t n, const uint32_t* hist /* [n*3] */,
+                         const int32_t* hist_len, const int32_t* word, double* inc,
+                         uint32_t* succ /* [n*3] */, int32_t* succ_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

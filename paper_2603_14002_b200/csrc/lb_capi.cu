@@ -1,0 +1,810 @@
+// lb_capi.cu -- the extern "C" boundary (include/lightbeam_b200.h): model/batch lifetime,
+// device memory, launch orchestration, and host-side result assembly (ranking + n-best,
+// decoder.py:433-460).  No torch types cross this boundary.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lightbeam_b200.h"
+#include "lb_device.cuh"
+#include "lb_internal.h"
+
+using namespace lbd;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                   \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return fail(LB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+struct lb_model {
+  int device = 0;
+  ModelDev dev{};
+  int32_t* d_table = nullptr;
+  int32_t* d_comp_off = nullptr;
+  int32_t* d_comp_surf = nullptr;
+  int32_t* d_comp_lm = nullptr;
+  NgRec* d_ng = nullptr;
+  int64_t ng_cap = 0;
+  int max_probe = 0;
+  int64_t bytes = 0;
+  std::vector<std::string> surfaces;
+};
+
+struct lb_batch {
+  lb_model* m = nullptr;
+  lb_config cfg{};
+  CfgDev cdev{};
+  cudaStream_t st = nullptr;
+  int32_t Bmax = 0, Tmax = 0, K = 0, O = 0, VPD = 0;
+  BatchDev dev{};
+  Layout L{};
+  int32_t n_trials = 0;
+  std::vector<int32_t> T_host;
+  int32_t* d_T = nullptr;
+  double* d_D = nullptr;
+  float* d_x = nullptr;
+  // gather scratch
+  int64_t* d_counts = nullptr;
+  int64_t* d_entry_off = nullptr;
+  int64_t* d_word_off = nullptr;
+  int64_t cap_entries = 0, cap_words = 0;
+  int32_t* d_e_trial = nullptr;
+  int32_t* d_e_beam = nullptr;
+  int64_t* d_e_woff = nullptr;
+  int32_t* d_words = nullptr;
+  double* d_totals = nullptr;
+  int32_t* d_puncts = nullptr;
+  double* d_scores_in = nullptr;
+  int32_t* d_puncts_in = nullptr;
+  uint8_t* d_has_text = nullptr;
+  int64_t n_entries = 0, n_words = 0;
+  std::vector<int64_t> h_entry_off, h_word_off;
+  // results cache
+  std::string blob;
+  std::vector<int64_t> best_off, nb_off;
+  std::vector<int32_t> best_len, nb_count, nb_len;
+  std::vector<double> best_score, nb_score;
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  unsigned long long launch_mark = 0;
+};
+
+extern "C" {
+
+const char* lb_last_error(void) { return g_err.c_str(); }
+
+int lb_device_count(int32_t* out) {
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  *out = n;
+  return LB_OK;
+}
+
+int lb_model_create(const lb_table_desc* td, const lb_ngram_desc* nd, int32_t device,
+                    lb_model** out) {
+  if (!td || !nd || !out) return fail(LB_ERR_ARG, "null argument");
+  if (td->vocab_size < 3 || td->vocab_size > 64)
+    return fail(LB_ERR_ARG, "vocab_size must be in [3, 64]");
+  if (nd->order < 1 || nd->order > 4) return fail(LB_ERR_ARG, "n-gram order must be 1..4");
+  CK(cudaSetDevice(device));
+  lb_model* m = new lb_model();
+  m->device = device;
+  const int32_t S = td->num_states, V = td->vocab_size;
+  const int32_t VP = (int32_t)round_up(V, 4);
+  // lexicon table, padded rows
+  int32_t* tmp = nullptr;
+  CK(dalloc(&tmp, (size_t)S * V));
+  CK(cudaMemcpy(tmp, td->table, (size_t)S * V * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CK(dalloc(&m->d_table, (size_t)S * VP));
+  CK(lbk::pad_table(m->d_table, tmp, S, V, VP, 0));
+  CK(cudaDeviceSynchronize());
+  CK(cudaFree(tmp));
+  CK(dalloc(&m->d_comp_off, (size_t)S + 1));
+  CK(cudaMemcpy(m->d_comp_off, td->comp_offsets, ((size_t)S + 1) * sizeof(int32_t),
+                cudaMemcpyHostToDevice));
+  CK(dalloc(&m->d_comp_surf, (size_t)td->n_comp));
+  CK(dalloc(&m->d_comp_lm, (size_t)td->n_comp));
+  if (td->n_comp > 0) {
+    CK(cudaMemcpy(m->d_comp_surf, td->comp_surface, (size_t)td->n_comp * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(m->d_comp_lm, td->comp_lmword, (size_t)td->n_comp * 4, cudaMemcpyHostToDevice));
+  }
+  // n-gram hash image: capacity = next power of two >= 2 * n (load factor <= 0.5)
+  int64_t cap = 1024;
+  while (cap < 2 * nd->n_grams) cap <<= 1;
+  m->ng_cap = cap;
+  CK(dalloc(&m->d_ng, (size_t)cap));
+  CK(cudaMemset(m->d_ng, 0xFF, (size_t)cap * sizeof(NgRec)));
+  if (nd->n_grams > 0) {
+    uint32_t* dw = nullptr;
+    double *dp = nullptr, *db = nullptr;
+    int* dmax = nullptr;
+    CK(dalloc(&dw, (size_t)nd->n_grams * 4));
+    CK(dalloc(&dp, (size_t)nd->n_grams));
+    CK(dalloc(&db, (size_t)nd->n_grams));
+    CK(dalloc(&dmax, 1));
+    CK(cudaMemset(dmax, 0, sizeof(int)));
+    CK(cudaMemcpy(dw, nd->words, (size_t)nd->n_grams * 16, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dp, nd->probs, (size_t)nd->n_grams * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db, nd->backoffs, (size_t)nd->n_grams * 8, cudaMemcpyHostToDevice));
+    CK(lbk::build_ngram_table(m->d_ng, (uint64_t)(cap - 1), dw, dp, db, nd->n_grams, dmax, 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(&m->max_probe, dmax, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(dw);
+    cudaFree(dp);
+    cudaFree(db);
+    cudaFree(dmax);
+  }
+  m->bytes = (int64_t)S * VP * 4 + ((int64_t)S + 1) * 4 + (int64_t)td->n_comp * 8 +
+             cap * (int64_t)sizeof(NgRec);
+  ModelDev& d = m->dev;
+  d.table = m->d_table;
+  d.S = S;
+  d.V = V;
+  d.VP = VP;
+  d.sink = td->sink;
+  d.blank = td->blank_id;
+  d.space = td->space_id;
+  d.comp_off = m->d_comp_off;
+  d.comp_surf = m->d_comp_surf;
+  d.comp_lm = m->d_comp_lm;
+  d.ng = m->d_ng;
+  d.ng_mask = (uint64_t)(cap - 1);
+  d.order = nd->order;
+  d.bos = nd->bos_id;
+  d.eos_word = nd->eos_word;
+  m->surfaces.resize(td->n_surfaces);
+  for (int32_t i = 0; i < td->n_surfaces; ++i)
+    m->surfaces[i].assign(td->surface_blob + td->surface_offsets[i],
+                          (size_t)(td->surface_offsets[i + 1] - td->surface_offsets[i]));
+  *out = m;
+  return LB_OK;
+}
+
+int lb_model_destroy(lb_model* m) {
+  if (!m) return LB_OK;
+  cudaSetDevice(m->device);
+  cudaFree(m->d_table);
+  cudaFree(m->d_comp_off);
+  cudaFree(m->d_comp_surf);
+  cudaFree(m->d_comp_lm);
+  cudaFree(m->d_ng);
+  delete m;
+  return LB_OK;
+}
+
+int lb_model_footprint(const lb_model* m, int64_t* bytes) {
+  if (!m || !bytes) return fail(LB_ERR_ARG, "null argument");
+  *bytes = m->bytes;
+  return LB_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Place the per-CTA working set: shared memory first, spilling the bulkiest regions to the
+// trial's global scratch when a wide beam would not fit in 227 KB.
+void plan_layout(lb_batch* b) {
+  const int64_t K = b->K, O = b->O, VP = b->m->dev.VP, VPD = b->VPD;
+  const int nt = lbk::max_threads_for((int)K);
+  const int64_t lcap = std::max<int64_t>(2 * K, K + 256);
+  int64_t sz[N_REGIONS] = {};
+  sz[R_DBUF] = 2 * CHUNK * VPD * 8;
+  sz[R_ROWS] = K * VP * 4;
+  const int64_t beam[7] = {K * 8, K * 8, K * 8, K * 4, K * 4, K * 4, K * O * 32};
+  for (int i = 0; i < 7; ++i) {
+    sz[R_CUR_SCORE + i] = beam[i];
+    sz[R_NXT_SCORE + i] = beam[i];
+  }
+  sz[R_MASK] = K * 8;
+  sz[R_CVAL] = lcap * 8;
+  sz[R_CKEY] = lcap * 4;
+  sz[R_SVAL] = K * 8;
+  sz[R_SKEY] = K * 4;
+  sz[R_NSCORE] = K * 8;
+  sz[R_NH1] = K * 8;
+  sz[R_NH2] = K * 8;
+  for (int r : {R_NLAST, R_NPRE, R_NPAR, R_RANK, R_BLIST, R_BNENT}) sz[r] = K * 4;
+  sz[R_BENTS] = K * O * 32;
+  sz[R_KEEP] = ((K + 31) / 32) * 4;
+  sz[R_WARP] = (nt / 32) * (int64_t)sizeof(WarpScratch);
+  const int64_t budget = 200 * 1024;  // leave room for static shared memory
+  int in_smem[N_REGIONS];
+  for (int i = 0; i < N_REGIONS; ++i) in_smem[i] = 1;
+  const int spill_order[] = {R_BENTS, R_NXT_ENTS, R_CUR_ENTS, R_ROWS, R_CVAL, R_CKEY,
+                             R_NXT_H1, R_NXT_H2, R_CUR_H1, R_CUR_H2, R_NH1, R_NH2};
+  auto total = [&]() {
+    int64_t t = 0;
+    for (int i = 0; i < N_REGIONS; ++i)
+      if (in_smem[i]) t += round_up(sz[i], 16);
+    return t;
+  };
+  for (int r : spill_order) {
+    if (total() <= budget) break;
+    in_smem[r] = 0;
+  }
+  int64_t so = 0, go = 0;
+  for (int i = 0; i < N_REGIONS; ++i) {
+    if (in_smem[i]) {
+      b->L.off[i] = so;
+      so += round_up(sz[i], 16);
+    } else {
+      b->L.off[i] = go;
+      go += round_up(sz[i], 16);
+    }
+    b->L.in_smem[i] = in_smem[i];
+  }
+  b->L.smem_bytes = so;
+  b->L.gscratch_bytes = go;
+  b->L.lcap = (int32_t)lcap;
+  b->L.stage_rows = in_smem[R_ROWS];
+  b->L.nthreads = nt;
+}
+
+void fill_cfg(lb_batch* b) {
+  const lb_config& c = b->cfg;
+  CfgDev& d = b->cdev;
+  d.theta = c.beam_prune_threshold;
+  d.lambda = c.homophone_prune_threshold;
+  d.beta = c.token_insertion_bonus;
+  d.gamma = c.word_boundary_bonus;
+  d.omega = c.ngram_weight;
+  d.phi = c.llm_weight;
+  const double span = std::min(c.beam_prune_threshold, 24.0);
+  d.inv_binw = (double)NBINS / span;
+  d.k = c.beam_size;
+  d.O = c.ortho_beams;
+  d.r = c.llm_rescore_interval;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32_t max_frames,
+                    void* stream, lb_batch** out) {
+  if (!m || !cfg || !out) return fail(LB_ERR_ARG, "null argument");
+  if (max_trials < 1 || max_frames < 1) return fail(LB_ERR_ARG, "empty batch");
+  if (cfg->beam_size < 1 || cfg->beam_size > 4096) return fail(LB_ERR_ARG, "beam_size out of range");
+  if (cfg->ortho_beams < 1 || cfg->ortho_beams > OMAX)
+    return fail(LB_ERR_ARG, "ortho_beams must be in [1, 8]");
+  CK(cudaSetDevice(m->device));
+  lb_batch* b = new lb_batch();
+  b->m = m;
+  b->cfg = *cfg;
+  b->st = reinterpret_cast<cudaStream_t>(stream);
+  b->Bmax = max_trials;
+  b->Tmax = max_frames;
+  b->K = cfg->beam_size;
+  b->O = cfg->ortho_beams;
+  b->VPD = (int32_t)round_up(m->dev.V, 2);
+  fill_cfg(b);
+  plan_layout(b);
+  CK(lbk::set_smem_limit(b->L.nthreads, b->L.smem_bytes));
+  const size_t B = (size_t)max_trials, K = (size_t)b->K, O = (size_t)b->O;
+  int64_t ncap = (int64_t)max_frames * b->K * b->O + 1;
+  const int64_t budget_nodes = (int64_t)16e9 / (20 * (int64_t)B);
+  ncap = std::min<int64_t>(ncap, std::max<int64_t>(4096, budget_nodes));
+  ncap = std::min<int64_t>(ncap, (int64_t)1 << 30);
+  BatchDev& d = b->dev;
+  d.Tmax = max_frames;
+  d.K = b->K;
+  d.O = b->O;
+  d.VPD = b->VPD;
+  d.ncap = (int32_t)ncap;
+  CK(dalloc(&b->d_T, B));
+  CK(dalloc(&b->d_D, B * max_frames * b->VPD));
+  CK(dalloc(&d.nbeam, B));
+  CK(dalloc(&d.score, B * K));
+  CK(dalloc(&d.h1, B * K));
+  CK(dalloc(&d.h2, B * K));
+  CK(dalloc(&d.last, B * K));
+  CK(dalloc(&d.prefix, B * K));
+  CK(dalloc(&d.nent, B * K));
+  CK(dalloc(&d.ents, B * K * O));
+  CK(dalloc(&d.nparent, B * ncap));
+  CK(dalloc(&d.nsurf, B * ncap));
+  CK(dalloc(&d.ndepth, B * ncap));
+  CK(dalloc(&d.ncum, B * ncap));
+  CK(dalloc(&d.ncount, B));
+  CK(dalloc(&d.status, B));
+  CK(dalloc(&d.fail_frame, B));
+  CK(dalloc(&d.stats, B * 8));
+  CK(cudaMemset(d.stats, 0, B * 8 * sizeof(unsigned long long)));
+  CK(dalloc(&d.gscratch, std::max<int64_t>(16, b->L.gscratch_bytes) * B));
+  d.gscratch_stride = std::max<int64_t>(16, b->L.gscratch_bytes);
+  CK(dalloc(&b->d_counts, 2 * B));
+  CK(dalloc(&b->d_entry_off, B + 1));
+  CK(dalloc(&b->d_word_off, B + 1));
+  d.T = b->d_T;
+  d.D = b->d_D;
+  CK(cudaEventCreate(&b->ev0));
+  CK(cudaEventCreate(&b->ev1));
+  b->T_host.assign(B, 0);
+  *out = b;
+  return LB_OK;
+}
+
+int lb_batch_destroy(lb_batch* b) {
+  if (!b) return LB_OK;
+  cudaSetDevice(b->m->device);
+  cudaStreamSynchronize(b->st);
+  BatchDev& d = b->dev;
+  void* ptrs[] = {b->d_T, b->d_D, b->d_x, d.nbeam, d.score, d.h1, d.h2, d.last, d.prefix, d.nent,
+                  d.ents, d.nparent, d.nsurf, d.ndepth, d.ncum, d.ncount, d.status,
+                  d.fail_frame, d.stats, d.gscratch, b->d_counts, b->d_entry_off,
+                  b->d_word_off, b->d_e_trial, b->d_e_beam, b->d_e_woff, b->d_words,
+                  b->d_totals, b->d_puncts, b->d_scores_in, b->d_puncts_in, b->d_has_text,
+                  d.dump_h1, d.dump_h2, d.dump_pre, d.dump_last, d.dump_score, d.dump_k};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (b->ev0) cudaEventDestroy(b->ev0);
+  if (b->ev1) cudaEventDestroy(b->ev1);
+  delete b;
+  return LB_OK;
+}
+
+static int set_trials(lb_batch* b, int32_t n, const int32_t* frames) {
+  if (n < 1 || n > b->Bmax) return fail(LB_ERR_ARG, "n_trials out of range");
+  for (int32_t i = 0; i < n; ++i)
+    if (frames[i] < 0 || frames[i] > b->Tmax) return fail(LB_ERR_ARG, "frames out of range");
+  b->n_trials = n;
+  b->dev.B = n;
+  b->T_host.assign(frames, frames + n);
+  CK(cudaMemcpyAsync(b->d_T, frames, n * sizeof(int32_t), cudaMemcpyHostToDevice, b->st));
+  return LB_OK;
+}
+
+int lb_batch_set_logprobs(lb_batch* b, int32_t n, const double* x, const int32_t* frames,
+                          int32_t on_device) {
+  if (!b || !x || !frames) return fail(LB_ERR_ARG, "null argument");
+  int rc = set_trials(b, n, frames);
+  if (rc) return rc;
+  const int V = b->m->dev.V;
+  CK(cudaMemcpy2DAsync(b->d_D, b->VPD * sizeof(double), x, V * sizeof(double), V * sizeof(double),
+                       (size_t)n * b->Tmax,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, b->st));
+  return LB_OK;
+}
+
+int lb_batch_set_logits(lb_batch* b, int32_t n, const float* x, const int32_t* frames,
+                        int32_t on_device) {
+  if (!b || !x || !frames) return fail(LB_ERR_ARG, "null argument");
+  int rc = set_trials(b, n, frames);
+  if (rc) return rc;
+  const int V = b->m->dev.V;
+  const size_t rows = (size_t)n * b->Tmax;
+  const float* src = x;
+  if (!on_device) {
+    if (!b->d_x) CK(dalloc(&b->d_x, (size_t)b->Bmax * b->Tmax * V));
+    CK(cudaMemcpyAsync(b->d_x, x, rows * V * sizeof(float), cudaMemcpyHostToDevice, b->st));
+    src = b->d_x;
+  }
+  CK(lbk::log_softmax(src, (int64_t)rows, V, V, b->cfg.acoustic_scale, b->d_D, b->VPD, b->st));
+  return LB_OK;
+}
+
+int lb_batch_get_logprobs(lb_batch* b, double* out) {
+  if (!b || !out) return fail(LB_ERR_ARG, "null argument");
+  const int V = b->m->dev.V;
+  CK(cudaMemcpy2DAsync(out, V * sizeof(double), b->d_D, b->VPD * sizeof(double), V * sizeof(double),
+                       (size_t)b->n_trials * b->Tmax, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  return LB_OK;
+}
+
+int lb_batch_reset(lb_batch* b) {
+  if (!b || b->n_trials < 1) return fail(LB_ERR_STATE, "no trials loaded");
+  CK(lbk::reset(b->m->dev, b->dev, b->st));
+  return LB_OK;
+}
+
+int lb_batch_run(lb_batch* b, int32_t t_begin, int32_t t_end, int32_t fusion_mode,
+                 double scorer_scale) {
+  if (!b || b->n_trials < 1) return fail(LB_ERR_STATE, "no trials loaded");
+  if (t_begin < 0 || t_end > b->Tmax || t_begin > t_end) return fail(LB_ERR_ARG, "bad frame range");
+  if (t_begin == t_end) return LB_OK;
+  CK(lbk::frames(b->m->dev, b->cdev, b->dev, b->L, t_begin, t_end, fusion_mode, scorer_scale,
+                 b->st));
+  return LB_OK;
+}
+
+int lb_batch_close(lb_batch* b) {
+  if (!b || b->n_trials < 1) return fail(LB_ERR_STATE, "no trials loaded");
+  CK(lbk::close(b->m->dev, b->cdev, b->dev, b->st));
+  return LB_OK;
+}
+
+int lb_batch_device_ngram_fusion(lb_batch* b, int32_t final_, double scale, int32_t min_frames) {
+  if (!b || b->n_trials < 1) return fail(LB_ERR_STATE, "no trials loaded");
+  CK(lbk::device_ngram_fusion(b->m->dev, b->cdev, b->dev, final_, scale, min_frames, b->st));
+  return LB_OK;
+}
+
+int lb_batch_gather_entries(lb_batch* b, int64_t* n_entries, int64_t* n_words) {
+  if (!b || b->n_trials < 1) return fail(LB_ERR_STATE, "no trials loaded");
+  const int B = b->n_trials;
+  CK(lbk::count_entries(b->dev, b->d_counts, b->st));
+  std::vector<int64_t> counts(2 * (size_t)B);
+  CK(cudaMemcpyAsync(counts.data(), b->d_counts, counts.size() * 8, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  b->h_entry_off.assign(B + 1, 0);
+  b->h_word_off.assign(B + 1, 0);
+  for (int i = 0; i < B; ++i) {
+    b->h_entry_off[i + 1] = b->h_entry_off[i] + counts[2 * i];
+    b->h_word_off[i + 1] = b->h_word_off[i] + counts[2 * i + 1];
+  }
+  const int64_t ne = b->h_entry_off[B], nw = b->h_word_off[B];
+  if (ne > b->cap_entries) {
+    const int64_t cap = std::max<int64_t>(ne, 2 * b->cap_entries);
+    for (void* p : {(void*)b->d_e_trial, (void*)b->d_e_beam, (void*)b->d_e_woff,
+                    (void*)b->d_totals, (void*)b->d_puncts, (void*)b->d_scores_in,
+                    (void*)b->d_puncts_in, (void*)b->d_has_text})
+      if (p) cudaFree(p);
+    CK(dalloc(&b->d_e_trial, cap));
+    CK(dalloc(&b->d_e_beam, cap));
+    CK(dalloc(&b->d_e_woff, cap + 1));
+    CK(dalloc(&b->d_totals, cap));
+    CK(dalloc(&b->d_puncts, cap));
+    CK(dalloc(&b->d_scores_in, cap));
+    CK(dalloc(&b->d_puncts_in, cap));
+    CK(dalloc(&b->d_has_text, cap));
+    b->cap_entries = cap;
+  }
+  if (nw > b->cap_words) {
+    const int64_t cap = std::max<int64_t>(nw, 2 * b->cap_words);
+    if (b->d_words) cudaFree(b->d_words);
+    CK(dalloc(&b->d_words, cap));
+    b->cap_words = cap;
+  }
+  CK(cudaMemcpyAsync(b->d_entry_off, b->h_entry_off.data(), (B + 1) * 8, cudaMemcpyHostToDevice, b->st));
+  CK(cudaMemcpyAsync(b->d_word_off, b->h_word_off.data(), (B + 1) * 8, cudaMemcpyHostToDevice, b->st));
+  CK(lbk::write_entries(b->dev, b->d_entry_off, b->d_word_off, b->d_e_trial, b->d_e_beam,
+                        b->d_e_woff, b->d_words, b->d_totals, b->d_puncts, b->st));
+  b->n_entries = ne;
+  b->n_words = nw;
+  if (n_entries) *n_entries = ne;
+  if (n_words) *n_words = nw;
+  return LB_OK;
+}
+
+int lb_batch_copy_entries(lb_batch* b, int32_t* entry_trial, int32_t* entry_beam,
+                          int64_t* word_offsets, int32_t* words, double* totals, int32_t* puncts) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  const int64_t ne = b->n_entries, nw = b->n_words;
+  if (ne > 0) {
+    if (entry_trial) CK(cudaMemcpyAsync(entry_trial, b->d_e_trial, ne * 4, cudaMemcpyDeviceToHost, b->st));
+    if (entry_beam) CK(cudaMemcpyAsync(entry_beam, b->d_e_beam, ne * 4, cudaMemcpyDeviceToHost, b->st));
+    if (word_offsets) CK(cudaMemcpyAsync(word_offsets, b->d_e_woff, ne * 8, cudaMemcpyDeviceToHost, b->st));
+    if (totals) CK(cudaMemcpyAsync(totals, b->d_totals, ne * 8, cudaMemcpyDeviceToHost, b->st));
+    if (puncts) CK(cudaMemcpyAsync(puncts, b->d_puncts, ne * 4, cudaMemcpyDeviceToHost, b->st));
+  }
+  if (nw > 0 && words) CK(cudaMemcpyAsync(words, b->d_words, nw * 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  if (word_offsets) word_offsets[ne] = nw;
+  return LB_OK;
+}
+
+int lb_batch_apply_scores(lb_batch* b, const double* scores, const int32_t* puncts,
+                          const uint8_t* has_text, int32_t final_, int32_t min_frames) {
+  if (!b || !scores || !has_text) return fail(LB_ERR_ARG, "null argument");
+  const int64_t ne = b->n_entries;
+  if (ne > 0) {
+    CK(cudaMemcpyAsync(b->d_scores_in, scores, ne * 8, cudaMemcpyHostToDevice, b->st));
+    CK(cudaMemcpyAsync(b->d_has_text, has_text, ne, cudaMemcpyHostToDevice, b->st));
+    if (puncts) CK(cudaMemcpyAsync(b->d_puncts_in, puncts, ne * 4, cudaMemcpyHostToDevice, b->st));
+    else CK(cudaMemsetAsync(b->d_puncts_in, 0, ne * 4, b->st));
+  }
+  CK(lbk::apply_scores(b->cdev, b->dev, b->d_entry_off, b->d_scores_in, b->d_puncts_in,
+                       b->d_has_text, final_, min_frames, b->st));
+  return LB_OK;
+}
+
+int lb_batch_status(lb_batch* b, int32_t* status, int32_t* fail_frame) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  const int B = b->n_trials;
+  if (status) CK(cudaMemcpyAsync(status, b->dev.status, B * 4, cudaMemcpyDeviceToHost, b->st));
+  if (fail_frame) CK(cudaMemcpyAsync(fail_frame, b->dev.fail_frame, B * 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  return LB_OK;
+}
+
+int lb_batch_stats(lb_batch* b, lb_stats* out) {
+  if (!b || !out) return fail(LB_ERR_ARG, "null argument");
+  const int B = b->n_trials;
+  std::vector<unsigned long long> s((size_t)B * 8);
+  std::vector<int32_t> nc(B);
+  CK(cudaMemcpyAsync(s.data(), b->dev.stats, s.size() * 8, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(nc.data(), b->dev.ncount, B * 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  std::memset(out, 0, sizeof(*out));
+  for (int i = 0; i < B; ++i) {
+    out->frames += s[8 * i + 0];
+    out->beams_in += s[8 * i + 1];
+    out->beams_out += s[8 * i + 2];
+    out->ngram_calls += s[8 * i + 3];
+    out->ngram_probes += s[8 * i + 4];
+    out->boundary_beams += s[8 * i + 5];
+    out->fallback_selects += s[8 * i + 7];
+    out->history_nodes += (uint64_t)std::max(0, nc[i] - 1);
+  }
+  return LB_OK;
+}
+
+int lb_batch_clear_stats(lb_batch* b) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  CK(cudaMemsetAsync(b->dev.stats, 0, (size_t)b->Bmax * 8 * 8, b->st));
+  return LB_OK;
+}
+
+int lb_batch_dump_beams(lb_batch* b, int32_t trial, int32_t* k, double* scores, uint64_t* h1,
+                        uint64_t* h2, int32_t* prefix, int32_t* last) {
+  if (!b || trial < 0 || trial >= b->n_trials) return fail(LB_ERR_ARG, "bad trial");
+  int32_t kk = 0;
+  CK(cudaMemcpyAsync(&kk, b->dev.nbeam + trial, 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  const size_t hb = (size_t)trial * b->K;
+  *k = kk;
+  if (kk > 0) {
+    CK(cudaMemcpyAsync(scores, b->dev.score + hb, kk * 8, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(h1, b->dev.h1 + hb, kk * 8, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(h2, b->dev.h2 + hb, kk * 8, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(prefix, b->dev.prefix + hb, kk * 4, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(last, b->dev.last + hb, kk * 4, cudaMemcpyDeviceToHost, b->st));
+  }
+  CK(cudaStreamSynchronize(b->st));
+  return LB_OK;
+}
+
+int lb_batch_enable_dump(lb_batch* b, int32_t on) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  BatchDev& d = b->dev;
+  if (on && !d.dump_k) {
+    const size_t n = (size_t)b->Bmax * b->Tmax * b->K;
+    CK(dalloc(&d.dump_h1, n));
+    CK(dalloc(&d.dump_h2, n));
+    CK(dalloc(&d.dump_pre, n));
+    CK(dalloc(&d.dump_last, n));
+    CK(dalloc(&d.dump_score, n));
+    CK(dalloc(&d.dump_k, (size_t)b->Bmax * b->Tmax));
+    CK(cudaMemset(d.dump_k, 0xFF, (size_t)b->Bmax * b->Tmax * 4));
+  } else if (!on && d.dump_k) {
+    for (void* p : {(void*)d.dump_h1, (void*)d.dump_h2, (void*)d.dump_pre, (void*)d.dump_last,
+                    (void*)d.dump_score, (void*)d.dump_k})
+      cudaFree(p);
+    d.dump_h1 = d.dump_h2 = nullptr;
+    d.dump_pre = d.dump_last = d.dump_k = nullptr;
+    d.dump_score = nullptr;
+  }
+  return LB_OK;
+}
+
+int lb_batch_dump_frame(lb_batch* b, int32_t trial, int32_t t, int32_t* k, double* scores,
+                        uint64_t* h1, uint64_t* h2, int32_t* prefix, int32_t* last) {
+  if (!b || !b->dev.dump_k) return fail(LB_ERR_STATE, "dump not enabled");
+  if (trial < 0 || trial >= b->n_trials || t < 0 || t >= b->Tmax) return fail(LB_ERR_ARG, "bad index");
+  const BatchDev& d = b->dev;
+  int32_t kk = 0;
+  CK(cudaMemcpyAsync(&kk, d.dump_k + (size_t)trial * b->Tmax + t, 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  *k = kk;
+  if (kk > 0) {
+    const size_t base = ((size_t)trial * b->Tmax + t) * b->K;
+    CK(cudaMemcpyAsync(scores, d.dump_score + base, kk * 8, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(h1, d.dump_h1 + base, kk * 8, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(h2, d.dump_h2 + base, kk * 8, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(prefix, d.dump_pre + base, kk * 4, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaMemcpyAsync(last, d.dump_last + base, kk * 4, cudaMemcpyDeviceToHost, b->st));
+    CK(cudaStreamSynchronize(b->st));
+  }
+  return LB_OK;
+}
+
+// ------------------------------------------------------------------ results (host assembly)
+int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest) {
+  if (!b || b->n_trials < 1) return fail(LB_ERR_STATE, "no trials loaded");
+  int rc = lb_batch_gather_entries(b, nullptr, nullptr);
+  if (rc) return rc;
+  const int B = b->n_trials;
+  const int64_t ne = b->n_entries, nw = b->n_words;
+  std::vector<int32_t> e_beam(ne), words(nw), puncts(ne), nbeam(B), status(B);
+  std::vector<int64_t> woff(ne + 1);
+  std::vector<double> totals(ne), scores((size_t)B * b->K);
+  rc = lb_batch_copy_entries(b, nullptr, e_beam.data(), woff.data(), words.data(), totals.data(),
+                             puncts.data());
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(nbeam.data(), b->dev.nbeam, B * 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(status.data(), b->dev.status, B * 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(scores.data(), b->dev.score, scores.size() * 8, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  static const char* PUN[4] = {"", ".", "?", "!"};
+  const auto& surf = b->m->surfaces;
+  b->blob.clear();
+  b->best_off.assign(B, 0);
+  b->best_len.assign(B, 0);
+  b->best_score.assign(B, 0.0);
+  b->nb_count.assign(B, 0);
+  b->nb_off.clear();
+  b->nb_len.clear();
+  b->nb_score.clear();
+  std::vector<std::string> texts;
+  std::vector<int> order;
+  struct Pair {
+    int text;
+    double score;
+  };
+  std::vector<Pair> pairs;
+  for (int t = 0; t < B; ++t) {
+    if (status[t] != 0) continue;
+    const int K = nbeam[t];
+    const int64_t e0 = b->h_entry_off[t], e1 = b->h_entry_off[t + 1];
+    // entries of beam i: contiguous, beam-major
+    std::vector<int64_t> first(K + 1, e1);
+    for (int64_t e = e1 - 1; e >= e0; --e) first[e_beam[e]] = e;
+    first[K] = e1;
+    for (int i = K - 1; i >= 0; --i)
+      if (first[i] > first[i + 1]) first[i] = first[i + 1];
+    texts.assign(e1 - e0, std::string());
+    for (int64_t e = e0; e < e1; ++e) {
+      std::string& s = texts[e - e0];
+      for (int64_t w = woff[e]; w < woff[e + 1]; ++w) {
+        if (w > woff[e]) s.push_back(' ');
+        s += surf[words[w]];
+      }
+      s += PUN[puncts[e] & 3];
+    }
+    const double* sc = scores.data() + (size_t)t * b->K;
+    order.resize(K);
+    for (int i = 0; i < K; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return sc[a] > sc[c]; });
+    pairs.clear();
+    for (int i : order) {
+      const double best_lm = totals[first[i]];
+      for (int64_t e = first[i]; e < first[i + 1]; ++e) {
+        const double s = (sc[i] - best_lm) + totals[e];
+        pairs.push_back({(int)(e - e0), s});
+      }
+    }
+    std::stable_sort(pairs.begin(), pairs.end(),
+                     [](const Pair& a, const Pair& c) { return a.score > c.score; });
+    const int best = order[0];
+    b->best_off[t] = (int64_t)b->blob.size();
+    b->blob += texts[first[best] - e0];
+    b->best_len[t] = (int32_t)(b->blob.size() - b->best_off[t]);
+    b->best_score[t] = sc[best];
+    std::vector<const std::string*> seen;
+    int cnt = 0;
+    for (const Pair& p : pairs) {
+      const std::string& tx = texts[p.text];
+      bool dup = false;
+      for (const std::string* s : seen)
+        if (*s == tx) {
+          dup = true;
+          break;
+        }
+      if (dup) continue;
+      seen.push_back(&tx);
+      b->nb_off.push_back((int64_t)b->blob.size());
+      b->blob += tx;
+      b->nb_len.push_back((int32_t)tx.size());
+      b->nb_score.push_back(p.score);
+      ++cnt;
+    }
+    b->nb_count[t] = cnt;
+  }
+  *blob_bytes = (int64_t)b->blob.size();
+  *total_nbest = (int64_t)b->nb_score.size();
+  return LB_OK;
+}
+
+int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* best_text_len,
+                     double* best_score, int32_t* nbest_count, int64_t* nbest_text_off,
+                     int32_t* nbest_text_len, double* nbest_score) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  const int B = b->n_trials;
+  if (blob && !b->blob.empty()) std::memcpy(blob, b->blob.data(), b->blob.size());
+  for (int t = 0; t < B; ++t) {
+    if (best_text_off) best_text_off[t] = b->best_off[t];
+    if (best_text_len) best_text_len[t] = b->best_len[t];
+    if (best_score) best_score[t] = b->best_score[t];
+    if (nbest_count) nbest_count[t] = b->nb_count[t];
+  }
+  const size_t n = b->nb_score.size();
+  for (size_t i = 0; i < n; ++i) {
+    if (nbest_text_off) nbest_text_off[i] = b->nb_off[i];
+    if (nbest_text_len) nbest_text_len[i] = b->nb_len[i];
+    if (nbest_score) nbest_score[i] = b->nb_score[i];
+  }
+  return LB_OK;
+}
+
+int lb_batch_mark_begin(lb_batch* b) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  b->launch_mark = lbk::g_launches;
+  CK(cudaEventRecord(b->ev0, b->st));
+  return LB_OK;
+}
+
+int lb_batch_mark_end(lb_batch* b, float* ms, int64_t* launches) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  CK(cudaEventRecord(b->ev1, b->st));
+  CK(cudaEventSynchronize(b->ev1));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, b->ev0, b->ev1));
+  if (ms) *ms = t;
+  if (launches) *launches = (int64_t)(lbk::g_launches - b->launch_mark);
+  return LB_OK;
+}
+
+int lb_batch_sync(lb_batch* b) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  CK(cudaStreamSynchronize(b->st));
+  return LB_OK;
+}
+
+int lb_log_softmax_host(const float* x, int64_t rows, int32_t cols, double alpha, double* out,
+                        int32_t device) {
+  if (!x || !out || cols < 1 || cols > 64) return fail(LB_ERR_ARG, "bad arguments");
+  CK(cudaSetDevice(device));
+  float* dx = nullptr;
+  double* dy = nullptr;
+  CK(dalloc(&dx, (size_t)rows * cols));
+  CK(dalloc(&dy, (size_t)rows * cols));
+  CK(cudaMemcpy(dx, x, (size_t)rows * cols * 4, cudaMemcpyHostToDevice));
+  CK(lbk::log_softmax(dx, rows, cols, cols, alpha, dy, cols, 0));
+  CK(cudaMemcpy(out, dy, (size_t)rows * cols * 8, cudaMemcpyDeviceToHost));
+  cudaFree(dx);
+  cudaFree(dy);
+  return LB_OK;
+}
+
+int lb_model_score_words(lb_model* m, int32_t n, const uint32_t* hist, const int32_t* hist_len,
+                         const int32_t* word, double* inc, uint32_t* succ, int32_t* succ_len) {
+  if (!m || n < 0) return fail(LB_ERR_ARG, "bad arguments");
+  if (n == 0) return LB_OK;
+  CK(cudaSetDevice(m->device));
+  uint32_t *dh = nullptr, *ds = nullptr;
+  int32_t *dl = nullptr, *dw = nullptr, *dsl = nullptr;
+  double* di = nullptr;
+  CK(dalloc(&dh, (size_t)n * 3));
+  CK(dalloc(&ds, (size_t)n * 3));
+  CK(dalloc(&dl, (size_t)n));
+  CK(dalloc(&dw, (size_t)n));
+  CK(dalloc(&dsl, (size_t)n));
+  CK(dalloc(&di, (size_t)n));
+  CK(cudaMemcpy(dh, hist, (size_t)n * 12, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dl, hist_len, (size_t)n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, word, (size_t)n * 4, cudaMemcpyHostToDevice));
+  CK(lbk::score_words(m->dev, n, dh, dl, dw, di, ds, dsl, 0));
+  CK(cudaMemcpy(inc, di, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(succ, ds, (size_t)n * 12, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(succ_len, dsl, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  for (void* p : {(void*)dh, (void*)ds, (void*)dl, (void*)dw, (void*)dsl, (void*)di}) cudaFree(p);
+  return LB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,465 @@
+"""Drop-in decode API over the CUDA beam-search kernels.
+
+`decode(d, config, tt, lm, scorer, final_llm_only=False)` has the signature, arguments,
+return type and error behaviour of the reference `lightbeam.decoder.decode`
+(`pkg/src/lightbeam/decoder.py:408-460`): a `LogProbMatrix` (or fp64 `(T, V)` array) in, a
+`DecodeResult` out, `DataValueError` on an empty matrix, `EmptyBeamError` when the beam dies,
+`ScorerError` propagated from the scorer.  It accepts the reference's own `TransitionTable`,
+`LmSession`/`NGramModel`, `DecodeConfig` and scorer objects as well as ours.
+
+`decode_batch` / `decode_batch_raw` run many utterances at once -- one CTA per utterance --
+which is how the GPU is meant to be fed.  Flow per batch:
+
+    frames kernel over [0, e1]  -> fusion event e1 -> frames (e1, e2] -> ... -> closure
+    -> final fusion -> ranking / n-best (host assembly in the C library)
+
+Fusion events (`t > 0 and t % r == 0`, `decoder.py:428`) with a host scorer gather the word
+histories on the device, send the unique texts through the scorer protocol, and apply the
+scores with a device kernel.  With a `DeviceNgramScorer` the events happen inside the frames
+kernel and the whole utterance is one launch plus closure and final fusion.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import images
+from .config import coerce_config
+from .errors import DataValueError, DeviceError, EmptyBeamError, ShapeError
+from .scorer import score_eos, score_texts
+
+PUNCT_CODE = {".": 1, "?": 2, "!": 3}
+PUNCT_CHAR = {0: "", 1: ".", 2: "?", 3: "!"}
+_STATUS_MSG = {
+    1: "all candidates pruned at frame {t}",
+    2: "all hypotheses pruned at frame {t}",
+    3: "no hypothesis survived end-of-utterance closure",
+}
+
+
+@dataclass
+class DecodeResult:
+    text: str
+    score: float
+    nbest: list
+    frame_count: int
+    wall_time_s: float
+    llm_events: int
+
+
+class DeviceModel:
+    """Device images of one (TransitionTable, NGramModel) pair, resident on one GPU."""
+
+    def __init__(self, tt, model, device: int = 0):
+        lib = N.lib()
+        ng = images.compile_ngram(model)
+        tab = images.compile_table(tt, model, ng)
+        self.ngram_image, self.table_image = ng, tab
+        self.surfaces = tab.surfaces
+        self.whitespace_free = tab.whitespace_free
+        self.vocab_size = tab.table.shape[1]
+        self.blank_id, self.space_id = tab.blank_id, tab.space_id
+        self.device = device
+        self.model = model
+        soff = tab.surface_off.astype(np.int64)
+        td = N.LbTableDesc(
+            N.ptr(tab.table), tab.table.shape[0], tab.table.shape[1], tab.sink, tab.blank_id,
+            tab.space_id, N.ptr(tab.comp_off), N.ptr(tab.comp_surface), N.ptr(tab.comp_lmword),
+            len(tab.comp_surface), tab.surface_blob, N.ptr(soff), len(tab.surfaces))
+        nd = N.LbNgramDesc(model.order, len(ng.probs), N.ptr(ng.words), N.ptr(ng.probs),
+                           N.ptr(ng.backoffs), ng.bos_id, ng.eos_eff)
+        handle = C.c_void_p()
+        N.check(lib.lb_model_create(C.byref(td), C.byref(nd), device, C.byref(handle)))
+        self.handle = handle
+        self._batches: dict = {}
+
+    def footprint(self) -> int:
+        out = C.c_int64()
+        N.check(N.lib().lb_model_footprint(self.handle, C.byref(out)))
+        return out.value
+
+    def batch(self, cfg, n_trials: int, n_frames: int) -> "DeviceBatch":
+        key = tuple(getattr(cfg, f) for f in (
+            "acoustic_scale", "beam_prune_threshold", "homophone_prune_threshold",
+            "token_insertion_bonus", "word_boundary_bonus", "ngram_weight", "llm_weight",
+            "beam_size", "ortho_beams", "llm_rescore_interval", "llm_chunk_size"))
+        got = self._batches.get(key)
+        if got is None or got.max_trials < n_trials or got.max_frames < n_frames:
+            if got is not None:
+                got.destroy()
+            got = DeviceBatch(self, cfg, max(n_trials, 1), max(n_frames, 1))
+            self._batches[key] = got
+        return got
+
+    def score_words(self, hist: list, words: list):
+        """Device score_word for (history word ids, LM word id) pairs -- parity helper."""
+        n = len(words)
+        h = np.zeros((n, 3), dtype=np.uint32)
+        hl = np.zeros(n, dtype=np.int32)
+        for i, hh in enumerate(hist):
+            h[i, : len(hh)] = hh
+            hl[i] = len(hh)
+        w = np.asarray(words, dtype=np.int32)
+        inc = np.empty(n, dtype=np.float64)
+        succ = np.empty((n, 3), dtype=np.uint32)
+        sl = np.empty(n, dtype=np.int32)
+        N.check(N.lib().lb_model_score_words(self.handle, n, N.ptr(h), N.ptr(hl), N.ptr(w),
+                                             N.ptr(inc), N.ptr(succ), N.ptr(sl)))
+        return inc, [tuple(int(x) for x in succ[i, : sl[i]]) for i in range(n)]
+
+    def __del__(self):
+        try:
+            for b in self._batches.values():
+                b.destroy()
+            if getattr(self, "handle", None):
+                N.lib(False).lb_model_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+_MODELS: dict = {}
+
+
+def device_model(tt, lm, device: int = 0) -> DeviceModel:
+    """Cached DeviceModel for (tt, lm-model, device); entries die with their components."""
+    model = getattr(lm, "model", lm)
+    key = (id(tt), id(model), device)
+    hit = _MODELS.get(key)
+    if hit is not None:
+        wt, wm, dm = hit
+        if wt() is tt and wm() is model:
+            return dm
+    dm = DeviceModel(tt, model, device)
+    _MODELS[key] = (weakref.ref(tt), weakref.ref(model), dm)
+    return dm
+
+
+class DeviceBatch:
+    """One lb_batch: device beam state for up to `max_trials` utterances of `max_frames`."""
+
+    def __init__(self, dm: DeviceModel, cfg, max_trials: int, max_frames: int, stream=None):
+        self.dm = dm
+        self.cfg = cfg
+        self.max_trials, self.max_frames = max_trials, max_frames
+        c = N.LbConfig(cfg.acoustic_scale, cfg.beam_prune_threshold, cfg.homophone_prune_threshold,
+                       cfg.token_insertion_bonus, cfg.word_boundary_bonus, cfg.ngram_weight,
+                       cfg.llm_weight, cfg.beam_size, cfg.ortho_beams, cfg.llm_rescore_interval,
+                       cfg.llm_chunk_size)
+        h = C.c_void_p()
+        N.check(N.lib().lb_batch_create(dm.handle, C.byref(c), max_trials, max_frames,
+                                        C.c_void_p(stream or 0), C.byref(h)))
+        self.h = h
+        self.n = 0
+        self.frames = np.zeros(0, dtype=np.int32)
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            N.lib(False).lb_batch_destroy(self.h)
+            self.h = None
+
+    # ---- inputs
+    def _frames(self, frames) -> np.ndarray:
+        fr = np.ascontiguousarray(frames, dtype=np.int32)
+        if fr.size and (fr.min() < 0 or fr.max() > self.max_frames):
+            raise ShapeError("frame counts exceed the batch capacity")
+        self.n = len(fr)
+        self.frames = fr
+        return fr
+
+    def load_logprobs(self, d: np.ndarray, frames, on_device_ptr: int | None = None):
+        fr = self._frames(frames)
+        if on_device_ptr is not None:
+            N.check(N.lib().lb_batch_set_logprobs(self.h, len(fr), C.c_void_p(on_device_ptr),
+                                                  N.ptr(fr), 1))
+            return
+        x = np.ascontiguousarray(d, dtype=np.float64)
+        if x.shape[1] != self.max_frames:
+            pad = np.zeros((x.shape[0], self.max_frames, x.shape[2]), dtype=np.float64)
+            pad[:, : x.shape[1]] = x
+            x = pad
+        N.check(N.lib().lb_batch_set_logprobs(self.h, len(fr), N.ptr(x), N.ptr(fr), 0))
+
+    def load_logits(self, x: np.ndarray | None, frames, on_device_ptr: int | None = None):
+        fr = self._frames(frames)
+        if on_device_ptr is not None:
+            N.check(N.lib().lb_batch_set_logits(self.h, len(fr), C.c_void_p(on_device_ptr),
+                                                N.ptr(fr), 1))
+            return
+        a = np.ascontiguousarray(x, dtype=np.float32)
+        if a.shape[1] != self.max_frames:
+            pad = np.zeros((a.shape[0], self.max_frames, a.shape[2]), dtype=np.float32)
+            pad[:, : a.shape[1]] = a
+            a = pad
+        self._hold = a  # the copy is stream-ordered; keep the host buffer alive
+        N.check(N.lib().lb_batch_set_logits(self.h, len(fr), N.ptr(a), N.ptr(fr), 0))
+
+    def get_logprobs(self) -> np.ndarray:
+        out = np.empty((self.n, self.max_frames, self.dm.vocab_size), dtype=np.float64)
+        N.check(N.lib().lb_batch_get_logprobs(self.h, N.ptr(out)))
+        return out
+
+    # ---- search steps
+    def reset(self):
+        N.check(N.lib().lb_batch_reset(self.h))
+
+    def run(self, t0: int, t1: int, fusion_mode: int = 0, scale: float = 0.0):
+        N.check(N.lib().lb_batch_run(self.h, t0, t1, fusion_mode, scale))
+
+    def close(self):
+        N.check(N.lib().lb_batch_close(self.h))
+
+    def device_fusion(self, final: bool, scale: float, min_frames: int = 0):
+        N.check(N.lib().lb_batch_device_ngram_fusion(self.h, int(final), scale, min_frames))
+
+    def gather(self):
+        ne, nw = C.c_int64(), C.c_int64()
+        lib = N.lib()
+        N.check(lib.lb_batch_gather_entries(self.h, C.byref(ne), C.byref(nw)))
+        n_e, n_w = ne.value, nw.value
+        et = np.empty(n_e, dtype=np.int32)
+        eb = np.empty(n_e, dtype=np.int32)
+        wo = np.empty(n_e + 1, dtype=np.int64)
+        words = np.empty(max(n_w, 1), dtype=np.int32)
+        tot = np.empty(n_e, dtype=np.float64)
+        pun = np.empty(n_e, dtype=np.int32)
+        N.check(lib.lb_batch_copy_entries(self.h, N.ptr(et), N.ptr(eb), N.ptr(wo), N.ptr(words),
+                                          N.ptr(tot), N.ptr(pun)))
+        return et, eb, wo, words, tot, pun
+
+    def apply_scores(self, scores, puncts, has_text, final: bool, min_frames: int):
+        s = np.ascontiguousarray(scores, dtype=np.float64)
+        p = np.ascontiguousarray(puncts, dtype=np.int32)
+        h = np.ascontiguousarray(has_text, dtype=np.uint8)
+        N.check(N.lib().lb_batch_apply_scores(self.h, N.ptr(s), N.ptr(p), N.ptr(h), int(final),
+                                              min_frames))
+
+    def status(self):
+        st = np.empty(self.n, dtype=np.int32)
+        ff = np.empty(self.n, dtype=np.int32)
+        N.check(N.lib().lb_batch_status(self.h, N.ptr(st), N.ptr(ff)))
+        return st, ff
+
+    def stats(self) -> dict:
+        s = N.LbStats()
+        N.check(N.lib().lb_batch_stats(self.h, C.byref(s)))
+        return {name: int(getattr(s, name)) for name, _ in N.LbStats._fields_}
+
+    def clear_stats(self):
+        N.check(N.lib().lb_batch_clear_stats(self.h))
+
+    def enable_dump(self, on: bool = True):
+        N.check(N.lib().lb_batch_enable_dump(self.h, int(on)))
+
+    def dump_frame(self, trial: int, t: int):
+        k = C.c_int32()
+        K = self.cfg.beam_size
+        sc = np.empty(K, dtype=np.float64)
+        a = np.empty(K, dtype=np.uint64)
+        b = np.empty(K, dtype=np.uint64)
+        p = np.empty(K, dtype=np.int32)
+        la = np.empty(K, dtype=np.int32)
+        N.check(N.lib().lb_batch_dump_frame(self.h, trial, t, C.byref(k), N.ptr(sc), N.ptr(a),
+                                            N.ptr(b), N.ptr(p), N.ptr(la)))
+        n = k.value
+        return [(int(a[i]), int(b[i]), int(p[i]), int(la[i]), float(sc[i])) for i in range(max(n, 0))]
+
+    def beams(self, trial: int):
+        k = C.c_int32()
+        K = self.cfg.beam_size
+        sc = np.empty(K, dtype=np.float64)
+        a = np.empty(K, dtype=np.uint64)
+        b = np.empty(K, dtype=np.uint64)
+        p = np.empty(K, dtype=np.int32)
+        la = np.empty(K, dtype=np.int32)
+        N.check(N.lib().lb_batch_dump_beams(self.h, trial, C.byref(k), N.ptr(sc), N.ptr(a),
+                                            N.ptr(b), N.ptr(p), N.ptr(la)))
+        return [(int(a[i]), int(b[i]), int(p[i]), int(la[i]), float(sc[i])) for i in range(k.value)]
+
+    def mark_begin(self):
+        N.check(N.lib().lb_batch_mark_begin(self.h))
+
+    def mark_end(self):
+        ms, launches = C.c_float(), C.c_int64()
+        N.check(N.lib().lb_batch_mark_end(self.h, C.byref(ms), C.byref(launches)))
+        return ms.value, launches.value
+
+    def sync(self):
+        N.check(N.lib().lb_batch_sync(self.h))
+
+    def results(self):
+        """[(text, score, nbest)] per trial (None for failed trials)."""
+        lib = N.lib()
+        nbytes, ntot = C.c_int64(), C.c_int64()
+        N.check(lib.lb_batch_results_size(self.h, C.byref(nbytes), C.byref(ntot)))
+        n = self.n
+        blob = C.create_string_buffer(max(nbytes.value, 1))
+        boff = np.empty(n, dtype=np.int64)
+        blen = np.empty(n, dtype=np.int32)
+        bsc = np.empty(n, dtype=np.float64)
+        cnt = np.empty(n, dtype=np.int32)
+        m = max(ntot.value, 1)
+        noff = np.empty(m, dtype=np.int64)
+        nlen = np.empty(m, dtype=np.int32)
+        nsc = np.empty(m, dtype=np.float64)
+        N.check(lib.lb_batch_results(self.h, blob, N.ptr(boff), N.ptr(blen), N.ptr(bsc),
+                                     N.ptr(cnt), N.ptr(noff), N.ptr(nlen), N.ptr(nsc)))
+        raw = blob.raw[: nbytes.value]
+        st, _ = self.status()
+        out = []
+        k = 0
+        for i in range(n):
+            if st[i] != 0:
+                out.append(None)
+                continue
+            text = raw[boff[i]: boff[i] + blen[i]].decode("utf-8")
+            nb = []
+            for j in range(k, k + cnt[i]):
+                nb.append((raw[noff[j]: noff[j] + nlen[j]].decode("utf-8"), float(nsc[j])))
+            k += cnt[i]
+            out.append((text, float(bsc[i]), nb))
+        return out
+
+
+def _host_fusion(batch: DeviceBatch, scorer, cfg, final: bool, min_frames: int):
+    """apply_llm (decoder.py:329-372) with a host scorer: device gather -> protocol -> device."""
+    et, eb, wo, words, _tot, _pun = batch.gather()
+    surf = batch.dm.surfaces
+    n_e = len(et)
+    texts = [" ".join([surf[w] for w in words[wo[i]: wo[i + 1]]]) for i in range(n_e)]
+    live = batch.frames[et] > min_frames if n_e else np.zeros(0, dtype=bool)
+    uniq: list = []
+    seen: set = set()
+    for i in range(n_e):
+        tx = texts[i]
+        if live[i] and tx and tx not in seen:
+            seen.add(tx)
+            uniq.append(tx)
+    scores = np.zeros(n_e, dtype=np.float64)
+    puncts = np.zeros(n_e, dtype=np.int32)
+    has = np.zeros(n_e, dtype=np.uint8)
+    if final:
+        lut = dict(zip(uniq, score_eos(scorer, uniq, cfg.llm_chunk_size)))
+    else:
+        lut = {t: ("", s) for t, s in zip(uniq, score_texts(scorer, uniq, cfg.llm_chunk_size))}
+    for i in range(n_e):
+        tx = texts[i]
+        if live[i] and tx:
+            p, s = lut[tx]
+            scores[i] = s
+            puncts[i] = PUNCT_CODE.get(p, 0)
+            has[i] = 1
+    batch.apply_scores(scores, puncts, has, final, min_frames)
+
+
+def _uses_device_scorer(scorer, model, dm: DeviceModel) -> bool:
+    return getattr(scorer, "device_ngram_model", None) is model and dm.whitespace_free
+
+
+def run_search(batch: DeviceBatch, cfg, scorer, model, final_llm_only: bool):
+    """Everything after the inputs are on the device: frames, events, closure, final fusion."""
+    frames = batch.frames
+    t_max = int(frames.max()) if len(frames) else 0
+    r = cfg.llm_rescore_interval
+    batch.reset()
+    if _uses_device_scorer(scorer, model, batch.dm):
+        scale = scorer.scale
+        batch.run(0, t_max, 0 if final_llm_only else 1, scale)
+        batch.close()
+        batch.device_fusion(True, scale, 0)
+        return
+    t = 0
+    if not final_llm_only:
+        for e in range(r, t_max, r):  # events after frames e = r, 2r, ... (< the longest T)
+            batch.run(t, e + 1)
+            _host_fusion(batch, scorer, cfg, final=False, min_frames=e)
+            t = e + 1
+    batch.run(t, t_max)
+    batch.close()
+    _host_fusion(batch, scorer, cfg, final=True, min_frames=0)
+
+
+def _collect(batch: DeviceBatch, cfg, final_llm_only: bool, wall: float):
+    st, ff = batch.status()
+    res = batch.results()
+    out = []
+    for i in range(batch.n):
+        if st[i] != 0:
+            if st[i] == 4:
+                out.append(DeviceError("device word-history arena exhausted"))
+            else:
+                out.append(EmptyBeamError(_STATUS_MSG[int(st[i])].format(t=int(ff[i]))))
+            continue
+        text, score, nbest = res[i]
+        t_i = int(batch.frames[i])
+        events = 0 if final_llm_only else (t_i - 1) // cfg.llm_rescore_interval
+        out.append(DecodeResult(text, score, nbest, t_i, wall, events))
+    return out
+
+
+def _stack(mats, dtype):
+    frames = np.array([m.shape[0] for m in mats], dtype=np.int32)
+    v = mats[0].shape[1]
+    out = np.zeros((len(mats), int(frames.max()) if len(mats) else 0, v), dtype=dtype)
+    for i, m in enumerate(mats):
+        out[i, : m.shape[0]] = m
+    return out, frames
+
+
+def _prepare(cfg, tt, lm, device):
+    cfg = coerce_config(cfg)
+    model = getattr(lm, "model", lm)
+    return cfg, model, device_model(tt, model, device)
+
+
+def decode_batch(ds, config, tt, lm, scorer, final_llm_only: bool = False, device: int = 0):
+    """Decode many fp64 log-prob matrices (LogProbMatrix / (T, V) arrays, or (B, T, V) + lengths
+    via `ds=(array, frames)`).  Returns a list with a DecodeResult or the exception per item."""
+    cfg, model, dm = _prepare(config, tt, lm, device)
+    if isinstance(ds, tuple):
+        arr, frames = np.asarray(ds[0], dtype=np.float64), np.asarray(ds[1], dtype=np.int32)
+    else:
+        mats = [np.asarray(getattr(d, "frames", d), dtype=np.float64) for d in ds]
+        arr, frames = _stack(mats, np.float64)
+    if arr.ndim != 3 or arr.shape[2] != dm.vocab_size:
+        raise ShapeError(f"log-prob width must equal the table vocabulary ({dm.vocab_size})")
+    t0 = time.perf_counter()
+    batch = dm.batch(cfg, arr.shape[0], max(arr.shape[1], 1))
+    batch.load_logprobs(arr, frames)
+    run_search(batch, cfg, scorer, model, final_llm_only)
+    return _collect(batch, cfg, final_llm_only, time.perf_counter() - t0)
+
+
+def decode_batch_raw(raws, config, tt, lm, scorer, final_llm_only: bool = False, device: int = 0):
+    """Raw fp32 logits in (RawLogits list or `(array, frames)`): the log-softmax prologue runs
+    on the device (kernel K1) and feeds the search directly."""
+    cfg, model, dm = _prepare(config, tt, lm, device)
+    if isinstance(raws, tuple):
+        arr, frames = np.asarray(raws[0], dtype=np.float32), np.asarray(raws[1], dtype=np.int32)
+    else:
+        mats = [np.asarray(getattr(r, "frames", r), dtype=np.float32) for r in raws]
+        arr, frames = _stack(mats, np.float32)
+    if arr.ndim != 3 or arr.shape[2] != dm.vocab_size:
+        raise ShapeError(f"logit width must equal the table vocabulary ({dm.vocab_size})")
+    t0 = time.perf_counter()
+    batch = dm.batch(cfg, arr.shape[0], max(arr.shape[1], 1))
+    batch.load_logits(arr, frames)
+    run_search(batch, cfg, scorer, model, final_llm_only)
+    return _collect(batch, cfg, final_llm_only, time.perf_counter() - t0)
+
+
+def decode(d, config, tt, lm, scorer, final_llm_only: bool = False) -> DecodeResult:
+    """Drop-in for `lightbeam.decoder.decode` (decoder.py:408-460)."""
+    frames = np.asarray(getattr(d, "frames", d), dtype=np.float64)
+    if frames.ndim != 2 or frames.shape[0] == 0:
+        raise DataValueError("cannot decode an empty log-probability matrix")
+    res = decode_batch([frames], config, tt, lm, scorer, final_llm_only)[0]
+    if isinstance(res, Exception):
+        raise res
+    return res

@@ -1,0 +1,15 @@
+"""pytest setup: `-m gpu` marks tests that need a B200 (run through gpurun); everything else
+runs on the CPU build container."""
+
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+for p in (str(ROOT), str(ROOT / "tests")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run via gpurun")
+    config.addinivalue_line("markers", "slow: long-running (full BASELINE sizes)")

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA decoder (through the C ABI) against the oracle and the reference's
+golden fixtures.  Bar: bit-exact texts, fp64 scores, n-best lists, event counts, per-frame
+ordered beams (hash lanes, prefix ids, last token, score) and error messages."""
+
+import numpy as np
+import pytest
+
+import goldens as G
+from oracle import lightbeam_oracle as O
+from paper_2603_14002_b200 import (PROFILES, DeviceNgramScorer, StubScorer, decode, decode_batch,
+                                   decode_batch_raw, synth)
+from paper_2603_14002_b200.decoder import device_model
+
+pytestmark = pytest.mark.gpu
+
+
+def test_prologue_kernel_vs_numpy():
+    from paper_2603_14002_b200 import _native
+
+    for case in G.load("prologue"):
+        x = np.asarray(case["x"], dtype=np.float32)
+        got = _native.log_softmax_host(x, case["alpha"])
+        want = np.asarray(case["d"])
+        # numpy's SIMD exp is not libm-exact: allow a few ulps (north star: "within a few ulps")
+        np.testing.assert_allclose(got, want, rtol=8 * np.finfo(np.float64).eps, atol=1e-15)
+
+
+def test_device_score_word_hand_cases():
+    g = G.load("hand_ngram")
+    model = G.model_of({"arpa": g["arpa"]})
+    vocab = G.vocab_of(G.TINY_VOCAB)
+    tt = G.build_transition_table(G.lexicon_of([["a", "a", [1]], ["b", "b", [2]]]), vocab)
+    dm = device_model(tt, model)
+    wid = dm.ngram_image.word_id
+    hist, words = [], []
+    for case in g["cases"]:
+        hist.append([wid[w] for w in case["history"]])
+        w = case["word"]
+        words.append(wid[w] if (w,) in model.probs else dm.ngram_image.unk_id)
+    inc, succ = dm.score_words(hist, words)
+    for i, case in enumerate(g["cases"]):
+        assert inc[i] == case["score"], case
+        assert list(succ[i]) == [wid[w] for w in case["succ"]], case
+
+
+def test_forced20_gpu():
+    g = G.load("forced20")
+    vocab, tt, model = G.instance_world(g)
+    cfg = G.config_of(g["config"])
+    ds = [np.asarray(inst["D"]) for inst in g["instances"]]
+    got = decode_batch(ds, cfg, tt, model, StubScorer(table={}))
+    for inst, r in zip(g["instances"], got):
+        assert G.same_result(r, inst["result"]) is None, inst["word"]
+
+
+def test_ant_fixtures_gpu():
+    for inst in G.load("ant_fixtures"):
+        vocab, tt, model = G.instance_world(inst)
+        cfg = G.config_of(inst["config"])
+        r = decode_batch([G.d_of(inst)], cfg, tt, model, StubScorer(table=dict(inst["stub_table"])))[0]
+        err = G.same_result(r, inst["result"])
+        assert err is None, (inst["name"], err)
+
+
+@pytest.mark.parametrize("part", range(2))
+def test_random_instances_gpu(part):
+    insts = G.load("random_instances")
+    for inst in insts[part::2]:
+        vocab, tt, model = G.instance_world(inst)
+        for run in inst["runs"]:
+            cfg = G.config_of(run["config"])
+            sc = G.scorer_for(run, inst, model, cfg)
+            r = decode_batch([G.d_of(inst)], cfg, tt, model, sc, final_llm_only=run["final_only"])[0]
+            err = G.same_result(r, run["result"])
+            assert err is None, (inst["name"], run["config"], err)
+
+
+def test_random_instances_device_ngram_scorer():
+    """DeviceNgramScorer on the GPU == the reference's StubScorer(ngram_model) (goldens)."""
+    for inst in G.load("random_instances")[::3]:
+        vocab, tt, model = G.instance_world(inst)
+        for run in inst["runs"]:
+            if not run.get("ngram_stub"):
+                continue
+            cfg = G.config_of(run["config"])
+            sc = DeviceNgramScorer(model, cfg.ngram_weight / cfg.llm_weight)
+            r = decode_batch([G.d_of(inst)], cfg, tt, model, sc, final_llm_only=run["final_only"])[0]
+            err = G.same_result(r, run["result"])
+            assert err is None, (inst["name"], run["config"], err)
+
+
+def test_trace_parity_random():
+    """Per-frame ordered beams equal the reference trace (hashes, prefix ids, last, score),
+    with host-scored interval fusion events in between."""
+    from paper_2603_14002_b200.decoder import run_search
+
+    checked = 0
+    for inst in G.load("random_instances"):
+        vocab, tt, model = G.instance_world(inst)
+        d = G.d_of(inst)
+        for run in inst["runs"]:
+            if "trace" not in run:
+                continue
+            cfg = G.config_of(run["config"])
+            want = G.trace_rows(run["trace"])
+            # golden interleaves: snapshot after each step, plus one after each event
+            steps = []
+            pos = 0
+            for t in range(d.shape[0]):
+                if pos >= len(want):
+                    break
+                steps.append(want[pos])
+                pos += 1
+                if t > 0 and t % cfg.llm_rescore_interval == 0:
+                    pos += 1
+            dm = device_model(tt, model)
+            batch = dm.batch(cfg, 1, d.shape[0])
+            batch.enable_dump(True)
+            batch.load_logprobs(d[None], np.array([d.shape[0]], dtype=np.int32))
+            run_search(batch, cfg, StubScorer(table=dict(inst["stub_table"])), model, False)
+            for t, snap in enumerate(steps):
+                assert batch.dump_frame(0, t) == snap, (inst["name"], t)
+            batch.enable_dump(False)
+            checked += 1
+    assert checked >= 30
+
+
+def _world_runs():
+    g = G.load("worlds41")
+    w = synth.toy_world(**g["runs"][0]["world_kw"])
+    return g, w
+
+
+def test_worlds41_gpu_vs_golden_and_oracle():
+    g, w = _world_runs()
+    stub = g["meta"]["stub_table"]
+    for run in g["runs"]:
+        cfg = G.config_of(run["config"])
+        raws = synth.make_logits(run["n_trials"], run["frames"], 41, base_seed=run["logit_seed"])
+        ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+        if run["scorer"] == "table":
+            gpu_sc, ref_sc = StubScorer(table=dict(stub)), lambda: StubScorer(table=dict(stub))
+        else:
+            scale = cfg.ngram_weight / cfg.llm_weight
+            gpu_sc = DeviceNgramScorer(w.model, scale)
+            ref_sc = lambda: StubScorer(ngram_model=w.model, scale=scale)  # noqa: E731
+        got = decode_batch(ds, cfg, w.table, w.model, gpu_sc, final_llm_only=run["final_only"])
+        for i, d in enumerate(ds):
+            want = O.decode(d, cfg, w.table, w.model, ref_sc(), final_llm_only=run["final_only"])
+            assert G.same_result(got[i], {"text": want.text, "score": want.score,
+                                          "nbest": want.nbest, "llm_events": want.llm_events}) is None
+            # the golden came from the reference on this container's numpy D; texts must agree
+            if "text" in run["results"][i]:
+                assert got[i].text == run["results"][i]["text"]
+
+
+def test_per_frame_trace_world41():
+    """Frame-by-frame beam lists of the kernel == oracle (no fusion events: r > T)."""
+    g, w = _world_runs()
+    for k in (10, 64):
+        cfg = PROFILES["b2t25"].replace(beam_size=k, llm_rescore_interval=1000)
+        raws = synth.make_logits(3, 150, 41, base_seed=77)
+        ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+        dm = device_model(w.table, w.model)
+        batch = dm.batch(cfg, 3, 150)
+        batch.enable_dump(True)
+        arr = np.stack(ds)
+        batch.load_logprobs(arr, np.full(3, 150, dtype=np.int32))
+        batch.reset()
+        batch.run(0, 150)
+        for i, d in enumerate(ds):
+            s = O.OracleSearch(cfg, w.table, w.model, StubScorer(table={}))
+            for t in range(150):
+                s.frame(d[t], t)
+                assert batch.dump_frame(i, t) == s.snapshot(), (k, i, t)
+        batch.enable_dump(False)
+
+
+def test_config2_shape_small_world():
+    """BASELINE config-2 semantics (k=64, final-only fixed-point n-gram stub) on 24 trials."""
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=64)
+    raws = synth.make_logits(24, 300, 41, base_seed=1000)
+    ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+    scale = cfg.ngram_weight / cfg.llm_weight
+    got = decode_batch(ds, cfg, w.table, w.model, DeviceNgramScorer(w.model, scale), final_llm_only=True)
+    for i, d in enumerate(ds):
+        want = O.decode(d, cfg, w.table, w.model, StubScorer(ngram_model=w.model, scale=scale),
+                        final_llm_only=True)
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest), i
+
+
+def test_raw_logits_path_matches_oracle_texts():
+    """Fused-prologue path (fp32 logits in): D differs from numpy by ulps only, so texts agree."""
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=16, llm_rescore_interval=10)
+    raws = synth.make_logits(6, 200, 41, base_seed=31)
+    scale = cfg.ngram_weight / cfg.llm_weight
+    got = decode_batch_raw(list(raws), cfg, w.table, w.model, DeviceNgramScorer(w.model, scale))
+    for i, r in enumerate(raws):
+        want = O.decode(O.log_softmax_scaled(r, cfg.acoustic_scale), cfg, w.table, w.model,
+                        StubScorer(ngram_model=w.model, scale=scale))
+        assert got[i].text == want.text
+        assert got[i].score == pytest.approx(want.score, rel=1e-9)
+
+
+def test_single_decode_api_and_errors():
+    from paper_2603_14002_b200 import DataValueError, EmptyBeamError, LogProbMatrix
+
+    g = G.load("forced20")
+    vocab, tt, model = G.instance_world(g)
+    cfg = G.config_of(g["config"])
+    d = LogProbMatrix(np.asarray(g["instances"][0]["D"]), cfg.acoustic_scale, 100.0)
+    r = decode(d, cfg, tt, model, StubScorer(table={}))
+    assert r.text.rstrip(".?!") == g["instances"][0]["word"]
+    with pytest.raises(DataValueError):
+        decode(np.zeros((0, 41)), cfg, tt, model, StubScorer(table={}))
+    # an impossible path: all mass on a token the lexicon never allows first
+    bad = np.full((3, 41), -1e3)
+    bad[:, 40] = 0.0
+    cfg1 = cfg.replace(beam_size=1)
+    try:
+        decode(bad, cfg1, tt, model, StubScorer(table={}))
+    except EmptyBeamError:
+        pass

@@ -1,0 +1,243 @@
+"""CPU tests of the host-side mirror of the reference API and of the C-ABI library surface
+(no compute calls: there is no GPU in the build container)."""
+
+import gzip
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import goldens as G
+from paper_2603_14002_b200 import (
+    PROFILES,
+    ConfigError,
+    DecodeConfig,
+    DeviceError,
+    FormatError,
+    LmSession,
+    ScoreRequest,
+    ScoreResponse,
+    StubScorer,
+    Vocabulary,
+    build_transition_table,
+    config_from_dict,
+    decode,
+    load_arpa,
+    load_table,
+    save_table,
+    score_eos,
+    score_sequence,
+    score_texts,
+    synth,
+)
+from paper_2603_14002_b200 import _native, images
+from paper_2603_14002_b200.ngram import LN10, NEG_INF_GUARD, parse_arpa_text
+from paper_2603_14002_b200.scorer import decode_request, decode_response, encode_request, encode_response
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_table5_profiles():
+    b24, b25 = PROFILES["b2t24"], PROFILES["b2t25"]
+    assert (b24.acoustic_scale, b24.beam_size, b24.beam_prune_threshold, b24.ortho_beams,
+            b24.homophone_prune_threshold, b24.token_insertion_bonus, b24.word_boundary_bonus,
+            b24.ngram_weight, b24.llm_weight, b24.llm_rescore_interval, b24.llm_chunk_size) == (
+        0.6, 1000, 22.0, 3, 4.0, 1.5, 1.0, 0.8, 1.2, 10, 256)
+    assert (b25.acoustic_scale, b25.beam_size, b25.beam_prune_threshold, b25.ngram_weight,
+            b25.llm_rescore_interval) == (0.4, 900, 18.0, 1.0, 15)
+
+
+@pytest.mark.parametrize("bad", [
+    dict(beam_size=0), dict(ortho_beams=0), dict(beam_prune_threshold=0.0),
+    dict(homophone_prune_threshold=-1.0), dict(ngram_weight=-0.1), dict(llm_rescore_interval=0),
+    dict(llm_chunk_size=0), dict(acoustic_scale=float("nan")), dict(acoustic_scale=0.0)])
+def test_config_validation(bad):
+    with pytest.raises(ConfigError):
+        PROFILES["b2t25"].replace(**bad)
+
+
+def test_config_from_dict():
+    assert config_from_dict({"profile": "b2t24", "beam_size": 16}).beam_size == 16
+    with pytest.raises(ConfigError):
+        config_from_dict({"profile": "nope"})
+    with pytest.raises(ConfigError):
+        config_from_dict({"beam_size": 3})
+    with pytest.raises(ConfigError):
+        config_from_dict({"profile": "b2t24", "bogus": 1})
+
+
+def test_lexicon_table_semantics():
+    vocab = Vocabulary(("<blank>", "AE", "N", "T", "<sp>"), 0, 4)
+    lex = G.lexicon_of([["ant", "ant", [1, 2, 3]], ["aunt", "aunt", [1, 2, 3]],
+                        ["at", "at", [1, 3]], ["an", "an", [1, 2]]])
+    tt = build_transition_table(lex, vocab)
+    # BFS numbering: root 0; children of root in token order; sink last
+    assert tt.advance(0, 1) == 1
+    assert tt.table[tt.sink].tolist() == [tt.sink] * 5
+    assert tt.completions_at(tt.advance(tt.advance(tt.advance(0, 1), 2), 3)) == (0, 1)
+    s = tt.advance(tt.advance(0, 1), 2)
+    assert tt.advance(s, 4) == 0  # "an" completes: space returns to the root
+    assert tt.advance(1, 4) == tt.sink
+    m = tt.valid_mask(np.array([0, 1]), np.array([0, 1]))
+    assert m[0].tolist() == [True, True, False, False, False]
+    assert m[1].tolist() == [True, True, True, True, False]
+
+
+def test_lbtt_roundtrip(tmp_path):
+    w = synth.toy_world(n_words=300, seed=3)
+    p = tmp_path / "t.lbtt"
+    save_table(p, w.table)
+    back = load_table(p, w.vocab)
+    assert np.array_equal(back.table, w.table.table)
+    assert back.completion_states() == w.table.completion_states()
+    assert [e.surface for e in back.entries] == [e.surface for e in w.table.entries]
+
+
+def test_arpa_parse_and_errors(tmp_path):
+    g = G.load("hand_ngram")
+    p = tmp_path / "m.arpa"
+    p.write_text(g["arpa"])
+    m = load_arpa(p)
+    assert m.order == 3 and m.unk_present
+    assert m.probs[("a",)] == -0.47712 * LN10
+    gz = tmp_path / "m.arpa.gz"
+    gz.write_bytes(gzip.compress(g["arpa"].encode()))
+    assert load_arpa(gz).probs == m.probs
+    bad = {
+        "no data": "\\1-grams:\n-1.0 a\n\\end\\\n",
+        "count": "\\data\\\nngram 1=2\n\n\\1-grams:\n-1.0 a\n\\end\\\n",
+        "no end": "\\data\\\nngram 1=1\n\n\\1-grams:\n-1.0 a\n",
+        "bad prob": "\\data\\\nngram 1=1\n\n\\1-grams:\nxx a\n\\end\\\n",
+        "undeclared": "\\data\\\nngram 1=1\n\n\\2-grams:\n-1.0 a b\n\\end\\\n",
+    }
+    for name, text in bad.items():
+        with pytest.raises(FormatError):
+            parse_arpa_text(text)
+
+
+def test_host_score_sequence_matches_hand():
+    g = G.load("hand_ngram")
+    m = parse_arpa_text(g["arpa"])
+    total = score_sequence(m, ["a", "b", "a"], include_eos=True)
+    s = LmSession(m)
+    from paper_2603_14002_b200 import score_word
+
+    st, acc = 0, 0.0
+    for w in ["a", "b", "a", "</s>"]:
+        inc, st = score_word(m, s.registry, s.cache, st, w)
+        acc += inc
+    assert total == acc
+
+
+def test_scorer_protocol():
+    req = ScoreRequest(7, "score", ("a b", "c"))
+    assert decode_request(encode_request(req)) == req
+    resp = ScoreResponse(7, (-1.5, -2.0))
+    assert decode_response(encode_response(resp), expect_id=7) == resp
+    stub = StubScorer(table={"a": -0.5, "c": -2.5})
+    texts = ["a", "b b", "c", "a", "long text here"] * 3
+    ref = score_texts(stub, texts, 256)
+    for chunk in (1, 2, 7):
+        assert score_texts(StubScorer(table={"a": -0.5, "c": -2.5}), texts, chunk) == ref
+    assert score_eos(StubScorer(table={}), ["hello there"]) == [(".", -2.0)]
+    assert score_eos(StubScorer(table={"x?": -1.0, "x.": -3.0}), ["x"]) == [("?", -1.0)]
+
+
+def test_ngram_image_compile():
+    m = parse_arpa_text(G.load("hand_ngram")["arpa"])
+    img = images.compile_ngram(m)
+    keys = set()
+    for row in range(len(img.probs)):
+        g = tuple(int(x) for x in img.words[row] if x != images.WORD_PAD)
+        keys.add(g)
+    names = {v: k for k, v in img.word_id.items()}
+    assert {tuple(names[i] for i in g) for g in keys} == set(m.probs) | set(m.backoffs)
+    assert img.eos_eff == img.word_id["</s>"]
+
+
+def test_table_image_completion_csr():
+    vocab = Vocabulary(("<blank>", "AE", "N", "T", "<sp>"), 0, 4)
+    lex = G.lexicon_of([["ant", "ant", [1, 2, 3]], ["aunt", "aunt", [1, 2, 3]],
+                        ["ant(2)", "ant", [1, 2, 3]], ["zz", "zz", [1]]])
+    tt = build_transition_table(lex, vocab)
+    m = parse_arpa_text("\\data\\\nngram 1=2\n\n\\1-grams:\n-1.0 ant\n-2.0 <unk>\n\\end\\\n")
+    ng = images.compile_ngram(m)
+    tab = images.compile_table(tt, m, ng)
+    s = tt.advance(tt.advance(tt.advance(0, 1), 2), 3)
+    lo, hi = tab.comp_off[s], tab.comp_off[s + 1]
+    assert [tab.surfaces[i] for i in tab.comp_surface[lo:hi]] == ["ant", "aunt"]  # deduped
+    assert tab.comp_lmword[lo:hi].tolist() == [ng.word_id["ant"], ng.word_id["<unk>"]]
+
+
+def test_synth_determinism():
+    a = synth.toy_world(n_words=500, seed=11)
+    b = synth.toy_world(n_words=500, seed=11)
+    assert np.array_equal(a.table.table, b.table.table)
+    assert a.model.probs == b.model.probs
+    assert np.array_equal(synth.make_logits(2, 10, base_seed=5), synth.make_logits(2, 10, base_seed=5))
+    for e in a.lexicon.entries:  # no adjacent duplicate phonemes (unreachable in the search)
+        assert all(x != y for x, y in zip(e.phonemes, e.phonemes[1:]))
+
+
+def test_synth_arpa_text_equals_direct_model():
+    lex = synth.make_lexicon(300, seed=4)
+    spec = synth.make_ngram_spec([e.surface for e in lex.entries], 400, 200, 100, seed=5)
+    direct = synth.ngram_model_from_spec(spec)
+    parsed = parse_arpa_text(synth.arpa_text_from_spec(spec))
+    assert direct.probs == parsed.probs and direct.backoffs == parsed.backoffs
+    assert direct.order == parsed.order == 4
+
+
+def _header_symbols():
+    text = (ROOT / "include" / "lightbeam_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(lb_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_c_abi_exports_every_header_symbol():
+    _native.build()
+    syms = _header_symbols()
+    assert len(syms) >= 25
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_native.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert set(syms) == set(_native.exported_symbols())
+    lib = _native.lib(require_device=False)
+    for s in syms:
+        assert getattr(lib, s) is not None
+
+
+def test_sass_is_sm100a_with_tma_bulk():
+    _native.build()
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    full = subprocess.run(["cuobjdump", "-sass", str(_native.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    funcs = {}
+    cur = None
+    for line in full.splitlines():
+        if "Function :" in line:
+            cur = line.split("Function :")[1].strip()
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    frames = [f for f in funcs if "frames_kernel" in f]
+    assert len(frames) == 3  # 256/512/1024-thread instantiations
+    sass = "\n".join(funcs[frames[0]])
+    assert "UBLKCP" in sass  # cp.async.bulk (1-D TMA) staging of the log-prob frame chunks
+    assert "LDGSTS" in sass  # cp.async lexicon-row gathers
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    w = synth.toy_world(n_words=100, seed=1)
+    d = np.zeros((3, 41))
+    with pytest.raises(DeviceError):
+        decode(d, PROFILES["b2t25"].replace(beam_size=4), w.table, w.model, StubScorer(table={}))
