@@ -41,7 +41,7 @@ FRAME_MS = 80.0  # B2T'25 frame duration
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--trials", type=int, default=256, help="utterances per GPU")
@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="add per-phase cycle breakdown of K2")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostic: keep L2 warm between steps")
     return ap.parse_args()
 
 
@@ -139,7 +141,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -225,7 +227,8 @@ def run_ours(args):
     ms_steps, launches = [], 0
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
-            flush.zero_()
+            if not args.no_flush:
+                flush.zero_()
             batch.mark_begin()
             step()
             ms, nl = batch.mark_end()
@@ -259,6 +262,21 @@ def run_ours(args):
         peaks = json.loads(pp.read_text())
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg / (k_ms / 1e3) / 1e9
+
+    phases = None
+    if args.phases:
+        batch.enable_phase_timing(True)
+        if not args.no_flush:
+            flush.zero_()
+        batch.load_logits(None, frames, on_device_ptr=x_dev.data_ptr())
+        batch.reset()
+        batch.run(0, T, 0, scale)
+        batch.sync()
+        cyc = batch.phase_cycles()
+        n_cta_frames = B * T
+        phases = {k: v / n_cta_frames for k, v in cyc.items() if v}
+        phases["total_cycles_per_frame"] = sum(phases.values())
+        batch.enable_phase_timing(False)
 
     # correctness spot check of this very run against the oracle (2 utterances)
     check = None
@@ -337,6 +355,8 @@ def run_ours(args):
             "counters": stats,
             "setup_s": setup_s,
             "parity_check": check,
+            "phase_cycles_per_frame": phases,
+            "layout": batch.layout(),
         }
         print(json.dumps(line))
     if world_n > 1:

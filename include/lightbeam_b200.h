@@ -12,7 +12,8 @@
  * Reference interface replaced by each entry point:
  *   lb_model_create      build_transition_table / load_table (lexicon.py:149-209,236-277) and
  *                        load_arpa (ngram.py:90-174) results uploaded as device images:
- *                        dense (S,V) int32 table + completion CSR, hashed 4-gram records.
+ *                        dense (S,V) int32 table with completion headers + completion CSR,
+ *                        4-gram records in a bucketized cuckoo table.
  *   lb_batch_create      init_beams (decoder.py:177-179) for B utterances at once.
  *   lb_batch_set_logits  scale_log_softmax (logits.py:119-130) fused on upload (kernel K1).
  *   lb_batch_set_logprobs  the LogProbMatrix argument of decode (decoder.py:408) in fp64.
@@ -97,6 +98,7 @@ typedef struct {
   const double* backoffs;  /* [n_grams], 0.0 if absent */
   uint32_t bos_id;         /* id of "<s>" (initial history) */
   int32_t eos_word;        /* LM id "</s>" is scored as, -1 = kill */
+  double bos_backoff;      /* backoffs.get(("<s>",), 0.0) */
 } lb_ngram_desc;
 
 /* Counters a run accumulates (summed over trials and frames). */
@@ -124,6 +126,9 @@ int lb_model_footprint(const lb_model* m, int64_t* bytes);
 int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32_t max_frames,
                     void* stream, lb_batch** out);
 int lb_batch_destroy(lb_batch* b);
+/* Working-set placement of the frames kernel: dynamic shared memory per CTA, per-trial global
+ * spill scratch, threads per CTA. */
+int lb_batch_layout(lb_batch* b, int64_t* smem_bytes, int64_t* gscratch_bytes, int32_t* nthreads);
 
 /* Inputs.  `x` is [n_trials, max_frames, vocab_size] row-major; frames[i] <= max_frames.
  * `on_device` != 0: x is a device pointer (stream-ordered), else a host pointer (pinned or
@@ -183,6 +188,11 @@ int lb_batch_dump_beams(lb_batch* b, int32_t trial, int32_t* k, double* scores, 
 int lb_batch_enable_dump(lb_batch* b, int32_t on);
 int lb_batch_dump_frame(lb_batch* b, int32_t trial, int32_t t, int32_t* k, double* scores,
                         uint64_t* h1, uint64_t* h2, int32_t* prefix, int32_t* last);
+
+/* Per-phase cycle counters of the frames kernel (clock64 deltas between its barriers,
+ * thread 0 of each CTA; 12 slots, summed over trials) -- profiling aid, off by default. */
+int lb_batch_enable_phase_timing(lb_batch* b, int32_t on);
+int lb_batch_phase_cycles(lb_batch* b, uint64_t* out);
 
 /* Results (decoder.py:433-460).  Two-step: lb_batch_results_size gives the byte size of the
  * text blob and the total n-best count; lb_batch_results fills caller buffers:

@@ -94,6 +94,7 @@ class LbNgramDesc(C.Structure):
         ("backoffs", C.c_void_p),
         ("bos_id", C.c_uint32),
         ("eos_word", C.c_int32),
+        ("bos_backoff", C.c_double),
     ]
 
 
@@ -115,6 +116,7 @@ _SIGS = {
     "lb_model_footprint": (C.c_int, [_P, _P]),
     "lb_batch_create": (C.c_int, [_P, C.POINTER(LbConfig), _I32, _I32, _P, _P]),
     "lb_batch_destroy": (C.c_int, [_P]),
+    "lb_batch_layout": (C.c_int, [_P, _P, _P, _P]),
     "lb_batch_set_logits": (C.c_int, [_P, _I32, _P, _P, _I32]),
     "lb_batch_set_logprobs": (C.c_int, [_P, _I32, _P, _P, _I32]),
     "lb_batch_get_logprobs": (C.c_int, [_P, _P]),
@@ -130,6 +132,8 @@ _SIGS = {
     "lb_batch_clear_stats": (C.c_int, [_P]),
     "lb_batch_dump_beams": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "lb_batch_enable_dump": (C.c_int, [_P, _I32]),
+    "lb_batch_enable_phase_timing": (C.c_int, [_P, _I32]),
+    "lb_batch_phase_cycles": (C.c_int, [_P, _P]),
     "lb_batch_dump_frame": (C.c_int, [_P, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "lb_batch_results_size": (C.c_int, [_P, _P, _P]),
     "lb_batch_results": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -38,6 +39,48 @@ cudaError_t dalloc(T** p, size_t n) {
 }
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Cuckoo insertion with random-walk eviction; every key ends in one of its two buckets.
+bool cuckoo_build(const lb_ngram_desc* nd, uint32_t nb, std::vector<NgRec>& tab, int* max_kicks) {
+  NgRec empty;
+  for (int q = 0; q < 4; ++q) empty.w[q] = WPAD;
+  empty.prob = 0.0;
+  empty.bo = 0.0;
+  tab.assign((size_t)nb * NG_WAYS, empty);
+  uint64_t rng = 0x2545F4914F6CDD1Dull;
+  int worst = 0;
+  for (int64_t i = 0; i < nd->n_grams; ++i) {
+    NgRec cur;
+    for (int q = 0; q < 4; ++q) cur.w[q] = nd->words[4 * i + q];
+    cur.prob = nd->probs[i];
+    cur.bo = nd->backoffs[i];
+    bool placed = false;
+    int kicks = 0;
+    for (; kicks < 2000 && !placed; ++kicks) {
+      uint32_t b[2];
+      ng_buckets(ng_hash(cur.w[0], cur.w[1], cur.w[2], cur.w[3]), nb, b[0], b[1]);
+      for (int c2 = 0; c2 < 2 && !placed; ++c2)
+        for (int q = 0; q < NG_WAYS; ++q) {
+          NgRec& slot = tab[(size_t)b[c2] * NG_WAYS + q];
+          if (slot.w[0] == WPAD) {
+            slot = cur;
+            placed = true;
+            break;
+          }
+        }
+      if (placed) break;
+      rng ^= rng << 13;
+      rng ^= rng >> 7;
+      rng ^= rng << 17;
+      NgRec& victim = tab[(size_t)b[rng & 1] * NG_WAYS + ((rng >> 1) & (NG_WAYS - 1))];
+      std::swap(cur, victim);
+    }
+    if (!placed) return false;
+    worst = std::max(worst, kicks);
+  }
+  *max_kicks = worst;
+  return true;
+}
 }  // namespace
 
 struct lb_model {
@@ -114,15 +157,7 @@ int lb_model_create(const lb_table_desc* td, const lb_ngram_desc* nd, int32_t de
   lb_model* m = new lb_model();
   m->device = device;
   const int32_t S = td->num_states, V = td->vocab_size;
-  const int32_t VP = (int32_t)round_up(V, 4);
-  // lexicon table, padded rows
-  int32_t* tmp = nullptr;
-  CK(dalloc(&tmp, (size_t)S * V));
-  CK(cudaMemcpy(tmp, td->table, (size_t)S * V * sizeof(int32_t), cudaMemcpyHostToDevice));
-  CK(dalloc(&m->d_table, (size_t)S * VP));
-  CK(lbk::pad_table(m->d_table, tmp, S, V, VP, 0));
-  CK(cudaDeviceSynchronize());
-  CK(cudaFree(tmp));
+  const int32_t VP = (int32_t)round_up(V + ROW_HDR, 4);
   CK(dalloc(&m->d_comp_off, (size_t)S + 1));
   CK(cudaMemcpy(m->d_comp_off, td->comp_offsets, ((size_t)S + 1) * sizeof(int32_t),
                 cudaMemcpyHostToDevice));
@@ -132,32 +167,27 @@ int lb_model_create(const lb_table_desc* td, const lb_ngram_desc* nd, int32_t de
     CK(cudaMemcpy(m->d_comp_surf, td->comp_surface, (size_t)td->n_comp * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(m->d_comp_lm, td->comp_lmword, (size_t)td->n_comp * 4, cudaMemcpyHostToDevice));
   }
-  // n-gram hash image: capacity = next power of two >= 2 * n (load factor <= 0.5)
-  int64_t cap = 1024;
-  while (cap < 2 * nd->n_grams) cap <<= 1;
-  m->ng_cap = cap;
-  CK(dalloc(&m->d_ng, (size_t)cap));
-  CK(cudaMemset(m->d_ng, 0xFF, (size_t)cap * sizeof(NgRec)));
-  if (nd->n_grams > 0) {
-    uint32_t* dw = nullptr;
-    double *dp = nullptr, *db = nullptr;
-    int* dmax = nullptr;
-    CK(dalloc(&dw, (size_t)nd->n_grams * 4));
-    CK(dalloc(&dp, (size_t)nd->n_grams));
-    CK(dalloc(&db, (size_t)nd->n_grams));
-    CK(dalloc(&dmax, 1));
-    CK(cudaMemset(dmax, 0, sizeof(int)));
-    CK(cudaMemcpy(dw, nd->words, (size_t)nd->n_grams * 16, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dp, nd->probs, (size_t)nd->n_grams * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(db, nd->backoffs, (size_t)nd->n_grams * 8, cudaMemcpyHostToDevice));
-    CK(lbk::build_ngram_table(m->d_ng, (uint64_t)(cap - 1), dw, dp, db, nd->n_grams, dmax, 0));
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(&m->max_probe, dmax, sizeof(int), cudaMemcpyDeviceToHost));
-    cudaFree(dw);
-    cudaFree(dp);
-    cudaFree(db);
-    cudaFree(dmax);
+  // lexicon table: rows padded to VP with the completion header after the V transitions
+  int32_t* tmp = nullptr;
+  CK(dalloc(&tmp, (size_t)S * V));
+  CK(cudaMemcpy(tmp, td->table, (size_t)S * V * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CK(dalloc(&m->d_table, (size_t)S * VP));
+  CK(lbk::pad_table(m->d_table, tmp, S, V, VP, m->d_comp_off, m->d_comp_surf, m->d_comp_lm, 0));
+  CK(cudaDeviceSynchronize());
+  CK(cudaFree(tmp));
+  // n-gram image: bucketized cuckoo table (4 records per 128-byte bucket, 2 candidate buckets)
+  // built on the host -- deterministic and a few hundred ms for 1M grams
+  std::vector<NgRec> tab;
+  uint32_t nb = (uint32_t)std::max<int64_t>(8, (int64_t)(nd->n_grams / (NG_WAYS * 0.85)) + 1);
+  for (int attempt = 0;; ++attempt) {
+    if (cuckoo_build(nd, nb, tab, &m->max_probe)) break;
+    if (attempt > 20) return fail(LB_ERR_CAPACITY, "cuckoo n-gram table build failed");
+    nb = (uint32_t)(nb * 1.15) + 1;
   }
+  m->ng_cap = (int64_t)nb * NG_WAYS;
+  CK(dalloc(&m->d_ng, tab.size()));
+  CK(cudaMemcpy(m->d_ng, tab.data(), tab.size() * sizeof(NgRec), cudaMemcpyHostToDevice));
+  const int64_t cap = m->ng_cap;
   m->bytes = (int64_t)S * VP * 4 + ((int64_t)S + 1) * 4 + (int64_t)td->n_comp * 8 +
              cap * (int64_t)sizeof(NgRec);
   ModelDev& d = m->dev;
@@ -172,7 +202,8 @@ int lb_model_create(const lb_table_desc* td, const lb_ngram_desc* nd, int32_t de
   d.comp_surf = m->d_comp_surf;
   d.comp_lm = m->d_comp_lm;
   d.ng = m->d_ng;
-  d.ng_mask = (uint64_t)(cap - 1);
+  d.ng_nb = nb;
+  d.bos_bo = nd->bos_backoff;
   d.order = nd->order;
   d.bos = nd->bos_id;
   d.eos_word = nd->eos_word;
@@ -210,17 +241,22 @@ namespace {
 // trial's global scratch when a wide beam would not fit in 227 KB.
 void plan_layout(lb_batch* b) {
   const int64_t K = b->K, O = b->O, VP = b->m->dev.VP, VPD = b->VPD;
-  const int nt = lbk::max_threads_for((int)K);
+  int nt = lbk::max_threads_for((int)K);
+  if (const char* env = std::getenv("LB_THREADS")) {
+    const int v = std::atoi(env);
+    if (v == 256 || v == 512 || v == 1024) nt = v;
+  }
   const int64_t lcap = std::max<int64_t>(2 * K, K + 256);
   int64_t sz[N_REGIONS] = {};
   sz[R_DBUF] = 2 * CHUNK * VPD * 8;
   sz[R_ROWS] = K * VP * 4;
-  const int64_t beam[7] = {K * 8, K * 8, K * 8, K * 4, K * 4, K * 4, K * O * 32};
+  const int64_t beam[7] = {K * 8, K * 8, K * 8, K * 4, K * 4, K * 4, K * O * (int64_t)sizeof(Ent)};
   for (int i = 0; i < 7; ++i) {
     sz[R_CUR_SCORE + i] = beam[i];
     sz[R_NXT_SCORE + i] = beam[i];
   }
-  sz[R_MASK] = K * 8;
+  sz[R_CV] = 0;
+  sz[R_CBIN] = round_up(K * b->m->dev.V * 2, 16);
   sz[R_CVAL] = lcap * 8;
   sz[R_CKEY] = lcap * 4;
   sz[R_SVAL] = K * 8;
@@ -229,13 +265,22 @@ void plan_layout(lb_batch* b) {
   sz[R_NH1] = K * 8;
   sz[R_NH2] = K * 8;
   for (int r : {R_NLAST, R_NPRE, R_NPAR, R_RANK, R_BLIST, R_BNENT}) sz[r] = K * 4;
-  sz[R_BENTS] = K * O * 32;
+  sz[R_BENTS] = K * O * (int64_t)sizeof(Ent);
   sz[R_KEEP] = ((K + 31) / 32) * 4;
   sz[R_WARP] = (nt / 32) * (int64_t)sizeof(WarpScratch);
+  const int64_t pcap = std::max<int64_t>(128, K);
+  int64_t ts = 64;
+  while (ts < 2 * K) ts <<= 1;
+  sz[R_POFF] = (K + 1) * 4;
+  sz[R_PAIRS] = pcap * (int64_t)sizeof(PairRes);
+  sz[R_SLOTB] = ts * 4;
+  sz[R_SLOTM] = ts * 4;
+  sz[R_MYSLOT] = K * 4;
   const int64_t budget = 200 * 1024;  // leave room for static shared memory
   int in_smem[N_REGIONS];
   for (int i = 0; i < N_REGIONS; ++i) in_smem[i] = 1;
-  const int spill_order[] = {R_BENTS, R_NXT_ENTS, R_CUR_ENTS, R_ROWS, R_CVAL, R_CKEY,
+  in_smem[R_WARP] = 0;  // scratch of the rare warp-per-beam n-gram path: global (L1-cached)
+  const int spill_order[] = {R_BENTS, R_NXT_ENTS, R_CUR_ENTS, R_ROWS, R_CV, R_CVAL, R_CKEY,
                              R_NXT_H1, R_NXT_H2, R_CUR_H1, R_CUR_H2, R_NH1, R_NH2};
   auto total = [&]() {
     int64_t t = 0;
@@ -263,6 +308,8 @@ void plan_layout(lb_batch* b) {
   b->L.lcap = (int32_t)lcap;
   b->L.stage_rows = in_smem[R_ROWS];
   b->L.nthreads = nt;
+  b->L.pcap = (int32_t)pcap;
+  b->L.tslots = (int32_t)ts;
 }
 
 void fill_cfg(lb_batch* b) {
@@ -274,8 +321,9 @@ void fill_cfg(lb_batch* b) {
   d.gamma = c.word_boundary_bonus;
   d.omega = c.ngram_weight;
   d.phi = c.llm_weight;
-  const double span = std::min(c.beam_prune_threshold, 24.0);
+  const double span = std::min(c.beam_prune_threshold, 24.0) + 12.0;
   d.inv_binw = (double)NBINS / span;
+  d.bonus_up = std::max(c.token_insertion_bonus, 0.0) + std::max(c.word_boundary_bonus, 0.0);
   d.k = c.beam_size;
   d.O = c.ortho_beams;
   d.r = c.llm_rescore_interval;
@@ -307,7 +355,7 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
   CK(lbk::set_smem_limit(b->L.nthreads, b->L.smem_bytes));
   const size_t B = (size_t)max_trials, K = (size_t)b->K, O = (size_t)b->O;
   int64_t ncap = (int64_t)max_frames * b->K * b->O + 1;
-  const int64_t budget_nodes = (int64_t)16e9 / (20 * (int64_t)B);
+  const int64_t budget_nodes = (int64_t)16e9 / (8 * (int64_t)B);
   ncap = std::min<int64_t>(ncap, std::max<int64_t>(4096, budget_nodes));
   ncap = std::min<int64_t>(ncap, (int64_t)1 << 30);
   BatchDev& d = b->dev;
@@ -328,8 +376,6 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
   CK(dalloc(&d.ents, B * K * O));
   CK(dalloc(&d.nparent, B * ncap));
   CK(dalloc(&d.nsurf, B * ncap));
-  CK(dalloc(&d.ndepth, B * ncap));
-  CK(dalloc(&d.ncum, B * ncap));
   CK(dalloc(&d.ncount, B));
   CK(dalloc(&d.status, B));
   CK(dalloc(&d.fail_frame, B));
@@ -349,17 +395,27 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
   return LB_OK;
 }
 
+int lb_batch_layout(lb_batch* b, int64_t* smem_bytes, int64_t* gscratch_bytes,
+                    int32_t* nthreads) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  if (smem_bytes) *smem_bytes = b->L.smem_bytes;
+  if (gscratch_bytes) *gscratch_bytes = b->L.gscratch_bytes;
+  if (nthreads) *nthreads = b->L.nthreads;
+  return LB_OK;
+}
+
 int lb_batch_destroy(lb_batch* b) {
   if (!b) return LB_OK;
   cudaSetDevice(b->m->device);
   cudaStreamSynchronize(b->st);
   BatchDev& d = b->dev;
   void* ptrs[] = {b->d_T, b->d_D, b->d_x, d.nbeam, d.score, d.h1, d.h2, d.last, d.prefix, d.nent,
-                  d.ents, d.nparent, d.nsurf, d.ndepth, d.ncum, d.ncount, d.status,
+                  d.ents, d.nparent, d.nsurf, d.ncount, d.status,
                   d.fail_frame, d.stats, d.gscratch, b->d_counts, b->d_entry_off,
                   b->d_word_off, b->d_e_trial, b->d_e_beam, b->d_e_woff, b->d_words,
                   b->d_totals, b->d_puncts, b->d_scores_in, b->d_puncts_in, b->d_has_text,
-                  d.dump_h1, d.dump_h2, d.dump_pre, d.dump_last, d.dump_score, d.dump_k};
+                  d.dump_h1, d.dump_h2, d.dump_pre, d.dump_last, d.dump_score, d.dump_k,
+                  d.phase_cycles};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (b->ev0) cudaEventDestroy(b->ev0);
@@ -577,6 +633,29 @@ int lb_batch_dump_beams(lb_batch* b, int32_t trial, int32_t* k, double* scores, 
     CK(cudaMemcpyAsync(last, b->dev.last + hb, kk * 4, cudaMemcpyDeviceToHost, b->st));
   }
   CK(cudaStreamSynchronize(b->st));
+  return LB_OK;
+}
+
+int lb_batch_enable_phase_timing(lb_batch* b, int32_t on) {
+  if (!b) return fail(LB_ERR_ARG, "null argument");
+  BatchDev& d = b->dev;
+  if (on && !d.phase_cycles) {
+    CK(dalloc(&d.phase_cycles, (size_t)b->Bmax * NPHASE));
+    CK(cudaMemset(d.phase_cycles, 0, (size_t)b->Bmax * NPHASE * 8));
+  } else if (!on && d.phase_cycles) {
+    cudaFree(d.phase_cycles);
+    d.phase_cycles = nullptr;
+  }
+  return LB_OK;
+}
+
+int lb_batch_phase_cycles(lb_batch* b, uint64_t* out /* [NPHASE] summed over trials */) {
+  if (!b || !b->dev.phase_cycles) return fail(LB_ERR_STATE, "phase timing not enabled");
+  std::vector<unsigned long long> v((size_t)b->n_trials * NPHASE);
+  CK(cudaMemcpy(v.data(), b->dev.phase_cycles, v.size() * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < NPHASE; ++i) out[i] = 0;
+  for (int t = 0; t < b->n_trials; ++t)
+    for (int i = 0; i < NPHASE; ++i) out[i] += v[(size_t)t * NPHASE + i];
   return LB_OK;
 }
 

@@ -23,7 +23,7 @@ constexpr uint64_t H_MULT2 = 0xC2B2AE3D27D4EB4Full;
 constexpr uint32_t WPAD = 0xFFFFFFFFu;    // unused word slot / empty hash slot marker
 constexpr uint64_t PROB_ABSENT = 0x7FF8DEAD00000000ull;
 constexpr int NBINS = 256;   // selection histogram bins
-constexpr int CHUNK = 16;    // frames per TMA-staged D chunk
+constexpr int CHUNK = 8;     // frames per TMA-staged D chunk
 constexpr int OMAX = 8;      // max ortho_beams supported
 constexpr int MAXH = 3;      // max LM history words (order <= 4)
 
@@ -33,17 +33,30 @@ struct __align__(32) NgRec {
   double bo;    // 0.0 if absent
 };
 
+// One ortho entry (OrthoEntry, decoder.py:44-51) plus two running sums carried with it so
+// no fusion step has to walk or load the word history: `cum` is the raw n-gram sum
+// sum(inc) from <s> (= score_sequence of its words), `depth` the number of words.
+// `bo[i]` caches backoffs.get(h[i:], 0.0) for the entry's own LM history (ngram.py:195): the
+// lookups that created the entry already returned those records, so the next score_word
+// only needs the (h[i:], w) probability lookups.
 struct __align__(16) Ent {
   double total;     // weighted LM total (OrthoEntry.lm_total)
+  double cum;       // raw n-gram log-prob of the word sequence (ngram.py:239-250 order)
+  double bo[MAXH];  // back-off weights of h[0:], h[1:], h[2:]
   uint32_t node;    // word-history node
   uint32_t seq;     // creation rank inside the apply_ngram call that made it
   uint32_t h[MAXH]; // LM history word ids (OrthoEntry.lm_state)
+  uint16_t depth;   // words in the history
   uint8_t hlen;
   uint8_t punct;    // LB_PUNCT_*
-  uint16_t pad;
 };
-static_assert(sizeof(Ent) == 32, "Ent must be 32 bytes");
+static_assert(sizeof(Ent) == 64, "Ent must be 64 bytes");
 
+// Lexicon rows are padded to VP = ceil4(V + 6) int32 and carry a completion header after the
+// V transitions, so the row gather of a frame also brings the word-boundary data:
+//   row[V+0] = number of distinct completing surfaces, row[V+1] = CSR offset,
+//   row[V+2], row[V+3] = (surface, LM word) of the first, row[V+4], row[V+5] of the second.
+constexpr int ROW_HDR = 6;
 struct ModelDev {
   const int32_t* table;
   int32_t S, V, VP;  // VP: int32 row pitch (multiple of 4)
@@ -51,16 +64,19 @@ struct ModelDev {
   const int32_t* comp_off;
   const int32_t* comp_surf;
   const int32_t* comp_lm;
-  const NgRec* ng;
-  uint64_t ng_mask;
+  const NgRec* ng;     // bucketized cuckoo table: ng_nb buckets x 4 records (128 B each)
+  uint32_t ng_nb;
   int32_t order;
   uint32_t bos;
   int32_t eos_word;
+  double bos_bo;       // backoffs.get(("<s>",), 0.0): the initial entry's cached back-off
 };
+constexpr int NG_WAYS = 4;
 
 struct CfgDev {
   double theta, lambda, beta, gamma, omega, phi;
-  double inv_binw;  // NBINS / theta
+  double inv_binw;  // NBINS / (min(theta, 24) + 12): histogram span below the upper bound U
+  double bonus_up;  // max(beta, 0) + max(gamma, 0), for U = max s + max D + bonus_up
   int32_t k, O, r;
 };
 
@@ -80,8 +96,6 @@ struct BatchDev {
   // word history
   uint32_t* nparent;
   uint32_t* nsurf;
-  uint32_t* ndepth;
-  double* ncum;
   int32_t* ncount;
   int32_t ncap;
   int32_t* status;
@@ -97,7 +111,10 @@ struct BatchDev {
   int32_t* dump_last;
   double* dump_score;
   int32_t* dump_k;  // [B][Tmax]
+  // optional per-phase cycle counters of the frames kernel: [B][NPHASE] (thread 0, clock64)
+  unsigned long long* phase_cycles;
 };
+constexpr int NPHASE = 12;
 
 // Byte layout of the per-CTA working set; each region lives in shared memory or, when the
 // beam is too wide for 227 KB, in the trial's global scratch (generic pointers either way).
@@ -106,13 +123,14 @@ enum Region {
   R_ROWS,
   R_CUR_SCORE, R_CUR_H1, R_CUR_H2, R_CUR_LAST, R_CUR_PRE, R_CUR_NENT, R_CUR_ENTS,
   R_NXT_SCORE, R_NXT_H1, R_NXT_H2, R_NXT_LAST, R_NXT_PRE, R_NXT_NENT, R_NXT_ENTS,
-  R_MASK,
+  R_CV, R_CBIN,
   R_CVAL, R_CKEY,
   R_SVAL, R_SKEY,
   R_NSCORE, R_NH1, R_NH2, R_NLAST, R_NPRE, R_NPAR, R_RANK, R_BLIST,
   R_BENTS, R_BNENT,
   R_KEEP,
   R_WARP,
+  R_POFF, R_PAIRS, R_SLOTB, R_SLOTM, R_MYSLOT,
   N_REGIONS
 };
 
@@ -124,14 +142,29 @@ struct Layout {
   int32_t lcap;        // candidate list capacity
   int32_t stage_rows;  // rows staged through shared memory
   int32_t nthreads;
+  int32_t pcap;        // n-gram (entry, surface) pair capacity of one flattened round
+  int32_t tslots;      // recombination hash-table slots (power of two >= 2k)
+};
+
+// one evaluated (entry, surface) pair of the flattened n-gram phase
+struct PairRes {
+  double total;  // entry.total + omega * inc
+  double cum;    // entry.cum + inc
+  double bo[MAXH];
+  uint32_t node, surf;
+  uint32_t h[MAXH];
+  uint16_t depth;
+  uint8_t hlen, valid;
 };
 
 struct NgCand {
   double total;
-  double inc;
+  double cum;
+  double bo[MAXH];
   uint32_t node, surf, seq, hlen;
   uint32_t h[MAXH];
   uint32_t valid;
+  uint32_t depth, pad;
 };
 
 struct WarpScratch {
@@ -151,6 +184,13 @@ __host__ __device__ inline uint64_t ng_hash(uint32_t a, uint32_t b, uint32_t c, 
   uint64_t lo = (uint64_t)a | ((uint64_t)b << 32);
   uint64_t hi = (uint64_t)c | ((uint64_t)d << 32);
   return mix64(lo ^ mix64(hi ^ 0x5BD1E9955BD1E995ull));
+}
+
+// the two candidate buckets of a key (multiply-shift range reduction, distinct buckets)
+__host__ __device__ inline void ng_buckets(uint64_t h, uint32_t nb, uint32_t& b1, uint32_t& b2) {
+  b1 = (uint32_t)(((uint64_t)(uint32_t)h * nb) >> 32);
+  b2 = (uint32_t)(((uint64_t)(uint32_t)(h >> 32) * nb) >> 32);
+  if (b2 == b1) b2 = (b1 + 1 == nb) ? 0u : b1 + 1u;
 }
 
 }  // namespace lbd

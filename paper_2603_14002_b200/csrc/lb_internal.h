@@ -9,10 +9,8 @@ namespace lbk {
 // total launches issued through these wrappers (gpu_launches accounting)
 extern unsigned long long g_launches;
 
-cudaError_t build_ngram_table(lbd::NgRec* table, uint64_t mask, const uint32_t* words,
-                              const double* probs, const double* bos, int64_t n, int* max_probe,
-                              cudaStream_t st);
 cudaError_t pad_table(int32_t* dst, const int32_t* src, int32_t S, int32_t V, int32_t VP,
+                      const int32_t* comp_off, const int32_t* comp_surf, const int32_t* comp_lm,
                       cudaStream_t st);
 cudaError_t log_softmax(const float* x, int64_t rows, int32_t V, int32_t in_pitch,
                         double alpha, double* out, int32_t out_pitch, cudaStream_t st);

@@ -107,94 +107,125 @@ __device__ __forceinline__ double cand_value(double s, double d, int v, int lp, 
 }
 
 // ---------------------------------------------------------------- n-gram probes
-__device__ __forceinline__ bool ng_lookup(const ModelDev& m, const uint32_t k[4], double& p,
-                                          double& bo, unsigned& probes) {
-  uint64_t h = ng_hash(k[0], k[1], k[2], k[3]) & m.ng_mask;
-  for (;;) {
-    const uint4* rec = reinterpret_cast<const uint4*>(m.ng + h);
-    const uint4 kw = __ldg(rec);
-    const double2 pb = __ldg(reinterpret_cast<const double2*>(rec) + 1);
+// score_word (ngram.py:208-236) for one (entry history, word) per 8-lane group; all 32 lanes
+// call.  Lane sub = 2*i + c scans candidate bucket c of the key K_i = (h[i:], w), i <= hlen,
+// in the bucketized cuckoo image: one 128-byte line, four 16-byte key loads in flight, so a
+// whole score_word is a single memory round trip.  The back-offs of the abandoned histories
+// h[i:] come from the entry's cache.  The group leader (sub 0) combines the right-nested sum
+// bo(h0) + (bo(h1) + (... + p)), the successor = longest listed suffix of (h + w) capped at
+// order-1 words, and the successor's own suffix back-offs (the new entry's cache).  `w < 0`
+// is the OOV-without-<unk> kill: increment NEG_INF, successor ().
+struct WordScore {
+  double inc;
+  double sbo[MAXH];
+  uint32_t succ[MAXH];
+  int slen;
+};
+
+__device__ void group_score_word(const ModelDev& m, bool act, const uint32_t h[MAXH], int hl,
+                                 const double hbo[MAXH], int w, WordScore& out,
+                                 unsigned& probes) {
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+  const bool valid = act && w >= 0;
+  const int ki = sub >> 1, cb = sub & 1;
+  bool hit = false;
+  double p = 0.0, bo = 0.0;
+  if (valid && ki <= hl) {
+    uint32_t k[4] = {WPAD, WPAD, WPAD, WPAD};
+    int n = 0;
+    for (int j = ki; j < hl; ++j) k[n++] = h[j];
+    k[n] = (uint32_t)w;
+    uint32_t b1, b2;
+    ng_buckets(ng_hash(k[0], k[1], k[2], k[3]), m.ng_nb, b1, b2);
+    const uint4* bucket = reinterpret_cast<const uint4*>(m.ng + (size_t)(cb ? b2 : b1) * NG_WAYS);
+    uint4 r[NG_WAYS];
+#pragma unroll
+    for (int q = 0; q < NG_WAYS; ++q) r[q] = __ldg(bucket + 2 * q);
     ++probes;
-    if (kw.x == WPAD) return false;
-    if (kw.x == k[0] && kw.y == k[1] && kw.z == k[2] && kw.w == k[3]) {
+    int slot = -1;
+#pragma unroll
+    for (int q = NG_WAYS - 1; q >= 0; --q)
+      if (r[q].x == k[0] && r[q].y == k[1] && r[q].z == k[2] && r[q].w == k[3]) slot = q;
+    if (slot >= 0) {
+      const double2 pb = __ldg(reinterpret_cast<const double2*>(bucket + 2 * slot + 1));
       p = pb.x;
       bo = pb.y;
-      return true;
+      hit = true;
     }
-    h = (h + 1) & m.ng_mask;
+  }
+  const unsigned bal = __ballot_sync(FULLMASK, hit);
+  const unsigned gb = (bal >> (grp * 8)) & 0xFFu;
+  double pk[4], bk[4];
+  bool fk[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int src = grp * 8 + 2 * j + (((gb >> (2 * j)) & 1u) ? 0 : 1);
+    pk[j] = __shfl_sync(FULLMASK, p, src);
+    bk[j] = __shfl_sync(FULLMASK, bo, src);
+    fk[j] = ((gb >> (2 * j)) & 3u) != 0;
+  }
+  out.slen = 0;
+  out.inc = NEG_INF;
+  if (sub != 0 || !valid) return;
+  double val = NEG_INF;
+  int hitk = hl + 1;
+#pragma unroll
+  for (int j = 3; j >= 0; --j)
+    if (j <= hl && fk[j] && prob_present(pk[j])) {
+      val = pk[j];
+      hitk = j;
+    }
+  for (int j = min(hitk, hl) - 1; j >= 0; --j) val = xadd(hbo[j], val);
+  out.inc = val;
+  if (m.order > 1) {
+    const int start = max(0, hl + 1 - (m.order - 1));
+    int sk = -1;
+#pragma unroll
+    for (int j = 3; j >= 0; --j)
+      if (j >= start && j <= hl && fk[j] && prob_present(pk[j])) sk = j;
+    if (sk >= 0) {
+      int n = 0;
+      for (int t = sk; t < hl; ++t) out.succ[n++] = h[t];
+      out.succ[n++] = (uint32_t)w;
+      out.slen = n;
+#pragma unroll
+      for (int t = 0; t < MAXH; ++t) {
+        const int j = sk + t;
+        double v = 0.0;
+        if (t < n) {
+          if (j == 0) v = fk[0] ? bk[0] : 0.0;
+          else if (j == 1) v = fk[1] ? bk[1] : 0.0;
+          else if (j == 2) v = fk[2] ? bk[2] : 0.0;
+          else v = fk[3] ? bk[3] : 0.0;
+        }
+        out.sbo[t] = v;
+      }
+    }
   }
 }
 
-// score_word (ngram.py:208-236) for one (history, word) per 8-lane group; all 32 lanes call.
-// Lane sub 0..3 probes K_sub = (h[sub:], w); lanes 4..6 probe the history H_{sub-4} = h[sub-4:]
-// for its back-off.  The group leader (sub 0) combines: right-nested back-off sum and the
-// successor = longest listed suffix of (h + w) capped at order-1 words.  `w < 0` is the
-// OOV-without-<unk> kill: increment NEG_INF, successor ().
-__device__ void group_score_word(const ModelDev& m, bool act, const uint32_t h[MAXH], int hl, int w,
-                                 double& inc, uint32_t succ[MAXH], int& slen, unsigned& probes) {
-  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
-  const bool valid = act && w >= 0;
-  bool hasp = false;
-  double p = 0.0, bo = 0.0;
-  if (valid) {
-    uint32_t k[4] = {WPAD, WPAD, WPAD, WPAD};
-    bool doit = false;
-    int n = 0;
-    if (sub <= 3) {
-      if (sub <= hl) {
-        for (int i = sub; i < hl; ++i) k[n++] = h[i];
-        k[n++] = (uint32_t)w;
-        doit = true;
-      }
-    } else if (sub <= 6) {
-      const int i0 = sub - 4;
-      if (i0 < hl) {
-        for (int i = i0; i < hl; ++i) k[n++] = h[i];
-        doit = true;
-      }
-    }
-    if (doit) {
-      const bool found = ng_lookup(m, k, p, bo, probes);
-      if (!found) bo = 0.0;
-      hasp = found && prob_present(p);
-    }
+__device__ __forceinline__ void new_entry(Ent& o, double total, double cum, const WordScore& ws,
+                                          uint32_t node, uint32_t seq, uint32_t depth) {
+  o.total = total;
+  o.cum = cum;
+  o.node = node;
+  o.seq = seq;
+  o.hlen = (uint8_t)ws.slen;
+  o.depth = (uint16_t)depth;
+  o.punct = 0;
+#pragma unroll
+  for (int t = 0; t < MAXH; ++t) {
+    o.h[t] = t < ws.slen ? ws.succ[t] : 0u;
+    o.bo[t] = t < ws.slen ? ws.sbo[t] : 0.0;
   }
-  const unsigned bal = __ballot_sync(FULLMASK, hasp);
-  const unsigned gb = (bal >> (grp * 8)) & 0xFFu;
-  double pk0 = __shfl_sync(FULLMASK, p, grp * 8 + 0);
-  double pk1 = __shfl_sync(FULLMASK, p, grp * 8 + 1);
-  double pk2 = __shfl_sync(FULLMASK, p, grp * 8 + 2);
-  double pk3 = __shfl_sync(FULLMASK, p, grp * 8 + 3);
-  double b0 = __shfl_sync(FULLMASK, bo, grp * 8 + 4);
-  double b1 = __shfl_sync(FULLMASK, bo, grp * 8 + 5);
-  double b2 = __shfl_sync(FULLMASK, bo, grp * 8 + 6);
-  slen = 0;
-  inc = NEG_INF;
-  if (sub != 0 || !act) return;
-  if (!valid) return;  // kill: NEG_INF, successor ()
-  const double pk[4] = {pk0, pk1, pk2, pk3};
-  const double bh[3] = {b0, b1, b2};
-  double val = NEG_INF;
-  int hit = hl + 1;
-  for (int i = 0; i <= hl; ++i)
-    if ((gb >> i) & 1u) {
-      val = pk[i];
-      hit = i;
-      break;
-    }
-  for (int i = min(hit, hl) - 1; i >= 0; --i) val = xadd(bh[i], val);
-  inc = val;
-  if (m.order > 1) {
-    const int start = max(0, hl + 1 - (m.order - 1));
-    for (int i = start; i <= hl; ++i)
-      if ((gb >> i) & 1u) {
-        int n = 0;
-        for (int j = i; j < hl; ++j) succ[n++] = h[j];
-        succ[n++] = (uint32_t)w;
-        slen = n;
-        break;
-      }
-  }
+}
+
+// Completion header embedded in a padded lexicon row (see ROW_HDR in lb_device.cuh).
+struct CompHdr {
+  int ns, off, s0, l0, s1, l1;
+};
+__device__ __forceinline__ CompHdr comp_hdr(const int32_t* row, int V) {
+  return CompHdr{row[V], row[V + 1], row[V + 2], row[V + 3], row[V + 4], row[V + 5]};
 }
 
 // apply_ngram (decoder.py:182-235) for one beam, one full warp.  Candidates are the
@@ -203,46 +234,54 @@ __device__ void group_score_word(const ModelDev& m, bool act, const uint32_t h[M
 // On return (lane 0 authoritative): *outn = kept entries (written to outents), or -1 when no
 // candidate survived (beam killed: *score = NEG_INF, decoder.py:223-225).
 __device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const BatchDev& b, int trial,
-                                 const Ent* pents, int pn, int st, WarpScratch* ws, Ent* outents,
-                                 int* outn, double* score, int* node_counter, int* fail,
-                                 unsigned& calls, unsigned& probes) {
+                                 const Ent* pents, int pn, const CompHdr ch, WarpScratch* ws,
+                                 Ent* outents, int* outn, double* score, int* node_counter,
+                                 int* fail, unsigned& calls, unsigned& probes) {
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
-  const int cbeg = m.comp_off[st];
-  const int ns = m.comp_off[st + 1] - cbeg;
+  const int ns = ch.ns;
   const int npairs = pn * ns;
   int ntop = 0;
   for (int base = 0; base < npairs; base += 4) {
     const int pi = base + grp;
     const bool act = pi < npairs;
-    int e = 0, s = 0, w = -1;
+    int e = 0, s = 0, w = -1, surf = -1;
     if (act) {
       e = pi / ns;
       s = pi - e * ns;
-      w = m.comp_lm[cbeg + s];
+      if (s == 0) {
+        w = ch.l0;
+        surf = ch.s0;
+      } else if (s == 1) {
+        w = ch.l1;
+        surf = ch.s1;
+      } else {
+        w = __ldg(m.comp_lm + ch.off + s);
+        surf = __ldg(m.comp_surf + ch.off + s);
+      }
     }
     const Ent& E = pents[act ? e : 0];
     uint32_t hh[MAXH] = {E.h[0], E.h[1], E.h[2]};
-    const int hl = E.hlen;
-    double inc;
-    uint32_t sh[MAXH] = {0, 0, 0};
-    int sl;
-    group_score_word(m, act, hh, hl, w, inc, sh, sl, probes);
+    double hb[MAXH] = {E.bo[0], E.bo[1], E.bo[2]};
+    WordScore sw;
+    group_score_word(m, act, hh, E.hlen, hb, w, sw, probes);
     if (sub == 0) {
       NgCand& pc = ws->pending[grp];
       pc.valid = 0;
       if (act) {
         ++calls;
-        if (inc > GUARD) {
+        if (sw.inc > GUARD) {
           pc.valid = 1;
-          pc.total = xadd(E.total, xmul(c.omega, inc));
-          pc.inc = inc;
+          pc.total = xadd(E.total, xmul(c.omega, sw.inc));
+          pc.cum = xadd(E.cum, sw.inc);
+          pc.depth = (uint32_t)E.depth + 1u;
           pc.node = E.node;
-          pc.surf = (uint32_t)m.comp_surf[cbeg + s];
+          pc.surf = (uint32_t)surf;
           pc.seq = (uint32_t)pi;
-          pc.hlen = (uint32_t)sl;
-          pc.h[0] = sh[0];
-          pc.h[1] = sh[1];
-          pc.h[2] = sh[2];
+          pc.hlen = (uint32_t)sw.slen;
+          for (int t = 0; t < MAXH; ++t) {
+            pc.h[t] = sw.succ[t];
+            pc.bo[t] = sw.sbo[t];
+          }
         }
       }
     }
@@ -278,7 +317,6 @@ __device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const Batch
       const int base = atomicAdd(node_counter, kept);
       if (base + kept > b.ncap) {
         *fail = 1;
-        kept = 0;
         *outn = -1;
         *score = NEG_INF;
       } else {
@@ -288,19 +326,13 @@ __device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const Batch
           const uint32_t node = (uint32_t)(base + i);
           b.nparent[nb + node] = cd.node;
           b.nsurf[nb + node] = cd.surf;
-          b.ndepth[nb + node] = b.ndepth[nb + cd.node] + 1;
-          b.ncum[nb + node] = xadd(b.ncum[nb + cd.node], cd.inc);
-          Ent o;
-          o.total = cd.total;
-          o.node = node;
-          o.seq = cd.seq;
-          o.h[0] = cd.h[0];
-          o.h[1] = cd.h[1];
-          o.h[2] = cd.h[2];
-          o.hlen = (uint8_t)cd.hlen;
-          o.punct = 0;
-          o.pad = 0;
-          outents[i] = o;
+          WordScore sw;
+          sw.slen = (int)cd.hlen;
+          for (int t = 0; t < MAXH; ++t) {
+            sw.succ[t] = cd.h[t];
+            sw.sbo[t] = cd.bo[t];
+          }
+          new_entry(outents[i], cd.total, cd.cum, sw, node, cd.seq, cd.depth);
         }
         *outn = kept;
         *score = xadd(*score, xsub(best, pents[0].total));
@@ -339,11 +371,8 @@ struct BeamPtrs {
   Ent* ents;
 };
 
-__device__ __forceinline__ void copy_ents(Ent* dst, const Ent* src, int n) {
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-  uint4* d = reinterpret_cast<uint4*>(dst);
-  for (int i = 0; i < 2 * n; ++i) d[i] = s[i];
-}
+constexpr int ENT_U4 = sizeof(Ent) / 16;
+
 
 }  // namespace
 
@@ -351,14 +380,20 @@ __device__ __forceinline__ void copy_ents(Ent* dst, const Ent* src, int n) {
 // K2: persistent frame loop
 // =====================================================================================
 template <int NT>
-__global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchDev b, Layout L,
-                                                    int t0, int t1, int fusion_mode, double scale) {
+__global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDev m, CfgDev c,
+                                                                       BatchDev b, Layout L,
+                                                                       int t0, int t1,
+                                                                       int fusion_mode,
+                                                                       double scale) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t dbar[2];
   __shared__ unsigned hist[NBINS];
   __shared__ double wmax[NW];
-  __shared__ int s_cnt, s_nb, s_ncount, s_fail;
+  __shared__ int s_cnt, s_ncount, s_fail;
+  __shared__ unsigned long long s_pack;  // (boundary beams << 32) | (n-gram pairs)
+  __shared__ int hcum[NBINS];            // exclusive prefix of hist (identical in every warp)
+  __shared__ int hfill[NBINS];           // counting-sort fill pointers
   __shared__ unsigned s_calls, s_probes;
 
   const int trial = blockIdx.x;
@@ -378,7 +413,7 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
   BeamPtrs nxt{(double*)R(R_NXT_SCORE), (uint64_t*)R(R_NXT_H1), (uint64_t*)R(R_NXT_H2),
                (int32_t*)R(R_NXT_LAST), (int32_t*)R(R_NXT_PRE), (int32_t*)R(R_NXT_NENT),
                (Ent*)R(R_NXT_ENTS)};
-  uint64_t* maskv = reinterpret_cast<uint64_t*>(R(R_MASK));
+  uint16_t* cbin = reinterpret_cast<uint16_t*>(R(R_CBIN));  // [K*V] histogram bin or 0xFFFF
   double* cval = reinterpret_cast<double*>(R(R_CVAL));
   uint32_t* ckey = reinterpret_cast<uint32_t*>(R(R_CKEY));
   double* sval = reinterpret_cast<double*>(R(R_SVAL));
@@ -395,12 +430,18 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
   int32_t* bnent = reinterpret_cast<int32_t*>(R(R_BNENT));
   uint32_t* keep = reinterpret_cast<uint32_t*>(R(R_KEEP));
   WarpScratch* wsc = reinterpret_cast<WarpScratch*>(R(R_WARP));
+  int32_t* poff = reinterpret_cast<int32_t*>(R(R_POFF));     // [K+1] pair offsets
+  PairRes* pres = reinterpret_cast<PairRes*>(R(R_PAIRS));    // [pcap]
+  int32_t* slotb = reinterpret_cast<int32_t*>(R(R_SLOTB));   // [tslots] beam claiming a slot
+  int32_t* slotm = reinterpret_cast<int32_t*>(R(R_SLOTM));   // [tslots] min rank in the group
+  int32_t* myslot = reinterpret_cast<int32_t*>(R(R_MYSLOT)); // [K]
 
   const int V = m.V, VP = m.VP, VPD = b.VPD, O = c.O, KC = b.K;
   const FrameConsts fc{c.beta, c.gamma, m.blank, m.space};
   const int nkw = (c.k + 31) >> 5;
+  const int TS = L.tslots;
 
-  // ---- load the home beam state
+  // ---- load the home beam state and gather the first frame's lexicon rows
   int K = b.nbeam[trial];
   {
     const size_t hb = (size_t)trial * KC;
@@ -411,10 +452,19 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
       cur.last[i] = b.last[hb + i];
       cur.pre[i] = b.prefix[hb + i];
       cur.nent[i] = b.nent[hb + i];
+      if (L.stage_rows) {
+        const int32_t* src = m.table + (size_t)b.prefix[hb + i] * VP;
+        for (int q = 0; q < VP; q += 4) cp_async16(rows + i * VP + q, src + q);
+      }
     }
+    if (L.stage_rows) cp_async_commit();
     const uint4* src = reinterpret_cast<const uint4*>(b.ents + hb * O);
     uint4* dst = reinterpret_cast<uint4*>(cur.ents);
-    for (int i = tid; i < K * O * 2; i += NT) dst[i] = src[i];
+    for (int i = tid; i < K * O * ENT_U4; i += NT) dst[i] = src[i];
+  }
+  for (int i = tid; i < NBINS; i += NT) {
+    hist[i] = 0;
+    hfill[i] = 0;
   }
   if (tid == 0) {
     s_ncount = b.ncount[trial];
@@ -425,6 +475,7 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
     mbar_init(&dbar[1], 1);
     fence_mbar_init();
   }
+  if (L.stage_rows) cp_async_wait_all();
   __syncthreads();
 
   const double* Dtrial = b.D + (size_t)trial * b.Tmax * VPD;
@@ -442,118 +493,130 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
   unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
   unsigned calls_l = 0, probes_l = 0;
   int status = 0, fail_t = -1;
+  // phase timing (thread 0 only, when b.phase_cycles is set)
+  const bool timing = b.phase_cycles != nullptr && tid == 0;
+  unsigned long long ph[NPHASE];
+  for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
+  long long tprev = timing ? clock64() : 0;
+#define LB_PHASE(i)                                \
+  if (timing) {                                    \
+    const long long tnow = clock64();              \
+    ph[i] += (unsigned long long)(tnow - tprev);   \
+    tprev = tnow;                                  \
+  }
 
   for (int t = tb; t < te; ++t) {
     const int rel = t - tb;
     const int ci = rel / CHUNK;
-    if (rel % CHUNK == 0) {
+    const int cr = rel - ci * CHUNK;
+    if (cr == 0) {
       mbar_wait(&dbar[ci & 1], (unsigned)((ci >> 1) & 1));
       if (tid == 0) issue_chunk(ci + 1);
     }
-    const double* drow = dbuf + ((size_t)(ci & 1) * CHUNK + (rel % CHUNK)) * VPD;
+    const double* drow = dbuf + ((size_t)(ci & 1) * CHUNK + cr) * VPD;
     st_beams_in += K;
+    const int KV = K * V;
 
-    // ---- A1: stage the K lexicon rows (16-byte cp.async, all in flight at once)
-    if (L.stage_rows) {
-      const int cpr = VP >> 2;
-      for (int q = tid; q < K * cpr; q += NT) {
-        const int p = q / cpr, part = q - p * cpr;
-        cp_async16(rows + p * VP + part * 4, m.table + (size_t)cur.pre[p] * VP + part * 4);
-      }
-      cp_async_commit();
+    // ---- A: candidate values (decoder.py:252-260) + histogram, one pass.  Bins are anchored
+    // at U = max s + max D + bonuses (>= every candidate up to rounding), so the pass does not
+    // need the true maximum; bins are monotone in the value (clamped floor of (U - x) * inv).
+    double U;
+    {
+      double ms = -DBL_MAX, md = -DBL_MAX;
+      for (int i = lane; i < K; i += 32) ms = fmax(ms, cur.score[i]);
+      for (int v = lane; v < V; v += 32) md = fmax(md, drow[v]);
+      ms = warp_max(ms);
+      md = warp_max(md);
+      U = __dadd_ru(__dadd_ru(ms, md), c.bonus_up);
     }
-    for (int i = tid; i < NBINS; i += NT) hist[i] = 0;
-    for (int i = tid; i < nkw; i += NT) keep[i] = 0;
-    if (tid == 0) {
-      s_cnt = 0;
-      s_nb = 0;
-    }
-    if (L.stage_rows) cp_async_wait_all();
-    __syncthreads();  // S1
-
-    // ---- A2: validity masks + per-warp maximum of eligible candidates
     double wm = -DBL_MAX;
+#pragma unroll 2
     for (int p = warp; p < K; p += NW) {
       const int lp = cur.last[p];
       const double s = cur.score[p];
       const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
-      uint64_t mk = 0;
-      for (int v0 = 0; v0 < V; v0 += 32) {
-        const int v = v0 + lane;
-        bool ok = false;
-        if (v < V) {
-          const int nx = row[v];
-          ok = (nx != m.sink) || (v == m.blank) || (v == lp);
-          if (ok) {
-            const double x = cand_value(s, drow[v], v, lp, fc);
-            ok = x > GUARD;
-            if (ok) wm = fmax(wm, x);
+      for (int v = lane; v < V; v += 32) {
+        const int nx = row[v];
+        double x = -DBL_MAX;
+        uint16_t bin = 0xFFFF;
+        if ((nx != m.sink) || (v == m.blank) || (v == lp)) {
+          x = cand_value(s, drow[v], v, lp, fc);
+          if (x > GUARD) {
+            const double fb = fmin(fmax(xmul(xsub(U, x), c.inv_binw), 0.0), (double)(NBINS - 1));
+            bin = (uint16_t)(int)fb;
+            atomicAdd(&hist[bin], 1u);
+          } else {
+            x = -DBL_MAX;
           }
         }
-        mk |= (uint64_t)__ballot_sync(FULLMASK, ok) << v0;
+        cbin[p * V + v] = bin;
+        wm = fmax(wm, x);
       }
-      if (lane == 0) maskv[p] = mk;
     }
     wm = warp_max(wm);
     if (lane == 0) wmax[warp] = wm;
-    __syncthreads();  // S2
+    if (tid == 0) {
+      s_cnt = 0;
+      s_pack = 0ull;
+    }
+    for (int i = tid; i < nkw; i += NT) keep[i] = 0;
+    for (int i = tid; i < TS; i += NT) {
+      slotb[i] = -1;
+      slotm[i] = 0x7FFFFFFF;
+    }
+    __syncthreads();  // S1
+    LB_PHASE(1);
 
     double M = -DBL_MAX;
     for (int w = 0; w < NW; ++w) M = fmax(M, wmax[w]);
-    if (M <= GUARD) {  // decoder.py:267-268
+    if (!(M > GUARD)) {  // decoder.py:267-268
       status = 1;
       fail_t = t;
       break;
     }
     const double thr = xsub(M, c.theta);
+    const int bthr = (int)fmin(fmax(xmul(xsub(U, thr), c.inv_binw), 0.0), (double)(NBINS - 1));
 
-    // ---- B: histogram of in-range candidates over [thr, M]
-    for (int p = warp; p < K; p += NW) {
-      const uint64_t mk = maskv[p];
-      const int lp = cur.last[p];
-      const double s = cur.score[p];
-      for (int v = lane; v < V; v += 32) {
-        if (!((mk >> v) & 1ull)) continue;
-        const double x = cand_value(s, drow[v], v, lp, fc);
-        if (x >= thr) {
-          int bin = (int)xmul(xsub(M, x), c.inv_binw);
-          bin = min(bin, NBINS - 1);
-          atomicAdd(&hist[bin], 1u);
-        }
-      }
-    }
-    __syncthreads();  // S3
-
-    // ---- C: every warp scans the histogram (no extra barrier): boundary bin bstar
-    int bstar = NBINS - 1, total = 0, m_sel = 0;
+    // ---- C: every warp scans the histogram (no extra barrier): first bin reaching k.  Each
+    // warp also writes the exclusive prefix hcum[] (identical values from every warp).
+    int bstar = NBINS;
+    int cum_thr = 0;  // candidates in bins <= bthr (upper bound of the exact-filter set)
+    int cum_bstar = 0;
     {
-      unsigned part[NBINS / 32];
-      unsigned ls = 0;
+      constexpr int PB = NBINS / 32;
+      int part[PB];
+      int ls = 0;
 #pragma unroll
-      for (int i = 0; i < NBINS / 32; ++i) {
-        part[i] = hist[lane * (NBINS / 32) + i];
+      for (int i = 0; i < PB; ++i) {
+        part[i] = (int)hist[lane * PB + i];
         ls += part[i];
       }
-      unsigned incl = ls;
+      int incl = ls;
       for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(FULLMASK, incl, o);
+        const int y = __shfl_up_sync(FULLMASK, incl, o);
         if (lane >= o) incl += y;
       }
-      total = (int)__shfl_sync(FULLMASK, incl, 31);
-      if (total <= c.k) {
-        bstar = NBINS - 1;
-        m_sel = total;
-      } else {
-        const unsigned excl = incl - ls;
-        const bool here = excl < (unsigned)c.k && incl >= (unsigned)c.k;
-        const unsigned bl = __ballot_sync(FULLMASK, here);
+      const int excl = incl - ls;
+      {
+        int run = excl;
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+          hcum[lane * PB + i] = run;
+          run += part[i];
+        }
+      }
+      __syncwarp();
+      cum_thr = hcum[bthr] + (int)hist[bthr];
+      const bool here = excl < c.k && incl >= c.k;
+      const unsigned bl = __ballot_sync(FULLMASK, here);
+      if (bl) {
         const int src = __ffs(bl) - 1;
         int lb = 0;
-        unsigned cum = excl;
         if (lane == src) {
+          int cum = excl;
 #pragma unroll
-          for (int i = 0; i < NBINS / 32; ++i) {
-            if (cum + part[i] >= (unsigned)c.k) {
+          for (int i = 0; i < PB; ++i) {
+            if (cum + part[i] >= c.k) {
               lb = i;
               break;
             }
@@ -561,71 +624,67 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
           }
         }
         lb = __shfl_sync(FULLMASK, lb, src);
-        cum = __shfl_sync(FULLMASK, cum, src);
-        bstar = src * (NBINS / 32) + lb;
-        m_sel = (int)(cum + hist[bstar]);
+        bstar = src * PB + lb;
+        cum_bstar = hcum[bstar] + (int)hist[bstar];
       }
     }
-    const int nsel = min(c.k, total);
-
-    if (m_sel <= L.lcap) {
-      // ---- D: collect candidates in bins <= bstar (warp-aggregated appends)
-      for (int p = warp; p < K; p += NW) {
-        const uint64_t mk = maskv[p];
-        const int lp = cur.last[p];
-        const double s = cur.score[p];
-        for (int v0 = 0; v0 < V; v0 += 32) {
-          const int v = v0 + lane;
-          bool take = false;
-          double x = 0.0;
-          if (v < V && ((mk >> v) & 1ull)) {
-            x = cand_value(s, drow[v], v, lp, fc);
-            if (x >= thr) {
-              const int bin = min((int)xmul(xsub(M, x), c.inv_binw), NBINS - 1);
-              take = bin <= bstar;
-            }
-          }
-          const unsigned bl = __ballot_sync(FULLMASK, take);
-          if (bl) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(&s_cnt, __popc(bl));
-            base = __shfl_sync(FULLMASK, base, 0);
-            if (take) {
-              const int pos = base + __popc(bl & ((1u << lane) - 1u));
-              cval[pos] = x;
-              ckey[pos] = (uint32_t)(p * V + v);
-            }
+    // bins < bthr hold only in-range (x >= thr) candidates; bin bthr is mixed
+    const bool sure = bstar < bthr;
+    const int take_bin = sure ? bstar : bthr;
+    const int bound = sure ? cum_bstar : cum_thr;
+    int nsel = 0, m_sel = L.lcap + 1;
+    if (bound <= L.lcap) {
+      // ---- D: collect = counting sort by bin (bins are strictly ordered by value)
+      for (int f = tid; f < KV; f += NT) {
+        const int bn = cbin[f];
+        if (bn <= take_bin) {
+          const int p = f / V, v = f - (f / V) * V;
+          const double x = cand_value(cur.score[p], drow[v], v, cur.last[p], fc);
+          if (sure || x >= thr) {
+            const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
+            cval[pos] = x;
+            ckey[pos] = (uint32_t)f;
           }
         }
       }
-      __syncthreads();  // S4
-      // ---- E: exact rank sort of the collected set, keep the first nsel
-      {
-        const int mm = m_sel;
-        int G = 1;
-        while (G < 32 && 2 * G * mm <= NT) G <<= 1;
-        const int groups = NT / G, g = tid / G, r = tid & (G - 1);
-        for (int i0 = 0; i0 < mm; i0 += groups) {
-          const int i = i0 + g;
-          const bool act = i < mm;
-          const double vi = act ? cval[i] : 0.0;
-          const uint32_t ki = act ? ckey[i] : 0u;
-          int cnt = 0;
-          if (act)
-            for (int j = r; j < mm; j += G) {
-              const double vj = cval[j];
-              cnt += (vj > vi) || (vj == vi && ckey[j] < ki);
-            }
-          for (int o = G >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULLMASK, cnt, o);
-          if (act && r == 0 && cnt < nsel) {
-            sval[cnt] = vi;
-            skey[cnt] = ki;
-          }
+      __syncthreads();  // S2
+      m_sel = hcum[take_bin] + hfill[take_bin];
+      nsel = min(c.k, m_sel);
+      LB_PHASE(2);
+      // ---- E: exact order inside each bin (value desc, flat index asc); bins are disjoint
+      // value ranges, so an element's rank is hcum[bin] + the bin-mates that beat it
+      for (int a = tid; a < m_sel; a += NT) {
+        const double va = cval[a];
+        const uint32_t ka = ckey[a];
+        const int bn = cbin[ka];
+        const int lo = hcum[bn], n = hfill[bn];
+        int r = lo;
+        for (int q = lo; q < lo + n; ++q) {
+          const double vq = cval[q];
+          r += (vq > va) || (vq == va && ckey[q] < ka);
+        }
+        if (r < nsel) {
+          sval[r] = va;
+          skey[r] = ka;
         }
       }
     } else {
       // ---- fallback: exact radix select on the 96-bit key (ord64(value), ~flat index)
       ++st_fallback;
+      __syncthreads();
+      if (tid == 0) s_cnt = 0;
+      // exact in-range count
+      for (int i = tid; i < NBINS; i += NT) hist[i] = 0;
+      __syncthreads();
+      auto cval_at = [&](int f) -> double {
+        if (cbin[f] == 0xFFFF) return -DBL_MAX;
+        const int p = f / V, v = f - (f / V) * V;
+        return cand_value(cur.score[p], drow[v], v, cur.last[p], fc);
+      };
+      for (int f = tid; f < KV; f += NT)
+        if (cval_at(f) >= thr) atomicAdd(&hist[0], 1u);
+      __syncthreads();
+      nsel = min(c.k, (int)hist[0]);
       uint64_t phi = 0, pmask_hi = 0;
       uint32_t plo = 0, pmask_lo = 0;
       int rem = nsel;
@@ -633,24 +692,17 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
         __syncthreads();
         for (int i = tid; i < NBINS; i += NT) hist[i] = 0;
         __syncthreads();
-        for (int p = warp; p < K; p += NW) {
-          const uint64_t mk = maskv[p];
-          const int lp = cur.last[p];
-          const double s = cur.score[p];
-          for (int v = lane; v < V; v += 32) {
-            if (!((mk >> v) & 1ull)) continue;
-            const double x = cand_value(s, drow[v], v, lp, fc);
-            if (x < thr) continue;
-            const uint64_t kh = ord64(x);
-            const uint32_t kl = ~(uint32_t)(p * V + v);
-            if ((kh & pmask_hi) != phi || (kl & pmask_lo) != plo) continue;
-            const unsigned dg = pass < 8 ? (unsigned)((kh >> (56 - 8 * pass)) & 0xFF)
-                                         : (unsigned)((kl >> (24 - 8 * (pass - 8))) & 0xFF);
-            atomicAdd(&hist[dg], 1u);
-          }
+        for (int f = tid; f < KV; f += NT) {
+          const double x = cval_at(f);
+          if (!(x >= thr)) continue;
+          const uint64_t kh = ord64(x);
+          const uint32_t kl = ~(uint32_t)f;
+          if ((kh & pmask_hi) != phi || (kl & pmask_lo) != plo) continue;
+          const unsigned dg = pass < 8 ? (unsigned)((kh >> (56 - 8 * pass)) & 0xFF)
+                                       : (unsigned)((kl >> (24 - 8 * (pass - 8))) & 0xFF);
+          atomicAdd(&hist[dg], 1u);
         }
         __syncthreads();
-        // scan digits from 255 down (each thread redundantly; NBINS small)
         int above = 0, dsel = 0;
         for (int d = NBINS - 1; d >= 0; --d) {
           const int h = (int)hist[d];
@@ -670,33 +722,27 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
         }
       }
       __syncthreads();
-      // collect every candidate with key >= (phi, plo): exactly nsel of them
-      for (int p = warp; p < K; p += NW) {
-        const uint64_t mk = maskv[p];
-        const int lp = cur.last[p];
-        const double s = cur.score[p];
-        for (int v0 = 0; v0 < V; v0 += 32) {
-          const int v = v0 + lane;
-          bool take = false;
-          double x = 0.0;
-          if (v < V && ((mk >> v) & 1ull)) {
-            x = cand_value(s, drow[v], v, lp, fc);
-            if (x >= thr) {
-              const uint64_t kh = ord64(x);
-              const uint32_t kl = ~(uint32_t)(p * V + v);
-              take = kh > phi || (kh == phi && kl >= plo);
-            }
+      for (int f0 = 0; f0 < KV; f0 += NT) {
+        const int f = f0 + tid;
+        bool take = false;
+        double x = 0.0;
+        if (f < KV) {
+          x = cval_at(f);
+          if (x >= thr) {
+            const uint64_t kh = ord64(x);
+            const uint32_t kl = ~(uint32_t)f;
+            take = kh > phi || (kh == phi && kl >= plo);
           }
-          const unsigned bl = __ballot_sync(FULLMASK, take);
-          if (bl) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(&s_cnt, __popc(bl));
-            base = __shfl_sync(FULLMASK, base, 0);
-            if (take) {
-              const int pos = base + __popc(bl & ((1u << lane) - 1u));
-              cval[pos] = x;
-              ckey[pos] = (uint32_t)(p * V + v);
-            }
+        }
+        const unsigned bl = __ballot_sync(FULLMASK, take);
+        if (bl) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&s_cnt, __popc(bl));
+          base = __shfl_sync(FULLMASK, base, 0);
+          if (take) {
+            const int pos = base + __popc(bl & ((1u << lane) - 1u));
+            cval[pos] = x;
+            ckey[pos] = (uint32_t)f;
           }
         }
       }
@@ -713,7 +759,8 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
         skey[cnt] = ki;
       }
     }
-    __syncthreads();  // S5
+    __syncthreads();  // S3
+    LB_PHASE(3);
 
     // ---- F: materialise survivors in selection order (decoder.py:272-291)
     for (int j = tid; j < nsel; j += NT) {
@@ -737,28 +784,159 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
       npre[j] = np;
       npar[j] = p;
       bnent[j] = -1;
-      if (emit && tok == m.space) blist[atomicAdd(&s_nb, 1)] = j;
-    }
-    __syncthreads();  // S6
-
-    // ---- G: n-gram fusion for new word-boundary emissions, one warp per beam
-    const int nb = s_nb;
-    st_bound += nb;
-    for (int bi = warp; bi < nb; bi += NW) {
-      const int j = blist[bi];
-      const int p = npar[j];
-      int outn = -1;
-      double sc = nscore[j];
-      warp_apply_ngram(m, c, b, trial, cur.ents + (size_t)p * O, cur.nent[p], cur.pre[p], &wsc[warp],
-                       bents + (size_t)j * O, &outn, &sc, &s_ncount, &s_fail, calls_l, probes_l);
-      if (lane == 0) {
-        nscore[j] = sc;
-        bnent[j] = outn;
+      if (emit && tok == m.space) {
+        // boundary beam: reserve its slot and its (entry, surface) pair range in one atomic
+        const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)pp * VP;
+        const unsigned np2 = (unsigned)(cur.nent[p] * row[V]);
+        const unsigned long long old = atomicAdd(&s_pack, (1ull << 32) | np2);
+        const int bi = (int)(old >> 32);
+        blist[bi] = j;
+        poff[bi] = (int)(old & 0xFFFFFFFFull);
       }
     }
-    __syncthreads();  // S7
+    __syncthreads();  // S4
+    LB_PHASE(4);
 
-    // ---- H: recombination ranking (post-fusion score desc, index asc) + hash dedupe
+    // ---- G: n-gram fusion for new word-boundary emissions (decoder.py:293-295)
+    const int nb = (int)(s_pack >> 32);
+    st_bound += nb;
+    if (nb > 0) {
+      const int P = (int)(s_pack & 0xFFFFFFFFull);
+      if (P <= L.pcap) {
+        // G2: one 8-lane group per (beam, entry, surface) pair: parallel score_word probes
+        constexpr int NG = NT / 8;
+        const int grp = tid >> 3, sub = lane & 7;
+        for (int q0 = 0; q0 < P; q0 += NG) {
+          const int q = q0 + grp;
+          const bool act = q < P;
+          int w = -1, surf = -1, p = 0, e = 0;
+          if (act) {
+            int lo = 0, hi = nb - 1;  // last bi with poff[bi] <= q
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (poff[mid] <= q) lo = mid;
+              else hi = mid - 1;
+            }
+            p = npar[blist[lo]];
+            const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
+            const CompHdr ch = comp_hdr(row, V);
+            const int local = q - poff[lo];
+            e = local / ch.ns;
+            const int sidx = local - e * ch.ns;
+            if (sidx == 0) {
+              w = ch.l0;
+              surf = ch.s0;
+            } else if (sidx == 1) {
+              w = ch.l1;
+              surf = ch.s1;
+            } else {
+              w = __ldg(m.comp_lm + ch.off + sidx);
+              surf = __ldg(m.comp_surf + ch.off + sidx);
+            }
+          }
+          const Ent& E = cur.ents[(size_t)p * O + e];
+          uint32_t hh[MAXH] = {E.h[0], E.h[1], E.h[2]};
+          double hb[MAXH] = {E.bo[0], E.bo[1], E.bo[2]};
+          WordScore sw;
+          group_score_word(m, act, hh, E.hlen, hb, w, sw, probes_l);
+          if (act && sub == 0) {
+            ++calls_l;
+            PairRes pr;
+            pr.valid = sw.inc > GUARD;
+            pr.total = xadd(E.total, xmul(c.omega, sw.inc));
+            pr.cum = xadd(E.cum, sw.inc);
+            pr.node = E.node;
+            pr.surf = (uint32_t)surf;
+            for (int t = 0; t < MAXH; ++t) {
+              pr.h[t] = sw.succ[t];
+              pr.bo[t] = sw.sbo[t];
+            }
+            pr.depth = (uint16_t)(E.depth + 1);
+            pr.hlen = (uint8_t)sw.slen;
+            pres[q] = pr;
+          }
+        }
+        __syncthreads();
+        // G3: thread per boundary beam: top-O by (-total, seq), lambda filter, new entries
+        for (int bi = tid; bi < nb; bi += NT) {
+          const int j = blist[bi];
+          const int p = npar[j];
+          const int q0 = poff[bi], q1 = bi + 1 < nb ? poff[bi + 1] : P;
+          int top[OMAX];
+          int ntop = 0;
+          for (int q = q0; q < q1; ++q) {
+            if (!pres[q].valid) continue;
+            const double tq = pres[q].total;
+            int pos = ntop;
+            for (int i = 0; i < ntop; ++i)
+              if (tq > pres[top[i]].total) {
+                pos = i;
+                break;
+              }
+            if (pos >= O) continue;
+            for (int i = min(ntop, O - 1); i > pos; --i) top[i] = top[i - 1];
+            top[pos] = q;
+            ntop = min(ntop + 1, O);
+          }
+          if (ntop == 0) {
+            nscore[j] = NEG_INF;  // decoder.py:223-225
+            bnent[j] = -1;
+            continue;
+          }
+          const double best = pres[top[0]].total;
+          const double floor_ = xsub(best, c.lambda);
+          int kept = 0;
+          while (kept < ntop && pres[top[kept]].total >= floor_) ++kept;
+          const int base = atomicAdd(&s_ncount, kept);
+          if (base + kept > b.ncap) {
+            s_fail = 1;
+            nscore[j] = NEG_INF;
+            bnent[j] = -1;
+            continue;
+          }
+          const size_t nbase = (size_t)trial * b.ncap;
+          Ent* out = bents + (size_t)j * O;
+          for (int i = 0; i < kept; ++i) {
+            const PairRes& pr = pres[top[i]];
+            const uint32_t node = (uint32_t)(base + i);
+            b.nparent[nbase + node] = pr.node;
+            b.nsurf[nbase + node] = pr.surf;
+            WordScore sw;
+            sw.slen = pr.hlen;
+            for (int t = 0; t < MAXH; ++t) {
+              sw.succ[t] = pr.h[t];
+              sw.sbo[t] = pr.bo[t];
+            }
+            new_entry(out[i], pr.total, pr.cum, sw, node, (uint32_t)(top[i] - q0), pr.depth);
+          }
+          bnent[j] = kept;
+          nscore[j] = xadd(nscore[j], xsub(best, cur.ents[(size_t)p * O].total));
+        }
+      } else {
+        // rare: more pairs than one flattened round holds -> one warp per boundary beam
+        for (int bi = warp; bi < nb; bi += NW) {
+          const int j = blist[bi];
+          const int p = npar[j];
+          const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
+          int outn = -1;
+          double sc = nscore[j];
+          warp_apply_ngram(m, c, b, trial, cur.ents + (size_t)p * O, cur.nent[p],
+                           comp_hdr(row, V), &wsc[warp], bents + (size_t)j * O, &outn, &sc,
+                           &s_ncount, &s_fail, calls_l, probes_l);
+          if (lane == 0) {
+            nscore[j] = sc;
+            bnent[j] = outn;
+          }
+        }
+      }
+    }
+    __syncthreads();  // S5
+    LB_PHASE(5);
+
+    // ---- H1: recombination ranking by (post-fusion score desc, index asc).  Beams that did
+    // not cross a word boundary keep their selection scores, which are already in that order,
+    // so only the nb boundary beams need explicit comparisons.  Equal-hash groups are found
+    // with a shared-memory table (exact (h1, h2) equality); each group keeps its best rank.
     {
       const int n = nsel;
       int G = 1;
@@ -768,61 +946,106 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
         const int i = i0 + g;
         const bool act = i < n;
         const double si = act ? nscore[i] : 0.0;
-        const uint64_t a1 = act ? nh1[i] : 0, a2 = act ? nh2[i] : 0;
-        int cnt = 0, dup = 0;
-        if (act)
-          for (int j = r; j < n; j += G) {
+        const bool ib = act && (bnent[i] != -1 || si <= GUARD);  // crossed a boundary
+        int cnt = 0;
+        if (act) {
+          // boundary beams beating i (+ count of boundary beams before i when i is regular)
+          for (int k2 = r; k2 < nb; k2 += G) {
+            const int j = blist[k2];
             const double sj = nscore[j];
-            const bool beats = (sj > si) || (sj == si && j < i);
-            cnt += beats;
-            dup |= beats && (sj > GUARD) && nh1[j] == a1 && nh2[j] == a2;
+            cnt += (sj > si) || (sj == si && j < i);
+            if (!ib) cnt -= (j < i);
           }
-        for (int o = G >> 1; o > 0; o >>= 1) {
-          cnt += __shfl_xor_sync(FULLMASK, cnt, o);
-          dup |= __shfl_xor_sync(FULLMASK, dup, o);
+          if (ib) {
+            // regular beams beating a boundary beam: scan (they are the non-boundary indices)
+            for (int j = r; j < n; j += G) {
+              if (bnent[j] != -1 || nscore[j] <= GUARD) continue;
+              const double sj = nscore[j];
+              cnt += (sj > si) || (sj == si && j < i);
+            }
+          }
         }
+        for (int o = G >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULLMASK, cnt, o);
         if (act && r == 0) {
+          if (!ib) cnt += i;  // regular beams before i all beat it
           rankv[i] = cnt;
-          if (si > GUARD && !dup) atomicOr(&keep[cnt >> 5], 1u << (cnt & 31));
+          if (si > GUARD) {
+            const uint64_t a1 = nh1[i], a2 = nh2[i];
+            int h = (int)((a1 ^ (a2 * 0x9E3779B97F4A7C15ull)) >> 20) & (TS - 1);
+            for (;;) {
+              const int owner = atomicCAS(&slotb[h], -1, i);
+              if (owner == -1 || (nh1[owner] == a1 && nh2[owner] == a2)) break;
+              h = (h + 1) & (TS - 1);
+            }
+            myslot[i] = h;
+            atomicMin(&slotm[h], cnt);
+          }
         }
       }
     }
-    __syncthreads();  // S8
+    __syncthreads();  // S6
+    LB_PHASE(6);
+    // ---- H2: survivors = best rank of each hash group, killed beams dropped
+    for (int i = tid; i < nsel; i += NT) {
+      if (nscore[i] > GUARD && slotm[myslot[i]] == rankv[i])
+        atomicOr(&keep[rankv[i] >> 5], 1u << (rankv[i] & 31));
+    }
+    __syncthreads();  // S7
+    LB_PHASE(7);
 
-    // ---- scatter survivors into the next buffer in rank order
+    // ---- scatter survivors into the next buffer in rank order; prefetch their lexicon rows
+    for (int i = tid; i < NBINS; i += NT) {  // scanned after S1 / filled before S2: free again
+      hist[i] = 0;
+      hfill[i] = 0;
+    }
     int newK = 0;
     for (int w = 0; w < nkw; ++w) newK += __popc(keep[w]);
-    for (int i = tid; i < nsel; i += NT) {
-      const int rk = rankv[i];
-      if (!((keep[rk >> 5] >> (rk & 31)) & 1u)) continue;
-      int pos = __popc(keep[rk >> 5] & ((1u << (rk & 31)) - 1u));
-      for (int w = 0; w < (rk >> 5); ++w) pos += __popc(keep[w]);
-      nxt.score[pos] = nscore[i];
-      nxt.h1[pos] = nh1[i];
-      nxt.h2[pos] = nh2[i];
-      nxt.last[pos] = nlast[i];
-      nxt.pre[pos] = npre[i];
-      const int bn = bnent[i];
-      if (bn >= 0) {
-        nxt.nent[pos] = bn;
-        copy_ents(nxt.ents + (size_t)pos * O, bents + (size_t)i * O, bn);
-      } else {
-        const int p = npar[i];
-        const int pn = cur.nent[p];
-        nxt.nent[pos] = pn;
-        copy_ents(nxt.ents + (size_t)pos * O, cur.ents + (size_t)p * O, pn);
+    {
+      int G = 1;
+      while (G < 32 && 2 * G * nsel <= NT) G <<= 1;
+      const int groups = NT / G, g = tid / G, r = tid & (G - 1);
+      for (int i0 = 0; i0 < nsel; i0 += groups) {
+        const int i = i0 + g;
+        if (i >= nsel) continue;
+        const int rk = rankv[i];
+        if (!((keep[rk >> 5] >> (rk & 31)) & 1u)) continue;
+        int pos = __popc(keep[rk >> 5] & ((1u << (rk & 31)) - 1u));
+        for (int w = 0; w < (rk >> 5); ++w) pos += __popc(keep[w]);
+        const int bn = bnent[i];
+        const Ent* srcE = bn >= 0 ? bents + (size_t)i * O : cur.ents + (size_t)npar[i] * O;
+        const int cnt = bn >= 0 ? bn : cur.nent[npar[i]];
+        if (r == 0) {
+          nxt.score[pos] = nscore[i];
+          nxt.h1[pos] = nh1[i];
+          nxt.h2[pos] = nh2[i];
+          nxt.last[pos] = nlast[i];
+          nxt.pre[pos] = npre[i];
+          nxt.nent[pos] = cnt;
+          if (b.dump_k) {
+            const size_t di = ((size_t)trial * b.Tmax + t) * KC + pos;
+            b.dump_h1[di] = nh1[i];
+            b.dump_h2[di] = nh2[i];
+            b.dump_pre[di] = npre[i];
+            b.dump_last[di] = nlast[i];
+            b.dump_score[di] = nscore[i];
+          }
+        }
+        const uint4* su = reinterpret_cast<const uint4*>(srcE);
+        uint4* du = reinterpret_cast<uint4*>(nxt.ents + (size_t)pos * O);
+        for (int u = r; u < cnt * ENT_U4; u += G) du[u] = su[u];
+        if (L.stage_rows) {
+          const int32_t* srow = m.table + (size_t)npre[i] * VP;
+          for (int u = r; u < (VP >> 2); u += G) cp_async16(rows + pos * VP + u * 4, srow + u * 4);
+        }
       }
-      if (b.dump_k) {
-        const size_t di = ((size_t)trial * b.Tmax + t) * KC + pos;
-        b.dump_h1[di] = nh1[i];
-        b.dump_h2[di] = nh2[i];
-        b.dump_pre[di] = npre[i];
-        b.dump_last[di] = nlast[i];
-        b.dump_score[di] = nscore[i];
+      if (L.stage_rows) {
+        cp_async_commit();
+        cp_async_wait_all();
       }
     }
     if (b.dump_k && tid == 0) b.dump_k[(size_t)trial * b.Tmax + t] = newK;
-    __syncthreads();  // S9
+    __syncthreads();  // S8
+    LB_PHASE(8);
     {
       BeamPtrs tmp = cur;
       cur = nxt;
@@ -843,7 +1066,6 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
 
     // ---- optional interval fusion of the device n-gram scorer (decoder.py:428-430)
     if (fusion_mode == 1 && t > 0 && (t % c.r) == 0) {
-      const size_t nbase = (size_t)trial * b.ncap;
       for (int i = tid; i < K; i += NT) {
         Ent* e = cur.ents + (size_t)i * O;
         const int n = cur.nent[i];
@@ -853,18 +1075,23 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
             e[q].total = 0.0;
             e[q].punct = 0;
           } else {
-            e[q].total = xmul(c.phi, xmul(scale, b.ncum[nbase + e[q].node]));
+            e[q].total = xmul(c.phi, xmul(scale, e[q].cum));
           }
         }
         sort_entries(e, n);
         cur.score[i] = xadd(cur.score[i], xsub(e[0].total, prev));
       }
       __syncthreads();
+      LB_PHASE(10);
     }
+    LB_PHASE(9);
   }
 
   // ---- write back
   __syncthreads();
+  if (timing)
+    for (int i = 0; i < NPHASE; ++i) b.phase_cycles[(size_t)trial * NPHASE + i] += ph[i];
+#undef LB_PHASE
   if (tid == 0) {
     if (status != 0) {
       b.status[trial] = status;
@@ -885,7 +1112,7 @@ __global__ void __launch_bounds__(NT) frames_kernel(ModelDev m, CfgDev c, BatchD
     }
     const uint4* src = reinterpret_cast<const uint4*>(cur.ents);
     uint4* dst = reinterpret_cast<uint4*>(b.ents + hb * O);
-    for (int i = tid; i < K * O * 2; i += NT) dst[i] = src[i];
+    for (int i = tid; i < K * O * ENT_U4; i += NT) dst[i] = src[i];
   }
   atomicAdd(&s_calls, calls_l);
   atomicAdd(&s_probes, probes_l);
@@ -929,15 +1156,15 @@ __global__ void __launch_bounds__(256) close_kernel(ModelDev m, CfgDev c, BatchD
   for (int i = warp; i < K; i += NW) {
     const int st = b.prefix[hb + i];
     if (st == 0) continue;  // root: nothing pending
-    const int ncomp = m.comp_off[st + 1] - m.comp_off[st];
-    if (ncomp == 0) {
+    const CompHdr ch = comp_hdr(m.table + (size_t)st * m.VP, m.V);
+    if (ch.ns == 0) {
       if (lane == 0) b.score[hb + i] = NEG_INF;
       continue;
     }
     double sc = b.score[hb + i];
     int outn = -1;
     Ent* pe = b.ents + (hb + i) * O;
-    warp_apply_ngram(m, c, b, trial, pe, b.nent[hb + i], st, &wsc[warp], tmp, &outn, &sc,
+    warp_apply_ngram(m, c, b, trial, pe, b.nent[hb + i], ch, &wsc[warp], tmp, &outn, &sc,
                      &s_ncount, &s_fail, calls, probes);
     if (lane == 0) {
       b.score[hb + i] = sc;
@@ -996,8 +1223,7 @@ __global__ void __launch_bounds__(256) device_fusion_kernel(ModelDev m, CfgDev c
   if (b.status[trial] != 0 || b.T[trial] <= min_frames) return;
   const int KC = b.K, O = c.O;
   const size_t hb = (size_t)trial * KC;
-  const size_t nbase = (size_t)trial * b.ncap;
-  const int K = b.nbeam[trial];
+    const int K = b.nbeam[trial];
   if (tid == 0) s_probes = 0;
   __syncthreads();
   unsigned probes = 0;
@@ -1011,11 +1237,12 @@ __global__ void __launch_bounds__(256) device_fusion_kernel(ModelDev m, CfgDev c
       const bool act = q < n;
       const Ent E = e[act ? q : 0];
       double inc = 0.0;
-      uint32_t sh[MAXH];
-      int sl;
       if (final_) {
         uint32_t hh[MAXH] = {E.h[0], E.h[1], E.h[2]};
-        group_score_word(m, act && E.node != 0, hh, E.hlen, m.eos_word, inc, sh, sl, probes);
+        double hb[MAXH] = {E.bo[0], E.bo[1], E.bo[2]};
+        WordScore sw;
+        group_score_word(m, act && E.node != 0, hh, E.hlen, hb, m.eos_word, sw, probes);
+        inc = sw.inc;
       }
       if (act && sub == 0) {
         Ent o = E;
@@ -1023,10 +1250,10 @@ __global__ void __launch_bounds__(256) device_fusion_kernel(ModelDev m, CfgDev c
           o.total = 0.0;
           o.punct = 0;
         } else if (final_) {
-          o.total = xmul(c.phi, xmul(scale, xadd(b.ncum[nbase + E.node], inc)));
+          o.total = xmul(c.phi, xmul(scale, xadd(E.cum, inc)));
           o.punct = 1;  // "." (scorer.py:136-139)
         } else {
-          o.total = xmul(c.phi, xmul(scale, b.ncum[nbase + E.node]));
+          o.total = xmul(c.phi, xmul(scale, E.cum));
         }
         e[q] = o;
       }
@@ -1057,13 +1284,12 @@ __global__ void count_entries_kernel(BatchDev b, int64_t* counts) {
   __syncthreads();
   if (b.status[trial] == 0) {
     const size_t hb = (size_t)trial * b.K;
-    const size_t nbase = (size_t)trial * b.ncap;
     const int K = b.nbeam[trial];
     unsigned long long ne = 0, nw = 0;
     for (int i = tid; i < K; i += blockDim.x) {
       const int n = b.nent[hb + i];
       ne += n;
-      for (int q = 0; q < n; ++q) nw += b.ndepth[nbase + b.ents[(hb + i) * b.O + q].node];
+      for (int q = 0; q < n; ++q) nw += b.ents[(hb + i) * b.O + q].depth;
     }
     atomicAdd(&s_e, ne);
     atomicAdd(&s_w, nw);
@@ -1103,7 +1329,7 @@ __global__ void write_entries_kernel(BatchDev b, const int64_t* entry_off, const
       for (int q = 0; q < n; ++q) {
         const int64_t idx = ebase + sh_off[i] + q;
         e_woff[idx] = w;
-        w += b.ndepth[nbase + b.ents[(hb + i) * O + q].node];
+        w += b.ents[(hb + i) * O + q].depth;
       }
     }
   }
@@ -1118,7 +1344,7 @@ __global__ void write_entries_kernel(BatchDev b, const int64_t* entry_off, const
       totals[idx] = E.total;
       puncts[idx] = E.punct;
       uint32_t node = E.node;
-      const uint32_t d = b.ndepth[nbase + node];
+      const uint32_t d = E.depth;
       int64_t wp = e_woff[idx] + d - 1;
       while (node != 0) {
         words[wp--] = (int32_t)b.nsurf[nbase + node];
@@ -1182,58 +1408,50 @@ __global__ void reset_kernel(ModelDev m, BatchDev b) {
   b.nent[hb] = 1;
   Ent e;
   e.total = 0.0;
+  e.cum = 0.0;
+  e.bo[0] = m.bos_bo;
+  e.bo[1] = 0.0;
+  e.bo[2] = 0.0;
   e.node = 0;
   e.seq = 0;
   e.h[0] = m.bos;
   e.h[1] = 0;
   e.h[2] = 0;
+  e.depth = 0;
   e.hlen = 1;
   e.punct = 0;
-  e.pad = 0;
   b.ents[hb * b.O] = e;
   const size_t nb = (size_t)trial * b.ncap;
   b.nparent[nb] = WPAD;
   b.nsurf[nb] = WPAD;
-  b.ndepth[nb] = 0;
-  b.ncum[nb] = 0.0;
   b.ncount[trial] = 1;
   b.status[trial] = 0;
   b.fail_frame[trial] = -1;
   for (int q = 0; q < 8; ++q) b.stats[(size_t)trial * 8 + q] = 0;
 }
 
-__global__ void ngram_build_kernel(NgRec* tab, uint64_t mask, const uint32_t* words,
-                                   const double* probs, const double* bos, int64_t n,
-                                   int* max_probe) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t w0 = words[4 * i], w1 = words[4 * i + 1], w2 = words[4 * i + 2],
-                 w3 = words[4 * i + 3];
-  uint64_t h = ng_hash(w0, w1, w2, w3) & mask;
-  int probe = 1;
-  for (;;) {
-    const unsigned old = atomicCAS(&tab[h].w[0], WPAD, w0);
-    if (old == WPAD) {
-      tab[h].w[1] = w1;
-      tab[h].w[2] = w2;
-      tab[h].w[3] = w3;
-      tab[h].prob = probs[i];
-      tab[h].bo = bos[i];
-      break;
-    }
-    h = (h + 1) & mask;
-    ++probe;
-  }
-  atomicMax(max_probe, probe);
-}
-
 __global__ void pad_table_kernel(int32_t* dst, const int32_t* src, int32_t S, int32_t V,
-                                 int32_t VP) {
+                                 int32_t VP, const int32_t* comp_off, const int32_t* comp_surf,
+                                 const int32_t* comp_lm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)S * VP) return;
   const int64_t s = i / VP;
   const int v = (int)(i - s * VP);
-  dst[i] = v < V ? src[s * V + v] : 0;
+  int32_t out = 0;
+  if (v < V) {
+    out = src[s * V + v];
+  } else if (v < V + ROW_HDR) {
+    const int off = comp_off[s], n = comp_off[s + 1] - off;
+    switch (v - V) {
+      case 0: out = n; break;
+      case 1: out = off; break;
+      case 2: out = n > 0 ? comp_surf[off] : -1; break;
+      case 3: out = n > 0 ? comp_lm[off] : -1; break;
+      case 4: out = n > 1 ? comp_surf[off + 1] : -1; break;
+      default: out = n > 1 ? comp_lm[off + 1] : -1; break;
+    }
+  }
+  dst[i] = out;
 }
 
 // K1: one warp per row; numpy's pairwise sum (8 accumulators + sequential tail, n <= 128)
@@ -1279,7 +1497,20 @@ __global__ void log_softmax_kernel(const float* x, int64_t rows, int32_t V, int3
   if (lane + 32 < V) orow[lane + 32] = xmul(alpha, xsub(xv1, lse));
 }
 
-// device score_word for parity tests of the hashed n-gram image
+// single-thread exact lookup (parity helper): record of `k` or nullptr
+__device__ const NgRec* ng_find(const ModelDev& m, const uint32_t k[4]) {
+  uint32_t b1, b2;
+  ng_buckets(ng_hash(k[0], k[1], k[2], k[3]), m.ng_nb, b1, b2);
+  for (int c2 = 0; c2 < 2; ++c2) {
+    const NgRec* bk = m.ng + (size_t)(c2 ? b2 : b1) * NG_WAYS;
+    for (int q = 0; q < NG_WAYS; ++q)
+      if (bk[q].w[0] == k[0] && bk[q].w[1] == k[1] && bk[q].w[2] == k[2] && bk[q].w[3] == k[3])
+        return bk + q;
+  }
+  return nullptr;
+}
+
+// device score_word for parity tests of the n-gram image (history back-offs looked up here)
 __global__ void score_words_kernel(ModelDev m, int n, const uint32_t* hist, const int32_t* hlen,
                                    const int32_t* word, double* inc, uint32_t* succ,
                                    int32_t* slen) {
@@ -1288,21 +1519,26 @@ __global__ void score_words_kernel(ModelDev m, int n, const uint32_t* hist, cons
   const int q = warp_global * 4 + grp;
   const bool act = q < n;
   uint32_t hh[MAXH] = {0, 0, 0};
+  double hb[MAXH] = {0.0, 0.0, 0.0};
   int hl = 0, w = -1;
   if (act) {
     hl = hlen[q];
     for (int i = 0; i < hl; ++i) hh[i] = hist[3 * q + i];
     w = word[q];
+    for (int i = 0; i < hl; ++i) {
+      uint32_t k[4] = {WPAD, WPAD, WPAD, WPAD};
+      for (int j = i; j < hl; ++j) k[j - i] = hh[j];
+      const NgRec* r = ng_find(m, k);
+      hb[i] = r ? r->bo : 0.0;
+    }
   }
-  double v;
-  uint32_t sh[MAXH] = {0, 0, 0};
-  int sl;
+  WordScore sw;
   unsigned probes = 0;
-  group_score_word(m, act, hh, hl, w, v, sh, sl, probes);
+  group_score_word(m, act, hh, hl, hb, w, sw, probes);
   if (act && sub == 0) {
-    inc[q] = v;
-    slen[q] = sl;
-    for (int i = 0; i < 3; ++i) succ[3 * q + i] = i < sl ? sh[i] : 0u;
+    inc[q] = sw.inc;
+    slen[q] = sw.slen;
+    for (int i = 0; i < 3; ++i) succ[3 * q + i] = i < sw.slen ? sw.succ[i] : 0u;
   }
 }
 
@@ -1324,21 +1560,12 @@ cudaError_t set_smem_limit(int nthreads, int64_t bytes) {
   return e;
 }
 
-cudaError_t build_ngram_table(NgRec* table, uint64_t mask, const uint32_t* words,
-                              const double* probs, const double* bos, int64_t n, int* max_probe,
-                              cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  const int bs = 256;
-  ngram_build_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(table, mask, words, probs, bos,
-                                                                   n, max_probe);
-  ++g_launches;
-  return cudaGetLastError();
-}
-
 cudaError_t pad_table(int32_t* dst, const int32_t* src, int32_t S, int32_t V, int32_t VP,
+                      const int32_t* comp_off, const int32_t* comp_surf, const int32_t* comp_lm,
                       cudaStream_t st) {
   const int64_t n = (int64_t)S * VP;
-  pad_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dst, src, S, V, VP);
+  pad_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dst, src, S, V, VP, comp_off,
+                                                                comp_surf, comp_lm);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -73,7 +73,8 @@ class DeviceModel:
             tab.space_id, N.ptr(tab.comp_off), N.ptr(tab.comp_surface), N.ptr(tab.comp_lmword),
             len(tab.comp_surface), tab.surface_blob, N.ptr(soff), len(tab.surfaces))
         nd = N.LbNgramDesc(model.order, len(ng.probs), N.ptr(ng.words), N.ptr(ng.probs),
-                           N.ptr(ng.backoffs), ng.bos_id, ng.eos_eff)
+                           N.ptr(ng.backoffs), ng.bos_id, ng.eos_eff,
+                           float(model.backoffs.get(("<s>",), 0.0)))
         handle = C.c_void_p()
         N.check(lib.lb_model_create(C.byref(td), C.byref(nd), device, C.byref(handle)))
         self.handle = handle
@@ -158,6 +159,11 @@ class DeviceBatch:
         self.h = h
         self.n = 0
         self.frames = np.zeros(0, dtype=np.int32)
+
+    def layout(self) -> dict:
+        sm, gs, nt = C.c_int64(), C.c_int64(), C.c_int32()
+        N.check(N.lib().lb_batch_layout(self.h, C.byref(sm), C.byref(gs), C.byref(nt)))
+        return {"smem_bytes": sm.value, "gscratch_bytes": gs.value, "threads": nt.value}
 
     def destroy(self):
         if getattr(self, "h", None):
@@ -253,6 +259,17 @@ class DeviceBatch:
 
     def clear_stats(self):
         N.check(N.lib().lb_batch_clear_stats(self.h))
+
+    PHASES = ("unused", "cand_hist", "collect", "sort", "materialise", "ngram", "recomb_rank",
+              "recomb_keep", "scatter", "loop_tail", "fusion", "spare")
+
+    def enable_phase_timing(self, on: bool = True):
+        N.check(N.lib().lb_batch_enable_phase_timing(self.h, int(on)))
+
+    def phase_cycles(self) -> dict:
+        out = np.zeros(12, dtype=np.uint64)
+        N.check(N.lib().lb_batch_phase_cycles(self.h, N.ptr(out)))
+        return {name: int(v) for name, v in zip(self.PHASES, out)}
 
     def enable_dump(self, on: bool = True):
         N.check(N.lib().lb_batch_enable_dump(self.h, int(on)))
