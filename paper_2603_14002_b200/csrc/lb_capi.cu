@@ -244,7 +244,7 @@ void plan_layout(lb_batch* b) {
   int nt = lbk::max_threads_for((int)K);
   if (const char* env = std::getenv("LB_THREADS")) {
     const int v = std::atoi(env);
-    if (v == 256 || v == 512 || v == 1024) nt = v;
+    if (v == 256 || v == 512 || v == 960) nt = v;
   }
   const int64_t lcap = std::max<int64_t>(2 * K, K + 256);
   int64_t sz[N_REGIONS] = {};
@@ -349,7 +349,7 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
   b->Tmax = max_frames;
   b->K = cfg->beam_size;
   b->O = cfg->ortho_beams;
-  b->VPD = (int32_t)round_up(m->dev.V, 2);
+  b->VPD = (int32_t)round_up(m->dev.V + 1, 2);  // slot V: row maximum
   fill_cfg(b);
   plan_layout(b);
   CK(lbk::set_smem_limit(b->L.nthreads, b->L.smem_bytes));
@@ -444,6 +444,7 @@ int lb_batch_set_logprobs(lb_batch* b, int32_t n, const double* x, const int32_t
   CK(cudaMemcpy2DAsync(b->d_D, b->VPD * sizeof(double), x, V * sizeof(double), V * sizeof(double),
                        (size_t)n * b->Tmax,
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, b->st));
+  CK(lbk::rowmax(b->d_D, (int64_t)n * b->Tmax, V, b->VPD, b->st));
   return LB_OK;
 }
 

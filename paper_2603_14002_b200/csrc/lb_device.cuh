@@ -114,7 +114,7 @@ struct BatchDev {
   // optional per-phase cycle counters of the frames kernel: [B][NPHASE] (thread 0, clock64)
   unsigned long long* phase_cycles;
 };
-constexpr int NPHASE = 12;
+constexpr int NPHASE = 16;
 
 // Byte layout of the per-CTA working set; each region lives in shared memory or, when the
 // beam is too wide for 227 KB, in the trial's global scratch (generic pointers either way).
@@ -141,7 +141,7 @@ struct Layout {
   int64_t gscratch_bytes;
   int32_t lcap;        // candidate list capacity
   int32_t stage_rows;  // rows staged through shared memory
-  int32_t nthreads;
+  int32_t nthreads;    // compute threads (the kernel adds two speculative n-gram warps)
   int32_t pcap;        // n-gram (entry, surface) pair capacity of one flattened round
   int32_t tslots;      // recombination hash-table slots (power of two >= 2k)
 };

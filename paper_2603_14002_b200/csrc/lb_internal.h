@@ -14,6 +14,7 @@ cudaError_t pad_table(int32_t* dst, const int32_t* src, int32_t S, int32_t V, in
                       cudaStream_t st);
 cudaError_t log_softmax(const float* x, int64_t rows, int32_t V, int32_t in_pitch,
                         double alpha, double* out, int32_t out_pitch, cudaStream_t st);
+cudaError_t rowmax(double* d, int64_t rows, int32_t V, int32_t pitch, cudaStream_t st);
 cudaError_t reset(const lbd::ModelDev& m, const lbd::BatchDev& b, cudaStream_t st);
 cudaError_t frames(const lbd::ModelDev& m, const lbd::CfgDev& c, const lbd::BatchDev& b,
                    const lbd::Layout& L, int t0, int t1, int fusion_mode, double scale,

@@ -379,21 +379,36 @@ constexpr int ENT_U4 = sizeof(Ent) / 16;
 // =====================================================================================
 // K2: persistent frame loop
 // =====================================================================================
-template <int NT>
-__global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDev m, CfgDev c,
-                                                                       BatchDev b, Layout L,
-                                                                       int t0, int t1,
-                                                                       int fusion_mode,
-                                                                       double scale) {
-  constexpr int NW = NT / 32;
+// Named barriers: 0 = whole CTA, 1 = compute warps, 2 = n-gram -> compute hand-off,
+// 3 = n-gram warps.
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+constexpr int NGT = 64;  // threads of the speculative n-gram warps
+
+// K2: the frame loop.  NC compute threads (8+ warps) run the search; NGT extra threads (two
+// warps) evaluate, for every parent that can emit a word boundary this frame, all its
+// (entry, surface) score_word lookups speculatively while the compute warps select the top-k,
+// so the n-gram memory latency is off the critical path.
+template <int NC, bool SMEM_ONLY>
+__global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
+    frames_kernel(ModelDev m, CfgDev c, BatchDev b, Layout L, int t0, int t1, int fusion_mode,
+                  double scale) {
+  constexpr int NT = NC + NGT;
+  constexpr int NWC = NC / 32;
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t dbar[2];
   __shared__ unsigned hist[NBINS];
-  __shared__ double wmax[NW];
-  __shared__ int s_cnt, s_ncount, s_fail;
-  __shared__ unsigned long long s_pack;  // (boundary beams << 32) | (n-gram pairs)
-  __shared__ int hcum[NBINS];            // exclusive prefix of hist (identical in every warp)
-  __shared__ int hfill[NBINS];           // counting-sort fill pointers
+  __shared__ int hcum[NBINS];   // exclusive prefix of hist (identical in every warp)
+  __shared__ int hfill[NBINS];  // counting-sort fill pointers
+  __shared__ double wmax[NWC];
+  __shared__ double s_maxs;     // max beam score entering the frame
+  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP;
+  __shared__ int ngtot[2];
   __shared__ unsigned s_calls, s_probes;
 
   const int trial = blockIdx.x;
@@ -404,7 +419,10 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
   if (tb >= te) return;
 
   char* gs = b.gscratch + (int64_t)trial * b.gscratch_stride;
-  auto R = [&](int r) -> char* { return L.in_smem[r] ? smem + L.off[r] : gs + L.off[r]; };
+  auto R = [&](int r) -> char* {
+    if (SMEM_ONLY) return smem + L.off[r];
+    return L.in_smem[r] ? smem + L.off[r] : gs + L.off[r];
+  };
   double* dbuf = reinterpret_cast<double*>(R(R_DBUF));
   int32_t* rows = reinterpret_cast<int32_t*>(R(R_ROWS));
   BeamPtrs cur{(double*)R(R_CUR_SCORE), (uint64_t*)R(R_CUR_H1), (uint64_t*)R(R_CUR_H2),
@@ -429,17 +447,20 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
   Ent* bents = reinterpret_cast<Ent*>(R(R_BENTS));
   int32_t* bnent = reinterpret_cast<int32_t*>(R(R_BNENT));
   uint32_t* keep = reinterpret_cast<uint32_t*>(R(R_KEEP));
-  WarpScratch* wsc = reinterpret_cast<WarpScratch*>(R(R_WARP));
-  int32_t* poff = reinterpret_cast<int32_t*>(R(R_POFF));     // [K+1] pair offsets
+  WarpScratch* wsc = reinterpret_cast<WarpScratch*>(gs + L.off[R_WARP]);  // always global
+  int32_t* ppoff = reinterpret_cast<int32_t*>(R(R_POFF));    // [K+1] per-parent pair offsets
   PairRes* pres = reinterpret_cast<PairRes*>(R(R_PAIRS));    // [pcap]
-  int32_t* slotb = reinterpret_cast<int32_t*>(R(R_SLOTB));   // [tslots] beam claiming a slot
-  int32_t* slotm = reinterpret_cast<int32_t*>(R(R_SLOTM));   // [tslots] min rank in the group
+  int32_t* slotb = reinterpret_cast<int32_t*>(R(R_SLOTB));   // [tslots]
+  int32_t* slotm = reinterpret_cast<int32_t*>(R(R_SLOTM));   // [tslots]
   int32_t* myslot = reinterpret_cast<int32_t*>(R(R_MYSLOT)); // [K]
 
   const int V = m.V, VP = m.VP, VPD = b.VPD, O = c.O, KC = b.K;
-  const FrameConsts fc{c.beta, c.gamma, m.blank, m.space};
   const int nkw = (c.k + 31) >> 5;
   const int TS = L.tslots;
+  const float invV = 1.0f / (float)V;
+  // exact `beta * mask` / `gamma * mask` of decoder.py:254-256 as selects (x*1.0 == x)
+  const double b_on = c.beta, b_off = xmul(c.beta, 0.0);
+  const double g_on = c.gamma, g_off = xmul(c.gamma, 0.0);
 
   // ---- load the home beam state and gather the first frame's lexicon rows
   int K = b.nbeam[trial];
@@ -469,13 +490,22 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
   if (tid == 0) {
     s_ncount = b.ncount[trial];
     s_fail = 0;
+    s_status = 0;
     s_calls = 0;
     s_probes = 0;
+    s_K = K;
     mbar_init(&dbar[0], 1);
     mbar_init(&dbar[1], 1);
     fence_mbar_init();
   }
   if (L.stage_rows) cp_async_wait_all();
+  __syncthreads();
+  if (warp == 0) {  // max beam score entering the first frame (home state is not sorted)
+    double ms = -DBL_MAX;
+    for (int i = lane; i < K; i += 32) ms = fmax(ms, cur.score[i]);
+    ms = warp_max(ms);
+    if (lane == 0) s_maxs = ms;
+  }
   __syncthreads();
 
   const double* Dtrial = b.D + (size_t)trial * b.Tmax * VPD;
@@ -492,8 +522,7 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
 
   unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
   unsigned calls_l = 0, probes_l = 0;
-  int status = 0, fail_t = -1;
-  // phase timing (thread 0 only, when b.phase_cycles is set)
+  int fail_t = -1;
   const bool timing = b.phase_cycles != nullptr && tid == 0;
   unsigned long long ph[NPHASE];
   for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
@@ -504,323 +533,63 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
     ph[i] += (unsigned long long)(tnow - tprev);   \
     tprev = tnow;                                  \
   }
+  auto rowp = [&](int p) -> const int32_t* {
+    return L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
+  };
 
   for (int t = tb; t < te; ++t) {
     const int rel = t - tb;
     const int ci = rel / CHUNK;
     const int cr = rel - ci * CHUNK;
-    if (cr == 0) {
-      mbar_wait(&dbar[ci & 1], (unsigned)((ci >> 1) & 1));
-      if (tid == 0) issue_chunk(ci + 1);
-    }
-    const double* drow = dbuf + ((size_t)(ci & 1) * CHUNK + cr) * VPD;
     st_beams_in += K;
     const int KV = K * V;
 
-    // ---- A: candidate values (decoder.py:252-260) + histogram, one pass.  Bins are anchored
-    // at U = max s + max D + bonuses (>= every candidate up to rounding), so the pass does not
-    // need the true maximum; bins are monotone in the value (clamped floor of (U - x) * inv).
-    double U;
-    {
-      double ms = -DBL_MAX, md = -DBL_MAX;
-      for (int i = lane; i < K; i += 32) ms = fmax(ms, cur.score[i]);
-      for (int v = lane; v < V; v += 32) md = fmax(md, drow[v]);
-      ms = warp_max(ms);
-      md = warp_max(md);
-      U = __dadd_ru(__dadd_ru(ms, md), c.bonus_up);
-    }
-    double wm = -DBL_MAX;
-#pragma unroll 2
-    for (int p = warp; p < K; p += NW) {
-      const int lp = cur.last[p];
-      const double s = cur.score[p];
-      const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
-      for (int v = lane; v < V; v += 32) {
-        const int nx = row[v];
-        double x = -DBL_MAX;
-        uint16_t bin = 0xFFFF;
-        if ((nx != m.sink) || (v == m.blank) || (v == lp)) {
-          x = cand_value(s, drow[v], v, lp, fc);
-          if (x > GUARD) {
-            const double fb = fmin(fmax(xmul(xsub(U, x), c.inv_binw), 0.0), (double)(NBINS - 1));
-            bin = (uint16_t)(int)fb;
-            atomicAdd(&hist[bin], 1u);
-          } else {
-            x = -DBL_MAX;
-          }
+    if (warp >= NWC) {
+      // ============ speculative n-gram warps (decoder.py:293-295 / 182-235 lookups) ============
+      const int gt = tid - NC, ngw = warp - NWC;
+      int carry = 0;
+      for (int base = 0; base < K; base += NGT) {
+        const int p = base + gt;
+        int np = 0;
+        if (p < K) {
+          const int32_t* row = rowp(p);
+          if (row[V] > 0 && cur.last[p] != m.space) np = cur.nent[p] * row[V];
         }
-        cbin[p * V + v] = bin;
-        wm = fmax(wm, x);
-      }
-    }
-    wm = warp_max(wm);
-    if (lane == 0) wmax[warp] = wm;
-    if (tid == 0) {
-      s_cnt = 0;
-      s_pack = 0ull;
-    }
-    for (int i = tid; i < nkw; i += NT) keep[i] = 0;
-    for (int i = tid; i < TS; i += NT) {
-      slotb[i] = -1;
-      slotm[i] = 0x7FFFFFFF;
-    }
-    __syncthreads();  // S1
-    LB_PHASE(1);
-
-    double M = -DBL_MAX;
-    for (int w = 0; w < NW; ++w) M = fmax(M, wmax[w]);
-    if (!(M > GUARD)) {  // decoder.py:267-268
-      status = 1;
-      fail_t = t;
-      break;
-    }
-    const double thr = xsub(M, c.theta);
-    const int bthr = (int)fmin(fmax(xmul(xsub(U, thr), c.inv_binw), 0.0), (double)(NBINS - 1));
-
-    // ---- C: every warp scans the histogram (no extra barrier): first bin reaching k.  Each
-    // warp also writes the exclusive prefix hcum[] (identical values from every warp).
-    int bstar = NBINS;
-    int cum_thr = 0;  // candidates in bins <= bthr (upper bound of the exact-filter set)
-    int cum_bstar = 0;
-    {
-      constexpr int PB = NBINS / 32;
-      int part[PB];
-      int ls = 0;
-#pragma unroll
-      for (int i = 0; i < PB; ++i) {
-        part[i] = (int)hist[lane * PB + i];
-        ls += part[i];
-      }
-      int incl = ls;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULLMASK, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - ls;
-      {
-        int run = excl;
-#pragma unroll
-        for (int i = 0; i < PB; ++i) {
-          hcum[lane * PB + i] = run;
-          run += part[i];
+        int incl = np;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULLMASK, incl, o);
+          if (lane >= o) incl += y;
         }
+        if (lane == 31) ngtot[ngw] = incl;
+        bar_sync(3, NGT);
+        const int woff = ngw ? ngtot[0] : 0;
+        const int tot = ngtot[0] + ngtot[1];
+        if (p < K) ppoff[p] = carry + woff + incl - np;
+        carry += tot;
+        bar_sync(3, NGT);
       }
-      __syncwarp();
-      cum_thr = hcum[bthr] + (int)hist[bthr];
-      const bool here = excl < c.k && incl >= c.k;
-      const unsigned bl = __ballot_sync(FULLMASK, here);
-      if (bl) {
-        const int src = __ffs(bl) - 1;
-        int lb = 0;
-        if (lane == src) {
-          int cum = excl;
-#pragma unroll
-          for (int i = 0; i < PB; ++i) {
-            if (cum + part[i] >= c.k) {
-              lb = i;
-              break;
-            }
-            cum += part[i];
-          }
-        }
-        lb = __shfl_sync(FULLMASK, lb, src);
-        bstar = src * PB + lb;
-        cum_bstar = hcum[bstar] + (int)hist[bstar];
+      if (gt == 0) {
+        ppoff[K] = carry;
+        s_ngP = carry;
       }
-    }
-    // bins < bthr hold only in-range (x >= thr) candidates; bin bthr is mixed
-    const bool sure = bstar < bthr;
-    const int take_bin = sure ? bstar : bthr;
-    const int bound = sure ? cum_bstar : cum_thr;
-    int nsel = 0, m_sel = L.lcap + 1;
-    if (bound <= L.lcap) {
-      // ---- D: collect = counting sort by bin (bins are strictly ordered by value)
-      for (int f = tid; f < KV; f += NT) {
-        const int bn = cbin[f];
-        if (bn <= take_bin) {
-          const int p = f / V, v = f - (f / V) * V;
-          const double x = cand_value(cur.score[p], drow[v], v, cur.last[p], fc);
-          if (sure || x >= thr) {
-            const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
-            cval[pos] = x;
-            ckey[pos] = (uint32_t)f;
-          }
-        }
-      }
-      __syncthreads();  // S2
-      m_sel = hcum[take_bin] + hfill[take_bin];
-      nsel = min(c.k, m_sel);
-      LB_PHASE(2);
-      // ---- E: exact order inside each bin (value desc, flat index asc); bins are disjoint
-      // value ranges, so an element's rank is hcum[bin] + the bin-mates that beat it
-      for (int a = tid; a < m_sel; a += NT) {
-        const double va = cval[a];
-        const uint32_t ka = ckey[a];
-        const int bn = cbin[ka];
-        const int lo = hcum[bn], n = hfill[bn];
-        int r = lo;
-        for (int q = lo; q < lo + n; ++q) {
-          const double vq = cval[q];
-          r += (vq > va) || (vq == va && ckey[q] < ka);
-        }
-        if (r < nsel) {
-          sval[r] = va;
-          skey[r] = ka;
-        }
-      }
-    } else {
-      // ---- fallback: exact radix select on the 96-bit key (ord64(value), ~flat index)
-      ++st_fallback;
-      __syncthreads();
-      if (tid == 0) s_cnt = 0;
-      // exact in-range count
-      for (int i = tid; i < NBINS; i += NT) hist[i] = 0;
-      __syncthreads();
-      auto cval_at = [&](int f) -> double {
-        if (cbin[f] == 0xFFFF) return -DBL_MAX;
-        const int p = f / V, v = f - (f / V) * V;
-        return cand_value(cur.score[p], drow[v], v, cur.last[p], fc);
-      };
-      for (int f = tid; f < KV; f += NT)
-        if (cval_at(f) >= thr) atomicAdd(&hist[0], 1u);
-      __syncthreads();
-      nsel = min(c.k, (int)hist[0]);
-      uint64_t phi = 0, pmask_hi = 0;
-      uint32_t plo = 0, pmask_lo = 0;
-      int rem = nsel;
-      for (int pass = 0; pass < 12; ++pass) {
-        __syncthreads();
-        for (int i = tid; i < NBINS; i += NT) hist[i] = 0;
-        __syncthreads();
-        for (int f = tid; f < KV; f += NT) {
-          const double x = cval_at(f);
-          if (!(x >= thr)) continue;
-          const uint64_t kh = ord64(x);
-          const uint32_t kl = ~(uint32_t)f;
-          if ((kh & pmask_hi) != phi || (kl & pmask_lo) != plo) continue;
-          const unsigned dg = pass < 8 ? (unsigned)((kh >> (56 - 8 * pass)) & 0xFF)
-                                       : (unsigned)((kl >> (24 - 8 * (pass - 8))) & 0xFF);
-          atomicAdd(&hist[dg], 1u);
-        }
-        __syncthreads();
-        int above = 0, dsel = 0;
-        for (int d = NBINS - 1; d >= 0; --d) {
-          const int h = (int)hist[d];
-          if (above + h >= rem) {
-            dsel = d;
-            break;
-          }
-          above += h;
-        }
-        rem -= above;
-        if (pass < 8) {
-          phi |= (uint64_t)dsel << (56 - 8 * pass);
-          pmask_hi |= 0xFFull << (56 - 8 * pass);
-        } else {
-          plo |= (uint32_t)dsel << (24 - 8 * (pass - 8));
-          pmask_lo |= 0xFFu << (24 - 8 * (pass - 8));
-        }
-      }
-      __syncthreads();
-      for (int f0 = 0; f0 < KV; f0 += NT) {
-        const int f = f0 + tid;
-        bool take = false;
-        double x = 0.0;
-        if (f < KV) {
-          x = cval_at(f);
-          if (x >= thr) {
-            const uint64_t kh = ord64(x);
-            const uint32_t kl = ~(uint32_t)f;
-            take = kh > phi || (kh == phi && kl >= plo);
-          }
-        }
-        const unsigned bl = __ballot_sync(FULLMASK, take);
-        if (bl) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&s_cnt, __popc(bl));
-          base = __shfl_sync(FULLMASK, base, 0);
-          if (take) {
-            const int pos = base + __popc(bl & ((1u << lane) - 1u));
-            cval[pos] = x;
-            ckey[pos] = (uint32_t)f;
-          }
-        }
-      }
-      __syncthreads();
-      for (int i = tid; i < nsel; i += NT) {
-        const double vi = cval[i];
-        const uint32_t ki = ckey[i];
-        int cnt = 0;
-        for (int j = 0; j < nsel; ++j) {
-          const double vj = cval[j];
-          cnt += (vj > vi) || (vj == vi && ckey[j] < ki);
-        }
-        sval[cnt] = vi;
-        skey[cnt] = ki;
-      }
-    }
-    __syncthreads();  // S3
-    LB_PHASE(3);
-
-    // ---- F: materialise survivors in selection order (decoder.py:272-291)
-    for (int j = tid; j < nsel; j += NT) {
-      const double x = sval[j];
-      const uint32_t f = skey[j];
-      const int p = (int)(f / (uint32_t)V);
-      const int tok = (int)(f - (uint32_t)p * V);
-      const int lp = cur.last[p], pp = cur.pre[p];
-      const bool emit = (tok != m.blank) && (tok != lp);
-      uint64_t a1 = cur.h1[p], a2 = cur.h2[p];
-      int np = pp;
-      if (emit) {
-        a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
-        a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
-        np = L.stage_rows ? rows[p * VP + tok] : m.table[(size_t)pp * VP + tok];
-      }
-      nscore[j] = x;
-      nh1[j] = a1;
-      nh2[j] = a2;
-      nlast[j] = (tok == m.blank) ? lp : tok;
-      npre[j] = np;
-      npar[j] = p;
-      bnent[j] = -1;
-      if (emit && tok == m.space) {
-        // boundary beam: reserve its slot and its (entry, surface) pair range in one atomic
-        const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)pp * VP;
-        const unsigned np2 = (unsigned)(cur.nent[p] * row[V]);
-        const unsigned long long old = atomicAdd(&s_pack, (1ull << 32) | np2);
-        const int bi = (int)(old >> 32);
-        blist[bi] = j;
-        poff[bi] = (int)(old & 0xFFFFFFFFull);
-      }
-    }
-    __syncthreads();  // S4
-    LB_PHASE(4);
-
-    // ---- G: n-gram fusion for new word-boundary emissions (decoder.py:293-295)
-    const int nb = (int)(s_pack >> 32);
-    st_bound += nb;
-    if (nb > 0) {
-      const int P = (int)(s_pack & 0xFFFFFFFFull);
+      const int P = carry;
       if (P <= L.pcap) {
-        // G2: one 8-lane group per (beam, entry, surface) pair: parallel score_word probes
-        constexpr int NG = NT / 8;
-        const int grp = tid >> 3, sub = lane & 7;
+        constexpr int NG = NGT / 8;
+        const int grp = gt >> 3, sub = lane & 7;
         for (int q0 = 0; q0 < P; q0 += NG) {
           const int q = q0 + grp;
           const bool act = q < P;
           int w = -1, surf = -1, p = 0, e = 0;
           if (act) {
-            int lo = 0, hi = nb - 1;  // last bi with poff[bi] <= q
+            int lo = 0, hi = K - 1;  // last parent with ppoff[p] <= q
             while (lo < hi) {
               const int mid = (lo + hi + 1) >> 1;
-              if (poff[mid] <= q) lo = mid;
+              if (ppoff[mid] <= q) lo = mid;
               else hi = mid - 1;
             }
-            p = npar[blist[lo]];
-            const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
-            const CompHdr ch = comp_hdr(row, V);
-            const int local = q - poff[lo];
+            p = lo;
+            const CompHdr ch = comp_hdr(rowp(p), V);
+            const int local = q - ppoff[p];
             e = local / ch.ns;
             const int sidx = local - e * ch.ns;
             if (sidx == 0) {
@@ -847,92 +616,370 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
             pr.cum = xadd(E.cum, sw.inc);
             pr.node = E.node;
             pr.surf = (uint32_t)surf;
-            for (int t = 0; t < MAXH; ++t) {
-              pr.h[t] = sw.succ[t];
-              pr.bo[t] = sw.sbo[t];
+            for (int tt = 0; tt < MAXH; ++tt) {
+              pr.h[tt] = sw.succ[tt];
+              pr.bo[tt] = sw.sbo[tt];
             }
             pr.depth = (uint16_t)(E.depth + 1);
             pr.hlen = (uint8_t)sw.slen;
             pres[q] = pr;
           }
         }
-        __syncthreads();
-        // G3: thread per boundary beam: top-O by (-total, seq), lambda filter, new entries
-        for (int bi = tid; bi < nb; bi += NT) {
-          const int j = blist[bi];
-          const int p = npar[j];
-          const int q0 = poff[bi], q1 = bi + 1 < nb ? poff[bi + 1] : P;
-          int top[OMAX];
-          int ntop = 0;
-          for (int q = q0; q < q1; ++q) {
-            if (!pres[q].valid) continue;
-            const double tq = pres[q].total;
-            int pos = ntop;
-            for (int i = 0; i < ntop; ++i)
-              if (tq > pres[top[i]].total) {
-                pos = i;
+      }
+      bar_arrive(2, NT);
+    } else {
+      // ======================================= compute warps =======================================
+      if (cr == 0) {
+        mbar_wait(&dbar[ci & 1], (unsigned)((ci >> 1) & 1));
+        if (tid == 0) issue_chunk(ci + 1);
+      }
+      const double* drow = dbuf + ((size_t)(ci & 1) * CHUNK + cr) * VPD;
+      // U >= every candidate (rounding up each step of (s + d) + beta + gamma)
+      const double U = __dadd_ru(__dadd_ru(__dadd_ru(s_maxs, drow[V]), fmax(c.beta, 0.0)),
+                                 fmax(c.gamma, 0.0));
+      LB_PHASE(0);
+
+      // ---- A: candidate values (decoder.py:252-260) + histogram over bins anchored at U
+      double wm = -DBL_MAX;
+      for (int f = tid; f < KV; f += NC) {
+        const int p = (int)(((float)f + 0.5f) * invV);
+        const int v = f - p * V;
+        const int lp = cur.last[p];
+        const int nx = rowp(p)[v];
+        uint16_t bin = 0xFFFF;
+        if ((nx != m.sink) || (v == m.blank) || (v == lp)) {
+          double x = xadd(cur.score[p], drow[v]);
+          const bool ph2 = (v != m.blank) & (v != m.space);
+          x = xadd(x, (ph2 && v != lp) ? b_on : b_off);
+          if (v == m.space) x = xadd(x, lp != m.space ? g_on : g_off);
+          if (x > GUARD) {
+            const double fb = fmin(fmax(xmul(xsub(U, x), c.inv_binw), 0.0), (double)(NBINS - 1));
+            bin = (uint16_t)(int)fb;
+            atomicAdd(&hist[bin], 1u);
+            wm = fmax(wm, x);
+          }
+        }
+        cbin[f] = bin;
+      }
+      wm = warp_max(wm);
+      LB_PHASE(11);
+      if (lane == 0) wmax[warp] = wm;
+      if (tid == 0) s_nb = 0;
+      for (int i = tid; i < nkw; i += NC) keep[i] = 0;
+      for (int i = tid; i < TS; i += NC) {
+        slotb[i] = -1;
+        slotm[i] = 0x7FFFFFFF;
+      }
+      bar_sync(1, NC);  // S1
+      LB_PHASE(1);
+
+      double M = -DBL_MAX;
+      for (int w = 0; w < NWC; ++w) M = fmax(M, wmax[w]);
+      int nsel = 0;
+      bool dead = !(M > GUARD);  // decoder.py:267-268
+      if (dead) {
+        if (tid == 0) {
+          s_status = 1;
+          s_K = 0;
+        }
+        fail_t = t;
+      } else {
+        const double thr = xsub(M, c.theta);
+        const int bthr =
+            (int)fmin(fmax(xmul(xsub(U, thr), c.inv_binw), 0.0), (double)(NBINS - 1));
+        // ---- C: every warp scans the histogram; hcum[] written identically by all warps
+        int bstar = NBINS, cum_thr = 0, cum_bstar = 0;
+        {
+          constexpr int PB = NBINS / 32;
+          int part[PB];
+          int ls = 0;
+#pragma unroll
+          for (int i = 0; i < PB; ++i) {
+            part[i] = (int)hist[lane * PB + i];
+            ls += part[i];
+          }
+          int incl = ls;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int excl = incl - ls;
+          {
+            int run = excl;
+#pragma unroll
+            for (int i = 0; i < PB; ++i) {
+              hcum[lane * PB + i] = run;
+              run += part[i];
+            }
+          }
+          __syncwarp();
+          cum_thr = hcum[bthr] + (int)hist[bthr];
+          const bool here = excl < c.k && incl >= c.k;
+          const unsigned bl = __ballot_sync(FULLMASK, here);
+          if (bl) {
+            const int src = __ffs(bl) - 1;
+            int lb = 0;
+            if (lane == src) {
+              int cum = excl;
+#pragma unroll
+              for (int i = 0; i < PB; ++i) {
+                if (cum + part[i] >= c.k) {
+                  lb = i;
+                  break;
+                }
+                cum += part[i];
+              }
+            }
+            lb = __shfl_sync(FULLMASK, lb, src);
+            bstar = src * PB + lb;
+            cum_bstar = hcum[bstar] + (int)hist[bstar];
+          }
+        }
+        const bool sure = bstar < bthr;  // bins < bthr are entirely >= thr
+        const int take_bin = sure ? bstar : bthr;
+        const int bound = sure ? cum_bstar : cum_thr;
+        if (bound <= L.lcap) {
+          // ---- D: collect = counting sort by bin (bins are strictly ordered by value)
+          for (int f = tid; f < KV; f += NC) {
+            const int bn = cbin[f];
+            if (bn <= take_bin) {
+              const int p = (int)(((float)f + 0.5f) * invV);
+              const int v = f - p * V;
+              const double x = cand_value(cur.score[p], drow[v], v, cur.last[p],
+                                          FrameConsts{c.beta, c.gamma, m.blank, m.space});
+              if (sure || x >= thr) {
+                const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
+                cval[pos] = x;
+                ckey[pos] = (uint32_t)f;
+              }
+            }
+          }
+          bar_sync(1, NC);  // S2
+          const int m_sel = hcum[take_bin] + hfill[take_bin];
+          nsel = min(c.k, m_sel);
+          LB_PHASE(2);
+          // ---- E: exact order inside each bin (value desc, flat index asc)
+          for (int a = tid; a < m_sel; a += NC) {
+            const double va = cval[a];
+            const uint32_t ka = ckey[a];
+            const int bn = cbin[ka];
+            const int lo = hcum[bn], n = hfill[bn];
+            int r = lo;
+            for (int q = lo; q < lo + n; ++q) {
+              const double vq = cval[q];
+              r += (vq > va) || (vq == va && ckey[q] < ka);
+            }
+            if (r < nsel) {
+              sval[r] = va;
+              skey[r] = ka;
+            }
+          }
+        } else {
+          // ---- fallback: exact radix select on the 96-bit key (ord64(value), ~flat index)
+          ++st_fallback;
+          auto cval_at = [&](int f) -> double {
+            if (cbin[f] == 0xFFFF) return -DBL_MAX;
+            const int p = (int)(((float)f + 0.5f) * invV);
+            const int v = f - p * V;
+            return cand_value(cur.score[p], drow[v], v, cur.last[p],
+                              FrameConsts{c.beta, c.gamma, m.blank, m.space});
+          };
+          __shared__ int s_cnt2, s_inr;
+          bar_sync(1, NC);
+          if (tid == 0) {
+            s_cnt2 = 0;
+            s_inr = 0;
+          }
+          bar_sync(1, NC);
+          for (int f = tid; f < KV; f += NC)
+            if (cval_at(f) >= thr) atomicAdd(&s_inr, 1);
+          bar_sync(1, NC);
+          nsel = min(c.k, s_inr);
+          uint64_t phi = 0, pmask_hi = 0;
+          uint32_t plo = 0, pmask_lo = 0;
+          int rem = nsel;
+          for (int pass = 0; pass < 12; ++pass) {
+            bar_sync(1, NC);
+            for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
+            bar_sync(1, NC);
+            for (int f = tid; f < KV; f += NC) {
+              const double x = cval_at(f);
+              if (!(x >= thr)) continue;
+              const uint64_t kh = ord64(x);
+              const uint32_t kl = ~(uint32_t)f;
+              if ((kh & pmask_hi) != phi || (kl & pmask_lo) != plo) continue;
+              const unsigned dg = pass < 8 ? (unsigned)((kh >> (56 - 8 * pass)) & 0xFF)
+                                           : (unsigned)((kl >> (24 - 8 * (pass - 8))) & 0xFF);
+              atomicAdd(&hist[dg], 1u);
+            }
+            bar_sync(1, NC);
+            int above = 0, dsel = 0;
+            for (int d = NBINS - 1; d >= 0; --d) {
+              const int h = (int)hist[d];
+              if (above + h >= rem) {
+                dsel = d;
                 break;
               }
-            if (pos >= O) continue;
-            for (int i = min(ntop, O - 1); i > pos; --i) top[i] = top[i - 1];
-            top[pos] = q;
-            ntop = min(ntop + 1, O);
-          }
-          if (ntop == 0) {
-            nscore[j] = NEG_INF;  // decoder.py:223-225
-            bnent[j] = -1;
-            continue;
-          }
-          const double best = pres[top[0]].total;
-          const double floor_ = xsub(best, c.lambda);
-          int kept = 0;
-          while (kept < ntop && pres[top[kept]].total >= floor_) ++kept;
-          const int base = atomicAdd(&s_ncount, kept);
-          if (base + kept > b.ncap) {
-            s_fail = 1;
-            nscore[j] = NEG_INF;
-            bnent[j] = -1;
-            continue;
-          }
-          const size_t nbase = (size_t)trial * b.ncap;
-          Ent* out = bents + (size_t)j * O;
-          for (int i = 0; i < kept; ++i) {
-            const PairRes& pr = pres[top[i]];
-            const uint32_t node = (uint32_t)(base + i);
-            b.nparent[nbase + node] = pr.node;
-            b.nsurf[nbase + node] = pr.surf;
-            WordScore sw;
-            sw.slen = pr.hlen;
-            for (int t = 0; t < MAXH; ++t) {
-              sw.succ[t] = pr.h[t];
-              sw.sbo[t] = pr.bo[t];
+              above += h;
             }
-            new_entry(out[i], pr.total, pr.cum, sw, node, (uint32_t)(top[i] - q0), pr.depth);
+            rem -= above;
+            if (pass < 8) {
+              phi |= (uint64_t)dsel << (56 - 8 * pass);
+              pmask_hi |= 0xFFull << (56 - 8 * pass);
+            } else {
+              plo |= (uint32_t)dsel << (24 - 8 * (pass - 8));
+              pmask_lo |= 0xFFu << (24 - 8 * (pass - 8));
+            }
           }
-          bnent[j] = kept;
-          nscore[j] = xadd(nscore[j], xsub(best, cur.ents[(size_t)p * O].total));
-        }
-      } else {
-        // rare: more pairs than one flattened round holds -> one warp per boundary beam
-        for (int bi = warp; bi < nb; bi += NW) {
-          const int j = blist[bi];
-          const int p = npar[j];
-          const int32_t* row = L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
-          int outn = -1;
-          double sc = nscore[j];
-          warp_apply_ngram(m, c, b, trial, cur.ents + (size_t)p * O, cur.nent[p],
-                           comp_hdr(row, V), &wsc[warp], bents + (size_t)j * O, &outn, &sc,
-                           &s_ncount, &s_fail, calls_l, probes_l);
-          if (lane == 0) {
-            nscore[j] = sc;
-            bnent[j] = outn;
+          bar_sync(1, NC);
+          for (int f0 = 0; f0 < KV; f0 += NC) {
+            const int f = f0 + tid;
+            bool take = false;
+            double x = 0.0;
+            if (f < KV) {
+              x = cval_at(f);
+              if (x >= thr) {
+                const uint64_t kh = ord64(x);
+                const uint32_t kl = ~(uint32_t)f;
+                take = kh > phi || (kh == phi && kl >= plo);
+              }
+            }
+            const unsigned bl = __ballot_sync(FULLMASK, take);
+            if (bl) {
+              int base = 0;
+              if (lane == 0) base = atomicAdd(&s_cnt2, __popc(bl));
+              base = __shfl_sync(FULLMASK, base, 0);
+              if (take) {
+                const int pos = base + __popc(bl & ((1u << lane) - 1u));
+                cval[pos] = x;
+                ckey[pos] = (uint32_t)f;
+              }
+            }
           }
+          bar_sync(1, NC);
+          for (int i = tid; i < nsel; i += NC) {
+            const double vi = cval[i];
+            const uint32_t ki = ckey[i];
+            int cnt = 0;
+            for (int j = 0; j < nsel; ++j) {
+              const double vj = cval[j];
+              cnt += (vj > vi) || (vj == vi && ckey[j] < ki);
+            }
+            sval[cnt] = vi;
+            skey[cnt] = ki;
+          }
+          for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
         }
       }
-    }
-    __syncthreads();  // S5
-    LB_PHASE(5);
+      bar_sync(2, NT);  // S3: selection done + speculative n-gram results ready
+      LB_PHASE(3);
 
+      if (!dead) {
+        const bool ngover = s_ngP > L.pcap;
+        // ---- F: materialise survivors (decoder.py:272-291); a new word-boundary emitter merges
+        // its parent's precomputed (entry, surface) pairs (decoder.py:208-235) right here
+        for (int j = tid; j < nsel; j += NC) {
+          const double x = sval[j];
+          const uint32_t f = skey[j];
+          const int p = (int)(((float)f + 0.5f) * invV);
+          const int tok = (int)f - p * V;
+          const int lp = cur.last[p], pp = cur.pre[p];
+          const bool emit = (tok != m.blank) && (tok != lp);
+          uint64_t a1 = cur.h1[p], a2 = cur.h2[p];
+          int np = pp;
+          if (emit) {
+            a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
+            a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
+            np = rowp(p)[tok];
+          }
+          double sc = x;
+          int bn = -1;
+          if (emit && tok == m.space) {
+            blist[atomicAdd(&s_nb, 1)] = j;
+            if (ngover) {
+              bn = -2;  // resolved below by the warp-per-beam path
+            } else {
+              const int q0 = ppoff[p], q1 = ppoff[p + 1];
+              int top[OMAX];
+              int ntop = 0;
+              for (int q = q0; q < q1; ++q) {
+                if (!pres[q].valid) continue;
+                const double tq = pres[q].total;
+                int pos = ntop;
+                for (int i = 0; i < ntop; ++i)
+                  if (tq > pres[top[i]].total) {
+                    pos = i;
+                    break;
+                  }
+                if (pos >= O) continue;
+                for (int i = min(ntop, O - 1); i > pos; --i) top[i] = top[i - 1];
+                top[pos] = q;
+                ntop = min(ntop + 1, O);
+              }
+              if (ntop == 0) {
+                sc = NEG_INF;  // decoder.py:223-225
+              } else {
+                const double best = pres[top[0]].total;
+                const double floor_ = xsub(best, c.lambda);
+                int kept = 0;
+                while (kept < ntop && pres[top[kept]].total >= floor_) ++kept;
+                const int base = atomicAdd(&s_ncount, kept);
+                if (base + kept > b.ncap) {
+                  s_fail = 1;
+                  sc = NEG_INF;
+                } else {
+                  const size_t nbase = (size_t)trial * b.ncap;
+                  Ent* out = bents + (size_t)j * O;
+                  for (int i = 0; i < kept; ++i) {
+                    const PairRes& pr = pres[top[i]];
+                    const uint32_t node = (uint32_t)(base + i);
+                    b.nparent[nbase + node] = pr.node;
+                    b.nsurf[nbase + node] = pr.surf;
+                    WordScore sw;
+                    sw.slen = pr.hlen;
+                    for (int tt = 0; tt < MAXH; ++tt) {
+                      sw.succ[tt] = pr.h[tt];
+                      sw.sbo[tt] = pr.bo[tt];
+                    }
+                    new_entry(out[i], pr.total, pr.cum, sw, node, (uint32_t)(top[i] - q0),
+                              pr.depth);
+                  }
+                  bn = kept;
+                  sc = xadd(x, xsub(best, cur.ents[(size_t)p * O].total));
+                }
+              }
+            }
+          }
+          nscore[j] = sc;
+          nh1[j] = a1;
+          nh2[j] = a2;
+          nlast[j] = (tok == m.blank) ? lp : tok;
+          npre[j] = np;
+          npar[j] = p;
+          bnent[j] = bn;
+        }
+        bar_sync(1, NC);  // S4
+        LB_PHASE(4);
+        const int nb = s_nb;
+        st_bound += nb;
+        if (ngover && nb > 0) {
+          // rare: more pairs than the speculative round holds -> one warp per boundary beam
+          for (int bi = warp; bi < nb; bi += NWC) {
+            const int j = blist[bi];
+            const int p = npar[j];
+            int outn = -1;
+            double sc = nscore[j];
+            warp_apply_ngram(m, c, b, trial, cur.ents + (size_t)p * O, cur.nent[p],
+                             comp_hdr(rowp(p), V), &wsc[warp], bents + (size_t)j * O, &outn, &sc,
+                             &s_ncount, &s_fail, calls_l, probes_l);
+            if (lane == 0) {
+              nscore[j] = sc;
+              bnent[j] = outn;
+            }
+          }
+          bar_sync(1, NC);
+        }
+        LB_PHASE(5);
     // ---- H1: recombination ranking by (post-fusion score desc, index asc).  Beams that did
     // not cross a word boundary keep their selection scores, which are already in that order,
     // so only the nb boundary beams need explicit comparisons.  Equal-hash groups are found
@@ -940,8 +987,8 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
     {
       const int n = nsel;
       int G = 1;
-      while (G < 32 && 2 * G * n <= NT) G <<= 1;
-      const int groups = NT / G, g = tid / G, r = tid & (G - 1);
+      while (G < 32 && 2 * G * n <= NC) G <<= 1;
+      const int groups = NC / G, g = tid / G, r = tid & (G - 1);
       for (int i0 = 0; i0 < n; i0 += groups) {
         const int i = i0 + g;
         const bool act = i < n;
@@ -983,18 +1030,18 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
         }
       }
     }
-    __syncthreads();  // S6
+    bar_sync(1, NC);  // S6
     LB_PHASE(6);
     // ---- H2: survivors = best rank of each hash group, killed beams dropped
-    for (int i = tid; i < nsel; i += NT) {
+    for (int i = tid; i < nsel; i += NC) {
       if (nscore[i] > GUARD && slotm[myslot[i]] == rankv[i])
         atomicOr(&keep[rankv[i] >> 5], 1u << (rankv[i] & 31));
     }
-    __syncthreads();  // S7
+    bar_sync(1, NC);  // S7
     LB_PHASE(7);
 
     // ---- scatter survivors into the next buffer in rank order; prefetch their lexicon rows
-    for (int i = tid; i < NBINS; i += NT) {  // scanned after S1 / filled before S2: free again
+    for (int i = tid; i < NBINS; i += NC) {  // scanned after S1 / filled before S2: free again
       hist[i] = 0;
       hfill[i] = 0;
     }
@@ -1002,8 +1049,8 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
     for (int w = 0; w < nkw; ++w) newK += __popc(keep[w]);
     {
       int G = 1;
-      while (G < 32 && 2 * G * nsel <= NT) G <<= 1;
-      const int groups = NT / G, g = tid / G, r = tid & (G - 1);
+      while (G < 32 && 2 * G * nsel <= NC) G <<= 1;
+      const int groups = NC / G, g = tid / G, r = tid & (G - 1);
       for (int i0 = 0; i0 < nsel; i0 += groups) {
         const int i = i0 + g;
         if (i >= nsel) continue;
@@ -1015,6 +1062,7 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
         const Ent* srcE = bn >= 0 ? bents + (size_t)i * O : cur.ents + (size_t)npar[i] * O;
         const int cnt = bn >= 0 ? bn : cur.nent[npar[i]];
         if (r == 0) {
+          if (pos == 0) s_maxs = nscore[i];  // survivors are sorted: rank 0 is the maximum
           nxt.score[pos] = nscore[i];
           nxt.h1[pos] = nh1[i];
           nxt.h2[pos] = nh2[i];
@@ -1044,25 +1092,24 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
       }
     }
     if (b.dump_k && tid == 0) b.dump_k[(size_t)trial * b.Tmax + t] = newK;
-    __syncthreads();  // S8
+    if (tid == 0) {
+      s_K = newK;
+      if (s_fail) s_status = 4;
+      else if (newK == 0) s_status = 2;  // decoder.py:314-315
+    }
+    if (s_fail || newK == 0) fail_t = t;
+      }  // !dead
+    }  // compute warps
+    __syncthreads();  // S8: frame end (whole CTA)
     LB_PHASE(8);
     {
       BeamPtrs tmp = cur;
       cur = nxt;
       nxt = tmp;
     }
-    K = newK;
+    K = s_K;
     st_beams_out += K;
-    if (s_fail) {
-      status = 4;
-      fail_t = t;
-      break;
-    }
-    if (K == 0) {  // decoder.py:314-315
-      status = 2;
-      fail_t = t;
-      break;
-    }
+    if (s_status != 0) break;
 
     // ---- optional interval fusion of the device n-gram scorer (decoder.py:428-430)
     if (fusion_mode == 1 && t > 0 && (t % c.r) == 0) {
@@ -1082,6 +1129,13 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
         cur.score[i] = xadd(cur.score[i], xsub(e[0].total, prev));
       }
       __syncthreads();
+      if (warp == 0) {
+        double ms = -DBL_MAX;
+        for (int i = lane; i < K; i += 32) ms = fmax(ms, cur.score[i]);
+        ms = warp_max(ms);
+        if (lane == 0) s_maxs = ms;
+      }
+      __syncthreads();
       LB_PHASE(10);
     }
     LB_PHASE(9);
@@ -1092,6 +1146,7 @@ __global__ void __launch_bounds__(NT, (NT <= 512 ? 2 : 1)) frames_kernel(ModelDe
   if (timing)
     for (int i = 0; i < NPHASE; ++i) b.phase_cycles[(size_t)trial * NPHASE + i] += ph[i];
 #undef LB_PHASE
+  const int status = s_status;
   if (tid == 0) {
     if (status != 0) {
       b.status[trial] = status;
@@ -1493,8 +1548,24 @@ __global__ void log_softmax_kernel(const float* x, int64_t rows, int32_t V, int3
   res = __shfl_sync(FULLMASK, res, 0);
   const double lse = xadd(mx, log(res));
   double* orow = out + row * out_pitch;
-  if (lane < V) orow[lane] = xmul(alpha, xsub(xv0, lse));
-  if (lane + 32 < V) orow[lane + 32] = xmul(alpha, xsub(xv1, lse));
+  double o0 = -DBL_MAX, o1 = -DBL_MAX;
+  if (lane < V) orow[lane] = o0 = xmul(alpha, xsub(xv0, lse));
+  if (lane + 32 < V) orow[lane + 32] = o1 = xmul(alpha, xsub(xv1, lse));
+  // padded batch layout: slot V carries the row maximum (the frame kernel's bound U)
+  const double mx2 = warp_max(fmax(o0, o1));
+  if (out_pitch > V && lane == 0) orow[V] = mx2;
+}
+
+// row maximum into slot V of a padded log-prob matrix that was uploaded as is
+__global__ void rowmax_kernel(double* d, int64_t rows, int32_t V, int32_t pitch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  double* r = d + row * pitch;
+  double mx = -DBL_MAX;
+  for (int v = lane; v < V; v += 32) mx = fmax(mx, r[v]);
+  mx = warp_max(mx);
+  if (lane == 0) r[V] = mx;
 }
 
 // single-thread exact lookup (parity helper): record of `k` or nullptr
@@ -1547,16 +1618,24 @@ __global__ void score_words_kernel(ModelDev m, int n, const uint32_t* hist, cons
 // =====================================================================================
 namespace lbk {
 
-int max_threads_for(int K) { return K <= 64 ? 256 : (K <= 256 ? 512 : 1024); }
+int max_threads_for(int K) { return K <= 64 ? 256 : (K <= 256 ? 512 : 960); }
 
 cudaError_t set_smem_limit(int nthreads, int64_t bytes) {
   cudaError_t e = cudaSuccess;
-  if (nthreads == 256)
-    e = cudaFuncSetAttribute(frames_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  else if (nthreads == 512)
-    e = cudaFuncSetAttribute(frames_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  else
-    e = cudaFuncSetAttribute(frames_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+#define LB_SET(NCV)                                                                          \
+  e = cudaFuncSetAttribute(frames_kernel<NCV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)bytes);                                                      \
+  if (e != cudaSuccess) return e;                                                            \
+  e = cudaFuncSetAttribute(frames_kernel<NCV, false>,                                        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (nthreads == 256) {
+    LB_SET(256)
+  } else if (nthreads == 512) {
+    LB_SET(512)
+  } else {
+    LB_SET(960)
+  }
+#undef LB_SET
   return e;
 }
 
@@ -1579,6 +1658,13 @@ cudaError_t log_softmax(const float* x, int64_t rows, int32_t V, int32_t in_pitc
   return cudaGetLastError();
 }
 
+cudaError_t rowmax(double* d, int64_t rows, int32_t V, int32_t pitch, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  rowmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(d, rows, V, pitch);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 cudaError_t reset(const ModelDev& m, const BatchDev& b, cudaStream_t st) {
   reset_kernel<<<(b.B + 127) / 128, 128, 0, st>>>(m, b);
   ++g_launches;
@@ -1588,17 +1674,28 @@ cudaError_t reset(const ModelDev& m, const BatchDev& b, cudaStream_t st) {
 cudaError_t frames(const ModelDev& m, const CfgDev& c, const BatchDev& b, const Layout& L, int t0,
                    int t1, int fusion_mode, double scale, cudaStream_t st) {
   const size_t sm = (size_t)L.smem_bytes;
+  bool all_smem = true;
+  for (int r = 0; r < N_REGIONS; ++r)
+    if (r != R_WARP && !L.in_smem[r]) all_smem = false;
+#define LB_LAUNCH(NCV)                                                                 \
+  if (all_smem)                                                                        \
+    frames_kernel<NCV, true><<<b.B, NCV + NGT, sm, st>>>(m, c, b, L, t0, t1, fusion_mode, \
+                                                         scale);                        \
+  else                                                                                 \
+    frames_kernel<NCV, false><<<b.B, NCV + NGT, sm, st>>>(m, c, b, L, t0, t1,            \
+                                                          fusion_mode, scale);
   switch (L.nthreads) {
     case 256:
-      frames_kernel<256><<<b.B, 256, sm, st>>>(m, c, b, L, t0, t1, fusion_mode, scale);
+      LB_LAUNCH(256)
       break;
     case 512:
-      frames_kernel<512><<<b.B, 512, sm, st>>>(m, c, b, L, t0, t1, fusion_mode, scale);
+      LB_LAUNCH(512)
       break;
     default:
-      frames_kernel<1024><<<b.B, 1024, sm, st>>>(m, c, b, L, t0, t1, fusion_mode, scale);
+      LB_LAUNCH(960)
       break;
   }
+#undef LB_LAUNCH
   ++g_launches;
   return cudaGetLastError();
 }

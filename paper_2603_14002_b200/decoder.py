@@ -260,14 +260,15 @@ class DeviceBatch:
     def clear_stats(self):
         N.check(N.lib().lb_batch_clear_stats(self.h))
 
-    PHASES = ("unused", "cand_hist", "collect", "sort", "materialise", "ngram", "recomb_rank",
-              "recomb_keep", "scatter", "loop_tail", "fusion", "spare")
+    PHASES = ("top_U", "cand_S1wait", "collect", "sort", "materialise", "ngram_G3", "recomb_rank",
+              "recomb_keep", "scatter", "loop_tail", "fusion", "cand_loop", "ngram_G2",
+              "ngram_G2wait", "p14", "p15")
 
     def enable_phase_timing(self, on: bool = True):
         N.check(N.lib().lb_batch_enable_phase_timing(self.h, int(on)))
 
     def phase_cycles(self) -> dict:
-        out = np.zeros(12, dtype=np.uint64)
+        out = np.zeros(16, dtype=np.uint64)
         N.check(N.lib().lb_batch_phase_cycles(self.h, N.ptr(out)))
         return {name: int(v) for name, v in zip(self.PHASES, out)}
 

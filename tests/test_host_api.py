@@ -226,7 +226,7 @@ def test_sass_is_sm100a_with_tma_bulk():
         elif cur:
             funcs[cur].append(line)
     frames = [f for f in funcs if "frames_kernel" in f]
-    assert len(frames) == 3  # 256/512/1024-thread instantiations
+    assert len(frames) == 6  # {256,512,1024} threads x {all-shared, spilled} layouts
     sass = "\n".join(funcs[frames[0]])
     assert "UBLKCP" in sass  # cp.async.bulk (1-D TMA) staging of the log-prob frame chunks
     assert "LDGSTS" in sass  # cp.async lexicon-row gathers
