@@ -144,6 +144,7 @@ struct Layout {
   int32_t nthreads;    // compute threads (the kernel adds two speculative n-gram warps)
   int32_t pcap;        // n-gram (entry, surface) pair capacity of one flattened round
   int32_t tslots;      // recombination hash-table slots (power of two >= 2k)
+  int32_t small;       // 1: the specialised kernel (k <= 64, o <= 4, V <= 48) with its own layout
 };
 
 // one evaluated (entry, surface) pair of the flattened n-gram phase

@@ -36,6 +36,8 @@ cudaError_t score_words(const lbd::ModelDev& m, int n, const uint32_t* hist, con
                         const int32_t* word, double* inc, uint32_t* succ, int32_t* slen,
                         cudaStream_t st);
 int max_threads_for(int K);
+int small_smem_bytes();
+int small_gscratch_bytes();
 cudaError_t set_smem_limit(int nthreads, int64_t bytes);
 
 }  // namespace lbk

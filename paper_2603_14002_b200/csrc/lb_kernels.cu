@@ -204,6 +204,92 @@ __device__ void group_score_word(const ModelDev& m, bool act, const uint32_t h[M
   }
 }
 
+// score_word with 4 lanes per query (quad): lane sub = i probes BOTH candidate buckets of
+// K_i = (h[i:], w); 8 pairs per warp per round.  Same combination as group_score_word.
+__device__ void quad_score_word(const ModelDev& m, bool act, const uint32_t h[MAXH], int hl,
+                                const double hbo[MAXH], int w, WordScore& out, unsigned& probes) {
+  const int lane = threadIdx.x & 31, ki = lane & 3, grp = lane >> 2;
+  const bool valid = act && w >= 0;
+  bool hit = false;
+  double p = 0.0, bo = 0.0;
+  if (valid && ki <= hl) {
+    uint32_t k[4] = {WPAD, WPAD, WPAD, WPAD};
+    int n = 0;
+    for (int j = ki; j < hl; ++j) k[n++] = h[j];
+    k[n] = (uint32_t)w;
+    uint32_t b1, b2;
+    ng_buckets(ng_hash(k[0], k[1], k[2], k[3]), m.ng_nb, b1, b2);
+    const uint4* bk1 = reinterpret_cast<const uint4*>(m.ng + (size_t)b1 * NG_WAYS);
+    const uint4* bk2 = reinterpret_cast<const uint4*>(m.ng + (size_t)b2 * NG_WAYS);
+    uint4 r[2 * NG_WAYS];
+#pragma unroll
+    for (int q = 0; q < NG_WAYS; ++q) {
+      r[q] = __ldg(bk1 + 2 * q);
+      r[NG_WAYS + q] = __ldg(bk2 + 2 * q);
+    }
+    probes += 2;
+    int slot = -1;
+#pragma unroll
+    for (int q = 2 * NG_WAYS - 1; q >= 0; --q)
+      if (r[q].x == k[0] && r[q].y == k[1] && r[q].z == k[2] && r[q].w == k[3]) slot = q;
+    if (slot >= 0) {
+      const uint4* rec = (slot < NG_WAYS ? bk1 : bk2) + 2 * (slot & (NG_WAYS - 1));
+      const double2 pb = __ldg(reinterpret_cast<const double2*>(rec + 1));
+      p = pb.x;
+      bo = pb.y;
+      hit = true;
+    }
+  }
+  const unsigned bal = __ballot_sync(FULLMASK, hit);
+  const unsigned gb = (bal >> (grp * 4)) & 0xFu;
+  double pk[4], bk[4];
+  bool fk[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    pk[j] = __shfl_sync(FULLMASK, p, grp * 4 + j);
+    bk[j] = __shfl_sync(FULLMASK, bo, grp * 4 + j);
+    fk[j] = (gb >> j) & 1u;
+  }
+  out.slen = 0;
+  out.inc = NEG_INF;
+  if (ki != 0 || !valid) return;
+  double val = NEG_INF;
+  int hitk = hl + 1;
+#pragma unroll
+  for (int j = 3; j >= 0; --j)
+    if (j <= hl && fk[j] && prob_present(pk[j])) {
+      val = pk[j];
+      hitk = j;
+    }
+  for (int j = min(hitk, hl) - 1; j >= 0; --j) val = xadd(hbo[j], val);
+  out.inc = val;
+  if (m.order > 1) {
+    const int start = max(0, hl + 1 - (m.order - 1));
+    int sk = -1;
+#pragma unroll
+    for (int j = 3; j >= 0; --j)
+      if (j >= start && j <= hl && fk[j] && prob_present(pk[j])) sk = j;
+    if (sk >= 0) {
+      int n = 0;
+      for (int t = sk; t < hl; ++t) out.succ[n++] = h[t];
+      out.succ[n++] = (uint32_t)w;
+      out.slen = n;
+#pragma unroll
+      for (int t = 0; t < MAXH; ++t) {
+        const int j = sk + t;
+        double v = 0.0;
+        if (t < n) {
+          if (j == 0) v = fk[0] ? bk[0] : 0.0;
+          else if (j == 1) v = fk[1] ? bk[1] : 0.0;
+          else if (j == 2) v = fk[2] ? bk[2] : 0.0;
+          else v = fk[3] ? bk[3] : 0.0;
+        }
+        out.sbo[t] = v;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void new_entry(Ent& o, double total, double cum, const WordScore& ws,
                                           uint32_t node, uint32_t seq, uint32_t depth) {
   o.total = total;
@@ -1185,6 +1271,881 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
 }
 
 // =====================================================================================
+// K2s: frames kernel specialised for k <= 64, ortho_beams <= 4, V <= 48 (every BASELINE
+// config at beam 16/64 and all reference fixtures).  Same algorithm as frames_kernel; the
+// whole working set has a compile-time shared-memory layout (immediate-offset addressing, no
+// pointer registers), candidate bins stay in registers (transposed thread <-> token mapping),
+// and word-boundary entries are built straight from the speculative pair results.
+// =====================================================================================
+namespace small {
+constexpr int KC = 64, OC = 4, VC = 48, VPC = 56, VPDC = 50;
+constexpr int LC = 320, PC = 256, TSC = 128;
+constexpr int NC = 256, NWC = NC / 32, NT = NC + NGT;
+constexpr int MAXI = (KC + (NC / VC) - 1) / (NC / VC);  // items per thread (13)
+constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8,
+              B_PRE = 3 * KC * 8 + KC * 4, B_NENT = 3 * KC * 8 + 2 * KC * 4,
+              B_ENTS = 3 * KC * 8 + 3 * KC * 4;
+constexpr int BEAM_BYTES = B_ENTS + KC * OC * (int)sizeof(Ent);
+constexpr int O_DBUF = 0;
+constexpr int O_ROWS = O_DBUF + 2 * CHUNK * VPDC * 8;
+constexpr int O_BEAM = O_ROWS + KC * VPC * 4;
+constexpr int O_CVAL = O_BEAM + 2 * BEAM_BYTES;
+constexpr int O_CKEY = O_CVAL + LC * 8;
+constexpr int O_CBINL = O_CKEY + LC * 4;
+constexpr int O_SVAL = O_CBINL + LC * 2;
+constexpr int O_SKEY = O_SVAL + KC * 8;
+constexpr int O_NSCORE = O_SKEY + KC * 4;
+constexpr int O_NH1 = O_NSCORE + KC * 8;
+constexpr int O_NH2 = O_NH1 + KC * 8;
+constexpr int O_NLAST = O_NH2 + KC * 8;
+constexpr int O_NPRE = O_NLAST + KC * 4;
+constexpr int O_NPAR = O_NPRE + KC * 4;
+constexpr int O_RANK = O_NPAR + KC * 4;
+constexpr int O_BLIST = O_RANK + KC * 4;
+constexpr int O_BSEL = O_BLIST + KC * 4;
+constexpr int O_KEEP = O_BSEL + KC * 16;
+constexpr int O_POFF = O_KEEP + 16;
+constexpr int O_PRES = O_POFF + ((KC + 1) * 4 + 15) / 16 * 16;
+constexpr int O_SLOTB = O_PRES + PC * (int)sizeof(PairRes);
+constexpr int O_SLOTM = O_SLOTB + TSC * 4;
+constexpr int O_MYSLOT = O_SLOTM + TSC * 4;
+constexpr int O_QINFO = O_MYSLOT + KC * 4;  // int4 per speculative pair: (entry, word, surface, -)
+constexpr int TOTAL = O_QINFO + PC * 16;
+static_assert(O_BEAM % 16 == 0 && O_CVAL % 16 == 0 && O_PRES % 16 == 0 && BEAM_BYTES % 16 == 0,
+              "16-byte alignment");
+// global scratch per trial: entries of boundary beams on the rare overflow path + warp scratch
+constexpr int G_BENTS = 0;
+constexpr int G_WARP = KC * OC * (int)sizeof(Ent);
+constexpr int GTOTAL = G_WARP + NWC * (int)sizeof(WarpScratch);
+}  // namespace small
+
+__global__ void __launch_bounds__(small::NT, 2)
+    frames_small_kernel(ModelDev m, CfgDev c, BatchDev b, int t0, int t1, int fusion_mode,
+                        double scale) {
+  using namespace small;
+  extern __shared__ __align__(128) char sm[];
+  __shared__ __align__(8) uint64_t dbar[2];
+  __shared__ unsigned hist[NBINS];
+  __shared__ int hcum[NBINS];
+  __shared__ int hfill[NBINS];
+  __shared__ double wmax[NWC];
+  __shared__ double s_maxs;
+  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_inr, s_cnt2;
+  __shared__ int ngtot[2];
+  __shared__ unsigned s_calls, s_probes;
+
+  const int trial = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (b.status[trial] != 0) return;
+  const int T = b.T[trial];
+  const int tb = t0, te = min(t1, T);
+  if (tb >= te) return;
+  char* gs = b.gscratch + (int64_t)trial * b.gscratch_stride;
+
+  double* dbuf = reinterpret_cast<double*>(sm + O_DBUF);
+  int32_t* rows = reinterpret_cast<int32_t*>(sm + O_ROWS);
+  double* cval = reinterpret_cast<double*>(sm + O_CVAL);
+  uint32_t* ckey = reinterpret_cast<uint32_t*>(sm + O_CKEY);
+  uint16_t* cbinl = reinterpret_cast<uint16_t*>(sm + O_CBINL);
+  double* sval = reinterpret_cast<double*>(sm + O_SVAL);
+  uint32_t* skey = reinterpret_cast<uint32_t*>(sm + O_SKEY);
+  double* nscore = reinterpret_cast<double*>(sm + O_NSCORE);
+  uint64_t* nh1 = reinterpret_cast<uint64_t*>(sm + O_NH1);
+  uint64_t* nh2 = reinterpret_cast<uint64_t*>(sm + O_NH2);
+  int32_t* nlast = reinterpret_cast<int32_t*>(sm + O_NLAST);
+  int32_t* npre = reinterpret_cast<int32_t*>(sm + O_NPRE);
+  int32_t* npar = reinterpret_cast<int32_t*>(sm + O_NPAR);
+  int32_t* rankv = reinterpret_cast<int32_t*>(sm + O_RANK);
+  int32_t* blist = reinterpret_cast<int32_t*>(sm + O_BLIST);
+  int4* bsel = reinterpret_cast<int4*>(sm + O_BSEL);  // {kept|-1|-2, node base, top01, top23}
+  uint32_t* keep = reinterpret_cast<uint32_t*>(sm + O_KEEP);
+  int32_t* ppoff = reinterpret_cast<int32_t*>(sm + O_POFF);
+  PairRes* pres = reinterpret_cast<PairRes*>(sm + O_PRES);
+  int32_t* slotb = reinterpret_cast<int32_t*>(sm + O_SLOTB);
+  int32_t* slotm = reinterpret_cast<int32_t*>(sm + O_SLOTM);
+  int32_t* myslot = reinterpret_cast<int32_t*>(sm + O_MYSLOT);
+  Ent* gbents = reinterpret_cast<Ent*>(gs + G_BENTS);
+  WarpScratch* wsc = reinterpret_cast<WarpScratch*>(gs + G_WARP);
+
+  // beam buffers selected by parity: cur = buffer `par`, nxt = buffer `par ^ 1`
+  int par = 0;
+#define BUF(pp) (sm + O_BEAM + (pp) * BEAM_BYTES)
+#define C_SCORE ((double*)(BUF(par) + B_SCORE))
+#define C_H1 ((uint64_t*)(BUF(par) + B_H1))
+#define C_H2 ((uint64_t*)(BUF(par) + B_H2))
+#define C_LAST ((int32_t*)(BUF(par) + B_LAST))
+#define C_PRE ((int32_t*)(BUF(par) + B_PRE))
+#define C_NENT ((int32_t*)(BUF(par) + B_NENT))
+#define C_ENTS ((Ent*)(BUF(par) + B_ENTS))
+#define X_SCORE ((double*)(BUF(par ^ 1) + B_SCORE))
+#define X_H1 ((uint64_t*)(BUF(par ^ 1) + B_H1))
+#define X_H2 ((uint64_t*)(BUF(par ^ 1) + B_H2))
+#define X_LAST ((int32_t*)(BUF(par ^ 1) + B_LAST))
+#define X_PRE ((int32_t*)(BUF(par ^ 1) + B_PRE))
+#define X_NENT ((int32_t*)(BUF(par ^ 1) + B_NENT))
+#define X_ENTS ((Ent*)(BUF(par ^ 1) + B_ENTS))
+
+  const int V = m.V, VP = m.VP, VPD = b.VPD, O = c.O, KC_ = b.K;
+  const int TS = TSC;
+  const double b_on = c.beta, b_off = xmul(c.beta, 0.0);
+  const double g_on = c.gamma, g_off = xmul(c.gamma, 0.0);
+  const int blank = m.blank, space = m.space, sink = m.sink;
+  // transposed candidate mapping: thread -> token tv, parents tg, tg + ngrp, ...
+  const int ngrp = NC / V;
+  const int tv = tid % V, tg = tid / V;
+
+  // ---- load the home beam state and gather the first frame's lexicon rows
+  int K = b.nbeam[trial];
+  {
+    const size_t hb = (size_t)trial * KC_;
+    for (int i = tid; i < K; i += NT) {
+      C_SCORE[i] = b.score[hb + i];
+      C_H1[i] = b.h1[hb + i];
+      C_H2[i] = b.h2[hb + i];
+      C_LAST[i] = b.last[hb + i];
+      C_PRE[i] = b.prefix[hb + i];
+      C_NENT[i] = b.nent[hb + i];
+      const int32_t* src = m.table + (size_t)b.prefix[hb + i] * VP;
+      for (int q = 0; q < VP; q += 4) cp_async16(rows + i * VP + q, src + q);
+    }
+    cp_async_commit();
+    for (int i = tid; i < K * O; i += NT) {
+      const int bi = i / O, e = i - bi * O;
+      if (e < b.nent[hb + bi]) C_ENTS[bi * OC + e] = b.ents[hb * O + i];
+    }
+  }
+  for (int i = tid; i < NBINS; i += NT) {
+    hist[i] = 0;
+    hfill[i] = 0;
+  }
+  if (tid == 0) {
+    s_ncount = b.ncount[trial];
+    s_fail = 0;
+    s_status = 0;
+    s_calls = 0;
+    s_probes = 0;
+    s_K = K;
+    mbar_init(&dbar[0], 1);
+    mbar_init(&dbar[1], 1);
+    fence_mbar_init();
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (warp == 0) {
+    double ms = -DBL_MAX;
+    for (int i = lane; i < K; i += 32) ms = fmax(ms, C_SCORE[i]);
+    ms = warp_max(ms);
+    if (lane == 0) s_maxs = ms;
+  }
+  __syncthreads();
+
+  const double* Dtrial = b.D + (size_t)trial * b.Tmax * VPD;
+  auto issue_chunk = [&](int ci) {
+    const int f0 = tb + ci * CHUNK;
+    if (f0 >= te) return;
+    const int nf = min(CHUNK, te - f0);
+    const unsigned bytes = (unsigned)(nf * VPD * sizeof(double));
+    mbar_expect_tx(&dbar[ci & 1], bytes);
+    tma_bulk_g2s(dbuf + (size_t)(ci & 1) * CHUNK * VPDC, Dtrial + (size_t)f0 * VPD, bytes,
+                 &dbar[ci & 1]);
+  };
+  if (tid == 0) issue_chunk(0);
+
+  unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
+  unsigned calls_l = 0, probes_l = 0;
+  int fail_t = -1;
+  const bool timing = b.phase_cycles != nullptr && tid == 0;
+  unsigned long long ph[NPHASE];
+  for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
+  long long tprev = timing ? clock64() : 0;
+#define LB_PHASE(i)                                \
+  if (timing) {                                    \
+    const long long tnow = clock64();              \
+    ph[i] += (unsigned long long)(tnow - tprev);   \
+    tprev = tnow;                                  \
+  }
+
+  for (int t = tb; t < te; ++t) {
+    const int rel = t - tb;
+    const int ci = rel / CHUNK;
+    const int cr = rel - ci * CHUNK;
+    st_beams_in += K;
+
+    if (warp >= NWC) {
+      // ================== speculative n-gram warps (as in frames_kernel) ==================
+      const int gt = tid - NC, ngw = warp - NWC;
+      int carry = 0;
+      for (int base = 0; base < K; base += NGT) {
+        const int p = base + gt;
+        int np = 0;
+        if (p < K) {
+          const int32_t* row = rows + p * VP;
+          if (row[V] > 0 && C_LAST[p] != space) np = C_NENT[p] * row[V];
+        }
+        int incl = np;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULLMASK, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane == 31) ngtot[ngw] = incl;
+        bar_sync(3, NGT);
+        const int woff = ngw ? ngtot[0] : 0;
+        const int tot = ngtot[0] + ngtot[1];
+        if (p < K) ppoff[p] = carry + woff + incl - np;
+        carry += tot;
+        bar_sync(3, NGT);
+      }
+      if (gt == 0) {
+        ppoff[K] = carry;
+        s_ngP = carry;
+      }
+      const int P = carry;
+      if (P <= PC) {
+        // pair table: each parent writes its own (entry, surface) pairs -- no search
+        int4* qinfo = reinterpret_cast<int4*>(sm + O_QINFO);
+        for (int p = gt; p < K; p += NGT) {
+          const int q0 = ppoff[p], q1 = ppoff[p + 1];
+          if (q0 == q1) continue;
+          const CompHdr ch = comp_hdr(rows + p * VP, V);
+          for (int q = q0; q < q1; ++q) {
+            const int local = q - q0;
+            const int e = local / ch.ns;
+            const int sidx = local - e * ch.ns;
+            int w, surf;
+            if (sidx == 0) {
+              w = ch.l0;
+              surf = ch.s0;
+            } else if (sidx == 1) {
+              w = ch.l1;
+              surf = ch.s1;
+            } else {
+              w = __ldg(m.comp_lm + ch.off + sidx);
+              surf = __ldg(m.comp_surf + ch.off + sidx);
+            }
+            qinfo[q] = make_int4(p * OC + e, w, surf, 0);
+          }
+        }
+        bar_sync(3, NGT);
+        constexpr int NQ = NGT / 4;
+        const int grp = gt >> 2, sub = lane & 3;
+        for (int q0 = 0; q0 < P; q0 += NQ) {
+          const int q = q0 + grp;
+          const bool act = q < P;
+          const int4 qi = act ? qinfo[q] : make_int4(0, -1, -1, 0);
+          const Ent& E = C_ENTS[qi.x];
+          uint32_t hh[MAXH] = {E.h[0], E.h[1], E.h[2]};
+          double hb2[MAXH] = {E.bo[0], E.bo[1], E.bo[2]};
+          WordScore sw;
+          quad_score_word(m, act, hh, E.hlen, hb2, qi.y, sw, probes_l);
+          if (act && sub == 0) {
+            ++calls_l;
+            PairRes pr;
+            pr.valid = sw.inc > GUARD;
+            pr.total = xadd(E.total, xmul(c.omega, sw.inc));
+            pr.cum = xadd(E.cum, sw.inc);
+            pr.node = E.node;
+            pr.surf = (uint32_t)qi.z;
+            for (int tt = 0; tt < MAXH; ++tt) {
+              pr.h[tt] = sw.succ[tt];
+              pr.bo[tt] = sw.sbo[tt];
+            }
+            pr.depth = (uint16_t)(E.depth + 1);
+            pr.hlen = (uint8_t)sw.slen;
+            pres[q] = pr;
+          }
+        }
+      }
+      bar_arrive(2, NT);
+    } else {
+      // ============================== compute warps ==============================
+      if (cr == 0) {
+        mbar_wait(&dbar[ci & 1], (unsigned)((ci >> 1) & 1));
+        if (tid == 0) issue_chunk(ci + 1);
+      }
+      const double* drow = dbuf + (size_t)(ci & 1) * CHUNK * VPDC + (size_t)cr * VPD;
+      const double U = __dadd_ru(__dadd_ru(__dadd_ru(s_maxs, drow[V]), fmax(c.beta, 0.0)),
+                                 fmax(c.gamma, 0.0));
+      // per-thread token constants
+      const bool tact = tg < ngrp;
+      const double dv = drow[tv];
+      const bool tph = (tv != blank) && (tv != space);
+      LB_PHASE(0);
+
+      // ---- A: candidates of token tv for parents tg, tg+ngrp, ... ; bins kept in registers
+      uint16_t bins[MAXI];
+      double wm = -DBL_MAX;
+#pragma unroll
+      for (int i = 0; i < MAXI; ++i) {
+        bins[i] = 0xFFFF;
+        const int p = tg + i * ngrp;
+        if (tact && p < K) {
+          const int lp = C_LAST[p];
+          const int nx = rows[p * VP + tv];
+          if ((nx != sink) || (tv == blank) || (tv == lp)) {
+            double x = xadd(C_SCORE[p], dv);
+            x = xadd(x, (tph && tv != lp) ? b_on : b_off);
+            if (tv == space) x = xadd(x, lp != space ? g_on : g_off);
+            if (x > GUARD) {
+              const double fb =
+                  fmin(fmax(xmul(xsub(U, x), c.inv_binw), 0.0), (double)(NBINS - 1));
+              bins[i] = (uint16_t)(int)fb;
+              atomicAdd(&hist[bins[i]], 1u);
+              wm = fmax(wm, x);
+            }
+          }
+        }
+      }
+      wm = warp_max(wm);
+      LB_PHASE(11);
+      if (lane == 0) wmax[warp] = wm;
+      if (tid == 0) s_nb = 0;
+      if (tid < 2) keep[tid] = 0;
+      for (int i = tid; i < TS; i += NC) {
+        slotb[i] = -1;
+        slotm[i] = 0x7FFFFFFF;
+      }
+      bar_sync(1, NC);  // S1
+      LB_PHASE(1);
+
+      double M = -DBL_MAX;
+#pragma unroll
+      for (int w = 0; w < NWC; ++w) M = fmax(M, wmax[w]);
+      int nsel = 0;
+      const bool dead = !(M > GUARD);  // decoder.py:267-268
+      if (dead) {
+        if (tid == 0) {
+          s_status = 1;
+          s_K = 0;
+        }
+        fail_t = t;
+      } else {
+        const double thr = xsub(M, c.theta);
+        const int bthr =
+            (int)fmin(fmax(xmul(xsub(U, thr), c.inv_binw), 0.0), (double)(NBINS - 1));
+        int bstar = NBINS, cum_thr = 0, cum_bstar = 0;
+        {
+          constexpr int PB = NBINS / 32;
+          int part[PB];
+          int ls = 0;
+#pragma unroll
+          for (int i = 0; i < PB; ++i) {
+            part[i] = (int)hist[lane * PB + i];
+            ls += part[i];
+          }
+          int incl = ls;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int excl = incl - ls;
+          {
+            int run = excl;
+#pragma unroll
+            for (int i = 0; i < PB; ++i) {
+              hcum[lane * PB + i] = run;
+              run += part[i];
+            }
+          }
+          __syncwarp();
+          cum_thr = hcum[bthr] + (int)hist[bthr];
+          const unsigned bl = __ballot_sync(FULLMASK, excl < c.k && incl >= c.k);
+          if (bl) {
+            const int src = __ffs(bl) - 1;
+            int lb = 0;
+            if (lane == src) {
+              int cum = excl;
+#pragma unroll
+              for (int i = 0; i < PB; ++i) {
+                if (cum + part[i] >= c.k) {
+                  lb = i;
+                  break;
+                }
+                cum += part[i];
+              }
+            }
+            lb = __shfl_sync(FULLMASK, lb, src);
+            bstar = src * PB + lb;
+            cum_bstar = hcum[bstar] + (int)hist[bstar];
+          }
+        }
+        const bool sure = bstar < bthr;
+        const int take_bin = sure ? bstar : bthr;
+        const int bound = sure ? cum_bstar : cum_thr;
+        if (bound <= LC) {
+          // ---- D: counting-sort collect from the register bins
+#pragma unroll
+          for (int i = 0; i < MAXI; ++i) {
+            const int bn = bins[i];
+            if (bn <= take_bin) {
+              const int p = tg + i * ngrp;
+              const int lp = C_LAST[p];
+              double x = xadd(C_SCORE[p], dv);
+              x = xadd(x, (tph && tv != lp) ? b_on : b_off);
+              if (tv == space) x = xadd(x, lp != space ? g_on : g_off);
+              if (sure || x >= thr) {
+                const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
+                cval[pos] = x;
+                ckey[pos] = (uint32_t)(p * V + tv);
+                cbinl[pos] = (uint16_t)bn;
+              }
+            }
+          }
+          bar_sync(1, NC);  // S2
+          const int m_sel = hcum[take_bin] + hfill[take_bin];
+          nsel = min(c.k, m_sel);
+          LB_PHASE(2);
+          for (int a = lane * NWC + warp; a < m_sel; a += NC) {
+            const double va = cval[a];
+            const uint32_t ka = ckey[a];
+            const int bn = cbinl[a];
+            const int lo = hcum[bn], n = hfill[bn];
+            int r = lo;
+            for (int q = lo; q < lo + n; ++q) {
+              const double vq = cval[q];
+              r += (vq > va) || (vq == va && ckey[q] < ka);
+            }
+            if (r < nsel) {
+              sval[r] = va;
+              skey[r] = ka;
+            }
+          }
+        } else {
+          // ---- fallback: exact radix select on the 96-bit key (ord64(value), ~flat index)
+          ++st_fallback;
+          auto cval_at = [&](int f) -> double {
+            const int p = f / V, v = f - (f / V) * V;
+            const int lp = C_LAST[p];
+            const int nx = rows[p * VP + v];
+            if (!((nx != sink) || (v == blank) || (v == lp))) return -DBL_MAX;
+            const double x = cand_value(C_SCORE[p], drow[v], v, lp,
+                                        FrameConsts{c.beta, c.gamma, blank, space});
+            return x > GUARD ? x : -DBL_MAX;
+          };
+          const int KV = K * V;
+          bar_sync(1, NC);
+          if (tid == 0) {
+            s_cnt2 = 0;
+            s_inr = 0;
+          }
+          bar_sync(1, NC);
+          for (int f = tid; f < KV; f += NC)
+            if (cval_at(f) >= thr) atomicAdd(&s_inr, 1);
+          bar_sync(1, NC);
+          nsel = min(c.k, s_inr);
+          uint64_t phi = 0, pmask_hi = 0;
+          uint32_t plo = 0, pmask_lo = 0;
+          int rem = nsel;
+          for (int pass = 0; pass < 12; ++pass) {
+            bar_sync(1, NC);
+            for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
+            bar_sync(1, NC);
+            for (int f = tid; f < KV; f += NC) {
+              const double x = cval_at(f);
+              if (!(x >= thr)) continue;
+              const uint64_t kh = ord64(x);
+              const uint32_t kl = ~(uint32_t)f;
+              if ((kh & pmask_hi) != phi || (kl & pmask_lo) != plo) continue;
+              const unsigned dg = pass < 8 ? (unsigned)((kh >> (56 - 8 * pass)) & 0xFF)
+                                           : (unsigned)((kl >> (24 - 8 * (pass - 8))) & 0xFF);
+              atomicAdd(&hist[dg], 1u);
+            }
+            bar_sync(1, NC);
+            int above = 0, dsel = 0;
+            for (int d = NBINS - 1; d >= 0; --d) {
+              const int h = (int)hist[d];
+              if (above + h >= rem) {
+                dsel = d;
+                break;
+              }
+              above += h;
+            }
+            rem -= above;
+            if (pass < 8) {
+              phi |= (uint64_t)dsel << (56 - 8 * pass);
+              pmask_hi |= 0xFFull << (56 - 8 * pass);
+            } else {
+              plo |= (uint32_t)dsel << (24 - 8 * (pass - 8));
+              pmask_lo |= 0xFFu << (24 - 8 * (pass - 8));
+            }
+          }
+          bar_sync(1, NC);
+          for (int f0 = 0; f0 < KV; f0 += NC) {
+            const int f = f0 + tid;
+            bool take = false;
+            double x = 0.0;
+            if (f < KV) {
+              x = cval_at(f);
+              if (x >= thr) {
+                const uint64_t kh = ord64(x);
+                const uint32_t kl = ~(uint32_t)f;
+                take = kh > phi || (kh == phi && kl >= plo);
+              }
+            }
+            const unsigned bl = __ballot_sync(FULLMASK, take);
+            if (bl) {
+              int base = 0;
+              if (lane == 0) base = atomicAdd(&s_cnt2, __popc(bl));
+              base = __shfl_sync(FULLMASK, base, 0);
+              if (take) {
+                const int pos = base + __popc(bl & ((1u << lane) - 1u));
+                cval[pos] = x;
+                ckey[pos] = (uint32_t)f;
+              }
+            }
+          }
+          bar_sync(1, NC);
+          for (int i = tid; i < nsel; i += NC) {
+            const double vi = cval[i];
+            const uint32_t ki = ckey[i];
+            int cnt = 0;
+            for (int j = 0; j < nsel; ++j) {
+              const double vj = cval[j];
+              cnt += (vj > vi) || (vj == vi && ckey[j] < ki);
+            }
+            sval[cnt] = vi;
+            skey[cnt] = ki;
+          }
+          for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
+        }
+      }
+      bar_sync(2, NT);  // S3: selection done + speculative n-gram results ready
+      LB_PHASE(3);
+
+      if (!dead) {
+        const bool ngover = s_ngP > PC;
+        LB_PHASE(13);
+        // ---- F: materialise survivors; new word boundaries pick their top-o pairs
+        // selected beams spread over all compute warps (j = lane * NWC + warp), so the few
+        // word-boundary merges run in parallel instead of serialising inside one warp
+        for (int j = lane * NWC + warp; j < nsel; j += NC) {
+          const double x = sval[j];
+          const uint32_t f = skey[j];
+          const int p = (int)f / V;
+          const int tok = (int)f - p * V;
+          const int lp = C_LAST[p], pp = C_PRE[p];
+          const bool emit = (tok != blank) && (tok != lp);
+          uint64_t a1 = C_H1[p], a2 = C_H2[p];
+          int np = pp;
+          if (emit) {
+            a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
+            a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
+            np = rows[p * VP + tok];
+          }
+          double sc = x;
+          int4 bs = make_int4(-1, 0, 0, 0);
+          LB_PHASE(14);
+          if (emit && tok == space) {
+            blist[atomicAdd(&s_nb, 1)] = j;
+            if (ngover) {
+              bs.x = -2;
+            } else {
+              const int q0 = ppoff[p], q1 = ppoff[p + 1];
+              int top[OC];
+              int ntop = 0;
+              for (int q = q0; q < q1; ++q) {
+                if (!pres[q].valid) continue;
+                const double tq = pres[q].total;
+                int pos = ntop;
+                for (int i = 0; i < ntop; ++i)
+                  if (tq > pres[top[i]].total) {
+                    pos = i;
+                    break;
+                  }
+                if (pos >= O) continue;
+                for (int i = min(ntop, O - 1); i > pos; --i) top[i] = top[i - 1];
+                top[pos] = q;
+                ntop = min(ntop + 1, O);
+              }
+              if (ntop == 0) {
+                sc = NEG_INF;  // decoder.py:223-225
+              } else {
+                const double best = pres[top[0]].total;
+                const double floor_ = xsub(best, c.lambda);
+                int kept = 0;
+                while (kept < ntop && pres[top[kept]].total >= floor_) ++kept;
+                const int base = atomicAdd(&s_ncount, kept);
+                if (base + kept > b.ncap) {
+                  s_fail = 1;
+                  sc = NEG_INF;
+                } else {
+                  const size_t nbase = (size_t)trial * b.ncap;
+                  for (int i = 0; i < kept; ++i) {
+                    b.nparent[nbase + base + i] = pres[top[i]].node;
+                    b.nsurf[nbase + base + i] = pres[top[i]].surf;
+                  }
+                  bs.x = kept;
+                  bs.y = base;
+                  bs.z = (top[0] & 0xFFFF) | ((kept > 1 ? top[1] : 0) << 16);
+                  bs.w = (kept > 2 ? top[2] : 0) | ((kept > 3 ? top[3] : 0) << 16);
+                  sc = xadd(x, xsub(best, C_ENTS[p * OC].total));
+                }
+              }
+            }
+          }
+          nscore[j] = sc;
+          nh1[j] = a1;
+          nh2[j] = a2;
+          nlast[j] = (tok == blank) ? lp : tok;
+          npre[j] = np;
+          npar[j] = p;
+          bsel[j] = bs;
+        }
+        LB_PHASE(12);
+        bar_sync(1, NC);  // S4
+        LB_PHASE(4);
+        const int nb = s_nb;
+        st_bound += nb;
+        if (ngover && nb > 0) {
+          for (int bi = warp; bi < nb; bi += NWC) {
+            const int j = blist[bi];
+            const int p = npar[j];
+            int outn = -1;
+            double sc = nscore[j];
+            warp_apply_ngram(m, c, b, trial, C_ENTS + p * OC, C_NENT[p], comp_hdr(rows + p * VP, V),
+                             &wsc[warp], gbents + (size_t)j * OC, &outn, &sc, &s_ncount, &s_fail,
+                             calls_l, probes_l);
+            if (lane == 0) {
+              nscore[j] = sc;
+              bsel[j] = make_int4(outn >= 0 ? -2 - outn : -1, 0, 0, 0);  // -2-n: n entries in gbents
+            }
+          }
+          bar_sync(1, NC);
+        }
+        LB_PHASE(5);
+
+        // ---- H1: recombination ranking; regular beams are already in (score desc, j asc)
+        // order, only the nb boundary beams need comparisons; hash groups via a smem table
+        {
+          const int n = nsel;
+          int G = 1;
+          while (G < 32 && 2 * G * n <= NC) G <<= 1;
+          const int groups = NC / G, g = tid / G, r = tid & (G - 1);
+          for (int i0 = 0; i0 < n; i0 += groups) {
+            const int i = i0 + g;
+            const bool act = i < n;
+            const double si = act ? nscore[i] : 0.0;
+            const int bx = act ? bsel[i].x : -1;
+            const bool ib = act && (bx != -1 || si <= GUARD);
+            int cnt = 0;
+            if (act) {
+              for (int k2 = r; k2 < nb; k2 += G) {
+                const int j = blist[k2];
+                const double sj = nscore[j];
+                cnt += (sj > si) || (sj == si && j < i);
+                if (!ib) cnt -= (j < i);
+              }
+              if (ib) {
+                for (int j = r; j < n; j += G) {
+                  if (bsel[j].x != -1 || nscore[j] <= GUARD) continue;
+                  const double sj = nscore[j];
+                  cnt += (sj > si) || (sj == si && j < i);
+                }
+              }
+            }
+            for (int o = G >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULLMASK, cnt, o);
+            if (act && r == 0) {
+              if (!ib) cnt += i;
+              rankv[i] = cnt;
+              if (si > GUARD) {
+                const uint64_t a1 = nh1[i], a2 = nh2[i];
+                int h = (int)((a1 ^ (a2 * 0x9E3779B97F4A7C15ull)) >> 20) & (TS - 1);
+                for (;;) {
+                  const int owner = atomicCAS(&slotb[h], -1, i);
+                  if (owner == -1 || (nh1[owner] == a1 && nh2[owner] == a2)) break;
+                  h = (h + 1) & (TS - 1);
+                }
+                myslot[i] = h;
+                atomicMin(&slotm[h], cnt);
+              }
+            }
+          }
+        }
+        bar_sync(1, NC);  // S5
+        LB_PHASE(6);
+        for (int i = tid; i < nsel; i += NC) {
+          if (nscore[i] > GUARD && slotm[myslot[i]] == rankv[i])
+            atomicOr(&keep[rankv[i] >> 5], 1u << (rankv[i] & 31));
+        }
+        bar_sync(1, NC);  // S6
+        LB_PHASE(7);
+
+        // ---- scatter in rank order; boundary entries built from the chosen pairs;
+        // next frame's lexicon rows prefetched with cp.async
+        for (int i = tid; i < NBINS; i += NC) {
+          hist[i] = 0;
+          hfill[i] = 0;
+        }
+        const int newK = __popc(keep[0]) + __popc(keep[1]);
+        {
+          int G = 1;
+          while (G < 32 && 2 * G * nsel <= NC) G <<= 1;
+          const int groups = NC / G, g = tid / G, r = tid & (G - 1);
+          for (int i0 = 0; i0 < nsel; i0 += groups) {
+            const int i = i0 + g;
+            if (i >= nsel) continue;
+            const int rk = rankv[i];
+            if (!((keep[rk >> 5] >> (rk & 31)) & 1u)) continue;
+            const int pos = __popc(keep[rk >> 5] & ((1u << (rk & 31)) - 1u)) +
+                            (rk >= 32 ? __popc(keep[0]) : 0);
+            const int4 bs = bsel[i];
+            Ent* dst = X_ENTS + pos * OC;
+            int cnt;
+            if (bs.x >= 0) {  // fresh word boundary: entries from the chosen pairs
+              cnt = bs.x;
+              for (int e = r; e < cnt; e += G) {
+                const int q = e == 0 ? (bs.z & 0xFFFF) : e == 1 ? (bs.z >> 16)
+                                                       : e == 2 ? (bs.w & 0xFFFF) : (bs.w >> 16);
+                const PairRes& pr = pres[q];
+                WordScore sw;
+                sw.slen = pr.hlen;
+                for (int tt = 0; tt < MAXH; ++tt) {
+                  sw.succ[tt] = pr.h[tt];
+                  sw.sbo[tt] = pr.bo[tt];
+                }
+                new_entry(dst[e], pr.total, pr.cum, sw, (uint32_t)(bs.y + e),
+                          (uint32_t)(q - ppoff[npar[i]]), pr.depth);
+              }
+            } else if (bs.x <= -2) {  // overflow path: entries in global scratch
+              cnt = -2 - bs.x;
+              const uint4* su = reinterpret_cast<const uint4*>(gbents + (size_t)i * OC);
+              uint4* du = reinterpret_cast<uint4*>(dst);
+              for (int u = r; u < cnt * ENT_U4; u += G) du[u] = su[u];
+            } else {  // inherit the parent's entries
+              const int p = npar[i];
+              cnt = C_NENT[p];
+              const uint4* su = reinterpret_cast<const uint4*>(C_ENTS + p * OC);
+              uint4* du = reinterpret_cast<uint4*>(dst);
+              for (int u = r; u < cnt * ENT_U4; u += G) du[u] = su[u];
+            }
+            if (r == 0) {
+              if (pos == 0) s_maxs = nscore[i];
+              X_SCORE[pos] = nscore[i];
+              X_H1[pos] = nh1[i];
+              X_H2[pos] = nh2[i];
+              X_LAST[pos] = nlast[i];
+              X_PRE[pos] = npre[i];
+              X_NENT[pos] = cnt;
+              if (b.dump_k) {
+                const size_t di = ((size_t)trial * b.Tmax + t) * KC_ + pos;
+                b.dump_h1[di] = nh1[i];
+                b.dump_h2[di] = nh2[i];
+                b.dump_pre[di] = npre[i];
+                b.dump_last[di] = nlast[i];
+                b.dump_score[di] = nscore[i];
+              }
+            }
+            const int32_t* srow = m.table + (size_t)npre[i] * VP;
+            for (int u = r; u < (VP >> 2); u += G) cp_async16(rows + pos * VP + u * 4, srow + u * 4);
+          }
+          cp_async_commit();
+          cp_async_wait_all();
+        }
+        if (b.dump_k && tid == 0) b.dump_k[(size_t)trial * b.Tmax + t] = newK;
+        if (tid == 0) {
+          s_K = newK;
+          if (s_fail) s_status = 4;
+          else if (newK == 0) s_status = 2;  // decoder.py:314-315
+        }
+        if (s_fail || newK == 0) fail_t = t;
+      }  // !dead
+    }  // compute warps
+    __syncthreads();  // frame end (whole CTA)
+    LB_PHASE(8);
+    par ^= 1;
+    K = s_K;
+    st_beams_out += K;
+    if (s_status != 0) break;
+
+    // ---- optional interval fusion of the device n-gram scorer (decoder.py:428-430)
+    if (fusion_mode == 1 && t > 0 && (t % c.r) == 0) {
+      for (int i = tid; i < K; i += NT) {
+        Ent* e = C_ENTS + i * OC;
+        const int n = C_NENT[i];
+        const double prev = e[0].total;
+        for (int q = 0; q < n; ++q) {
+          if (e[q].node == 0) {
+            e[q].total = 0.0;
+            e[q].punct = 0;
+          } else {
+            e[q].total = xmul(c.phi, xmul(scale, e[q].cum));
+          }
+        }
+        sort_entries(e, n);
+        C_SCORE[i] = xadd(C_SCORE[i], xsub(e[0].total, prev));
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double ms = -DBL_MAX;
+        for (int i = lane; i < K; i += 32) ms = fmax(ms, C_SCORE[i]);
+        ms = warp_max(ms);
+        if (lane == 0) s_maxs = ms;
+      }
+      __syncthreads();
+      LB_PHASE(10);
+    }
+    LB_PHASE(9);
+  }
+
+  // ---- write back
+  __syncthreads();
+  if (timing)
+    for (int i = 0; i < NPHASE; ++i) b.phase_cycles[(size_t)trial * NPHASE + i] += ph[i];
+#undef LB_PHASE
+  const int status = s_status;
+  if (tid == 0) {
+    if (status != 0) {
+      b.status[trial] = status;
+      b.fail_frame[trial] = fail_t;
+    }
+    b.nbeam[trial] = K;
+    b.ncount[trial] = s_ncount;
+  }
+  if (status == 0 || status == 4) {
+    const size_t hb = (size_t)trial * KC_;
+    for (int i = tid; i < K; i += NT) {
+      b.score[hb + i] = C_SCORE[i];
+      b.h1[hb + i] = C_H1[i];
+      b.h2[hb + i] = C_H2[i];
+      b.last[hb + i] = C_LAST[i];
+      b.prefix[hb + i] = C_PRE[i];
+      b.nent[hb + i] = C_NENT[i];
+    }
+    for (int i = tid; i < K * O; i += NT) {
+      const int bi = i / O, e = i - bi * O;
+      if (e < C_NENT[bi]) b.ents[hb * O + i] = C_ENTS[bi * OC + e];
+    }
+  }
+  atomicAdd(&s_calls, calls_l);
+  atomicAdd(&s_probes, probes_l);
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long* stt = b.stats + (size_t)trial * 8;
+    stt[0] += (unsigned long long)(te - tb);
+    stt[1] += st_beams_in;
+    stt[2] += st_beams_out;
+    stt[3] += s_calls;
+    stt[4] += s_probes;
+    stt[5] += st_bound;
+    stt[7] += st_fallback;
+  }
+#undef BUF
+#undef C_SCORE
+#undef C_H1
+#undef C_H2
+#undef C_LAST
+#undef C_PRE
+#undef C_NENT
+#undef C_ENTS
+#undef X_SCORE
+#undef X_H1
+#undef X_H2
+#undef X_LAST
+#undef X_PRE
+#undef X_NENT
+#undef X_ENTS
+}
+
+// =====================================================================================
 // K3: end-of-utterance closure (decoder.py:375-405), one CTA per trial, warp per beam
 // =====================================================================================
 __global__ void __launch_bounds__(256) close_kernel(ModelDev m, CfgDev c, BatchDev b) {
@@ -1620,8 +2581,14 @@ namespace lbk {
 
 int max_threads_for(int K) { return K <= 64 ? 256 : (K <= 256 ? 512 : 960); }
 
+int small_smem_bytes() { return small::TOTAL; }
+int small_gscratch_bytes() { return small::GTOTAL; }
+
 cudaError_t set_smem_limit(int nthreads, int64_t bytes) {
   cudaError_t e = cudaSuccess;
+  e = cudaFuncSetAttribute(frames_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           small::TOTAL);
+  if (e != cudaSuccess) return e;
 #define LB_SET(NCV)                                                                          \
   e = cudaFuncSetAttribute(frames_kernel<NCV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)bytes);                                                      \
@@ -1674,6 +2641,11 @@ cudaError_t reset(const ModelDev& m, const BatchDev& b, cudaStream_t st) {
 cudaError_t frames(const ModelDev& m, const CfgDev& c, const BatchDev& b, const Layout& L, int t0,
                    int t1, int fusion_mode, double scale, cudaStream_t st) {
   const size_t sm = (size_t)L.smem_bytes;
+  if (L.small) {
+    frames_small_kernel<<<b.B, small::NT, sm, st>>>(m, c, b, t0, t1, fusion_mode, scale);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   bool all_smem = true;
   for (int r = 0; r < N_REGIONS; ++r)
     if (r != R_WARP && !L.in_smem[r]) all_smem = false;

@@ -261,8 +261,8 @@ class DeviceBatch:
         N.check(N.lib().lb_batch_clear_stats(self.h))
 
     PHASES = ("top_U", "cand_S1wait", "collect", "sort", "materialise", "ngram_G3", "recomb_rank",
-              "recomb_keep", "scatter", "loop_tail", "fusion", "cand_loop", "ngram_G2",
-              "ngram_G2wait", "p14", "p15")
+              "recomb_keep", "scatter", "loop_tail", "fusion", "cand_loop", "F_work",
+              "F_start", "F_head", "p15")
 
     def enable_phase_timing(self, on: bool = True):
         N.check(N.lib().lb_batch_enable_phase_timing(self.h, int(on)))
