@@ -204,6 +204,11 @@ int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* b
                      double* best_score, int32_t* nbest_count, int64_t* nbest_text_off,
                      int32_t* nbest_text_len, double* nbest_score);
 
+/* Page-locked host memory (cudaHostAlloc) for input staging: H2D copies from it run at full
+ * link speed and stay asynchronous. */
+int lb_host_alloc(int64_t bytes, void** out);
+int lb_host_free(void* p);
+
 /* Device-side timing of everything enqueued between mark_begin and mark_end (CUDA events on
  * the batch stream); also the number of kernels this library launched in between. */
 int lb_batch_mark_begin(lb_batch* b);

@@ -140,6 +140,8 @@ _SIGS = {
     "lb_batch_mark_begin": (C.c_int, [_P]),
     "lb_batch_mark_end": (C.c_int, [_P, _P, _P]),
     "lb_batch_sync": (C.c_int, [_P]),
+    "lb_host_alloc": (C.c_int, [_I64, _P]),
+    "lb_host_free": (C.c_int, [_P]),
     "lb_log_softmax_host": (C.c_int, [_P, _I64, _I32, _D, _P, _I32]),
     "lb_model_score_words": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P]),
 }
@@ -178,6 +180,38 @@ def check(rc: int) -> None:
 
 def ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
+
+
+class PinnedArray(np.ndarray):
+    """numpy view of page-locked host memory; freed when the last view goes away."""
+
+    def __array_finalize__(self, obj):
+        self._owner = getattr(obj, "_owner", None)
+
+
+class _Pinned:
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        check(lib().lb_host_alloc(nbytes, C.byref(p)))
+        self.ptr = p
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib(False).lb_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
+    """Page-locked host array (fast, asynchronous H2D input staging for decode_batch_raw)."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) * dt.itemsize
+    owner = _Pinned(n)
+    buf = (C.c_char * max(n, 1)).from_address(owner.ptr.value)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape).view(PinnedArray)
+    arr._owner = owner
+    return arr
 
 
 def log_softmax_host(frames: np.ndarray, alpha: float, device: int = 0) -> np.ndarray:

@@ -9,6 +9,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <string_view>
+#include <thread>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/lightbeam_b200.h"
@@ -731,6 +734,77 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
   CK(cudaStreamSynchronize(b->st));
   static const char* PUN[4] = {"", ".", "?", "!"};
   const auto& surf = b->m->surfaces;
+  // per-trial assembly (decoder.py:433-460), trials spread over host threads
+  struct TrialOut {
+    std::string best;
+    double best_score = 0.0;
+    std::vector<std::string> texts;
+    std::vector<double> scores;
+  };
+  std::vector<TrialOut> outs(B);
+  auto assemble = [&](int t) {
+    if (status[t] != 0) return;
+    TrialOut& to = outs[t];
+    const int K = nbeam[t];
+    const int64_t e0 = b->h_entry_off[t], e1 = b->h_entry_off[t + 1];
+    std::vector<int64_t> first(K + 1, e1);
+    for (int64_t e = e1 - 1; e >= e0; --e) first[e_beam[e]] = e;
+    first[K] = e1;
+    for (int i = K - 1; i >= 0; --i)
+      if (first[i] > first[i + 1]) first[i] = first[i + 1];
+    std::vector<std::string> texts(e1 - e0);
+    for (int64_t e = e0; e < e1; ++e) {
+      std::string& s2 = texts[e - e0];
+      size_t len = 1;
+      for (int64_t w = woff[e]; w < woff[e + 1]; ++w) len += surf[words[w]].size() + 1;
+      s2.reserve(len);
+      for (int64_t w = woff[e]; w < woff[e + 1]; ++w) {
+        if (w > woff[e]) s2.push_back(' ');
+        s2 += surf[words[w]];
+      }
+      s2 += PUN[puncts[e] & 3];
+    }
+    const double* sc = scores.data() + (size_t)t * b->K;
+    std::vector<int> order(K);
+    for (int i = 0; i < K; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sc[x] > sc[y]; });
+    struct Pair {
+      int text;
+      double score;
+    };
+    std::vector<Pair> pairs;
+    pairs.reserve(e1 - e0);
+    for (int i : order) {
+      const double best_lm = totals[first[i]];
+      for (int64_t e = first[i]; e < first[i + 1]; ++e)
+        pairs.push_back({(int)(e - e0), (sc[i] - best_lm) + totals[e]});
+    }
+    std::stable_sort(pairs.begin(), pairs.end(),
+                     [](const Pair& x, const Pair& y) { return x.score > y.score; });
+    const int best = order[0];
+    to.best = texts[first[best] - e0];
+    to.best_score = sc[best];
+    std::unordered_set<std::string_view> seen;
+    seen.reserve(pairs.size() * 2);
+    for (const Pair& pr : pairs) {
+      const std::string& tx = texts[pr.text];
+      if (!seen.insert(std::string_view(tx)).second) continue;
+      to.texts.push_back(tx);
+      to.scores.push_back(pr.score);
+    }
+  };
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nthr = std::min(std::min(hw, 32), std::max(1, B / 8));
+  if (nthr <= 1) {
+    for (int t = 0; t < B; ++t) assemble(t);
+  } else {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nthr; ++w)
+      pool.emplace_back([&, w]() {
+        for (int t = w; t < B; t += nthr) assemble(t);
+      });
+    for (auto& th : pool) th.join();
+  }
   b->blob.clear();
   b->best_off.assign(B, 0);
   b->best_len.assign(B, 0);
@@ -739,70 +813,26 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
   b->nb_off.clear();
   b->nb_len.clear();
   b->nb_score.clear();
-  std::vector<std::string> texts;
-  std::vector<int> order;
-  struct Pair {
-    int text;
-    double score;
-  };
-  std::vector<Pair> pairs;
+  size_t total = 0;
+  for (int t = 0; t < B; ++t) {
+    total += outs[t].best.size();
+    for (const auto& x : outs[t].texts) total += x.size();
+  }
+  b->blob.reserve(total);
   for (int t = 0; t < B; ++t) {
     if (status[t] != 0) continue;
-    const int K = nbeam[t];
-    const int64_t e0 = b->h_entry_off[t], e1 = b->h_entry_off[t + 1];
-    // entries of beam i: contiguous, beam-major
-    std::vector<int64_t> first(K + 1, e1);
-    for (int64_t e = e1 - 1; e >= e0; --e) first[e_beam[e]] = e;
-    first[K] = e1;
-    for (int i = K - 1; i >= 0; --i)
-      if (first[i] > first[i + 1]) first[i] = first[i + 1];
-    texts.assign(e1 - e0, std::string());
-    for (int64_t e = e0; e < e1; ++e) {
-      std::string& s = texts[e - e0];
-      for (int64_t w = woff[e]; w < woff[e + 1]; ++w) {
-        if (w > woff[e]) s.push_back(' ');
-        s += surf[words[w]];
-      }
-      s += PUN[puncts[e] & 3];
-    }
-    const double* sc = scores.data() + (size_t)t * b->K;
-    order.resize(K);
-    for (int i = 0; i < K; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return sc[a] > sc[c]; });
-    pairs.clear();
-    for (int i : order) {
-      const double best_lm = totals[first[i]];
-      for (int64_t e = first[i]; e < first[i + 1]; ++e) {
-        const double s = (sc[i] - best_lm) + totals[e];
-        pairs.push_back({(int)(e - e0), s});
-      }
-    }
-    std::stable_sort(pairs.begin(), pairs.end(),
-                     [](const Pair& a, const Pair& c) { return a.score > c.score; });
-    const int best = order[0];
+    TrialOut& to = outs[t];
     b->best_off[t] = (int64_t)b->blob.size();
-    b->blob += texts[first[best] - e0];
-    b->best_len[t] = (int32_t)(b->blob.size() - b->best_off[t]);
-    b->best_score[t] = sc[best];
-    std::vector<const std::string*> seen;
-    int cnt = 0;
-    for (const Pair& p : pairs) {
-      const std::string& tx = texts[p.text];
-      bool dup = false;
-      for (const std::string* s : seen)
-        if (*s == tx) {
-          dup = true;
-          break;
-        }
-      if (dup) continue;
-      seen.push_back(&tx);
+    b->blob += to.best;
+    b->best_len[t] = (int32_t)to.best.size();
+    b->best_score[t] = to.best_score;
+    b->nb_count[t] = (int32_t)to.texts.size();
+    for (size_t i = 0; i < to.texts.size(); ++i) {
       b->nb_off.push_back((int64_t)b->blob.size());
-      b->blob += tx;
-      b->nb_len.push_back((int32_t)tx.size());
-      b->nb_score.push_back(p.score);
-      ++cnt;
+      b->blob += to.texts[i];
+      b->nb_len.push_back((int32_t)to.texts[i].size());
+      b->nb_score.push_back(to.scores[i]);
     }
-    b->nb_count[t] = cnt;
   }
   *blob_bytes = (int64_t)b->blob.size();
   *total_nbest = (int64_t)b->nb_score.size();
@@ -827,6 +857,17 @@ int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* b
     if (nbest_text_len) nbest_text_len[i] = b->nb_len[i];
     if (nbest_score) nbest_score[i] = b->nb_score[i];
   }
+  return LB_OK;
+}
+
+int lb_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(LB_ERR_ARG, "bad arguments");
+  CK(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocPortable));
+  return LB_OK;
+}
+
+int lb_host_free(void* p) {
+  if (p) CK(cudaFreeHost(p));
   return LB_OK;
 }
 

@@ -1504,7 +1504,8 @@ __global__ void __launch_bounds__(small::NT, 2)
         // pair table: each parent writes its own (entry, surface) pairs -- no search
         int4* qinfo = reinterpret_cast<int4*>(sm + O_QINFO);
         for (int p = gt; p < K; p += NGT) {
-          const int q0 = ppoff[p], q1 = ppoff[p + 1];
+          // ppoff[K] is written by thread 0 without a barrier: use the scan total instead
+          const int q0 = ppoff[p], q1 = p + 1 < K ? ppoff[p + 1] : P;
           if (q0 == q1) continue;
           const CompHdr ch = comp_hdr(rows + p * VP, V);
           for (int q = q0; q < q1; ++q) {
@@ -2317,6 +2318,35 @@ __global__ void count_entries_kernel(BatchDev b, int64_t* counts) {
   }
 }
 
+// block-wide exclusive scan of one int64 per thread (blockDim.x <= 1024); returns the block total
+__device__ int64_t block_excl_scan(int64_t v, int64_t* out_excl) {
+  __shared__ int64_t wsum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int64_t incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(FULLMASK, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < nw ? wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(FULLMASK, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) wsum[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const int64_t before = warp ? wsum[warp - 1] : 0;
+  const int64_t total = wsum[nw - 1];
+  *out_excl = before + incl - v;
+  __syncthreads();
+  return total;
+}
+
+// entries of every beam in beam order with their word-id sequences (apply_llm texts,
+// decoder.py:338-345); prefix sums are block scans, chains are walked in parallel
 __global__ void write_entries_kernel(BatchDev b, const int64_t* entry_off, const int64_t* word_off,
                                      int32_t* e_trial, int32_t* e_beam, int64_t* e_woff,
                                      int32_t* words, double* totals, int32_t* puncts) {
@@ -2326,47 +2356,38 @@ __global__ void write_entries_kernel(BatchDev b, const int64_t* entry_off, const
   const size_t nbase = (size_t)trial * b.ncap;
   const int K = b.nbeam[trial];
   const int O = b.O;
-  extern __shared__ int64_t sh_off[];  // [K + 1] entry prefix; then word prefix per entry
-  if (threadIdx.x == 0) {
-    int64_t e = 0;
-    for (int i = 0; i < K; ++i) {
-      sh_off[i] = e;
-      e += b.nent[hb + i];
+  int64_t ecarry = entry_off[trial], wcarry = word_off[trial];
+  for (int base = 0; base < K; base += blockDim.x) {  // uniform trip count over the block
+    const int i = base + threadIdx.x;
+    int ne = 0;
+    int64_t nw = 0;
+    if (i < K) {
+      ne = b.nent[hb + i];
+      for (int q = 0; q < ne; ++q) nw += b.ents[(hb + i) * O + q].depth;
     }
-    sh_off[K] = e;
-  }
-  __syncthreads();
-  const int64_t ebase = entry_off[trial];
-  // word offsets need a prefix over entries in order: do it serially per trial (<= K*O entries)
-  if (threadIdx.x == 0) {
-    int64_t w = word_off[trial];
-    for (int i = 0; i < K; ++i) {
-      const int n = b.nent[hb + i];
-      for (int q = 0; q < n; ++q) {
-        const int64_t idx = ebase + sh_off[i] + q;
-        e_woff[idx] = w;
-        w += b.ents[(hb + i) * O + q].depth;
+    int64_t eex, wex;
+    const int64_t etot = block_excl_scan(ne, &eex);
+    const int64_t wtot = block_excl_scan(nw, &wex);
+    if (i < K) {
+      int64_t idx = ecarry + eex, wp0 = wcarry + wex;
+      for (int q = 0; q < ne; ++q, ++idx) {
+        const Ent E = b.ents[(hb + i) * O + q];
+        e_trial[idx] = trial;
+        e_beam[idx] = i;
+        totals[idx] = E.total;
+        puncts[idx] = E.punct;
+        e_woff[idx] = wp0;
+        uint32_t node = E.node;
+        int64_t wp = wp0 + E.depth - 1;
+        while (node != 0) {
+          words[wp--] = (int32_t)b.nsurf[nbase + node];
+          node = b.nparent[nbase + node];
+        }
+        wp0 += E.depth;
       }
     }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    const int n = b.nent[hb + i];
-    for (int q = 0; q < n; ++q) {
-      const int64_t idx = ebase + sh_off[i] + q;
-      const Ent E = b.ents[(hb + i) * O + q];
-      e_trial[idx] = trial;
-      e_beam[idx] = i;
-      totals[idx] = E.total;
-      puncts[idx] = E.punct;
-      uint32_t node = E.node;
-      const uint32_t d = E.depth;
-      int64_t wp = e_woff[idx] + d - 1;
-      while (node != 0) {
-        words[wp--] = (int32_t)b.nsurf[nbase + node];
-        node = b.nparent[nbase + node];
-      }
-    }
+    ecarry += etot;
+    wcarry += wtot;
   }
 }
 
@@ -2695,9 +2716,8 @@ cudaError_t count_entries(const BatchDev& b, int64_t* counts, cudaStream_t st) {
 cudaError_t write_entries(const BatchDev& b, const int64_t* entry_off, const int64_t* word_off,
                           int32_t* e_trial, int32_t* e_beam, int64_t* e_woff, int32_t* words,
                           double* totals, int32_t* puncts, cudaStream_t st) {
-  const size_t sm = (size_t)(b.K + 1) * sizeof(int64_t);
-  write_entries_kernel<<<b.B, 128, sm, st>>>(b, entry_off, word_off, e_trial, e_beam, e_woff, words,
-                                             totals, puncts);
+  write_entries_kernel<<<b.B, 256, 0, st>>>(b, entry_off, word_off, e_trial, e_beam, e_woff, words,
+                                            totals, puncts);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -330,18 +330,26 @@ class DeviceBatch:
                                      N.ptr(cnt), N.ptr(noff), N.ptr(nlen), N.ptr(nsc)))
         raw = blob.raw[: nbytes.value]
         st, _ = self.status()
+        text_all = raw.decode("utf-8")
+        ascii_only = len(text_all) == len(raw)
+        boff_l, blen_l, bsc_l, cnt_l = boff.tolist(), blen.tolist(), bsc.tolist(), cnt.tolist()
+        noff_l, nlen_l, nsc_l = noff.tolist(), nlen.tolist(), nsc.tolist()
         out = []
         k = 0
         for i in range(n):
             if st[i] != 0:
                 out.append(None)
                 continue
-            text = raw[boff[i]: boff[i] + blen[i]].decode("utf-8")
-            nb = []
-            for j in range(k, k + cnt[i]):
-                nb.append((raw[noff[j]: noff[j] + nlen[j]].decode("utf-8"), float(nsc[j])))
-            k += cnt[i]
-            out.append((text, float(bsc[i]), nb))
+            if ascii_only:
+                text = text_all[boff_l[i]: boff_l[i] + blen_l[i]]
+                nb = [(text_all[noff_l[j]: noff_l[j] + nlen_l[j]], nsc_l[j])
+                      for j in range(k, k + cnt_l[i])]
+            else:
+                text = raw[boff_l[i]: boff_l[i] + blen_l[i]].decode("utf-8")
+                nb = [(raw[noff_l[j]: noff_l[j] + nlen_l[j]].decode("utf-8"), nsc_l[j])
+                      for j in range(k, k + cnt_l[i])]
+            k += cnt_l[i]
+            out.append((text, bsc_l[i], nb))
         return out
 
 

@@ -1,0 +1,27 @@
+"""Time the stages of decode_batch_raw on the BASELINE config-2 workload (diagnostic)."""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+
+from paper_2603_14002_b200 import DeviceNgramScorer, PROFILES, synth
+from paper_2603_14002_b200 import decoder as D
+
+w = synth.make_world()
+cfg = PROFILES["b2t25"].replace(beam_size=64)
+raws = synth.make_logits(256, 500, 41, base_seed=1000)
+frames = np.full(256, 500, dtype=np.int32)
+sc = DeviceNgramScorer(w.model, cfg.ngram_weight / cfg.llm_weight)
+dm = D.device_model(w.table, w.model)
+for rep in range(3):
+    t = [time.perf_counter()]
+    batch = dm.batch(cfg, 256, 500)
+    batch.load_logits(raws, frames); batch.sync(); t.append(time.perf_counter())
+    D.run_search(batch, cfg, sc, w.model, True); batch.sync(); t.append(time.perf_counter())
+    st, ff = batch.status(); t.append(time.perf_counter())
+    res = batch.results(); t.append(time.perf_counter())
+    out = D._collect(batch, cfg, True, 0.0); t.append(time.perf_counter())
+    names = ["h2d+prologue", "search", "status", "results(gather+assemble+py)", "collect(again)"]
+    print({n: round((b - a) * 1e3, 2) for n, a, b in zip(names, t, t[1:])})
