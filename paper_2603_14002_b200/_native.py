@@ -28,7 +28,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off",
     "-shared",
 ]
-SOURCES = ["lb_kernels.cu", "lb_capi.cu"]
+SOURCES = ["lb_kernels.cu", "lb_capi.cu", "lb_llm.cu"]
 
 
 def build(verbose: bool = False, force: bool = False) -> Path:
@@ -104,6 +104,25 @@ class LbStats(C.Structure):
         "history_nodes", "fallback_selects")]
 
 
+class LbLlmDesc(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int32),
+        ("n_heads", C.c_int32),
+        ("n_kv_heads", C.c_int32),
+        ("head_dim", C.c_int32),
+        ("hidden", C.c_int32),
+        ("vocab", C.c_int32),
+        ("max_slots", C.c_int64),
+        ("max_depth", C.c_int32),
+        ("bos_token", C.c_int32),
+        ("punct_tokens", C.c_int32 * 3),
+        ("surface_tokens", C.c_void_p),
+        ("surface_tokens_first", C.c_void_p),
+        ("n_surfaces", C.c_int32),
+        ("embedding", C.c_void_p),
+    ]
+
+
 _P = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
@@ -144,7 +163,23 @@ _SIGS = {
     "lb_host_free": (C.c_int, [_P]),
     "lb_log_softmax_host": (C.c_int, [_P, _I64, _I32, _D, _P, _I32]),
     "lb_model_score_words": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P]),
+    "lb_llm_create": (C.c_int, [_P, C.POINTER(LbLlmDesc), _P]),
+    "lb_llm_destroy": (C.c_int, [_P]),
+    "lb_llm_footprint": (C.c_int, [_P, _P]),
+    "lb_llm_reset": (C.c_int, [_P]),
+    "lb_llm_plan": (C.c_int, [_P, _I32, _I32, _P, _P]),
+    "lb_llm_wave_rows": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
+    "lb_llm_finish": (C.c_int, [_P, _I32, _I32]),
+    "lb_llm_rmsnorm": (C.c_int, [_P, _P, _P, _P, C.c_float, _I32, _P, _P]),
+    "lb_llm_rope_kv": (C.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _P, _P]),
+    "lb_llm_attention": (C.c_int, [_P, _I32, _P, _I32, _P, _P, _P]),
+    "lb_llm_swiglu": (C.c_int, [_P, _P, _I32, _I32, _P]),
+    "lb_llm_lse": (C.c_int, [_P, _P, _I32, _I64, _P]),
+    "lb_llm_stats": (C.c_int, [_P, _P]),
+    "lb_llm_export": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
 }
+
+LLM_MAX_WAVES = 512
 
 _lib = None
 

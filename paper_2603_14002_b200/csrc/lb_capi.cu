@@ -17,6 +17,7 @@
 #include "../../include/lightbeam_b200.h"
 #include "lb_device.cuh"
 #include "lb_internal.h"
+#include "lb_structs.h"
 
 using namespace lbd;
 
@@ -86,58 +87,11 @@ bool cuckoo_build(const lb_ngram_desc* nd, uint32_t nb, std::vector<NgRec>& tab,
 }
 }  // namespace
 
-struct lb_model {
-  int device = 0;
-  ModelDev dev{};
-  int32_t* d_table = nullptr;
-  int32_t* d_comp_off = nullptr;
-  int32_t* d_comp_surf = nullptr;
-  int32_t* d_comp_lm = nullptr;
-  NgRec* d_ng = nullptr;
-  int64_t ng_cap = 0;
-  int max_probe = 0;
-  int64_t bytes = 0;
-  std::vector<std::string> surfaces;
-};
 
-struct lb_batch {
-  lb_model* m = nullptr;
-  lb_config cfg{};
-  CfgDev cdev{};
-  cudaStream_t st = nullptr;
-  int32_t Bmax = 0, Tmax = 0, K = 0, O = 0, VPD = 0;
-  BatchDev dev{};
-  Layout L{};
-  int32_t n_trials = 0;
-  std::vector<int32_t> T_host;
-  int32_t* d_T = nullptr;
-  double* d_D = nullptr;
-  float* d_x = nullptr;
-  // gather scratch
-  int64_t* d_counts = nullptr;
-  int64_t* d_entry_off = nullptr;
-  int64_t* d_word_off = nullptr;
-  int64_t cap_entries = 0, cap_words = 0;
-  int32_t* d_e_trial = nullptr;
-  int32_t* d_e_beam = nullptr;
-  int64_t* d_e_woff = nullptr;
-  int32_t* d_words = nullptr;
-  double* d_totals = nullptr;
-  int32_t* d_puncts = nullptr;
-  double* d_scores_in = nullptr;
-  int32_t* d_puncts_in = nullptr;
-  uint8_t* d_has_text = nullptr;
-  int64_t n_entries = 0, n_words = 0;
-  std::vector<int64_t> h_entry_off, h_word_off;
-  // results cache
-  std::string blob;
-  std::vector<int64_t> best_off, nb_off;
-  std::vector<int32_t> best_len, nb_count, nb_len;
-  std::vector<double> best_score, nb_score;
-  // timing
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  unsigned long long launch_mark = 0;
-};
+
+namespace lbh {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace lbh
 
 extern "C" {
 

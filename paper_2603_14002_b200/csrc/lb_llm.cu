@@ -1,0 +1,1083 @@
+// lb_llm.cu -- delayed LLM fusion on the device: the prefix-trie KV cache behind a
+// Llama-architecture scorer and the kernels around its transformer body.
+//
+// Reference semantics (what is computed):
+//   apply_llm            decoder.py:329-372  (texts of every ortho entry, replace lm_total by
+//                        llm_weight * score, final pass picks punctuation, beam delta)
+//   score_texts/score_eos  scorer.py:285-325 (dedupe, chunking: results are chunk-invariant)
+//   sidecar convention   sidecar/src/model.ts:35-47,116-137 (BOS + tokens of the sentence-cased
+//                        text, score = sum of natural-log next-token probabilities, empty text
+//                        scores 0, eos = best of text+".", "?", "!" with strict > so ties -> ".")
+//
+// How (B200 design): every text at a fusion event is a path in the decoder's word-history
+// trie, and one word is one token, so the token sequences of all texts of all utterances form
+// one prefix trie.  Each trie node ("slot") is evaluated once per batch decode:
+//   - slots are hash-consed on (parent slot, token) so equal texts share one slot;
+//   - a slot's log-prob needs only its parent's final hidden state and log-sum-exp
+//     (lp = h_parent . E[token] - lse_parent), so the transformer forward runs only for slots
+//     that get children or need end-of-sentence punctuation ("forward set"), in dependency
+//     waves (a wave's rows attend to K/V of slots forwarded in earlier waves/events);
+//   - attention reads K/V straight from the slot cache through per-row ancestor chains (page
+//     size one token), so surviving beams never copy or reorder KV: the cache is indexed by
+//     text, not by beam, and a beam reorder is free.
+// Text score = cum[slot] = sum of lp along the path in root-to-leaf order (fp64), exactly the
+// order of the sidecar's full-sequence sum.
+//
+// Kernels:
+//   map_nodes_kernel      word-history nodes of live entries -> slots (per utterance CTA,
+//                         levels of unmapped ancestors resolved in order, global hash-consing)
+//   schedule_kernel       cum-needed slots and the forward set of this event
+//   level_kernel / scatter_kernel   dependency waves of the forward set (counting sort)
+//   wave_rows_kernel      tokens, positions, ancestor chains of a wave's rows
+//   add_rmsnorm_kernel    residual add + RMSNorm (fp32 residual stream, bf16 GEMM operand)
+//   rope_kv_kernel        rotary embedding of q/k, K/V written into the slot cache
+//   chain_attn_kernel     causal GQA attention of one new token over its ancestor chain
+//   swiglu_kernel         silu(gate) * up
+//   lse_kernel            K6: row log-sum-exp of the LM-head logits (128k vocab)
+//   lp_kernel / cum_kernel  K6 gather: next-token log-prob and running text score
+//   punct_kernel          end-of-sentence punctuation log-probs of final texts
+//   llm_apply_kernel      K7: fusion into the ortho entries and beam scores
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lightbeam_b200.h"
+#include "lb_device.cuh"
+#include "lb_internal.h"
+#include "lb_structs.h"
+
+using namespace lbd;
+typedef __nv_bfloat16 bf16;
+
+#define FULLMASK 0xffffffffu
+
+namespace {
+
+constexpr int MAX_LEVELS = LB_LLM_MAX_WAVES;
+
+struct LlmDev {
+  int32_t L, NH, NKV, HD, H, vocab;
+  int64_t cap;        // slot capacity
+  int32_t max_depth;  // deepest slot (tokens after BOS); chain pitch = max_depth + 1
+  int32_t* s_parent;
+  int32_t* s_token;
+  int32_t* s_depth;
+  int32_t* s_fwd;  // 0 none, 1 scheduled, 2 forwarded (K/V, hidden, lse present)
+  int32_t* s_cum;  // 0 none, 1 scheduled, 2 score ready
+  int32_t* s_pun;  // 0 none, 1 punctuation log-probs present
+  double* s_lp;
+  double* s_cumv;
+  double* s_plp;  // [cap][3]
+  float* s_lse;
+  float* s_h;  // [cap][H] final normed hidden state (fp32: the next-token dot products)
+  bf16* kc;    // [L][cap][NKV*HD]
+  bf16* vc;
+  int32_t* htab;
+  uint32_t hmask;
+  int32_t* ctr;  // see C_* below
+  int32_t* node_slot;  // [B][ncap]
+  int32_t* nlist;      // [B][nlist_cap] claimed nodes of this event
+  int32_t* nlist_depth;
+  int32_t nlist_cap;
+  int32_t* fwd_list;
+  int32_t* fwd_level;
+  int32_t* cum_list;
+  int32_t* wave_slots;
+  int32_t* lvl_count;  // [MAX_LEVELS]
+  int32_t* lvl_fill;   // [MAX_LEVELS]
+  const int32_t* tok_low;
+  const int32_t* tok_cap;
+  int32_t n_surf;
+  int32_t bos_tok;
+  int32_t punct_tok[3];
+  const bf16* emb;
+};
+
+enum {
+  C_SLOTS = 0,   // slots allocated
+  C_ERR = 1,     // bit 1: slot capacity, 2: node list, 4: depth, 8: levels
+  C_NFWD = 2,    // forward-set size of this event
+  C_NCUM = 3,    // cum-needed slots of this event
+  C_BOS = 4,     // 1: BOS slot still to be forwarded
+  C_NCTR = 8
+};
+
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+
+__device__ __forceinline__ int ld_vol(const int32_t* p) { return *(const volatile int32_t*)p; }
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_maxf(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULLMASK, v, o));
+  return v;
+}
+
+// insertion sort of <= OMAX entries by (-total, seq) (decoder.py:369)
+__device__ __forceinline__ void sort_ents(Ent* e, int n) {
+  for (int i = 1; i < n; ++i) {
+    Ent x = e[i];
+    int j = i - 1;
+    while (j >= 0 && (e[j].total < x.total || (e[j].total == x.total && e[j].seq > x.seq))) {
+      e[j + 1] = e[j];
+      --j;
+    }
+    e[j + 1] = x;
+  }
+}
+
+// ------------------------------------------------------------------ slot hash-consing
+// Slot ids live in an open-addressing table; a key (parent slot, token) is compared through
+// the slot's own fields, which the inserting thread publishes before its CAS.
+__device__ int hashcons(const LlmDev& l, int ps, int tok, int depth) {
+  const uint64_t key = ((uint64_t)(uint32_t)ps << 32) | (uint32_t)tok;
+  uint32_t h = (uint32_t)mix64(key) & l.hmask;
+  int mine = -1;
+  for (uint32_t probe = 0; probe <= l.hmask; ++probe) {
+    int v = ld_vol(l.htab + h);
+    if (v < 0) {
+      if (mine < 0) {
+        mine = atomicAdd(l.ctr + C_SLOTS, 1);
+        if (mine >= l.cap) {
+          atomicOr(l.ctr + C_ERR, 1);
+          return -1;
+        }
+        l.s_parent[mine] = ps;
+        l.s_token[mine] = tok;
+        l.s_depth[mine] = depth;
+        l.s_fwd[mine] = 0;
+        l.s_cum[mine] = 0;
+        l.s_pun[mine] = 0;
+        __threadfence();
+      }
+      v = atomicCAS(l.htab + h, -1, mine);
+      if (v < 0) return mine;
+    }
+    __threadfence();
+    if (ld_vol(l.s_parent + v) == ps && ld_vol(l.s_token + v) == tok) {
+      if (mine >= 0) l.s_parent[mine] = -2;  // lost an insert race: tombstone the spare slot
+      return v;
+    }
+    h = (h + 1) & l.hmask;
+  }
+  atomicOr(l.ctr + C_ERR, 1);
+  return -1;
+}
+
+// ------------------------------------------------------------------ event planning
+// Node -> slot for every node on the word-history path of a live entry.  Nodes without a slot
+// are claimed (-1 -> -2) by exactly one walker, listed, then resolved level by level: a node
+// is ready once its parent has a slot.
+__global__ void __launch_bounds__(256) map_nodes_kernel(BatchDev b, LlmDev l, int min_frames) {
+  const int trial = blockIdx.x;
+  if (b.status[trial] != 0 || b.T[trial] <= min_frames) return;
+  __shared__ int s_n, s_more;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  const size_t hb = (size_t)trial * b.K;
+  const size_t nb = (size_t)trial * b.ncap;
+  const size_t lb = (size_t)trial * l.nlist_cap;
+  int32_t* ns = l.node_slot + nb;
+  const int K = b.nbeam[trial], O = b.O;
+  for (int i = threadIdx.x; i < K * O; i += blockDim.x) {
+    const int beam = i / O, q = i - beam * O;
+    if (q >= b.nent[hb + beam]) continue;
+    const Ent& E = b.ents[(hb + beam) * O + q];
+    uint32_t n = E.node;
+    int d = E.depth;
+    while (true) {
+      if (ld_vol(ns + n) != -1) break;
+      if (atomicCAS(ns + n, -1, -2) != -1) break;
+      const int idx = atomicAdd(&s_n, 1);
+      if (idx < l.nlist_cap) {
+        l.nlist[lb + idx] = (int)n;
+        l.nlist_depth[lb + idx] = d;
+      } else {
+        atomicOr(l.ctr + C_ERR, 2);
+      }
+      n = b.nparent[nb + n];
+      --d;
+    }
+  }
+  __syncthreads();
+  const int nn = min(s_n, l.nlist_cap);
+  for (int iter = 0; iter < 4 * 1024; ++iter) {
+    if (threadIdx.x == 0) s_more = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < nn; j += blockDim.x) {
+      const int n = l.nlist[lb + j];
+      if (ld_vol(ns + n) >= 0) continue;
+      const int p = (int)b.nparent[nb + n];
+      const int ps = ld_vol(ns + p);
+      if (ps < 0) {
+        s_more = 1;
+        continue;
+      }
+      const int d = l.nlist_depth[lb + j];
+      int s = -1;
+      if (d > l.max_depth) {
+        atomicOr(l.ctr + C_ERR, 4);
+      } else {
+        const int surf = (int)b.nsurf[nb + n];
+        const int tok = (d == 1 ? l.tok_cap : l.tok_low)[surf];
+        s = hashcons(l, ps, tok, d);
+      }
+      ns[n] = s < 0 ? 0 : s;  // on error map to the root so the walk terminates
+    }
+    __syncthreads();
+    if (!s_more) break;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void push(int32_t* list, int32_t* ctr, int32_t v, int64_t cap) {
+  const int idx = atomicAdd(ctr, 1);
+  if (idx < cap) list[idx] = v;
+}
+
+// Scores still missing on the paths of live entries, and the slots whose forward they need.
+__global__ void __launch_bounds__(128) schedule_kernel(BatchDev b, LlmDev l, int min_frames,
+                                                       int final_) {
+  const int trial = blockIdx.x;
+  if (trial == 0 && threadIdx.x == 0 && l.ctr[C_BOS]) {
+    l.ctr[C_BOS] = 0;
+    push(l.fwd_list, l.ctr + C_NFWD, 0, l.cap);
+  }
+  if (b.status[trial] != 0 || b.T[trial] <= min_frames) return;
+  const size_t hb = (size_t)trial * b.K;
+  const int32_t* ns = l.node_slot + (size_t)trial * b.ncap;
+  const int K = b.nbeam[trial], O = b.O;
+  for (int i = threadIdx.x; i < K * O; i += blockDim.x) {
+    const int beam = i / O, q = i - beam * O;
+    if (q >= b.nent[hb + beam]) continue;
+    const Ent& E = b.ents[(hb + beam) * O + q];
+    int cur = ns[E.node];
+    if (final_ && cur != 0 && atomicCAS(l.s_fwd + cur, 0, 1) == 0)
+      push(l.fwd_list, l.ctr + C_NFWD, cur, l.cap);
+    while (cur != 0) {
+      if (ld_vol(l.s_cum + cur) != 0) break;
+      if (atomicCAS(l.s_cum + cur, 0, 1) != 0) break;
+      push(l.cum_list, l.ctr + C_NCUM, cur, l.cap);
+      const int p = l.s_parent[cur];
+      if (atomicCAS(l.s_fwd + p, 0, 1) == 0) push(l.fwd_list, l.ctr + C_NFWD, p, l.cap);
+      cur = p;
+    }
+  }
+}
+
+// wave index of a scheduled slot = number of scheduled ancestors
+__global__ void level_kernel(LlmDev l) {
+  const int n = min(l.ctr[C_NFWD], (int)l.cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = l.fwd_list[i];
+    int lvl = 0;
+    for (int cur = l.s_parent[s]; cur >= 0 && l.s_fwd[cur] == 1; cur = l.s_parent[cur]) ++lvl;
+    if (lvl >= MAX_LEVELS) {
+      atomicOr(l.ctr + C_ERR, 8);
+      lvl = MAX_LEVELS - 1;
+    }
+    l.fwd_level[i] = lvl;
+    atomicAdd(l.lvl_count + lvl, 1);
+  }
+}
+
+__global__ void scatter_kernel(LlmDev l) {
+  __shared__ int off[MAX_LEVELS];
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int v = 0; v < MAX_LEVELS; ++v) {
+      off[v] = a;
+      a += l.lvl_count[v];
+    }
+  }
+  __syncthreads();
+  const int n = min(l.ctr[C_NFWD], (int)l.cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int lvl = l.fwd_level[i];
+    const int pos = off[lvl] + atomicAdd(l.lvl_fill + lvl, 1);
+    l.wave_slots[pos] = l.fwd_list[i];
+  }
+}
+
+__global__ void wave_rows_kernel(LlmDev l, int64_t row0, int n, int32_t* tok, int32_t* pos,
+                                 int32_t* slots, int32_t* chains) {
+  const int pitch = l.max_depth + 1;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int s = l.wave_slots[row0 + r];
+    const int d = l.s_depth[s];
+    tok[r] = l.s_token[s];
+    pos[r] = d;
+    slots[r] = s;
+    int cur = s;
+    int32_t* ch = chains + (size_t)r * pitch;
+    for (int j = d; j >= 0; --j) {
+      ch[j] = cur;
+      cur = l.s_parent[cur];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ transformer body
+// x[M][H] fp32 residual (+= delta fp32 when given) -> out = bf16(x * rsqrt(mean(x^2) + eps) * w);
+// `store_slots` also keeps the fp32 row in the slot hidden-state table.
+__global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float* delta,
+                                                          const float* w, float eps, int H,
+                                                          bf16* out, const int32_t* store_slots,
+                                                          float* s_h) {
+  const int row = blockIdx.x;
+  float* xr = x + (size_t)row * H;
+  const float* dr = delta ? delta + (size_t)row * H : nullptr;
+  float ss = 0.f;
+  for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    if (dr) {
+      const float4 a = *reinterpret_cast<const float4*>(dr + i);
+      v.x += a.x;
+      v.y += a.y;
+      v.z += a.z;
+      v.w += a.w;
+      *reinterpret_cast<float4*>(xr + i) = v;
+    }
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / (float)H + eps);
+  bf16* orow = out + (size_t)row * H;
+  float* hrow = store_slots ? s_h + (size_t)store_slots[row] * H : nullptr;
+  for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + i);
+    const float4 g = *reinterpret_cast<const float4*>(w + i);
+    const float4 y = make_float4(v.x * r * g.x, v.y * r * g.y, v.z * r * g.z, v.w * r * g.w);
+    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(orow + i);
+    op[0] = __floats2bfloat162_rn(y.x, y.y);
+    op[1] = __floats2bfloat162_rn(y.z, y.w);
+    if (hrow) *reinterpret_cast<float4*>(hrow + i) = y;
+  }
+}
+
+// qkv[M][(NH + 2 NKV) HD] fp32 -> q_out[M][NH HD] bf16 rotated; rotated k and v stored (bf16)
+// at the row's slot.
+// rotate_half convention: (x1, x2) -> (x1 cos - x2 sin, x2 cos + x1 sin), x1/x2 = halves.
+__global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, const int32_t* pos,
+                               const int32_t* slots, const float* cosT, const float* sinT,
+                               bf16* q_out) {
+  const int row = blockIdx.x;
+  if (row >= M) return;
+  const int HD = l.HD, half = HD / 2, NH = l.NH, NKV = l.NKV;
+  const int W = (NH + 2 * NKV) * HD;
+  const float* in = qkv + (size_t)row * W;
+  const int p = pos[row];
+  const size_t slot = (size_t)slots[row];
+  const size_t kvw = (size_t)NKV * HD;
+  bf16* kd = l.kc + ((size_t)layer * l.cap + slot) * kvw;
+  bf16* vd = l.vc + ((size_t)layer * l.cap + slot) * kvw;
+  const float* cs = cosT + (size_t)p * half;
+  const float* sn = sinT + (size_t)p * half;
+  const int npairs = (NH + NKV) * half;
+  for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
+    const int head = t / half, i = t - head * half;
+    const float* src = in + head * HD;
+    const float x1 = src[i], x2 = src[i + half];
+    const float c = cs[i], s = sn[i];
+    const bf16 o1 = __float2bfloat16_rn(x1 * c - x2 * s);
+    const bf16 o2 = __float2bfloat16_rn(x2 * c + x1 * s);
+    if (head < NH) {
+      bf16* dst = q_out + (size_t)row * NH * HD + head * HD;
+      dst[i] = o1;
+      dst[i + half] = o2;
+    } else {
+      bf16* dst = kd + (head - NH) * HD;
+      dst[i] = o1;
+      dst[i + half] = o2;
+    }
+  }
+  const float* vin = in + (NH + NKV) * HD;
+  for (int t = threadIdx.x; t < NKV * HD; t += blockDim.x) vd[t] = __float2bfloat16_rn(vin[t]);
+}
+
+// One warp per (row, kv head): the G = NH/NKV query heads of the group attend over the row's
+// ancestor chain (BOS .. itself, causal by construction).  Lanes own chain positions for the
+// scores (each lane dots a whole K row held in one 128/256-B line) and head dims for the V sum.
+template <int HD, int G>
+__global__ void __launch_bounds__(256) chain_attn_kernel(LlmDev l, int layer, const bf16* q,
+                                                         int M, const int32_t* chains,
+                                                         const int32_t* pos, float scale,
+                                                         bf16* out) {
+  constexpr int NWB = 8;
+  constexpr int DPL = HD / 32;  // dims per lane in the V sum
+  __shared__ float qs[NWB][G][HD];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * NWB + warp;
+  const int NKV = l.NKV;
+  const int row = gw / NKV, kvh = gw - row * NKV;
+  if (row >= M) return;
+  const int NH = l.NH;
+  const bf16* qr = q + (size_t)row * NH * HD + (size_t)kvh * G * HD;
+  for (int t = lane; t < G * HD; t += 32) qs[warp][t / HD][t % HD] = __bfloat162float(qr[t]);
+  __syncwarp();
+  const int n = pos[row] + 1;
+  const int pitch = l.max_depth + 1;
+  const int32_t* ch = chains + (size_t)row * pitch;
+  const size_t kvw = (size_t)NKV * HD;
+  const bf16* kb = l.kc + (size_t)layer * l.cap * kvw + (size_t)kvh * HD;
+  const bf16* vb = l.vc + (size_t)layer * l.cap * kvw + (size_t)kvh * HD;
+  float m[G], den[G], acc[G][DPL];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    den[g] = 0.f;
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
+  }
+  for (int base = 0; base < n; base += 32) {
+    const int j = base + lane;
+    const bool valid = j < n;
+    const int s = valid ? ch[j] : 0;
+    float sc[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) sc[g] = 0.f;
+    if (valid) {
+      const uint4* kr = reinterpret_cast<const uint4*>(kb + (size_t)s * kvw);
+#pragma unroll
+      for (int c = 0; c < HD / 8; ++c) {
+        const uint4 u = kr[c];
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 kf = __bfloat1622float2(k2[e]);
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            sc[g] += qs[warp][g][c * 8 + 2 * e] * kf.x + qs[warp][g][c * 8 + 2 * e + 1] * kf.y;
+        }
+      }
+    }
+    float p[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float x = valid ? sc[g] * scale : -INFINITY;
+      const float mx = fmaxf(m[g], warp_maxf(x));
+      p[g] = valid ? expf(x - mx) : 0.f;
+      const float corr = expf(m[g] - mx);  // exp(-inf) = 0 on the first chunk
+      den[g] = den[g] * corr + warp_sum(p[g]);
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
+      m[g] = mx;
+    }
+    const int cnt = min(32, n - base);
+    for (int jj = 0; jj < cnt; ++jj) {
+      const int sj = __shfl_sync(FULLMASK, s, jj);
+      const bf16* vr = vb + (size_t)sj * kvw + lane * DPL;
+      float v[DPL];
+      if (DPL == 2) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
+        v[0] = f.x;
+        v[DPL - 1] = f.y;
+      } else {
+#pragma unroll
+        for (int d = 0; d < DPL; d += 2) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + d));
+          v[d] = f.x;
+          v[d + 1] = f.y;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float pj = __shfl_sync(FULLMASK, p[g], jj);
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) acc[g][d] += pj * v[d];
+      }
+    }
+  }
+  bf16* orow = out + (size_t)row * NH * HD + (size_t)kvh * G * HD;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float inv = 1.f / den[g];
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) orow[g * HD + lane * DPL + d] = __float2bfloat16_rn(acc[g][d] * inv);
+  }
+}
+
+// gu[M][2F] = [gate | up] -> out[M][F] = bf16(silu(gate) * up)
+__global__ void swiglu_kernel(const bf16* gu, int64_t M, int F, bf16* out) {
+  const int64_t n2 = M * (int64_t)F / 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 2 * i;
+    const int64_t row = e / F, col = e - row * F;
+    const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(gu + row * 2 * F + col));
+    const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(gu + row * 2 * F + F + col));
+    const float a = g.x / (1.f + expf(-g.x)) * u.x;
+    const float b = g.y / (1.f + expf(-g.y)) * u.y;
+    *reinterpret_cast<__nv_bfloat162*>(out + e) = __floats2bfloat162_rn(a, b);
+  }
+}
+
+// K6a: log-sum-exp of one LM-head logit row per CTA (16-B loads, online max/sum merge)
+__global__ void __launch_bounds__(512) lse_kernel(const bf16* logits, int64_t ld, int V,
+                                                  const int32_t* slots, float* s_lse) {
+  const int row = blockIdx.x;
+  const bf16* r = logits + (size_t)row * ld;
+  float m = -INFINITY, s = 0.f;
+  const int nv = V / 8;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const uint4 u = reinterpret_cast<const uint4*>(r)[i];
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+    float x[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(p[e]);
+      x[2 * e] = f.x;
+      x[2 * e + 1] = f.y;
+    }
+    float mx = x[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) mx = fmaxf(mx, x[e]);
+    const float nm = fmaxf(m, mx);
+    float acc = s * expf(m - nm);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc += expf(x[e] - nm);
+    m = nm;
+    s = acc;
+  }
+  for (int i = nv * 8 + threadIdx.x; i < V; i += blockDim.x) {
+    const float x = __bfloat162float(r[i]);
+    const float nm = fmaxf(m, x);
+    s = s * expf(m - nm) + expf(x - nm);
+    m = nm;
+  }
+  // merge (m, s) across the block
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(FULLMASK, m, o), s2 = __shfl_xor_sync(FULLMASK, s, o);
+    const float nm = fmaxf(m, m2);
+    s = (nm == -INFINITY) ? 0.f : s * expf(m - nm) + s2 * expf(m2 - nm);
+    m = nm;
+  }
+  __shared__ float sm[32], ssum[32];
+  if ((threadIdx.x & 31) == 0) {
+    sm[threadIdx.x >> 5] = m;
+    ssum[threadIdx.x >> 5] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M2 = sm[0], S2 = ssum[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      const float nm = fmaxf(M2, sm[w]);
+      if (nm == -INFINITY) continue;
+      S2 = S2 * expf(M2 - nm) + ssum[w] * expf(sm[w] - nm);
+      M2 = nm;
+    }
+    s_lse[slots[row]] = M2 + logf(S2);
+  }
+}
+
+// fp32 dot of an fp32 hidden row and a bf16 embedding row of length H by one warp (fixed
+// order: lane stride, xor tree)
+__device__ __forceinline__ float warp_dot(const float* a, const bf16* b, int H) {
+  float acc = 0.f;
+  for (int i = threadIdx.x % 32 * 8; i < H; i += 256) {
+    const float4 a0 = *reinterpret_cast<const float4*>(a + i);
+    const float4 a1 = *reinterpret_cast<const float4*>(a + i + 4);
+    const uint4 ub = *reinterpret_cast<const uint4*>(b + i);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&ub);
+    const float2 b0 = __bfloat1622float2(pb[0]), b1 = __bfloat1622float2(pb[1]);
+    const float2 b2 = __bfloat1622float2(pb[2]), b3 = __bfloat1622float2(pb[3]);
+    acc += a0.x * b0.x;
+    acc += a0.y * b0.y;
+    acc += a0.z * b1.x;
+    acc += a0.w * b1.y;
+    acc += a1.x * b2.x;
+    acc += a1.y * b2.y;
+    acc += a1.z * b3.x;
+    acc += a1.w * b3.y;
+  }
+  return warp_sum(acc);
+}
+
+// K6b: lp[s] = h[parent] . E[token] - lse[parent]
+__global__ void lp_kernel(LlmDev l) {
+  const int n = min(l.ctr[C_NCUM], (int)l.cap);
+  const int lane = threadIdx.x & 31;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
+    const int s = l.cum_list[w];
+    const int p = l.s_parent[s];
+    const float dot = warp_dot(l.s_h + (size_t)p * l.H, l.emb + (size_t)l.s_token[s] * l.H, l.H);
+    if (lane == 0) l.s_lp[s] = (double)dot - (double)l.s_lse[p];
+  }
+}
+
+// running score: cum[s] = (((cum[anchor] + lp[a1]) + lp[a2]) + ... + lp[s]) in root-to-leaf
+// order, anchor = nearest ancestor whose score was ready before this event
+__global__ void cum_kernel(LlmDev l) {
+  constexpr int LOC = 64;
+  const int n = min(l.ctr[C_NCUM], (int)l.cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = l.cum_list[i];
+    int chain[LOC];
+    int k = 0;
+    int cur = s;
+    while (cur != 0 && l.s_cum[cur] == 1) {
+      if (k < LOC) chain[k] = cur;
+      ++k;
+      cur = l.s_parent[cur];
+    }
+    double acc = l.s_cumv[cur];
+    for (int j = k - 1; j >= 0; --j) {
+      int a = 0;
+      if (j < LOC) {
+        a = chain[j];
+      } else {  // long fresh chains (final-only fusion): re-walk to the j-th ancestor
+        a = s;
+        for (int t = 0; t < j; ++t) a = l.s_parent[a];
+      }
+      acc = xadd(acc, l.s_lp[a]);
+    }
+    l.s_cumv[s] = acc;
+  }
+}
+
+__global__ void commit_kernel(LlmDev l) {
+  const int nf = min(l.ctr[C_NFWD], (int)l.cap), nc = min(l.ctr[C_NCUM], (int)l.cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < max(nf, nc); i += gridDim.x * blockDim.x) {
+    if (i < nf) l.s_fwd[l.fwd_list[i]] = 2;
+    if (i < nc) l.s_cum[l.cum_list[i]] = 2;
+  }
+}
+
+// end-of-sentence punctuation log-probs of the final texts (one warp per entry, claimed slots)
+__global__ void __launch_bounds__(256) punct_kernel(BatchDev b, LlmDev l, int min_frames) {
+  const int trial = blockIdx.x;
+  if (b.status[trial] != 0 || b.T[trial] <= min_frames) return;
+  const size_t hb = (size_t)trial * b.K;
+  const int32_t* ns = l.node_slot + (size_t)trial * b.ncap;
+  const int K = b.nbeam[trial], O = b.O;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < K * O; i += blockDim.x >> 5) {
+    const int beam = i / O, q = i - beam * O;
+    if (q >= b.nent[hb + beam]) continue;
+    const int s = ns[b.ents[(hb + beam) * O + q].node];
+    if (s == 0) continue;
+    int claim = 0;
+    if (lane == 0) claim = atomicCAS(l.s_pun + s, 0, 1) == 0;
+    if (!__shfl_sync(FULLMASK, claim, 0)) continue;
+    for (int j = 0; j < 3; ++j) {
+      const float dot = warp_dot(l.s_h + (size_t)s * l.H, l.emb + (size_t)l.punct_tok[j] * l.H, l.H);
+      if (lane == 0) l.s_plp[(size_t)s * 3 + j] = (double)dot - (double)l.s_lse[s];
+    }
+  }
+}
+
+// K7: apply_llm fusion (decoder.py:354-371) from the slot scores
+__global__ void llm_apply_kernel(CfgDev c, BatchDev b, LlmDev l, int final_, int min_frames) {
+  const int trial = blockIdx.x;
+  if (b.status[trial] != 0 || b.T[trial] <= min_frames) return;
+  const size_t hb = (size_t)trial * b.K;
+  const int32_t* ns = l.node_slot + (size_t)trial * b.ncap;
+  const int K = b.nbeam[trial], O = b.O;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    Ent* e = b.ents + (hb + i) * O;
+    const int n = b.nent[hb + i];
+    const double prev = e[0].total;
+    for (int q = 0; q < n; ++q) {
+      if (e[q].node == 0) {
+        e[q].total = 0.0;
+        e[q].punct = 0;
+        continue;
+      }
+      const int s = ns[e[q].node];
+      double score = l.s_cumv[s];
+      if (final_) {
+        int best = 0;
+        double bs = xadd(score, l.s_plp[(size_t)s * 3]);
+        for (int j = 1; j < 3; ++j) {
+          const double v = xadd(score, l.s_plp[(size_t)s * 3 + j]);
+          if (v > bs) {
+            bs = v;
+            best = j;
+          }
+        }
+        score = bs;
+        e[q].punct = (uint8_t)(best + 1);
+      }
+      e[q].total = xmul(c.phi, score);
+    }
+    sort_ents(e, n);
+    b.score[hb + i] = xadd(b.score[hb + i], xsub(e[0].total, prev));
+  }
+}
+
+__global__ void llm_reset_kernel(LlmDev l) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    l.s_parent[0] = -1;
+    l.s_token[0] = l.bos_tok;
+    l.s_depth[0] = 0;
+    l.s_cum[0] = 2;
+    l.s_cumv[0] = 0.0;
+    l.s_pun[0] = 0;
+    l.s_fwd[0] = 1;  // the BOS row is forwarded with the first event's waves
+  }
+}
+
+__global__ void root_slots_kernel(int32_t* node_slot, int B, int64_t ncap) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x)
+    node_slot[(size_t)i * ncap] = 0;
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+}  // namespace
+
+struct lb_llm {
+  lb_batch* b = nullptr;
+  LlmDev dev{};
+  int32_t* d_tok_low = nullptr;
+  int32_t* d_tok_cap = nullptr;
+  int64_t node_slot_elems = 0;
+  int64_t bytes = 0;
+  // stats
+  int64_t events = 0, waves = 0, rows = 0, cum = 0, max_wave_rows = 0;
+  int32_t cur_nwaves = 0;
+  std::vector<int64_t> wave_off, wave_rows;
+};
+
+#define CKL(expr)                                                                        \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return lbh::set_error(LB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+static int launched(cudaError_t e) {
+  ++lbk::g_launches;
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return lbh::set_error(LB_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return LB_OK;
+}
+#define LAUNCH(...)                 \
+  do {                              \
+    __VA_ARGS__;                    \
+    int _rc = launched(cudaSuccess); \
+    if (_rc) return _rc;            \
+  } while (0)
+
+static int check_err_flags(lb_llm* l) {
+  int32_t err = 0;
+  CKL(cudaMemcpyAsync(&err, l->dev.ctr + C_ERR, 4, cudaMemcpyDeviceToHost, l->b->st));
+  CKL(cudaStreamSynchronize(l->b->st));
+  if (err & 1) return lbh::set_error(LB_ERR_CAPACITY, "LLM prefix cache full (max_slots)");
+  if (err & 2) return lbh::set_error(LB_ERR_CAPACITY, "LLM node list full for one fusion event");
+  if (err & 4) return lbh::set_error(LB_ERR_CAPACITY, "text longer than the LLM max_depth");
+  if (err & 8) return lbh::set_error(LB_ERR_CAPACITY, "more than LB_LLM_MAX_WAVES dependency levels");
+  return LB_OK;
+}
+
+extern "C" {
+
+int lb_llm_create(lb_batch* b, const lb_llm_desc* d, lb_llm** out) {
+  if (!b || !d || !out || !d->surface_tokens || !d->surface_tokens_first || !d->embedding)
+    return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (d->head_dim != 64 && d->head_dim != 128)
+    return lbh::set_error(LB_ERR_ARG, "head_dim must be 64 or 128");
+  if (d->n_kv_heads < 1 || d->n_heads % d->n_kv_heads != 0)
+    return lbh::set_error(LB_ERR_ARG, "n_heads must be a multiple of n_kv_heads");
+  const int G = d->n_heads / d->n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return lbh::set_error(LB_ERR_ARG, "GQA group must be 1, 2, 4 or 8");
+  if (d->hidden % 8 != 0 || d->vocab % 8 != 0) return lbh::set_error(LB_ERR_ARG, "hidden and vocab must be multiples of 8");
+  if (d->max_slots < 2 || d->max_slots > ((int64_t)1 << 30)) return lbh::set_error(LB_ERR_ARG, "max_slots out of range");
+  if (d->max_depth < 1 || d->max_depth > 4095) return lbh::set_error(LB_ERR_ARG, "max_depth out of range");
+  if (d->n_surfaces != (int32_t)b->m->surfaces.size())
+    return lbh::set_error(LB_ERR_ARG, "surface token table does not match the model's surfaces");
+  CKL(cudaSetDevice(b->m->device));
+  lb_llm* l = new lb_llm();
+  l->b = b;
+  LlmDev& x = l->dev;
+  x.L = d->n_layers;
+  x.NH = d->n_heads;
+  x.NKV = d->n_kv_heads;
+  x.HD = d->head_dim;
+  x.H = d->hidden;
+  x.vocab = d->vocab;
+  x.cap = d->max_slots;
+  x.max_depth = d->max_depth;
+  x.bos_tok = d->bos_token;
+  for (int j = 0; j < 3; ++j) x.punct_tok[j] = d->punct_tokens[j];
+  x.emb = reinterpret_cast<const bf16*>(d->embedding);
+  x.n_surf = d->n_surfaces;
+  const size_t cap = (size_t)x.cap;
+  const size_t kvw = (size_t)x.NKV * x.HD;
+  uint32_t hsz = 1;
+  while (hsz < 2 * cap) hsz <<= 1;
+  x.hmask = hsz - 1;
+  const size_t B = (size_t)b->Bmax;
+  const int64_t ncap = b->dev.ncap;
+  x.nlist_cap = (int32_t)std::min<int64_t>(ncap, (int64_t)b->K * b->O * (b->Tmax / 2 + 2));
+  l->node_slot_elems = (int64_t)B * ncap;
+  CKL(dalloc(&x.s_parent, cap));
+  CKL(dalloc(&x.s_token, cap));
+  CKL(dalloc(&x.s_depth, cap));
+  CKL(dalloc(&x.s_fwd, cap));
+  CKL(dalloc(&x.s_cum, cap));
+  CKL(dalloc(&x.s_pun, cap));
+  CKL(dalloc(&x.s_lp, cap));
+  CKL(dalloc(&x.s_cumv, cap));
+  CKL(dalloc(&x.s_plp, cap * 3));
+  CKL(dalloc(&x.s_lse, cap));
+  CKL(dalloc(&x.s_h, cap * x.H));
+  CKL(dalloc(&x.kc, (size_t)x.L * cap * kvw));
+  CKL(dalloc(&x.vc, (size_t)x.L * cap * kvw));
+  CKL(dalloc(&x.htab, hsz));
+  CKL(dalloc(&x.ctr, C_NCTR));
+  CKL(dalloc(&x.node_slot, (size_t)l->node_slot_elems));
+  CKL(dalloc(&x.nlist, B * x.nlist_cap));
+  CKL(dalloc(&x.nlist_depth, B * x.nlist_cap));
+  CKL(dalloc(&x.fwd_list, cap));
+  CKL(dalloc(&x.fwd_level, cap));
+  CKL(dalloc(&x.cum_list, cap));
+  CKL(dalloc(&x.wave_slots, cap));
+  CKL(dalloc(&x.lvl_count, MAX_LEVELS));
+  CKL(dalloc(&x.lvl_fill, MAX_LEVELS));
+  CKL(dalloc(&l->d_tok_low, x.n_surf));
+  CKL(dalloc(&l->d_tok_cap, x.n_surf));
+  CKL(cudaMemcpy(l->d_tok_low, d->surface_tokens, x.n_surf * 4, cudaMemcpyHostToDevice));
+  CKL(cudaMemcpy(l->d_tok_cap, d->surface_tokens_first, x.n_surf * 4, cudaMemcpyHostToDevice));
+  x.tok_low = l->d_tok_low;
+  x.tok_cap = l->d_tok_cap;
+  l->bytes = (int64_t)cap * (4 * 6 + 8 * 5 + 4 + 4 * x.H + 4 * 4) + (int64_t)2 * x.L * cap * kvw * 2 +
+             (int64_t)hsz * 4 + l->node_slot_elems * 4 + (int64_t)B * x.nlist_cap * 8;
+  *out = l;
+  return lb_llm_reset(l);
+}
+
+int lb_llm_destroy(lb_llm* l) {
+  if (!l) return LB_OK;
+  cudaStreamSynchronize(l->b->st);
+  LlmDev& x = l->dev;
+  void* ptrs[] = {x.s_parent, x.s_token, x.s_depth, x.s_fwd, x.s_cum, x.s_pun, x.s_lp, x.s_cumv,
+                  x.s_plp, x.s_lse, x.s_h, x.kc, x.vc, x.htab, x.ctr, x.node_slot, x.nlist,
+                  x.nlist_depth, x.fwd_list, x.fwd_level, x.cum_list, x.wave_slots, x.lvl_count,
+                  x.lvl_fill, l->d_tok_low, l->d_tok_cap};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete l;
+  return LB_OK;
+}
+
+int lb_llm_footprint(lb_llm* l, int64_t* bytes) {
+  if (!l || !bytes) return lbh::set_error(LB_ERR_ARG, "null argument");
+  *bytes = l->bytes;
+  return LB_OK;
+}
+
+int lb_llm_reset(lb_llm* l) {
+  if (!l) return lbh::set_error(LB_ERR_ARG, "null argument");
+  LlmDev& x = l->dev;
+  cudaStream_t st = l->b->st;
+  CKL(cudaMemsetAsync(x.htab, 0xFF, ((size_t)x.hmask + 1) * 4, st));
+  CKL(cudaMemsetAsync(x.node_slot, 0xFF, (size_t)l->node_slot_elems * 4, st));
+  int32_t c[C_NCTR] = {1, 0, 0, 0, 1, 0, 0, 0};
+  CKL(cudaMemcpyAsync(x.ctr, c, sizeof(c), cudaMemcpyHostToDevice, st));
+  LAUNCH(llm_reset_kernel<<<1, 32, 0, st>>>(x));
+  const int B = l->b->Bmax;
+  LAUNCH(root_slots_kernel<<<(B + 127) / 128, 128, 0, st>>>(x.node_slot, B, l->b->dev.ncap));
+  l->events = l->waves = l->rows = l->cum = l->max_wave_rows = 0;
+  return LB_OK;
+}
+
+int lb_llm_plan(lb_llm* l, int32_t final_, int32_t min_frames, int32_t* n_waves,
+                int64_t* wave_rows) {
+  if (!l || !n_waves || !wave_rows) return lbh::set_error(LB_ERR_ARG, "null argument");
+  lb_batch* b = l->b;
+  if (b->n_trials < 1) return lbh::set_error(LB_ERR_STATE, "no trials loaded");
+  LlmDev& x = l->dev;
+  cudaStream_t st = b->st;
+  CKL(cudaMemsetAsync(x.ctr + C_NFWD, 0, 8, st));  // C_NFWD, C_NCUM
+  CKL(cudaMemsetAsync(x.lvl_count, 0, MAX_LEVELS * 4, st));
+  CKL(cudaMemsetAsync(x.lvl_fill, 0, MAX_LEVELS * 4, st));
+  const int B = b->n_trials;
+  LAUNCH(map_nodes_kernel<<<B, 256, 0, st>>>(b->dev, x, min_frames));
+  LAUNCH(schedule_kernel<<<B, 128, 0, st>>>(b->dev, x, min_frames, final_));
+  LAUNCH(level_kernel<<<4 * 148, 256, 0, st>>>(x));
+  LAUNCH(scatter_kernel<<<4 * 148, 256, 0, st>>>(x));
+  std::vector<int32_t> cnt(MAX_LEVELS);
+  CKL(cudaMemcpyAsync(cnt.data(), x.lvl_count, MAX_LEVELS * 4, cudaMemcpyDeviceToHost, st));
+  int rc = check_err_flags(l);  // synchronises
+  if (rc) return rc;
+  l->wave_off.clear();
+  l->wave_rows.clear();
+  int64_t off = 0;
+  int nw = 0;
+  for (int v = 0; v < MAX_LEVELS; ++v) {
+    if (cnt[v] == 0) break;
+    l->wave_off.push_back(off);
+    l->wave_rows.push_back(cnt[v]);
+    wave_rows[v] = cnt[v];
+    off += cnt[v];
+    l->max_wave_rows = std::max<int64_t>(l->max_wave_rows, cnt[v]);
+    ++nw;
+  }
+  *n_waves = nw;
+  l->cur_nwaves = nw;
+  l->events += 1;
+  l->waves += nw;
+  l->rows += off;
+  return LB_OK;
+}
+
+int lb_llm_wave_rows(lb_llm* l, int32_t wave, int64_t row0, int32_t n, int32_t* tokens,
+                     int32_t* positions, int32_t* slots, int32_t* chains) {
+  if (!l || !tokens || !positions || !slots || !chains) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (wave < 0 || wave >= l->cur_nwaves) return lbh::set_error(LB_ERR_ARG, "wave out of range");
+  if (row0 < 0 || n < 0 || row0 + n > l->wave_rows[wave]) return lbh::set_error(LB_ERR_ARG, "rows out of range");
+  if (n == 0) return LB_OK;
+  const int grid = std::min(4 * 148, (n + 127) / 128);
+  LAUNCH(wave_rows_kernel<<<grid, 128, 0, l->b->st>>>(l->dev, l->wave_off[wave] + row0, n, tokens,
+                                                      positions, slots, chains));
+  return LB_OK;
+}
+
+int lb_llm_finish(lb_llm* l, int32_t final_, int32_t min_frames) {
+  if (!l) return lbh::set_error(LB_ERR_ARG, "null argument");
+  lb_batch* b = l->b;
+  LlmDev& x = l->dev;
+  cudaStream_t st = b->st;
+  LAUNCH(lp_kernel<<<4 * 148, 256, 0, st>>>(x));
+  LAUNCH(cum_kernel<<<4 * 148, 256, 0, st>>>(x));
+  LAUNCH(commit_kernel<<<4 * 148, 256, 0, st>>>(x));
+  const int B = b->n_trials;
+  if (final_) LAUNCH(punct_kernel<<<B, 256, 0, st>>>(b->dev, x, min_frames));
+  LAUNCH(llm_apply_kernel<<<B, 128, 0, st>>>(b->cdev, b->dev, x, final_, min_frames));
+  return LB_OK;
+}
+
+int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float eps, int32_t M,
+                   void* out, const int32_t* store_slots) {
+  if (!l || !x || !w || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (M <= 0) return LB_OK;
+  LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
+                                                      l->dev.H, reinterpret_cast<bf16*>(out),
+                                                      store_slots, l->dev.s_h));
+  return LB_OK;
+}
+
+int lb_llm_rope_kv(lb_llm* l, int32_t layer, const void* qkv, int32_t M, const int32_t* pos,
+                   const int32_t* slots, const float* cos_tab, const float* sin_tab, void* q_out) {
+  if (!l || !qkv || !pos || !slots || !cos_tab || !sin_tab || !q_out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (layer < 0 || layer >= l->dev.L) return lbh::set_error(LB_ERR_ARG, "layer out of range");
+  if (M <= 0) return LB_OK;
+  LAUNCH(rope_kv_kernel<<<M, 128, 0, l->b->st>>>(l->dev, layer, reinterpret_cast<const float*>(qkv), M,
+                                                  pos, slots, cos_tab, sin_tab,
+                                                  reinterpret_cast<bf16*>(q_out)));
+  return LB_OK;
+}
+
+int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const int32_t* chains,
+                     const int32_t* pos, void* out) {
+  if (!l || !q || !chains || !pos || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (layer < 0 || layer >= l->dev.L) return lbh::set_error(LB_ERR_ARG, "layer out of range");
+  if (M <= 0) return LB_OK;
+  const LlmDev& x = l->dev;
+  const int G = x.NH / x.NKV;
+  const int64_t warps = (int64_t)M * x.NKV;
+  const int grid = (int)((warps + 7) / 8);
+  const float scale = 1.0f / sqrtf((float)x.HD);
+  const bf16* qq = reinterpret_cast<const bf16*>(q);
+  bf16* oo = reinterpret_cast<bf16*>(out);
+  cudaStream_t st = l->b->st;
+#define ATT(HDV, GV) \
+  LAUNCH(chain_attn_kernel<HDV, GV><<<grid, 256, 0, st>>>(x, layer, qq, M, chains, pos, scale, oo))
+  if (x.HD == 64) {
+    if (G == 1) ATT(64, 1); else if (G == 2) ATT(64, 2); else if (G == 4) ATT(64, 4); else ATT(64, 8);
+  } else {
+    if (G == 1) ATT(128, 1); else if (G == 2) ATT(128, 2); else if (G == 4) ATT(128, 4); else ATT(128, 8);
+  }
+#undef ATT
+  return LB_OK;
+}
+
+int lb_llm_swiglu(lb_llm* l, const void* gu, int32_t M, int32_t ffn, void* out) {
+  if (!l || !gu || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (ffn % 2 != 0) return lbh::set_error(LB_ERR_ARG, "ffn must be even");
+  if (M <= 0) return LB_OK;
+  const int64_t n2 = (int64_t)M * ffn / 2;
+  const int grid = (int)std::min<int64_t>(16 * 148, (n2 + 255) / 256);
+  LAUNCH(swiglu_kernel<<<grid, 256, 0, l->b->st>>>(reinterpret_cast<const bf16*>(gu), M, ffn,
+                                                   reinterpret_cast<bf16*>(out)));
+  return LB_OK;
+}
+
+int lb_llm_lse(lb_llm* l, const void* logits, int32_t M, int64_t ld, const int32_t* slots) {
+  if (!l || !logits || !slots) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (ld % 8 != 0) return lbh::set_error(LB_ERR_ARG, "logit row pitch must be a multiple of 8");
+  if (M <= 0) return LB_OK;
+  LAUNCH(lse_kernel<<<M, 512, 0, l->b->st>>>(reinterpret_cast<const bf16*>(logits), ld, l->dev.vocab,
+                                              slots, l->dev.s_lse));
+  return LB_OK;
+}
+
+int lb_llm_stats(lb_llm* l, int64_t* out) {
+  if (!l || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  int32_t slots = 0;
+  CKL(cudaMemcpyAsync(&slots, l->dev.ctr + C_SLOTS, 4, cudaMemcpyDeviceToHost, l->b->st));
+  CKL(cudaStreamSynchronize(l->b->st));
+  out[0] = slots;
+  out[1] = l->events;
+  out[2] = l->waves;
+  out[3] = l->rows;
+  out[4] = l->max_wave_rows;
+  out[5] = l->bytes;
+  out[6] = 0;
+  out[7] = 0;
+  return LB_OK;
+}
+
+int lb_llm_export(lb_llm* l, int64_t max_n, int64_t* n, int32_t* parent, int32_t* token,
+                  int32_t* depth, int32_t* state, double* cum, double* punct_lp) {
+  if (!l || !n) return lbh::set_error(LB_ERR_ARG, "null argument");
+  LlmDev& x = l->dev;
+  cudaStream_t st = l->b->st;
+  int32_t slots = 0;
+  CKL(cudaMemcpyAsync(&slots, x.ctr + C_SLOTS, 4, cudaMemcpyDeviceToHost, st));
+  CKL(cudaStreamSynchronize(st));
+  const int64_t avail = std::min<int64_t>(slots, x.cap);
+  *n = avail;  // rows available; min(avail, max_n) are copied
+  const int64_t k = std::min<int64_t>(avail, max_n);
+  if (k <= 0) return LB_OK;
+  if (parent) CKL(cudaMemcpyAsync(parent, x.s_parent, k * 4, cudaMemcpyDeviceToHost, st));
+  if (token) CKL(cudaMemcpyAsync(token, x.s_token, k * 4, cudaMemcpyDeviceToHost, st));
+  if (depth) CKL(cudaMemcpyAsync(depth, x.s_depth, k * 4, cudaMemcpyDeviceToHost, st));
+  if (state) {
+    std::vector<int32_t> a(k), c(k), p(k);
+    CKL(cudaMemcpyAsync(a.data(), x.s_fwd, k * 4, cudaMemcpyDeviceToHost, st));
+    CKL(cudaMemcpyAsync(c.data(), x.s_cum, k * 4, cudaMemcpyDeviceToHost, st));
+    CKL(cudaMemcpyAsync(p.data(), x.s_pun, k * 4, cudaMemcpyDeviceToHost, st));
+    CKL(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < k; ++i) state[i] = (a[i] == 2 ? 1 : 0) | (c[i] == 2 ? 2 : 0) | (p[i] ? 4 : 0);
+  }
+  if (cum) CKL(cudaMemcpyAsync(cum, x.s_cumv, k * 8, cudaMemcpyDeviceToHost, st));
+  if (punct_lp) CKL(cudaMemcpyAsync(punct_lp, x.s_plp, k * 24, cudaMemcpyDeviceToHost, st));
+  CKL(cudaStreamSynchronize(st));
+  return LB_OK;
+}
+
+}  // extern "C"

@@ -16,7 +16,10 @@ which is how the GPU is meant to be fed.  Flow per batch:
 Fusion events (`t > 0 and t % r == 0`, `decoder.py:428`) with a host scorer gather the word
 histories on the device, send the unique texts through the scorer protocol, and apply the
 scores with a device kernel.  With a `DeviceNgramScorer` the events happen inside the frames
-kernel and the whole utterance is one launch plus closure and final fusion.
+kernel and the whole utterance is one launch plus closure and final fusion.  With a
+`LlamaScorer` (llm.py) the events stay on the device: the word histories are mapped into the
+LLM's prefix-trie KV cache, only new trie nodes run through the transformer, and the fusion
+kernel reads the scores from the cache.
 """
 
 from __future__ import annotations
@@ -400,15 +403,23 @@ def run_search(batch: DeviceBatch, cfg, scorer, model, final_llm_only: bool):
         batch.close()
         batch.device_fusion(True, scale, 0)
         return
+    llm = getattr(scorer, "device_llm_scorer", None)
+    if llm is not None and batch.dm.whitespace_free:
+        sess = llm.session(batch)
+        sess.reset()
+        fuse = sess.event
+    else:
+        def fuse(final, min_frames):
+            _host_fusion(batch, scorer, cfg, final=final, min_frames=min_frames)
     t = 0
     if not final_llm_only:
         for e in range(r, t_max, r):  # events after frames e = r, 2r, ... (< the longest T)
             batch.run(t, e + 1)
-            _host_fusion(batch, scorer, cfg, final=False, min_frames=e)
+            fuse(False, e)
             t = e + 1
     batch.run(t, t_max)
     batch.close()
-    _host_fusion(batch, scorer, cfg, final=True, min_frames=0)
+    fuse(True, 0)
 
 
 def _collect(batch: DeviceBatch, cfg, final_llm_only: bool, wall: float):

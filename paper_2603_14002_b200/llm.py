@@ -1,0 +1,600 @@
+"""LLM scorer for delayed fusion: a random-init Llama-architecture model on the GPU.
+
+Plugin contract (the reference's, `pkg/src/lightbeam/scorer.py:93-163,269-325`): `LlamaScorer`
+has `submit(ScoreRequest) -> ScoreResponse` and `next_request_id()`, so any caller of the
+reference protocol (including the reference decoder itself) can use it with host strings.
+
+Scoring convention (the reference sidecar, `pkg/sidecar/src/model.ts:35-47,116-137`, at word
+rather than character granularity): tokens = [BOS] + tokens(sentenceCase(text)); score = sum over
+positions of the natural-log next-token probability; empty text scores 0; `score_eos` returns
+the best of `text + "."`, `"?"`, `"!"` with strict `>` (ties keep "."), where the punctuation is
+one more token after the text: score_eos(text, p) = score(text) + log P(p | text).
+
+Tokenizer (synthetic -- there is no Llama tokenizer offline): one token per
+whitespace-separated word, id = 8 + FNV-1a-64(utf-8 word) mod (vocab - 8); BOS = 1; ".", "?",
+"!" = 2, 3, 4.  Sentence case upper-cases the first character of the text (model.ts:35-38), so
+the first word has its own token.
+
+Two execution paths share the weights:
+  * `submit()` -- every text is a full forward pass (plain torch, bf16, SDPA), no KV reuse: the
+    "CPU search + GPU LLM" split of the paper and the reference arm of bench.py;
+  * the device path (`DeviceLlmSession`) the decoder drives when it decodes on the GPU: texts are
+    paths of one prefix trie whose nodes are evaluated once (lb_llm_* in csrc/lb_llm.cu); the
+    transformer body's GEMMs run on the tensor cores through torch (cuBLAS, bf16 in, fp32
+    accumulate), everything around them is hand-written kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import DeviceError, ScorerError
+from .scorer import PUNCTS, ScoreRequest, ScoreResponse
+
+BOS_ID = 1
+PUNCT_IDS = (2, 3, 4)
+FIRST_WORD_ID = 8
+
+
+@dataclass(frozen=True)
+class LlmConfig:
+    name: str
+    vocab_size: int
+    hidden: int
+    layers: int
+    heads: int
+    kv_heads: int
+    ffn: int
+    head_dim: int
+    rope_theta: float = 500000.0
+    rope_scaling: dict | None = None  # llama3 rope parameters
+    rms_eps: float = 1e-5
+    init_std: float = 0.02
+
+    def n_params(self) -> int:
+        att = self.hidden * (self.heads + 2 * self.kv_heads) * self.head_dim
+        att += self.heads * self.head_dim * self.hidden
+        mlp = 3 * self.hidden * self.ffn
+        return self.vocab_size * self.hidden + self.layers * (att + mlp + 2 * self.hidden) + self.hidden
+
+    def flops_per_token(self) -> float:
+        """2 x (body + LM head) multiply-adds per forwarded token (attention over the short
+        prefix excluded)."""
+        att = self.hidden * (self.heads + 2 * self.kv_heads) * self.head_dim
+        att += self.heads * self.head_dim * self.hidden
+        return 2.0 * (self.layers * (att + 3 * self.hidden * self.ffn) + self.vocab_size * self.hidden)
+
+
+_LLAMA3_1B_ROPE = {"factor": 32.0, "low_freq_factor": 1.0, "high_freq_factor": 4.0,
+                   "original_max_position_embeddings": 8192}
+_LLAMA3_8B_ROPE = {"factor": 8.0, "low_freq_factor": 1.0, "high_freq_factor": 4.0,
+                   "original_max_position_embeddings": 8192}
+
+PRESETS = {
+    # config 1 of BASELINE.json: a tiny model (Llama-architecture stand-in for the GPT-2-style toy)
+    "tiny": LlmConfig("tiny", 4096, 128, 2, 2, 1, 512, 64),
+    # config 3: Llama-3.2-1B architecture
+    "llama-3.2-1b": LlmConfig("llama-3.2-1b", 128256, 2048, 16, 32, 8, 8192, 64,
+                              rope_scaling=_LLAMA3_1B_ROPE),
+    # config 5: 8B-class = Llama-3.1-8B architecture
+    "llama-3.1-8b": LlmConfig("llama-3.1-8b", 128256, 4096, 32, 32, 8, 14336, 128,
+                              rope_scaling=_LLAMA3_8B_ROPE),
+}
+
+
+def get_config(cfg) -> LlmConfig:
+    if isinstance(cfg, LlmConfig):
+        return cfg
+    if cfg not in PRESETS:
+        raise ValueError(f"unknown LLM preset {cfg!r}; choose from {sorted(PRESETS)}")
+    return PRESETS[cfg]
+
+
+# ------------------------------------------------------------------------------ tokenizer
+def _fnv1a64(data: bytes) -> int:
+    h = 0xCBF29CE484222325
+    for x in data:
+        h ^= x
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def sentence_case(text: str) -> str:
+    """model.ts:35-38: upper-case the first character."""
+    return text[:1].upper() + text[1:] if text else text
+
+
+class WordTokenizer:
+    def __init__(self, vocab_size: int):
+        if vocab_size <= FIRST_WORD_ID:
+            raise ValueError("vocab too small")
+        self.vocab_size = vocab_size
+        self.bos = BOS_ID
+        self.punct = dict(zip(PUNCTS, PUNCT_IDS))
+        self._cache: dict[str, int] = {}
+
+    def word_id(self, word: str) -> int:
+        got = self._cache.get(word)
+        if got is None:
+            got = FIRST_WORD_ID + _fnv1a64(word.encode("utf-8")) % (self.vocab_size - FIRST_WORD_ID)
+            self._cache[word] = got
+        return got
+
+    def encode(self, text: str) -> list[int]:
+        """[BOS] + one id per word of the sentence-cased text."""
+        return [self.bos] + [self.word_id(w) for w in sentence_case(text).split()]
+
+    def surface_tables(self, surfaces) -> tuple[np.ndarray, np.ndarray]:
+        """(token mid-sentence, token as the first word) per lexicon surface."""
+        low = np.fromiter((self.word_id(s) for s in surfaces), dtype=np.int32, count=len(surfaces))
+        cap = np.fromiter((self.word_id(sentence_case(s)) for s in surfaces), dtype=np.int32,
+                          count=len(surfaces))
+        return low, cap
+
+
+# ------------------------------------------------------------------------------ weights
+def rope_inv_freq(cfg: LlmConfig):
+    """Llama rotary frequencies, llama3 frequency scaling when configured (the formula of the
+    Llama-3 release, as implemented by transformers' `_compute_llama3_parameters`)."""
+    import torch
+
+    hd = cfg.head_dim
+    inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
+    rs = cfg.rope_scaling
+    if not rs:
+        return inv
+    factor, lo, hi = rs["factor"], rs["low_freq_factor"], rs["high_freq_factor"]
+    old = rs["original_max_position_embeddings"]
+    lo_wl, hi_wl = old / lo, old / hi
+    wl = 2 * math.pi / inv
+    inv_l = torch.where(wl > lo_wl, inv / factor, inv)
+    smooth = (old / wl - lo) / (hi - lo)
+    smoothed = (1 - smooth) * inv_l / factor + smooth * inv_l
+    medium = ~(wl < hi_wl) * ~(wl > lo_wl)
+    return torch.where(medium, smoothed, inv_l)
+
+
+class LlamaWeights:
+    """Random-init weights (normal(0, init_std) for every linear/embedding, ones for RMSNorm --
+    the Llama initialisation) as bf16 device tensors; q/k/v and gate/up are stored fused."""
+
+    def __init__(self, cfg: LlmConfig, seed: int = 0, device: str = "cuda:0", max_pos: int = 4096):
+        import torch
+
+        self.cfg = cfg
+        self.device = torch.device(device)
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        std = cfg.init_std
+
+        def rnd(*shape):
+            w = torch.empty(shape, dtype=torch.float32, device=self.device)
+            w.normal_(0.0, std, generator=g)
+            return w.to(torch.bfloat16)
+
+        H, hd = cfg.hidden, cfg.head_dim
+        self.emb = rnd(cfg.vocab_size, H)
+        self.layers = []
+        for _ in range(cfg.layers):
+            wq = rnd(cfg.heads * hd, H)
+            wk = rnd(cfg.kv_heads * hd, H)
+            wv = rnd(cfg.kv_heads * hd, H)
+            wo = rnd(H, cfg.heads * hd)
+            wg = rnd(cfg.ffn, H)
+            wu = rnd(cfg.ffn, H)
+            wd = rnd(H, cfg.ffn)
+            self.layers.append({
+                "ln1": torch.ones(H, dtype=torch.float32, device=self.device),
+                "wqkv": torch.cat([wq, wk, wv], 0).contiguous(),
+                "wo": wo,
+                "ln2": torch.ones(H, dtype=torch.float32, device=self.device),
+                "wgu": torch.cat([wg, wu], 0).contiguous(),
+                "wd": wd,
+            })
+        self.norm = torch.ones(H, dtype=torch.float32, device=self.device)
+        inv = rope_inv_freq(cfg)
+        pos = torch.arange(max_pos, dtype=torch.float32)
+        freqs = pos[:, None] * inv[None, :]
+        self.cos = freqs.cos().to(self.device).contiguous()
+        self.sin = freqs.sin().to(self.device).contiguous()
+        self.max_pos = max_pos
+
+    def hf_state_dict(self) -> dict:
+        """fp32 CPU tensors under transformers' LlamaForCausalLM names (for the test oracle)."""
+        cfg = self.cfg
+        qn, kn = cfg.heads * cfg.head_dim, cfg.kv_heads * cfg.head_dim
+        sd = {"model.embed_tokens.weight": self.emb.float().cpu(),
+              "model.norm.weight": self.norm.float().cpu(),
+              "lm_head.weight": self.emb.float().cpu()}
+        for i, L in enumerate(self.layers):
+            p = f"model.layers.{i}."
+            w = L["wqkv"].float().cpu()
+            sd[p + "self_attn.q_proj.weight"] = w[:qn]
+            sd[p + "self_attn.k_proj.weight"] = w[qn: qn + kn]
+            sd[p + "self_attn.v_proj.weight"] = w[qn + kn:]
+            sd[p + "self_attn.o_proj.weight"] = L["wo"].float().cpu()
+            gu = L["wgu"].float().cpu()
+            sd[p + "mlp.gate_proj.weight"] = gu[: cfg.ffn]
+            sd[p + "mlp.up_proj.weight"] = gu[cfg.ffn:]
+            sd[p + "mlp.down_proj.weight"] = L["wd"].float().cpu()
+            sd[p + "input_layernorm.weight"] = L["ln1"].float().cpu()
+            sd[p + "post_attention_layernorm.weight"] = L["ln2"].float().cpu()
+        return sd
+
+
+# ------------------------------------------------------------------------------ scorer
+class LlamaScorer:
+    """Delayed-fusion scorer backed by a random-init Llama-architecture model on one GPU."""
+
+    def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
+                 max_depth: int = 255, row_chunk: int = 16384, lm_chunk: int = 1024):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise DeviceError("LlamaScorer needs a CUDA device (no CPU path)")
+        torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+        self.cfg = get_config(config)
+        self.device = device
+        self.seed = seed
+        self.weights = LlamaWeights(self.cfg, seed, f"cuda:{device}", max_pos=max(max_depth + 2, 1100))
+        self.tokenizer = WordTokenizer(self.cfg.vocab_size)
+        self.max_slots = max_slots
+        self.max_depth = max_depth
+        self.row_chunk = row_chunk
+        self.lm_chunk = lm_chunk
+        self.evaluations = 0
+        self._ids = itertools.count(1)
+        self.device_llm_scorer = self  # the GPU decoder drives this scorer on the device
+
+    # ---- reference protocol (host strings, one full forward per text, no KV reuse)
+    def next_request_id(self) -> int:
+        return next(self._ids)
+
+    def submit(self, request: ScoreRequest) -> ScoreResponse:
+        self.evaluations += len(request.texts)
+        if request.kind == "score":
+            return ScoreResponse(request.id, tuple(self.score_texts_dense(list(request.texts))))
+        if request.kind == "score_eos":
+            pairs = self.score_eos_dense(list(request.texts))
+            return ScoreResponse(request.id, tuple(s for _, s in pairs), tuple(p for p, _ in pairs))
+        raise ScorerError(f"unknown request kind {request.kind!r}", request.id)
+
+    def close(self):
+        pass
+
+    def score_texts_dense(self, texts: list[str]) -> list[float]:
+        return [s for s, _ in self._dense(texts, eos=False)]
+
+    def score_eos_dense(self, texts: list[str]) -> list[tuple[str, float]]:
+        out = []
+        for s, plp in self._dense(texts, eos=True):
+            best, bs = 0, s + plp[0]
+            for j in (1, 2):
+                v = s + plp[j]
+                if v > bs:
+                    best, bs = j, v
+            out.append((PUNCTS[best], bs))
+        return out
+
+    def _dense(self, texts: list[str], eos: bool, batch_tokens: int = 1 << 16):
+        """Full-sequence forward per text (plain torch: bf16 GEMMs, SDPA, fp32 log-softmax)."""
+        import torch
+
+        res: list = [None] * len(texts)
+        toks = [self.tokenizer.encode(t) for t in texts]
+        order = sorted(range(len(texts)), key=lambda i: len(toks[i]))
+        i = 0
+        while i < len(order):
+            S = len(toks[order[i]])
+            j = i
+            while j < len(order) and (j - i + 1) * len(toks[order[j]]) <= batch_tokens:
+                j += 1
+            j = max(j, i + 1)
+            idx = order[i:j]
+            S = max(len(toks[k]) for k in idx)
+            if S > self.weights.max_pos:
+                raise ScorerError(f"text longer than {self.weights.max_pos} tokens")
+            ids = torch.zeros((len(idx), S), dtype=torch.long)
+            for r, k in enumerate(idx):
+                ids[r, : len(toks[k])] = torch.tensor(toks[k])
+            with torch.no_grad():
+                lp_all, plp = self._dense_forward(ids.to(self.weights.device), [len(toks[k]) for k in idx],
+                                                  eos)
+            for r, k in enumerate(idx):
+                res[k] = (lp_all[r], plp[r] if eos else None)
+            i = j
+        return res
+
+    def _dense_forward(self, ids, lens, eos):
+        return dense_forward(self.weights, ids, lens, eos)
+
+    # ---- device path
+    def session(self, batch) -> "DeviceLlmSession":
+        sess = getattr(batch, "_llm_session", None)
+        if sess is None or sess.scorer is not self:
+            if sess is not None:
+                sess.destroy()
+            sess = DeviceLlmSession(self, batch)
+            batch._llm_session = sess
+        return sess
+
+
+def dense_forward(W: LlamaWeights, ids, lens, eos: bool, exact_fp32: bool = False):
+    """Full-sequence Llama forward of a padded [B, S] batch (plain torch: bf16 GEMMs with fp32
+    outputs and an fp32 residual stream; `exact_fp32` runs everything in fp32 -- the CPU
+    semantic check against transformers).  Returns (sum of next-token log-probs per row,
+    log-probs of ".?!" after each row's last token if `eos`)."""
+    import torch
+    import torch.nn.functional as F
+
+    cfg = W.cfg
+    B, S = ids.shape
+    hd, nh, nkv = cfg.head_dim, cfg.heads, cfg.kv_heads
+    opd = torch.float32 if exact_fp32 else torch.bfloat16
+
+    def mm(a, w):
+        a2 = a.reshape(-1, a.shape[-1])
+        if exact_fp32:
+            out = a2.float() @ w.float().t()
+        else:
+            out = torch.mm(a2.to(torch.bfloat16), w.t(), out_dtype=torch.float32)
+        return out.view(*a.shape[:-1], -1)
+
+    x = W.emb[ids].float()
+    cos = W.cos[:S].repeat(1, 2)[None, None]
+    sin = W.sin[:S].repeat(1, 2)[None, None]
+
+    def norm(v, w):
+        return (v * torch.rsqrt(v.pow(2).mean(-1, keepdim=True) + cfg.rms_eps) * w).to(opd)
+
+    def rope(t):
+        t1, t2 = t[..., : hd // 2], t[..., hd // 2:]
+        return (t * cos + torch.cat([-t2, t1], -1) * sin).to(opd)
+
+    for L in W.layers:
+        h = norm(x, L["ln1"])
+        qkv = mm(h, L["wqkv"])
+        q = qkv[..., : nh * hd].view(B, S, nh, hd).transpose(1, 2)
+        k = qkv[..., nh * hd: (nh + nkv) * hd].view(B, S, nkv, hd).transpose(1, 2)
+        v = qkv[..., (nh + nkv) * hd:].view(B, S, nkv, hd).transpose(1, 2).to(opd)
+        q, k = rope(q), rope(k)
+        a = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+        x = x + mm(a.transpose(1, 2).reshape(B, S, nh * hd), L["wo"])
+        h = norm(x, L["ln2"])
+        gu = mm(h, L["wgu"]).to(opd)
+        g, u = gu[..., : cfg.ffn], gu[..., cfg.ffn:]
+        x = x + mm((F.silu(g.float()) * u.float()).to(opd), L["wd"])
+    hn = (x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + cfg.rms_eps) * W.norm)
+    out_lp, out_p = [], []
+    for r in range(B):
+        n = lens[r]
+        logits = mm(hn[r, :n].to(opd), W.emb) if not exact_fp32 else hn[r, :n] @ W.emb.float().t()
+        lsm = torch.log_softmax(logits.float(), -1).double()
+        tgt = ids[r, 1:n]
+        total = 0.0
+        for t, v in enumerate(lsm[: n - 1].gather(1, tgt[:, None])[:, 0].tolist()):
+            total += v
+        out_lp.append(total)
+        if eos:
+            out_p.append([float(lsm[n - 1, p]) for p in PUNCT_IDS])
+    return out_lp, out_p
+
+
+def _surface_tokens(dm, tok: WordTokenizer):
+    key = ("llm_tokens", tok.vocab_size)
+    cache = dm.__dict__.setdefault("_tok_cache", {})
+    if key not in cache:
+        cache[key] = tok.surface_tables(dm.surfaces)
+    return cache[key]
+
+
+class DeviceLlmSession:
+    """The prefix-trie KV cache of one DeviceBatch plus the transformer body that fills it."""
+
+    def __init__(self, scorer: LlamaScorer, batch):
+        import torch
+
+        self.scorer = scorer
+        self.batch = batch
+        cfg, W = scorer.cfg, scorer.weights
+        low, cap = _surface_tokens(batch.dm, scorer.tokenizer)
+        self._low, self._cap = low, cap
+        per_slot = cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * 2 + cfg.hidden * 2 + 96
+        if scorer.max_slots:
+            max_slots = int(scorer.max_slots)
+        else:
+            free, _ = torch.cuda.mem_get_info(scorer.device)
+            want = max(1 << 16, batch.max_trials * 4096)
+            max_slots = int(min(want, 0.5 * free / per_slot, 1 << 26))
+        self.max_slots = max_slots
+        self.pitch = scorer.max_depth + 1
+        d = N.LbLlmDesc()
+        d.n_layers, d.n_heads, d.n_kv_heads = cfg.layers, cfg.heads, cfg.kv_heads
+        d.head_dim, d.hidden, d.vocab = cfg.head_dim, cfg.hidden, cfg.vocab_size
+        d.max_slots = max_slots
+        d.max_depth = scorer.max_depth
+        d.bos_token = BOS_ID
+        for j in range(3):
+            d.punct_tokens[j] = PUNCT_IDS[j]
+        d.surface_tokens = low.ctypes.data
+        d.surface_tokens_first = cap.ctypes.data
+        d.n_surfaces = len(low)
+        d.embedding = W.emb.data_ptr()
+        h = C.c_void_p()
+        N.check(N.lib().lb_llm_create(batch.h, C.byref(d), C.byref(h)))
+        self.h = h
+        self._ws = {}
+        self.waves_log: list = []
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            N.lib(False).lb_llm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def reset(self):
+        N.check(N.lib().lb_llm_reset(self.h))
+        self.waves_log = []
+
+    def _work(self, n: int):
+        import torch
+
+        cap = self._ws.get("n", 0)
+        if cap < n:
+            dev = self.scorer.weights.device
+            cfg = self.scorer.cfg
+            cap = max(n, 256)
+            i32 = dict(dtype=torch.int32, device=dev)
+            self._ws = {
+                "n": cap,
+                "tok": torch.empty(cap, **i32),
+                "pos": torch.empty(cap, **i32),
+                "slot": torch.empty(cap, **i32),
+                "chain": torch.empty((cap, self.pitch), **i32),
+                "q": torch.empty((cap, cfg.heads * cfg.head_dim), dtype=torch.bfloat16, device=dev),
+                "att": torch.empty((cap, cfg.heads * cfg.head_dim), dtype=torch.bfloat16, device=dev),
+                "hn": torch.empty((cap, cfg.hidden), dtype=torch.bfloat16, device=dev),
+                "act": torch.empty((cap, cfg.ffn), dtype=torch.bfloat16, device=dev),
+            }
+        return self._ws
+
+    def event(self, final: bool, min_frames: int):
+        lib = N.lib()
+        nw = C.c_int32()
+        rows = np.zeros(N.LLM_MAX_WAVES, dtype=np.int64)
+        N.check(lib.lb_llm_plan(self.h, int(final), int(min_frames), C.byref(nw), N.ptr(rows)))
+        sizes = [int(x) for x in rows[: nw.value]]
+        self.waves_log.append(sizes)
+        for w, m in enumerate(sizes):
+            for r0 in range(0, m, self.scorer.row_chunk):
+                self._forward_rows(w, r0, min(self.scorer.row_chunk, m - r0))
+        N.check(lib.lb_llm_finish(self.h, int(final), int(min_frames)))
+
+    def _forward_rows(self, wave: int, row0: int, n: int):
+        import torch
+
+        lib = N.lib()
+        cfg, W = self.scorer.cfg, self.scorer.weights
+        ws = self._work(n)
+        tok, pos, slot, chain = ws["tok"][:n], ws["pos"][:n], ws["slot"][:n], ws["chain"][:n]
+        N.check(lib.lb_llm_wave_rows(self.h, wave, row0, n, tok.data_ptr(), pos.data_ptr(),
+                                     slot.data_ptr(), chain.data_ptr()))
+        x = W.emb.index_select(0, tok.long()).float()
+        hn, q, att, act = ws["hn"][:n], ws["q"][:n], ws["att"][:n], ws["act"][:n]
+        eps = cfg.rms_eps
+        N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), None, W.layers[0]["ln1"].data_ptr(), eps, n,
+                                   hn.data_ptr(), None))
+        for li, L in enumerate(W.layers):
+            qkv = torch.mm(hn, L["wqkv"].t(), out_dtype=torch.float32)
+            N.check(lib.lb_llm_rope_kv(self.h, li, qkv.data_ptr(), n, pos.data_ptr(), slot.data_ptr(),
+                                       W.cos.data_ptr(), W.sin.data_ptr(), q.data_ptr()))
+            N.check(lib.lb_llm_attention(self.h, li, q.data_ptr(), n, chain.data_ptr(), pos.data_ptr(),
+                                         att.data_ptr()))
+            o = torch.mm(att, L["wo"].t(), out_dtype=torch.float32)
+            N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), o.data_ptr(), L["ln2"].data_ptr(), eps, n,
+                                       hn.data_ptr(), None))
+            gu = torch.mm(hn, L["wgu"].t())
+            N.check(lib.lb_llm_swiglu(self.h, gu.data_ptr(), n, cfg.ffn, act.data_ptr()))
+            del gu
+            dn = torch.mm(act, L["wd"].t(), out_dtype=torch.float32)
+            last = li + 1 == cfg.layers
+            wnext = W.norm if last else W.layers[li + 1]["ln1"]
+            N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), dn.data_ptr(), wnext.data_ptr(), eps, n,
+                                       hn.data_ptr(), slot.data_ptr() if last else None))
+        for c0 in range(0, n, self.scorer.lm_chunk):
+            c1 = min(n, c0 + self.scorer.lm_chunk)
+            logits = torch.mm(hn[c0:c1], W.emb.t())
+            N.check(lib.lb_llm_lse(self.h, logits.data_ptr(), c1 - c0, logits.stride(0),
+                                   slot[c0:].data_ptr()))
+
+    def stats(self) -> dict:
+        out = np.zeros(8, dtype=np.int64)
+        N.check(N.lib().lb_llm_stats(self.h, N.ptr(out)))
+        return {"slots": int(out[0]), "events": int(out[1]), "waves": int(out[2]),
+                "forward_rows": int(out[3]), "max_wave_rows": int(out[4]), "cache_bytes": int(out[5])}
+
+    def export(self) -> dict:
+        """Slot table for parity checks: parent, token, depth, state bits, score, punct lps."""
+        n = C.c_int64()
+        N.check(N.lib().lb_llm_export(self.h, 0, C.byref(n), None, None, None, None, None, None))
+        k = n.value
+        par = np.empty(k, np.int32)
+        tok = np.empty(k, np.int32)
+        dep = np.empty(k, np.int32)
+        st = np.empty(k, np.int32)
+        cum = np.empty(k, np.float64)
+        plp = np.empty((k, 3), np.float64)
+        N.check(N.lib().lb_llm_export(self.h, k, C.byref(n), N.ptr(par), N.ptr(tok), N.ptr(dep),
+                                      N.ptr(st), N.ptr(cum), N.ptr(plp)))
+        return {"parent": par, "token": tok, "depth": dep, "state": st, "cum": cum, "punct_lp": plp}
+
+    def replay_table(self) -> "ReplayTable":
+        return ReplayTable(self.export(), self.scorer.tokenizer)
+
+
+class ReplayTable:
+    """text -> the score the device assigned it (score-replay scorer of SURVEY.md §8c(3))."""
+
+    def __init__(self, ex: dict, tok: WordTokenizer):
+        self.tok = tok
+        self.child = {}
+        for s in range(1, len(ex["parent"])):
+            if ex["parent"][s] >= 0:  # -2: spare slot of a lost insert race, never referenced
+                self.child[(int(ex["parent"][s]), int(ex["token"][s]))] = s
+        self.ex = ex
+
+    def slot_of(self, text: str) -> int:
+        ids = self.tok.encode(text)
+        s = 0
+        for t in ids[1:]:
+            s = self.child[(s, t)]
+        return s
+
+    def score(self, text: str) -> float:
+        s = self.slot_of(text)
+        if not self.ex["state"][s] & 2:
+            raise KeyError(f"text never scored on the device: {text!r}")
+        return float(self.ex["cum"][s])
+
+    def score_eos(self, text: str) -> tuple[str, float]:
+        s = self.slot_of(text)
+        if not self.ex["state"][s] & 4:
+            raise KeyError(f"text never eos-scored on the device: {text!r}")
+        base = float(self.ex["cum"][s])
+        best, bs = 0, base + float(self.ex["punct_lp"][s][0])
+        for j in (1, 2):
+            v = base + float(self.ex["punct_lp"][s][j])
+            if v > bs:
+                best, bs = j, v
+        return PUNCTS[best], bs
+
+
+class ReplayScorer:
+    """Reference-protocol scorer answering from a device ReplayTable (parity harness)."""
+
+    def __init__(self, table: ReplayTable):
+        self.table = table
+        self._ids = itertools.count(1)
+
+    def next_request_id(self) -> int:
+        return next(self._ids)
+
+    def submit(self, request: ScoreRequest) -> ScoreResponse:
+        if request.kind == "score":
+            return ScoreResponse(request.id, tuple(self.table.score(t) for t in request.texts))
+        pairs = [self.table.score_eos(t) for t in request.texts]
+        return ScoreResponse(request.id, tuple(s for _, s in pairs), tuple(p for p, _ in pairs))
+
+    def close(self):
+        pass
