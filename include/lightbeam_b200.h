@@ -231,8 +231,10 @@ int lb_model_score_words(lb_model* m, int32_t n, const uint32_t* hist /* [n*3] *
  * hash-consed on (parent slot, token)); the caller owns the weights and runs the GEMMs of the
  * transformer body (bf16 tensor cores) between the kernels below, all on the batch stream.
  * Per fusion event:
- *   lb_llm_plan        map live entries' word histories to slots; returns the dependency waves
- *                      of the slots whose forward pass this event needs
+ *   lb_llm_plan        map live entries' word histories to slots; returns the rows (slots whose
+ *                      forward pass this event needs) as one wave in slot-id order, a dependency
+ *                      order: every row's new ancestors precede it, so the wave runs as one
+ *                      tree-causal prefill and any row-prefix chunk is self-contained
  *   per wave, per row chunk:
  *     lb_llm_wave_rows   tokens / positions / slots / ancestor chains of the rows
  *     body: lb_llm_rmsnorm, GEMM, lb_llm_rope_kv, lb_llm_attention, GEMM, lb_llm_rmsnorm,
@@ -247,13 +249,17 @@ typedef struct lb_llm lb_llm;
 typedef struct {
   int32_t n_layers, n_heads, n_kv_heads, head_dim, hidden, vocab;
   int64_t max_slots;   /* prefix-cache capacity (token positions over the whole batch decode) */
-  int32_t max_depth;   /* longest text in tokens after BOS (< LB_LLM_MAX_WAVES) */
+  int32_t max_depth;   /* longest text in tokens after BOS (<= 4095) */
   int32_t bos_token;
   int32_t punct_tokens[3];             /* ".", "?", "!" */
   const int32_t* surface_tokens;       /* host [n_surfaces]: token of each lexicon surface */
   const int32_t* surface_tokens_first; /* host [n_surfaces]: token of the sentence-cased surface */
   int32_t n_surfaces;
   const void* embedding; /* device bf16 [vocab][hidden]; tied LM head; caller-owned */
+  int32_t precision;     /* 0 = bf16: one bf16 GEMM operand per activation, bf16 q/K/V;
+                          * 1 = bf16x2: activations as hi+lo bf16 pairs ([M][2K] GEMM operands
+                          *     against [W | W]), fp32 q/K/V -- fp32-equivalent activations on
+                          *     the bf16 tensor cores at twice the body FLOPs */
 } lb_llm_desc;
 
 int lb_llm_create(lb_batch* b, const lb_llm_desc* desc, lb_llm** out);
@@ -268,23 +274,28 @@ int lb_llm_plan(lb_llm* l, int32_t final_, int32_t min_frames, int32_t* n_waves,
 int lb_llm_wave_rows(lb_llm* l, int32_t wave, int64_t row0, int32_t n, int32_t* tokens,
                      int32_t* positions, int32_t* slots, int32_t* chains);
 int lb_llm_finish(lb_llm* l, int32_t final_, int32_t min_frames);
-/* x[M][hidden] fp32 residual (+= delta fp32 [M][hidden] if non-NULL); out bf16 = RMSNorm(x)*w.
+/* x[M][hidden] fp32 residual (+= delta fp32 [M][hidden] if non-NULL); out bf16 = RMSNorm(x)*w
+ * ([M][2 hidden] hi|lo pairs in bf16x2 precision).
  * store_slots != NULL: the rows are the final hidden states of those slots (kept in fp32 for
  * later next-token log-probs). */
 int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float eps, int32_t M,
                    void* out, const int32_t* store_slots);
-/* qkv fp32 [M][(n_heads + 2 n_kv_heads) head_dim] -> q_out bf16 [M][n_heads head_dim] rotated;
+/* qkv fp32 [M][(n_heads + 2 n_kv_heads) head_dim] -> q_out [M][n_heads head_dim] rotated (bf16;
+ * fp32 in bf16x2 precision);
  * rotated K and V written to the rows' slots of layer `layer`.  cos/sin fp32 [pos][head_dim/2] */
 int lb_llm_rope_kv(lb_llm* l, int32_t layer, const void* qkv, int32_t M, const int32_t* pos,
                    const int32_t* slots, const float* cos_tab, const float* sin_tab, void* q_out);
-/* causal GQA attention of each row over its ancestor chain; out bf16 [M][n_heads head_dim] */
+/* causal GQA attention of each row over its ancestor chain; out bf16 [M][n_heads head_dim]
+ * ([M][2 n_heads head_dim] hi|lo pairs in bf16x2 precision) */
 int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const int32_t* chains,
                      const int32_t* pos, void* out);
-/* gu bf16 [M][2 ffn] = [gate | up] -> out bf16 [M][ffn] = silu(gate) * up */
+/* gu [M][2 ffn] = [gate | up] (bf16; fp32 in bf16x2 precision) -> out bf16 [M][ffn] =
+ * silu(gate) * up ([M][2 ffn] hi|lo pairs in bf16x2 precision) */
 int lb_llm_swiglu(lb_llm* l, const void* gu, int32_t M, int32_t ffn, void* out);
 /* K6: log-sum-exp of LM-head logit rows (bf16 [M][ld], vocab columns) into the rows' slots */
 int lb_llm_lse(lb_llm* l, const void* logits, int32_t M, int64_t ld, const int32_t* slots);
-/* out[8]: slots, events, waves, forwarded rows, widest wave, device bytes, 0, 0 */
+/* out[8]: slots, events, waves, forwarded rows, widest wave, device bytes, scores computed
+ * (next-token log-probs), 0 */
 int lb_llm_stats(lb_llm* l, int64_t* out);
 /* Parity/debug: the slot table.  *n = slots in use; the first min(*n, max_n) rows are copied
  * into the host buffers (NULL skips a field).  state bits:

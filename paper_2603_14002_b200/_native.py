@@ -120,6 +120,7 @@ class LbLlmDesc(C.Structure):
         ("surface_tokens_first", C.c_void_p),
         ("n_surfaces", C.c_int32),
         ("embedding", C.c_void_p),
+        ("precision", C.c_int32),
     ]
 
 

@@ -15,8 +15,9 @@
 //   - slots are hash-consed on (parent slot, token) so equal texts share one slot;
 //   - a slot's log-prob needs only its parent's final hidden state and log-sum-exp
 //     (lp = h_parent . E[token] - lse_parent), so the transformer forward runs only for slots
-//     that get children or need end-of-sentence punctuation ("forward set"), in dependency
-//     waves (a wave's rows attend to K/V of slots forwarded in earlier waves/events);
+//     that get children or need end-of-sentence punctuation ("forward set"), all of one event
+//     in one pass in slot-id order, which is a dependency order (a row attends to K/V written in
+//     the same layer by its new ancestors, or by earlier events: tree-causal prefill);
 //   - attention reads K/V straight from the slot cache through per-row ancestor chains (page
 //     size one token), so surviving beams never copy or reorder KV: the cache is indexed by
 //     text, not by beam, and a beam reorder is free.
@@ -25,9 +26,9 @@
 //
 // Kernels:
 //   map_nodes_kernel      word-history nodes of live entries -> slots (per utterance CTA,
-//                         levels of unmapped ancestors resolved in order, global hash-consing)
+//                         unmapped ancestors resolved parent-first, global hash-consing)
 //   schedule_kernel       cum-needed slots and the forward set of this event
-//   level_kernel / scatter_kernel   dependency waves of the forward set (counting sort)
+//   flag_count/blk_scan/compact_kernel   forward set in slot-id (= dependency) order
 //   wave_rows_kernel      tokens, positions, ancestor chains of a wave's rows
 //   add_rmsnorm_kernel    residual add + RMSNorm (fp32 residual stream, bf16 GEMM operand)
 //   rope_kv_kernel        rotary embedding of q/k, K/V written into the slot cache
@@ -75,8 +76,9 @@ struct LlmDev {
   double* s_plp;  // [cap][3]
   float* s_lse;
   float* s_h;  // [cap][H] final normed hidden state (fp32: the next-token dot products)
-  bf16* kc;    // [L][cap][NKV*HD]
-  bf16* vc;
+  void* kc;    // [L][cap][NKV*HD] bf16, or fp32 when split
+  void* vc;
+  int32_t split;  // 1: bf16x2 precision (activations as hi+lo bf16 pairs, fp32 q/K/V)
   int32_t* htab;
   uint32_t hmask;
   int32_t* ctr;  // see C_* below
@@ -85,11 +87,9 @@ struct LlmDev {
   int32_t* nlist_depth;
   int32_t nlist_cap;
   int32_t* fwd_list;
-  int32_t* fwd_level;
   int32_t* cum_list;
   int32_t* wave_slots;
-  int32_t* lvl_count;  // [MAX_LEVELS]
-  int32_t* lvl_fill;   // [MAX_LEVELS]
+  int32_t* blk;        // [ceil(cap / 1024)] compaction block offsets
   const int32_t* tok_low;
   const int32_t* tok_cap;
   int32_t n_surf;
@@ -100,7 +100,7 @@ struct LlmDev {
 
 enum {
   C_SLOTS = 0,   // slots allocated
-  C_ERR = 1,     // bit 1: slot capacity, 2: node list, 4: depth, 8: levels
+  C_ERR = 1,     // bit 1: slot capacity, 2: node list, 4: depth
   C_NFWD = 2,    // forward-set size of this event
   C_NCUM = 3,    // cum-needed slots of this event
   C_BOS = 4,     // 1: BOS slot still to be forwarded
@@ -274,38 +274,65 @@ __global__ void __launch_bounds__(128) schedule_kernel(BatchDev b, LlmDev l, int
   }
 }
 
-// wave index of a scheduled slot = number of scheduled ancestors
-__global__ void level_kernel(LlmDev l) {
-  const int n = min(l.ctr[C_NFWD], (int)l.cap);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int s = l.fwd_list[i];
-    int lvl = 0;
-    for (int cur = l.s_parent[s]; cur >= 0 && l.s_fwd[cur] == 1; cur = l.s_parent[cur]) ++lvl;
-    if (lvl >= MAX_LEVELS) {
-      atomicOr(l.ctr + C_ERR, 8);
-      lvl = MAX_LEVELS - 1;
-    }
-    l.fwd_level[i] = lvl;
-    atomicAdd(l.lvl_count + lvl, 1);
+// The event's rows = scheduled slots in slot-id order.  A slot is allocated after its parent,
+// so id order is a dependency order (every row's new ancestors precede it), and slots created by
+// one utterance in one event are close in id space, so consecutive rows share ancestors and the
+// attention gathers of neighbouring CTAs hit the same K/V lines in L2.
+constexpr int CB = 1024;
+__global__ void __launch_bounds__(CB) flag_count_kernel(LlmDev l, int32_t* blk) {
+  const int ns = min(l.ctr[C_SLOTS], (int)l.cap);
+  const int s = blockIdx.x * CB + threadIdx.x;
+  if (blockIdx.x * CB >= ns) {
+    if (threadIdx.x == 0) blk[blockIdx.x] = 0;
+    return;
+  }
+  const int f = s < ns && l.s_fwd[s] == 1;
+  const int c = __syncthreads_count(f);
+  if (threadIdx.x == 0) blk[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(CB) blk_scan_kernel(int32_t* blk, int nblk) {
+  __shared__ int part[CB];
+  const int per = (nblk + CB - 1) / CB;
+  const int b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
+  int sum = 0;
+  for (int i = b0; i < b1; ++i) sum += blk[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < CB; o <<= 1) {  // inclusive Hillis-Steele scan
+    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int run = part[threadIdx.x] - sum;
+  for (int i = b0; i < b1; ++i) {
+    const int c = blk[i];
+    blk[i] = run;
+    run += c;
   }
 }
 
-__global__ void scatter_kernel(LlmDev l) {
-  __shared__ int off[MAX_LEVELS];
-  if (threadIdx.x == 0) {
-    int a = 0;
-    for (int v = 0; v < MAX_LEVELS; ++v) {
-      off[v] = a;
-      a += l.lvl_count[v];
+__global__ void __launch_bounds__(CB) compact_kernel(LlmDev l, const int32_t* blk_off) {
+  __shared__ int wsum[CB / 32];
+  const int ns = min(l.ctr[C_SLOTS], (int)l.cap);
+  if (blockIdx.x * CB >= ns) return;
+  const int s = blockIdx.x * CB + threadIdx.x;
+  const int f = s < ns && l.s_fwd[s] == 1;
+  const unsigned bal = __ballot_sync(FULLMASK, f);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    int v = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULLMASK, v, o);
+      if (lane >= o) v += y;
     }
+    wsum[lane] = v - wsum[lane];  // exclusive
   }
   __syncthreads();
-  const int n = min(l.ctr[C_NFWD], (int)l.cap);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int lvl = l.fwd_level[i];
-    const int pos = off[lvl] + atomicAdd(l.lvl_fill + lvl, 1);
-    l.wave_slots[pos] = l.fwd_list[i];
-  }
+  if (f) l.wave_slots[blk_off[blockIdx.x] + wsum[warp] + __popc(bal & ((1u << lane) - 1))] = s;
 }
 
 __global__ void wave_rows_kernel(LlmDev l, int64_t row0, int n, int32_t* tok, int32_t* pos,
@@ -332,7 +359,7 @@ __global__ void wave_rows_kernel(LlmDev l, int64_t row0, int n, int32_t* tok, in
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float* delta,
                                                           const float* w, float eps, int H,
                                                           bf16* out, const int32_t* store_slots,
-                                                          float* s_h) {
+                                                          float* s_h, int split) {
   const int row = blockIdx.x;
   float* xr = x + (size_t)row * H;
   const float* dr = delta ? delta + (size_t)row * H : nullptr;
@@ -360,15 +387,22 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float*
   }
   __syncthreads();
   const float r = rsqrtf(red[0] / (float)H + eps);
-  bf16* orow = out + (size_t)row * H;
+  bf16* orow = out + (size_t)row * H * (split ? 2 : 1);
   float* hrow = store_slots ? s_h + (size_t)store_slots[row] * H : nullptr;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
     const float4 v = *reinterpret_cast<const float4*>(xr + i);
     const float4 g = *reinterpret_cast<const float4*>(w + i);
     const float4 y = make_float4(v.x * r * g.x, v.y * r * g.y, v.z * r * g.z, v.w * r * g.w);
     __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(orow + i);
-    op[0] = __floats2bfloat162_rn(y.x, y.y);
-    op[1] = __floats2bfloat162_rn(y.z, y.w);
+    const __nv_bfloat162 h0 = __floats2bfloat162_rn(y.x, y.y), h1 = __floats2bfloat162_rn(y.z, y.w);
+    op[0] = h0;
+    op[1] = h1;
+    if (split) {  // lo half: the bf16 rounding residual, so hi + lo carries ~16 mantissa bits
+      const float2 a = __bfloat1622float2(h0), c = __bfloat1622float2(h1);
+      __nv_bfloat162* lp = reinterpret_cast<__nv_bfloat162*>(orow + H + i);
+      lp[0] = __floats2bfloat162_rn(y.x - a.x, y.y - a.y);
+      lp[1] = __floats2bfloat162_rn(y.z - c.x, y.w - c.y);
+    }
     if (hrow) *reinterpret_cast<float4*>(hrow + i) = y;
   }
 }
@@ -376,9 +410,17 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float*
 // qkv[M][(NH + 2 NKV) HD] fp32 -> q_out[M][NH HD] bf16 rotated; rotated k and v stored (bf16)
 // at the row's slot.
 // rotate_half convention: (x1, x2) -> (x1 cos - x2 sin, x2 cos + x1 sin), x1/x2 = halves.
+template <typename T>
+__device__ __forceinline__ T to_store(float v);
+template <>
+__device__ __forceinline__ bf16 to_store<bf16>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ float to_store<float>(float v) { return v; }
+
+template <typename T>
 __global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, const int32_t* pos,
                                const int32_t* slots, const float* cosT, const float* sinT,
-                               bf16* q_out) {
+                               T* q_out) {
   const int row = blockIdx.x;
   if (row >= M) return;
   const int HD = l.HD, half = HD / 2, NH = l.NH, NKV = l.NKV;
@@ -387,8 +429,8 @@ __global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, con
   const int p = pos[row];
   const size_t slot = (size_t)slots[row];
   const size_t kvw = (size_t)NKV * HD;
-  bf16* kd = l.kc + ((size_t)layer * l.cap + slot) * kvw;
-  bf16* vd = l.vc + ((size_t)layer * l.cap + slot) * kvw;
+  T* kd = reinterpret_cast<T*>(l.kc) + ((size_t)layer * l.cap + slot) * kvw;
+  T* vd = reinterpret_cast<T*>(l.vc) + ((size_t)layer * l.cap + slot) * kvw;
   const float* cs = cosT + (size_t)p * half;
   const float* sn = sinT + (size_t)p * half;
   const int npairs = (NH + NKV) * half;
@@ -397,48 +439,152 @@ __global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, con
     const float* src = in + head * HD;
     const float x1 = src[i], x2 = src[i + half];
     const float c = cs[i], s = sn[i];
-    const bf16 o1 = __float2bfloat16_rn(x1 * c - x2 * s);
-    const bf16 o2 = __float2bfloat16_rn(x2 * c + x1 * s);
+    const T o1 = to_store<T>(x1 * c - x2 * s);
+    const T o2 = to_store<T>(x2 * c + x1 * s);
     if (head < NH) {
-      bf16* dst = q_out + (size_t)row * NH * HD + head * HD;
+      T* dst = q_out + (size_t)row * NH * HD + head * HD;
       dst[i] = o1;
       dst[i + half] = o2;
     } else {
-      bf16* dst = kd + (head - NH) * HD;
+      T* dst = kd + (head - NH) * HD;
       dst[i] = o1;
       dst[i + half] = o2;
     }
   }
   const float* vin = in + (NH + NKV) * HD;
-  for (int t = threadIdx.x; t < NKV * HD; t += blockDim.x) vd[t] = __float2bfloat16_rn(vin[t]);
+  for (int t = threadIdx.x; t < NKV * HD; t += blockDim.x) vd[t] = to_store<T>(vin[t]);
 }
 
-// One warp per (row, kv head): the G = NH/NKV query heads of the group attend over the row's
-// ancestor chain (BOS .. itself, causal by construction).  Lanes own chain positions for the
-// scores (each lane dots a whole K row held in one 128/256-B line) and head dims for the V sum.
-template <int HD, int G>
-__global__ void __launch_bounds__(256) chain_attn_kernel(LlmDev l, int layer, const bf16* q,
-                                                         int M, const int32_t* chains,
-                                                         const int32_t* pos, float scale,
-                                                         bf16* out) {
-  constexpr int NWB = 8;
-  constexpr int DPL = HD / 32;  // dims per lane in the V sum
-  __shared__ float qs[NWB][G][HD];
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// DPL consecutive elements of a bf16 / fp32 vector (16-B aligned) as floats
+template <int DPL>
+__device__ __forceinline__ void load_f(const bf16* p, float* out) {
+#pragma unroll
+  for (int c = 0; c < DPL / 8; ++c) {
+    const uint4 u = reinterpret_cast<const uint4*>(p)[c];
+    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(p2[e]);
+      out[c * 8 + 2 * e] = f.x;
+      out[c * 8 + 2 * e + 1] = f.y;
+    }
+  }
+}
+template <int DPL>
+__device__ __forceinline__ void load_f(const float* p, float* out) {
+#pragma unroll
+  for (int c = 0; c < DPL / 4; ++c) {
+    const float4 u = reinterpret_cast<const float4*>(p)[c];
+    out[c * 4] = u.x;
+    out[c * 4 + 1] = u.y;
+    out[c * 4 + 2] = u.z;
+    out[c * 4 + 3] = u.w;
+  }
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sa), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sa), "r"(bytes)
+               : "memory");
+}
+// 1-D TMA bulk copy global -> shared (a gather of one cache row), completion on an mbarrier
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                             uint64_t* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned bb = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(bb)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LLW%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LLW%=;\n}\n" ::"r"(sa),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int ATTN_STAGE_BYTES = 32 * 1024;  // K+V rows of one chunk of chain positions
+
+// chain positions per chunk for K/V cache rows of `rowb` bytes (all kv heads of a slot)
+__host__ __device__ inline int attn_chunk(int rowb) {
+  const int c = ATTN_STAGE_BYTES / (2 * rowb);
+  return c < 1 ? 1 : (c > 32 ? 32 : c);
+}
+
+// One CTA per row, one warp per kv head.  The row's ancestor chain (BOS .. itself; causal by
+// construction) is gathered chunk by chunk: lane j of warp 0 issues two 1-D TMA bulk copies
+// (the K and V cache rows of chain position j, all kv heads at once) onto a double-buffered
+// stage with an mbarrier, so the next chunk's gather is in flight while this one is consumed.
+// Each warp then covers PPW positions per pass with SUB = HD/DPL lanes per position: every lane
+// keeps its DPL-dim slice of the G query vectors (its kv head's group) in registers, reduces
+// partial dots over its SUB lanes and keeps (max, sum, acc) on a warp-uniform scale, so the
+// position groups' partial outputs are summed once at the end.
+// Output: bf16 [M][NH*HD], or hi|lo bf16 pairs [M][2*NH*HD] in split precision.
+template <int HD, int G, int DPL, typename T>
+__global__ void __launch_bounds__(256, 2) chain_attn_kernel(LlmDev l, int layer, const T* q,
+                                                            const int32_t* chains,
+                                                            const int32_t* pos, float scale,
+                                                            bf16* out) {
+  constexpr int SUB = HD / DPL;
+  constexpr int PPW = 32 / SUB;
+  extern __shared__ __align__(128) unsigned char attn_smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(attn_smem);
+  unsigned char* stages = attn_smem + 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * NWB + warp;
-  const int NKV = l.NKV;
-  const int row = gw / NKV, kvh = gw - row * NKV;
-  if (row >= M) return;
-  const int NH = l.NH;
-  const bf16* qr = q + (size_t)row * NH * HD + (size_t)kvh * G * HD;
-  for (int t = lane; t < G * HD; t += 32) qs[warp][t / HD][t % HD] = __bfloat162float(qr[t]);
-  __syncwarp();
+  const int row = blockIdx.x;
+  const int NKV = l.NKV, kvh = warp;
+  const int rowb = NKV * HD * (int)sizeof(T);
+  const int CH = attn_chunk(rowb);
+  const int stage_bytes = 2 * CH * rowb;
   const int n = pos[row] + 1;
-  const int pitch = l.max_depth + 1;
-  const int32_t* ch = chains + (size_t)row * pitch;
-  const size_t kvw = (size_t)NKV * HD;
-  const bf16* kb = l.kc + (size_t)layer * l.cap * kvw + (size_t)kvh * HD;
-  const bf16* vb = l.vc + (size_t)layer * l.cap * kvw + (size_t)kvh * HD;
+  const int nch = (n + CH - 1) / CH;
+  const int32_t* ch = chains + (size_t)row * (l.max_depth + 1);
+  const unsigned char* kbase = reinterpret_cast<const unsigned char*>(l.kc) + (size_t)layer * l.cap * rowb;
+  const unsigned char* vbase = reinterpret_cast<const unsigned char*>(l.vc) + (size_t)layer * l.cap * rowb;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int c) {  // warp 0
+    const int st = c & 1, c0 = c * CH, cn = min(CH, n - c0);
+    unsigned char* kd = stages + (size_t)st * stage_bytes;
+    unsigned char* vd = kd + (size_t)CH * rowb;
+    if (lane == 0) mbar_expect_tx(&bars[st], (unsigned)(2 * cn * rowb));
+    __syncwarp();
+    if (lane < cn) {
+      const size_t sl = (size_t)ch[c0 + lane];
+      tma_bulk_g2s(kd + (size_t)lane * rowb, kbase + sl * rowb, rowb, &bars[st]);
+      tma_bulk_g2s(vd + (size_t)lane * rowb, vbase + sl * rowb, rowb, &bars[st]);
+    }
+  };
+  if (warp == 0) issue(0);
+  const int sub = lane % SUB, pg = lane / SUB;
+  float qv[G][DPL];
+  {
+    const T* qr = q + (size_t)row * l.NH * HD + (size_t)kvh * G * HD + sub * DPL;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      load_f<DPL>(qr + g * HD, qv[g]);
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) qv[g][d] *= scale;
+    }
+  }
   float m[G], den[G], acc[G][DPL];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -447,106 +593,108 @@ __global__ void __launch_bounds__(256) chain_attn_kernel(LlmDev l, int layer, co
 #pragma unroll
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
   }
-  for (int base = 0; base < n; base += 32) {
-    const int j = base + lane;
-    const bool valid = j < n;
-    const int s = valid ? ch[j] : 0;
-    float sc[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) sc[g] = 0.f;
-    if (valid) {
-      const uint4* kr = reinterpret_cast<const uint4*>(kb + (size_t)s * kvw);
-#pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        const uint4 u = kr[c];
-        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 kf = __bfloat1622float2(k2[e]);
-#pragma unroll
-          for (int g = 0; g < G; ++g)
-            sc[g] += qs[warp][g][c * 8 + 2 * e] * kf.x + qs[warp][g][c * 8 + 2 * e + 1] * kf.y;
-        }
-      }
-    }
-    float p[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float x = valid ? sc[g] * scale : -INFINITY;
-      const float mx = fmaxf(m[g], warp_maxf(x));
-      p[g] = valid ? expf(x - mx) : 0.f;
-      const float corr = expf(m[g] - mx);  // exp(-inf) = 0 on the first chunk
-      den[g] = den[g] * corr + warp_sum(p[g]);
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
-      m[g] = mx;
-    }
-    const int cnt = min(32, n - base);
-    for (int jj = 0; jj < cnt; ++jj) {
-      const int sj = __shfl_sync(FULLMASK, s, jj);
-      const bf16* vr = vb + (size_t)sj * kvw + lane * DPL;
-      float v[DPL];
-      if (DPL == 2) {
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-        v[0] = f.x;
-        v[DPL - 1] = f.y;
-      } else {
-#pragma unroll
-        for (int d = 0; d < DPL; d += 2) {
-          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + d));
-          v[d] = f.x;
-          v[d + 1] = f.y;
-        }
-      }
+  const int hoff = (kvh * HD + sub * DPL) * (int)sizeof(T);
+  for (int c = 0; c < nch; ++c) {
+    if (warp == 0 && c + 1 < nch) issue(c + 1);  // its stage was released by the last barrier
+    mbar_wait(&bars[c & 1], (unsigned)((c >> 1) & 1));
+    const unsigned char* ks = stages + (size_t)(c & 1) * stage_bytes;
+    const unsigned char* vs = ks + (size_t)CH * rowb;
+    const int cn = min(CH, n - c * CH);
+    for (int pb = 0; pb < cn; pb += PPW) {
+      const int j = pb + pg;
+      const bool valid = j < cn;
+      const int jr = valid ? j : 0;
+      float kf[DPL], vf[DPL];
+      load_f<DPL>(reinterpret_cast<const T*>(ks + (size_t)jr * rowb + hoff), kf);
+      load_f<DPL>(reinterpret_cast<const T*>(vs + (size_t)jr * rowb + hoff), vf);
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const float pj = __shfl_sync(FULLMASK, p[g], jj);
+        float part = 0.f;
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[g][d] += pj * v[d];
+        for (int d = 0; d < DPL; ++d) part += qv[g][d] * kf[d];
+#pragma unroll
+        for (int o = SUB / 2; o > 0; o >>= 1) part += __shfl_xor_sync(FULLMASK, part, o);
+        const float x = valid ? part : -INFINITY;
+        const float mnew = fmaxf(m[g], warp_maxf(x));
+        const float p = valid ? __expf(x - mnew) : 0.f;
+        const float corr = __expf(m[g] - mnew);  // 0 on the first pass (m = -inf)
+        den[g] = den[g] * corr + warp_sum(sub == 0 ? p : 0.f);
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) acc[g][d] = acc[g][d] * corr + p * vf[d];
+        m[g] = mnew;
       }
     }
+    __syncthreads();  // every warp is done with this stage before it is refilled
   }
-  bf16* orow = out + (size_t)row * NH * HD + (size_t)kvh * G * HD;
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const float inv = 1.f / den[g];
+  for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int d = 0; d < DPL; ++d) orow[g * HD + lane * DPL + d] = __float2bfloat16_rn(acc[g][d] * inv);
+    for (int d = 0; d < DPL; ++d)
+#pragma unroll
+      for (int o = 16; o >= SUB; o >>= 1) acc[g][d] += __shfl_xor_sync(FULLMASK, acc[g][d], o);
+  if (pg == 0) {
+    const int W = l.NH * HD;
+    bf16* orow = out + (size_t)row * W * (l.split ? 2 : 1) + (size_t)kvh * G * HD + sub * DPL;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float inv = 1.f / den[g];
+#pragma unroll
+      for (int c = 0; c < DPL / 8; ++c) {
+        uint4 hi, lo;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&hi);
+        __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&lo);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float a = acc[g][c * 8 + 2 * e] * inv, b = acc[g][c * 8 + 2 * e + 1] * inv;
+          h2[e] = __floats2bfloat162_rn(a, b);
+          const float2 hf = __bfloat1622float2(h2[e]);
+          l2[e] = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+        }
+        reinterpret_cast<uint4*>(orow + g * HD)[c] = hi;
+        if (l.split) reinterpret_cast<uint4*>(orow + W + g * HD)[c] = lo;
+      }
+    }
   }
 }
 
-// gu[M][2F] = [gate | up] -> out[M][F] = bf16(silu(gate) * up)
-__global__ void swiglu_kernel(const bf16* gu, int64_t M, int F, bf16* out) {
-  const int64_t n2 = M * (int64_t)F / 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = 2 * i;
-    const int64_t row = e / F, col = e - row * F;
-    const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(gu + row * 2 * F + col));
-    const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(gu + row * 2 * F + F + col));
-    const float a = g.x / (1.f + expf(-g.x)) * u.x;
-    const float b = g.y / (1.f + expf(-g.y)) * u.y;
-    *reinterpret_cast<__nv_bfloat162*>(out + e) = __floats2bfloat162_rn(a, b);
+// gu[M][2F] = [gate | up] (bf16, or fp32 in split precision) -> out[M][F] = bf16(silu(gate) * up)
+// (split: hi|lo pairs [M][2F]); 8 columns per thread
+template <typename TI>
+__global__ void swiglu_kernel(const TI* gu, int F, bf16* out, int split) {
+  const int row = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= F) return;
+  const TI* gr = gu + (size_t)row * 2 * F;
+  float g[8], u[8];
+  load_f<8>(gr + c, g);
+  load_f<8>(gr + F + c, u);
+  uint4 ov, lv;
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&ov);
+  __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&lv);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float a = g[2 * e] / (1.f + __expf(-g[2 * e])) * u[2 * e];
+    const float b = g[2 * e + 1] / (1.f + __expf(-g[2 * e + 1])) * u[2 * e + 1];
+    o2[e] = __floats2bfloat162_rn(a, b);
+    const float2 h = __bfloat1622float2(o2[e]);
+    l2[e] = __floats2bfloat162_rn(a - h.x, b - h.y);
   }
+  bf16* orow = out + (size_t)row * F * (split ? 2 : 1);
+  *reinterpret_cast<uint4*>(orow + c) = ov;
+  if (split) *reinterpret_cast<uint4*>(orow + F + c) = lv;
 }
 
 // K6a: log-sum-exp of one LM-head logit row per CTA (16-B loads, online max/sum merge)
-__global__ void __launch_bounds__(512) lse_kernel(const bf16* logits, int64_t ld, int V,
+template <typename TL>
+__global__ void __launch_bounds__(512) lse_kernel(const TL* logits, int64_t ld, int V,
                                                   const int32_t* slots, float* s_lse) {
   const int row = blockIdx.x;
-  const bf16* r = logits + (size_t)row * ld;
+  const TL* r = logits + (size_t)row * ld;
   float m = -INFINITY, s = 0.f;
   const int nv = V / 8;
   for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-    const uint4 u = reinterpret_cast<const uint4*>(r)[i];
-    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
     float x[8];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(p[e]);
-      x[2 * e] = f.x;
-      x[2 * e + 1] = f.y;
-    }
+    load_f<8>(r + (size_t)i * 8, x);
     float mx = x[0];
 #pragma unroll
     for (int e = 1; e < 8; ++e) mx = fmaxf(mx, x[e]);
@@ -558,7 +706,7 @@ __global__ void __launch_bounds__(512) lse_kernel(const bf16* logits, int64_t ld
     s = acc;
   }
   for (int i = nv * 8 + threadIdx.x; i < V; i += blockDim.x) {
-    const float x = __bfloat162float(r[i]);
+    const float x = (float)r[i];
     const float nm = fmaxf(m, x);
     s = s * expf(m - nm) + expf(x - nm);
     m = nm;
@@ -788,7 +936,6 @@ static int check_err_flags(lb_llm* l) {
   if (err & 1) return lbh::set_error(LB_ERR_CAPACITY, "LLM prefix cache full (max_slots)");
   if (err & 2) return lbh::set_error(LB_ERR_CAPACITY, "LLM node list full for one fusion event");
   if (err & 4) return lbh::set_error(LB_ERR_CAPACITY, "text longer than the LLM max_depth");
-  if (err & 8) return lbh::set_error(LB_ERR_CAPACITY, "more than LB_LLM_MAX_WAVES dependency levels");
   return LB_OK;
 }
 
@@ -823,6 +970,8 @@ int lb_llm_create(lb_batch* b, const lb_llm_desc* d, lb_llm** out) {
   x.bos_tok = d->bos_token;
   for (int j = 0; j < 3; ++j) x.punct_tok[j] = d->punct_tokens[j];
   x.emb = reinterpret_cast<const bf16*>(d->embedding);
+  if (d->precision != 0 && d->precision != 1) return lbh::set_error(LB_ERR_ARG, "precision must be 0 (bf16) or 1 (bf16x2)");
+  x.split = d->precision;
   x.n_surf = d->n_surfaces;
   const size_t cap = (size_t)x.cap;
   const size_t kvw = (size_t)x.NKV * x.HD;
@@ -844,26 +993,25 @@ int lb_llm_create(lb_batch* b, const lb_llm_desc* d, lb_llm** out) {
   CKL(dalloc(&x.s_plp, cap * 3));
   CKL(dalloc(&x.s_lse, cap));
   CKL(dalloc(&x.s_h, cap * x.H));
-  CKL(dalloc(&x.kc, (size_t)x.L * cap * kvw));
-  CKL(dalloc(&x.vc, (size_t)x.L * cap * kvw));
+  const size_t esz = x.split ? 4 : 2;
+  CKL(cudaMalloc(&x.kc, (size_t)x.L * cap * kvw * esz));
+  CKL(cudaMalloc(&x.vc, (size_t)x.L * cap * kvw * esz));
   CKL(dalloc(&x.htab, hsz));
   CKL(dalloc(&x.ctr, C_NCTR));
   CKL(dalloc(&x.node_slot, (size_t)l->node_slot_elems));
   CKL(dalloc(&x.nlist, B * x.nlist_cap));
   CKL(dalloc(&x.nlist_depth, B * x.nlist_cap));
   CKL(dalloc(&x.fwd_list, cap));
-  CKL(dalloc(&x.fwd_level, cap));
   CKL(dalloc(&x.cum_list, cap));
   CKL(dalloc(&x.wave_slots, cap));
-  CKL(dalloc(&x.lvl_count, MAX_LEVELS));
-  CKL(dalloc(&x.lvl_fill, MAX_LEVELS));
+  CKL(dalloc(&x.blk, (cap + CB - 1) / CB));
   CKL(dalloc(&l->d_tok_low, x.n_surf));
   CKL(dalloc(&l->d_tok_cap, x.n_surf));
   CKL(cudaMemcpy(l->d_tok_low, d->surface_tokens, x.n_surf * 4, cudaMemcpyHostToDevice));
   CKL(cudaMemcpy(l->d_tok_cap, d->surface_tokens_first, x.n_surf * 4, cudaMemcpyHostToDevice));
   x.tok_low = l->d_tok_low;
   x.tok_cap = l->d_tok_cap;
-  l->bytes = (int64_t)cap * (4 * 6 + 8 * 5 + 4 + 4 * x.H + 4 * 4) + (int64_t)2 * x.L * cap * kvw * 2 +
+  l->bytes = (int64_t)cap * (4 * 6 + 8 * 5 + 4 + 4 * x.H + 4 * 4) + (int64_t)2 * x.L * cap * kvw * esz +
              (int64_t)hsz * 4 + l->node_slot_elems * 4 + (int64_t)B * x.nlist_cap * 8;
   *out = l;
   return lb_llm_reset(l);
@@ -875,8 +1023,8 @@ int lb_llm_destroy(lb_llm* l) {
   LlmDev& x = l->dev;
   void* ptrs[] = {x.s_parent, x.s_token, x.s_depth, x.s_fwd, x.s_cum, x.s_pun, x.s_lp, x.s_cumv,
                   x.s_plp, x.s_lse, x.s_h, x.kc, x.vc, x.htab, x.ctr, x.node_slot, x.nlist,
-                  x.nlist_depth, x.fwd_list, x.fwd_level, x.cum_list, x.wave_slots, x.lvl_count,
-                  x.lvl_fill, l->d_tok_low, l->d_tok_cap};
+                  x.nlist_depth, x.fwd_list, x.cum_list, x.wave_slots, x.blk,
+                  l->d_tok_low, l->d_tok_cap};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete l;
@@ -912,35 +1060,37 @@ int lb_llm_plan(lb_llm* l, int32_t final_, int32_t min_frames, int32_t* n_waves,
   LlmDev& x = l->dev;
   cudaStream_t st = b->st;
   CKL(cudaMemsetAsync(x.ctr + C_NFWD, 0, 8, st));  // C_NFWD, C_NCUM
-  CKL(cudaMemsetAsync(x.lvl_count, 0, MAX_LEVELS * 4, st));
-  CKL(cudaMemsetAsync(x.lvl_fill, 0, MAX_LEVELS * 4, st));
   const int B = b->n_trials;
+  const int nblk = (int)((x.cap + CB - 1) / CB);
   LAUNCH(map_nodes_kernel<<<B, 256, 0, st>>>(b->dev, x, min_frames));
   LAUNCH(schedule_kernel<<<B, 128, 0, st>>>(b->dev, x, min_frames, final_));
-  LAUNCH(level_kernel<<<4 * 148, 256, 0, st>>>(x));
-  LAUNCH(scatter_kernel<<<4 * 148, 256, 0, st>>>(x));
-  std::vector<int32_t> cnt(MAX_LEVELS);
-  CKL(cudaMemcpyAsync(cnt.data(), x.lvl_count, MAX_LEVELS * 4, cudaMemcpyDeviceToHost, st));
+  LAUNCH(flag_count_kernel<<<nblk, CB, 0, st>>>(x, x.blk));
+  LAUNCH(blk_scan_kernel<<<1, CB, 0, st>>>(x.blk, nblk));
+  LAUNCH(compact_kernel<<<nblk, CB, 0, st>>>(x, x.blk));
+  int32_t nfc[2] = {0, 0};  // C_NFWD, C_NCUM
+  CKL(cudaMemcpyAsync(nfc, x.ctr + C_NFWD, 8, cudaMemcpyDeviceToHost, st));
   int rc = check_err_flags(l);  // synchronises
   if (rc) return rc;
   l->wave_off.clear();
   l->wave_rows.clear();
-  int64_t off = 0;
+  // One wave per event (see compact_kernel): inside a layer the K/V of all rows are written
+  // before the attention kernel reads them (tree-causal prefill), and any row-prefix chunk of
+  // the wave holds the parents of its rows.
+  const int64_t total = std::min<int64_t>(nfc[0], x.cap);
+  l->cum += nfc[1];
   int nw = 0;
-  for (int v = 0; v < MAX_LEVELS; ++v) {
-    if (cnt[v] == 0) break;
-    l->wave_off.push_back(off);
-    l->wave_rows.push_back(cnt[v]);
-    wave_rows[v] = cnt[v];
-    off += cnt[v];
-    l->max_wave_rows = std::max<int64_t>(l->max_wave_rows, cnt[v]);
-    ++nw;
+  if (total > 0) {
+    l->wave_off.push_back(0);
+    l->wave_rows.push_back(total);
+    wave_rows[0] = total;
+    nw = 1;
   }
+  l->max_wave_rows = std::max<int64_t>(l->max_wave_rows, total);
   *n_waves = nw;
   l->cur_nwaves = nw;
   l->events += 1;
   l->waves += nw;
-  l->rows += off;
+  l->rows += total;
   return LB_OK;
 }
 
@@ -976,7 +1126,7 @@ int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float
   if (M <= 0) return LB_OK;
   LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
                                                       l->dev.H, reinterpret_cast<bf16*>(out),
-                                                      store_slots, l->dev.s_h));
+                                                      store_slots, l->dev.s_h, l->dev.split));
   return LB_OK;
 }
 
@@ -985,9 +1135,13 @@ int lb_llm_rope_kv(lb_llm* l, int32_t layer, const void* qkv, int32_t M, const i
   if (!l || !qkv || !pos || !slots || !cos_tab || !sin_tab || !q_out) return lbh::set_error(LB_ERR_ARG, "null argument");
   if (layer < 0 || layer >= l->dev.L) return lbh::set_error(LB_ERR_ARG, "layer out of range");
   if (M <= 0) return LB_OK;
-  LAUNCH(rope_kv_kernel<<<M, 128, 0, l->b->st>>>(l->dev, layer, reinterpret_cast<const float*>(qkv), M,
-                                                  pos, slots, cos_tab, sin_tab,
-                                                  reinterpret_cast<bf16*>(q_out)));
+  const float* in = reinterpret_cast<const float*>(qkv);
+  if (l->dev.split)
+    LAUNCH(rope_kv_kernel<float><<<M, 128, 0, l->b->st>>>(l->dev, layer, in, M, pos, slots, cos_tab,
+                                                           sin_tab, reinterpret_cast<float*>(q_out)));
+  else
+    LAUNCH(rope_kv_kernel<bf16><<<M, 128, 0, l->b->st>>>(l->dev, layer, in, M, pos, slots, cos_tab,
+                                                          sin_tab, reinterpret_cast<bf16*>(q_out)));
   return LB_OK;
 }
 
@@ -998,20 +1152,31 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
   if (M <= 0) return LB_OK;
   const LlmDev& x = l->dev;
   const int G = x.NH / x.NKV;
-  const int64_t warps = (int64_t)M * x.NKV;
-  const int grid = (int)((warps + 7) / 8);
+  if (x.NKV > 8) return lbh::set_error(LB_ERR_ARG, "n_kv_heads must be <= 8");
   const float scale = 1.0f / sqrtf((float)x.HD);
-  const bf16* qq = reinterpret_cast<const bf16*>(q);
   bf16* oo = reinterpret_cast<bf16*>(out);
   cudaStream_t st = l->b->st;
-#define ATT(HDV, GV) \
-  LAUNCH(chain_attn_kernel<HDV, GV><<<grid, 256, 0, st>>>(x, layer, qq, M, chains, pos, scale, oo))
+#define ATT_T(HDV, GV, DV, TV)                                                                  \
+  do {                                                                                          \
+    auto kfn = chain_attn_kernel<HDV, GV, DV, TV>;                                              \
+    const int rowb = x.NKV * HDV * (int)sizeof(TV);                                             \
+    const int smem = 128 + 2 * 2 * attn_chunk(rowb) * rowb;                                     \
+    CKL(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));          \
+    LAUNCH(kfn<<<M, 32 * x.NKV, smem, st>>>(x, layer, reinterpret_cast<const TV*>(q), chains,   \
+                                            pos, scale, oo));                                   \
+  } while (0)
+#define ATT(HDV, GV, DV)                      \
+  do {                                        \
+    if (x.split) ATT_T(HDV, GV, DV, float);   \
+    else ATT_T(HDV, GV, DV, bf16);            \
+  } while (0)
   if (x.HD == 64) {
-    if (G == 1) ATT(64, 1); else if (G == 2) ATT(64, 2); else if (G == 4) ATT(64, 4); else ATT(64, 8);
+    if (G == 1) ATT(64, 1, 16); else if (G == 2) ATT(64, 2, 16); else if (G == 4) ATT(64, 4, 8); else ATT(64, 8, 8);
   } else {
-    if (G == 1) ATT(128, 1); else if (G == 2) ATT(128, 2); else if (G == 4) ATT(128, 4); else ATT(128, 8);
+    if (G == 1) ATT(128, 1, 16); else if (G == 2) ATT(128, 2, 16); else if (G == 4) ATT(128, 4, 8); else ATT(128, 8, 8);
   }
 #undef ATT
+#undef ATT_T
   return LB_OK;
 }
 
@@ -1019,10 +1184,14 @@ int lb_llm_swiglu(lb_llm* l, const void* gu, int32_t M, int32_t ffn, void* out) 
   if (!l || !gu || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
   if (ffn % 2 != 0) return lbh::set_error(LB_ERR_ARG, "ffn must be even");
   if (M <= 0) return LB_OK;
-  const int64_t n2 = (int64_t)M * ffn / 2;
-  const int grid = (int)std::min<int64_t>(16 * 148, (n2 + 255) / 256);
-  LAUNCH(swiglu_kernel<<<grid, 256, 0, l->b->st>>>(reinterpret_cast<const bf16*>(gu), M, ffn,
-                                                   reinterpret_cast<bf16*>(out)));
+  if (ffn % 8 != 0) return lbh::set_error(LB_ERR_ARG, "ffn must be a multiple of 8");
+  const dim3 grid((ffn / 8 + 127) / 128, M);
+  if (l->dev.split)
+    LAUNCH(swiglu_kernel<float><<<grid, 128, 0, l->b->st>>>(reinterpret_cast<const float*>(gu), ffn,
+                                                            reinterpret_cast<bf16*>(out), 1));
+  else
+    LAUNCH(swiglu_kernel<bf16><<<grid, 128, 0, l->b->st>>>(reinterpret_cast<const bf16*>(gu), ffn,
+                                                           reinterpret_cast<bf16*>(out), 0));
   return LB_OK;
 }
 
@@ -1030,8 +1199,12 @@ int lb_llm_lse(lb_llm* l, const void* logits, int32_t M, int64_t ld, const int32
   if (!l || !logits || !slots) return lbh::set_error(LB_ERR_ARG, "null argument");
   if (ld % 8 != 0) return lbh::set_error(LB_ERR_ARG, "logit row pitch must be a multiple of 8");
   if (M <= 0) return LB_OK;
-  LAUNCH(lse_kernel<<<M, 512, 0, l->b->st>>>(reinterpret_cast<const bf16*>(logits), ld, l->dev.vocab,
-                                              slots, l->dev.s_lse));
+  if (l->dev.split)  // fp32 logits of the hi|lo LM-head GEMM
+    LAUNCH(lse_kernel<float><<<M, 512, 0, l->b->st>>>(reinterpret_cast<const float*>(logits), ld,
+                                                      l->dev.vocab, slots, l->dev.s_lse));
+  else
+    LAUNCH(lse_kernel<bf16><<<M, 512, 0, l->b->st>>>(reinterpret_cast<const bf16*>(logits), ld,
+                                                     l->dev.vocab, slots, l->dev.s_lse));
   return LB_OK;
 }
 
@@ -1046,7 +1219,7 @@ int lb_llm_stats(lb_llm* l, int64_t* out) {
   out[3] = l->rows;
   out[4] = l->max_wave_rows;
   out[5] = l->bytes;
-  out[6] = 0;
+  out[6] = l->cum;
   out[7] = 0;
   return LB_OK;
 }
