@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-llm", action="store_true",
+                    help="skip the BASELINE config-3 (LLM fusion) summary in the default line")
     ap.add_argument("--phases", action="store_true", help="add per-phase cycle breakdown of K2")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic: keep L2 warm between steps")
     ap.add_argument("--config", type=int, choices=(2, 3), default=2,
@@ -336,8 +338,32 @@ def run_ours(args):
     if rank == 0 and world_n == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(world, cfg, raws[: min(64, B)], args.cpu_seconds)
 
+    clocks = clk.summary()
+    llm = None
+    if not args.no_llm:  # BASELINE config 3 on the same utterances: + Llama-3.2-1B delayed fusion
+        cfg3 = cfg.replace(llm_rescore_interval=args.interval)
+        llm = {"workload": llm_workload(args, world, cfg3)["workload"]}
+        for prec in ("bf16x2", "bf16"):
+            core = llm_core(dev, world, cfg3, raws, args.llm, prec, max(1, min(args.steps, 3)), 1,
+                            world_n)
+            llm[prec] = {
+                "value": core["value"], "unit": "frames/s", "ms_per_step": core["ms_per_step"],
+                "rtf": (core["ms_per_step"] / 1e3) / (core["frames_per_step"] * FRAME_MS / 1e3),
+                "llm_share": core["llm_ms"] / core["total_ms"] if core["total_ms"] else None,
+                "forward_rows_per_step": core["rows"] / max(1, min(args.steps, 3)),
+                "gpu_launches": core["launches"],
+                "roofline": {"bound": "tensor", "achieved": core["achieved_tf"],
+                             "peak": core["peak_tf"], "unit": "TFLOP/s",
+                             "frac": core["achieved_tf"] / core["peak_tf"],
+                             "peak_source": core["peak_source"]},
+                "clocks": core["clocks"],
+            }
+            if prec == "bf16x2" and rank == 0:
+                llm[prec]["parity_check"] = llm_replay_check(world, cfg3, raws, core)
+            del core
+            torch.cuda.empty_cache()
+
     if rank == 0:
-        clocks = clk.summary()
         line = {
             "metric": "decoded frames/s (BASELINE config 2, beam 64, 1 x B200 per rank)",
             "value": value,
@@ -368,6 +394,7 @@ def run_ours(args):
             "parity_check": check,
             "phase_cycles_per_frame": phases,
             "layout": batch.layout(),
+            "llm_fusion": llm,
         }
         print(json.dumps(line))
     if world_n > 1:
@@ -390,26 +417,16 @@ def llm_workload(args, world, cfg):
     }
 
 
-def run_llm(args):
+def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1):
+    """Device-timed BASELINE-config-3 steps: K1 + frames + every fusion event (LLM on the
+    device) + closure + final fusion for the whole batch, L2 flushed between steps."""
     import torch
 
-    world_n, rank, local = dist_env()
-    if world_n > 1:
-        torch.cuda.set_device(local)
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
-    torch.cuda.set_device(dev)
-    from paper_2603_14002_b200 import LlamaScorer, ReplayScorer, decode_batch_raw
+    from paper_2603_14002_b200 import LlamaScorer
     from paper_2603_14002_b200.decoder import device_model, run_search
 
-    t_setup = time.perf_counter()
-    world, cfg, raws = make_inputs(args, rank)
-    cfg = cfg.replace(llm_rescore_interval=args.interval)
-    scorer = LlamaScorer(args.llm, seed=0, device=dev, precision=args.precision)
+    scorer = LlamaScorer(llm, seed=0, device=dev, precision=precision)
     dm = device_model(world.table, world.model, dev)
-    setup_s = time.perf_counter() - t_setup
     B, T = raws.shape[0], raws.shape[1]
     frames = np.full(B, T, dtype=np.int32)
     x_dev = torch.from_numpy(raws).to(f"cuda:{dev}")
@@ -420,7 +437,7 @@ def run_llm(args):
         batch.load_logits(None, frames, on_device_ptr=x_dev.data_ptr())
         run_search(batch, cfg, scorer, world.model, final_llm_only=False)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         flush.zero_()
         step()
     sess = batch._llm_session
@@ -430,7 +447,7 @@ def run_llm(args):
     torch.cuda.synchronize()
     ms_steps, llm_ms, launches, rows, slots, events, waves = [], 0.0, 0, 0, 0, 0, 0
     with ClockSampler(dev) as clk:
-        for _ in range(args.steps):
+        for _ in range(steps):
             flush.zero_()
             batch.mark_begin()
             step()
@@ -444,14 +461,14 @@ def run_llm(args):
             events += st["events"]
             waves += st["waves"]
         torch.cuda.synchronize()
+    sess.enable_timing(False)
     total_ms = float(sum(ms_steps))
     if world_n > 1:
         t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
+    ms_per_step = total_ms / steps
     frames_per_step = float(frames.sum()) * world_n
-    value = frames_per_step / (ms_per_step / 1e3)
     flops = rows * scorer.cfg.flops_per_token() * (2 if scorer.split else 1)
     achieved_tf = flops / (llm_ms / 1e3) / 1e12 if llm_ms > 0 else 0.0
     peaks = {}
@@ -459,21 +476,61 @@ def run_llm(args):
     if pp.exists():
         peaks = json.loads(pp.read_text())
     peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+    return {
+        "scorer": scorer, "batch": batch, "sess": sess, "frames": frames,
+        "value": frames_per_step / (ms_per_step / 1e3), "ms_per_step": ms_per_step,
+        "total_ms": total_ms, "launches": launches, "llm_ms": llm_ms,
+        "rows": rows, "slots": slots, "events": events, "waves": waves, "clocks": clk.summary(),
+        "achieved_tf": achieved_tf, "peak_tf": peak_tf,
+        "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if pp.exists() else "fallback 1400 TFLOP/s",
+        "frames_per_step": frames_per_step,
+    }
 
-    check = None
-    if rank == 0:
-        from oracle import lightbeam_oracle as O
 
-        replay = ReplayScorer(sess.replay_table())
-        got = batch.results()
-        ok = 0
-        for i in range(2):
-            want = O.decode(O.log_softmax_scaled(raws[i], cfg.acoustic_scale), cfg, world.table,
-                            world.model, replay)
-            g = got[i]
-            ok += int(g is not None and g[0] == want.text and g[1] == want.score)
-        check = (f"{ok}/2 utterances bit-exact vs the oracle decoder replaying this run's device "
-                 "LLM scores")
+def llm_replay_check(world, cfg, raws, core, n=2):
+    """Bit-exact check of this run: the oracle decoder replaying the device LLM's scores."""
+    from oracle import lightbeam_oracle as O
+    from paper_2603_14002_b200 import ReplayScorer
+
+    replay = ReplayScorer(core["sess"].replay_table())
+    got = core["batch"].results()
+    ok = 0
+    for i in range(n):
+        want = O.decode(O.log_softmax_scaled(raws[i], cfg.acoustic_scale), cfg, world.table,
+                        world.model, replay)
+        g = got[i]
+        ok += int(g is not None and g[0] == want.text and g[1] == want.score)
+    return f"{ok}/{n} utterances bit-exact vs the oracle decoder replaying this run's device LLM scores"
+
+
+def run_llm(args):
+    import torch
+
+    world_n, rank, local = dist_env()
+    if world_n > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    torch.cuda.set_device(dev)
+    from paper_2603_14002_b200 import decode_batch_raw
+
+    t_setup = time.perf_counter()
+    world, cfg, raws = make_inputs(args, rank)
+    cfg = cfg.replace(llm_rescore_interval=args.interval)
+    setup_s = time.perf_counter() - t_setup
+    core = llm_core(dev, world, cfg, raws, args.llm, args.precision, args.steps, args.warmup, world_n)
+    scorer, batch, frames = core["scorer"], core["batch"], core["frames"]
+    B, T = raws.shape[0], raws.shape[1]
+    ms_per_step, total_ms, llm_ms = core["ms_per_step"], core["total_ms"], core["llm_ms"]
+    frames_per_step = core["frames_per_step"]
+    value = core["value"]
+    launches, rows, slots, events, waves = (core[k] for k in ("launches", "rows", "slots", "events", "waves"))
+    achieved_tf, peak_tf = core["achieved_tf"], core["peak_tf"]
+    pp = ROOT / "MEASURED_PEAKS.json"
+
+    check = llm_replay_check(world, cfg, raws, core) if rank == 0 else None
 
     e2e = None
     if not args.no_e2e:
@@ -531,7 +588,7 @@ def run_llm(args):
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"
                          if pp.exists() else "fallback 1400 TFLOP/s"},
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": core["clocks"],
             "setup_s": setup_s,
             "parity_check": check,
         }

@@ -657,6 +657,180 @@ __global__ void __launch_bounds__(256, 2) chain_attn_kernel(LlmDev l, int layer,
   }
 }
 
+// ---------------------------------------------------------------- tensor-core chain attention
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t* r, const void* smem_row) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_row);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(sa));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+constexpr int MMA_CH = 16;  // chain positions per stage (one PV k-step)
+
+// bf16 precision: one CTA per row, one warp per kv head, the G query heads of the group packed
+// into the M dimension of m16n8k16 MMAs (rows >= G are zero): S = Q K^T over 8-position tiles,
+// online softmax on the accumulator fragments (quad shuffles), then O += P V with P taken
+// straight from the S fragments (the C->A register identity) and V read transposed by ldmatrix.
+// K/V cache rows (all kv heads of a slot) are gathered per 16-position chunk by 1-D TMA bulk
+// copies into a double-buffered stage whose row pitch is padded by 16 B (conflict-free fragment
+// loads).
+template <int HD>
+__global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer, const bf16* q,
+                                                             const int32_t* chains,
+                                                             const int32_t* pos, float scale,
+                                                             bf16* out) {
+  constexpr int KK = HD / 16;  // k-steps of Q K^T
+  constexpr int NT = HD / 8;   // n-tiles of P V
+  extern __shared__ __align__(128) unsigned char attn_smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(attn_smem);
+  unsigned char* stages = attn_smem + 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, qd = lane & 3;
+  const int row = blockIdx.x;
+  const int NKV = l.NKV, kvh = warp, G = l.NH / NKV;
+  const int rowb = NKV * HD * 2;
+  const int pitch = rowb + 16;
+  const int stage_bytes = 2 * MMA_CH * pitch;
+  const int n = pos[row] + 1;
+  const int nch = (n + MMA_CH - 1) / MMA_CH;
+  const int32_t* ch = chains + (size_t)row * (l.max_depth + 1);
+  const unsigned char* kbase = reinterpret_cast<const unsigned char*>(l.kc) + (size_t)layer * l.cap * rowb;
+  const unsigned char* vbase = reinterpret_cast<const unsigned char*>(l.vc) + (size_t)layer * l.cap * rowb;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int c) {  // warp 0
+    const int st = c & 1, c0 = c * MMA_CH, cn = min(MMA_CH, n - c0);
+    unsigned char* kd = stages + (size_t)st * stage_bytes;
+    unsigned char* vd = kd + (size_t)MMA_CH * pitch;
+    if (lane == 0) mbar_expect_tx(&bars[st], (unsigned)(2 * cn * rowb));
+    __syncwarp();
+    if (lane < cn) {
+      const size_t sl = (size_t)ch[c0 + lane];
+      tma_bulk_g2s(kd + (size_t)lane * pitch, kbase + sl * rowb, rowb, &bars[st]);
+      tma_bulk_g2s(vd + (size_t)lane * pitch, vbase + sl * rowb, rowb, &bars[st]);
+    }
+  };
+  if (warp == 0) issue(0);
+  // Q fragments (A operand): row = head grp (< G), cols = dims; rows >= G and grp + 8 are zero
+  uint32_t qa[KK][4];
+  {
+    const bf16* qr = q + (size_t)row * l.NH * HD + (size_t)(kvh * G + grp) * HD;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {
+      qa[kk][0] = grp < G ? *reinterpret_cast<const uint32_t*>(qr + kk * 16 + qd * 2) : 0u;
+      qa[kk][2] = grp < G ? *reinterpret_cast<const uint32_t*>(qr + kk * 16 + 8 + qd * 2) : 0u;
+      qa[kk][1] = 0u;
+      qa[kk][3] = 0u;
+    }
+  }
+  float o[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  float m = -INFINITY, den = 0.f;  // per head row grp (identical across the quad)
+  const int hoff = kvh * HD * 2;
+  for (int c = 0; c < nch; ++c) {
+    if (warp == 0 && c + 1 < nch) issue(c + 1);
+    const int cn = min(MMA_CH, n - c * MMA_CH);
+    unsigned char* ks = stages + (size_t)(c & 1) * stage_bytes;
+    unsigned char* vs = ks + (size_t)MMA_CH * pitch;
+    if (cn < MMA_CH) {  // zero this warp's slice of the unused V rows (0 * stale NaN = NaN)
+      constexpr int U = HD / 4;  // uint2 per head slice
+      for (int i = lane; i < (MMA_CH - cn) * U; i += 32)
+        reinterpret_cast<uint2*>(vs + (size_t)(cn + i / U) * pitch + hoff)[i % U] = make_uint2(0u, 0u);
+    }
+    mbar_wait(&bars[c & 1], (unsigned)((c >> 1) & 1));
+    __syncwarp();
+    float sc[2][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+      const unsigned char* kr = ks + (size_t)(t * 8 + grp) * pitch + hoff;
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk) {
+        uint32_t kb2[2];
+        kb2[0] = *reinterpret_cast<const uint32_t*>(kr + (kk * 16 + qd * 2) * 2);
+        kb2[1] = *reinterpret_cast<const uint32_t*>(kr + (kk * 16 + 8 + qd * 2) * 2);
+        mma_bf16_16816(sc[t], qa[kk], kb2);
+      }
+    }
+    // online softmax over this chunk's positions (t * 8 + qd * 2 + {0, 1})
+    float mx = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = t * 8 + qd * 2 + e;
+        sc[t][e] = j < cn ? sc[t][e] * scale : -INFINITY;
+        mx = fmaxf(mx, sc[t][e]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(FULLMASK, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(FULLMASK, mx, 2));
+    const float mnew = fmaxf(m, mx);
+    const float corr = __expf(m - mnew);
+    float ps = 0.f;
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sc[t][e] = __expf(sc[t][e] - mnew);
+        ps += sc[t][e];
+      }
+    ps += __shfl_xor_sync(FULLMASK, ps, 1);
+    ps += __shfl_xor_sync(FULLMASK, ps, 2);
+    den = den * corr + ps;
+    m = mnew;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      o[t][0] *= corr;
+      o[t][1] *= corr;
+    }
+    // P (A operand, 16 heads x 16 positions) from the S fragments
+    uint32_t pa[4];
+    pa[0] = pack_bf16(sc[0][0], sc[0][1]);
+    pa[1] = 0u;
+    pa[2] = pack_bf16(sc[1][0], sc[1][1]);
+    pa[3] = 0u;
+    // V (B operand, 16 positions x 8 dims) by ldmatrix.trans: matrices = (pos 0-7 | 8-15) x
+    // (dims nt*8 .. +8 | (nt+1)*8 .. +8)
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < NT; t += 2) {
+      const int mi = lane >> 3, r = lane & 7;
+      const unsigned char* addr = vs + (size_t)((mi & 1) * 8 + r) * pitch + hoff + ((t + (mi >> 1)) * 8) * 2;
+      uint32_t vb4[4];
+      ldsm_x4_trans(vb4, addr);
+      const uint32_t b0[2] = {vb4[0], vb4[1]};
+      const uint32_t b1[2] = {vb4[2], vb4[3]};
+      mma_bf16_16816(o[t], pa, b0);
+      mma_bf16_16816(o[t + 1], pa, b1);
+    }
+    __syncthreads();  // every warp is done with this stage before it is refilled
+  }
+  if (grp < G) {
+    const float inv = 1.f / den;
+    bf16* orow = out + (size_t)row * l.NH * HD + (size_t)(kvh * G + grp) * HD;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      *reinterpret_cast<__nv_bfloat162*>(orow + t * 8 + qd * 2) =
+          __floats2bfloat162_rn(o[t][0] * inv, o[t][1] * inv);
+  }
+}
+
 // gu[M][2F] = [gate | up] (bf16, or fp32 in split precision) -> out[M][F] = bf16(silu(gate) * up)
 // (split: hi|lo pairs [M][2F]); 8 columns per thread
 template <typename TI>
@@ -1170,6 +1344,19 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
     if (x.split) ATT_T(HDV, GV, DV, float);   \
     else ATT_T(HDV, GV, DV, bf16);            \
   } while (0)
+  if (!x.split && G <= 16) {  // tensor-core path (bf16 operands)
+    const int smem = 128 + 2 * 2 * MMA_CH * (x.NKV * x.HD * 2 + 16);
+    if (x.HD == 64) {
+      CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      LAUNCH(chain_attn_mma_kernel<64><<<M, 32 * x.NKV, smem, st>>>(
+          x, layer, reinterpret_cast<const bf16*>(q), chains, pos, scale, oo));
+    } else {
+      CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      LAUNCH(chain_attn_mma_kernel<128><<<M, 32 * x.NKV, smem, st>>>(
+          x, layer, reinterpret_cast<const bf16*>(q), chains, pos, scale, oo));
+    }
+    return LB_OK;
+  }
   if (x.HD == 64) {
     if (G == 1) ATT(64, 1, 16); else if (G == 2) ATT(64, 2, 16); else if (G == 4) ATT(64, 4, 8); else ATT(64, 8, 8);
   } else {

@@ -59,6 +59,8 @@ class DecodeResult:
 class DeviceModel:
     """Device images of one (TransitionTable, NGramModel) pair, resident on one GPU."""
 
+    MAX_CACHED_BATCHES = 2
+
     def __init__(self, tt, model, device: int = 0):
         lib = N.lib()
         ng = images.compile_ngram(model)
@@ -93,12 +95,15 @@ class DeviceModel:
             "acoustic_scale", "beam_prune_threshold", "homophone_prune_threshold",
             "token_insertion_bonus", "word_boundary_bonus", "ngram_weight", "llm_weight",
             "beam_size", "ortho_beams", "llm_rescore_interval", "llm_chunk_size"))
-        got = self._batches.get(key)
+        got = self._batches.pop(key, None)
         if got is None or got.max_trials < n_trials or got.max_frames < n_frames:
             if got is not None:
                 got.destroy()
+            while len(self._batches) >= self.MAX_CACHED_BATCHES:  # evict the least recently used
+                old = self._batches.pop(next(iter(self._batches)))
+                old.destroy()
             got = DeviceBatch(self, cfg, max(n_trials, 1), max(n_frames, 1))
-            self._batches[key] = got
+        self._batches[key] = got  # most recently used last
         return got
 
     def score_words(self, hist: list, words: list):
@@ -169,6 +174,10 @@ class DeviceBatch:
         return {"smem_bytes": sm.value, "gscratch_bytes": gs.value, "threads": nt.value}
 
     def destroy(self):
+        sess = getattr(self, "_llm_session", None)
+        if sess is not None:
+            sess.destroy()
+            self._llm_session = None
         if getattr(self, "h", None):
             N.lib(False).lb_batch_destroy(self.h)
             self.h = None

@@ -235,7 +235,7 @@ class LlamaScorer:
     PRECISIONS = ("bf16x2", "bf16")
 
     def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
-                 max_depth: int = 255, row_chunk: int = 16384, lm_chunk: int = 256,
+                 max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 256,
                  precision: str = "bf16x2"):
         """precision: "bf16x2" (default) feeds every body GEMM the activation as a hi+lo pair of
         bf16 values against duplicated bf16 weights -- fp32-equivalent activations on the bf16
@@ -434,13 +434,18 @@ class DeviceLlmSession:
         cfg, W = scorer.cfg, scorer.weights
         low, cap = _surface_tokens(batch.dm, scorer.tokenizer)
         self._low, self._cap = low, cap
-        per_slot = cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * 2 + cfg.hidden * 2 + 96
+        esz = 4 if scorer.split else 2
+        per_slot = cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * esz + cfg.hidden * 4 + 96
         if scorer.max_slots:
             max_slots = int(scorer.max_slots)
         else:
+            # measured on the synthetic B2T worlds: slots per utterance ~ T k (1 + 20/r) / 96
+            # (T=500: 743 at k=64 r=20, 3725 at k=256 r=10); sized 2x that, capped by memory
+            c = batch.cfg
+            per_trial = batch.max_frames * c.beam_size * (1 + 20 / c.llm_rescore_interval) / 48
+            want = max(1 << 16, int(batch.max_trials * per_trial))
             free, _ = torch.cuda.mem_get_info(scorer.device)
-            want = max(1 << 16, batch.max_trials * 4096)
-            max_slots = int(min(want, 0.5 * free / per_slot, 1 << 26))
+            max_slots = int(min(want, 0.4 * free / per_slot, 1 << 26))
         self.max_slots = max_slots
         self.pitch = scorer.max_depth + 1
         d = N.LbLlmDesc()
