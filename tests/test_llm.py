@@ -272,3 +272,48 @@ def test_llm_device_kernels_peaky_model_vs_oracle(precision):
     assert max(e_dev) <= 2.0 * max(e_dense) + 1e-4
     if precision == "bf16x2":  # fp32-equivalent activations: the north-star 1e-2 per text holds
         assert max(abs(a - b) for a, b in zip(devs, want)) <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["bf16", "bf16x2"])
+def test_llm_head_dim_128_gqa4_vs_oracle(precision):
+    """The 8B-class kernel shapes (head_dim 128, GQA group 4) on a small model: device scores
+    vs the fp32 oracle (bf16x2: 1e-2; bf16: no worse than plain torch) and replay parity."""
+    import dataclasses
+
+    from paper_2603_14002_b200 import LlamaScorer, ReplayScorer
+
+    cfg_llm = dataclasses.replace(PRESETS["tiny"], name="tiny-hd128", hidden=256, heads=8,
+                                  kv_heads=2, head_dim=128, ffn=512, init_std=0.1)
+    sc = LlamaScorer(cfg_llm, seed=9, precision=precision)
+    w, cfg = _world_cfg()
+    raws = synth.make_logits(3, 120, 41, base_seed=23)
+    ds, got, sess = _decode_with_session(sc, raws, cfg, w)
+    replay = ReplayScorer(sess.replay_table())
+    for i, d in enumerate(ds):
+        want = O.decode(d, cfg, w.table, w.model, replay)
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest)
+    ex = sess.export()
+    first = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._cap)}
+    mid = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._low)}
+    oracle = LO.OracleLlmScorer(sc.cfg, sc.weights.hf_state_dict())
+    texts, devs = [], []
+    for s in range(1, len(ex["parent"])):
+        if ex["parent"][s] < 0 or not ex["state"][s] & 2:
+            continue
+        words, cur = [], s
+        while cur != 0:
+            words.append(int(ex["token"][cur]))
+            cur = int(ex["parent"][cur])
+        words.reverse()
+        texts.append(" ".join([first[words[0]]] + [mid[t] for t in words[1:]]))
+        devs.append(ex["cum"][s])
+    texts, devs = texts[:150], devs[:150]
+    want = [oracle.score(t) for t in texts]
+    dense = sc.score_texts_dense(texts)
+    e_dev = max(abs(a - b) for a, b in zip(devs, want))
+    e_dense = max(abs(a - b) for a, b in zip(dense, want))
+    if precision == "bf16x2":
+        assert e_dev <= TOL, e_dev
+    else:
+        assert e_dev <= 2.0 * e_dense + 1e-4, (e_dev, e_dense)
