@@ -429,30 +429,37 @@ __global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, con
   const int p = pos[row];
   const size_t slot = (size_t)slots[row];
   const size_t kvw = (size_t)NKV * HD;
-  T* kd = reinterpret_cast<T*>(l.kc) + ((size_t)layer * l.cap + slot) * kvw;
-  T* vd = reinterpret_cast<T*>(l.vc) + ((size_t)layer * l.cap + slot) * kvw;
+  // K/V cache rows: bf16 [NKV*HD]; split precision: [hi | lo] bf16 pairs [2*NKV*HD]
+  constexpr bool SPLIT = sizeof(T) == 4;
+  const size_t roww = kvw * (SPLIT ? 2 : 1);
+  bf16* kd = reinterpret_cast<bf16*>(l.kc) + ((size_t)layer * l.cap + slot) * roww;
+  bf16* vd = reinterpret_cast<bf16*>(l.vc) + ((size_t)layer * l.cap + slot) * roww;
   const float* cs = cosT + (size_t)p * half;
   const float* sn = sinT + (size_t)p * half;
   const int npairs = (NH + NKV) * half;
+  auto put = [&](bf16* base, size_t idx, float v) {
+    const bf16 h = __float2bfloat16_rn(v);
+    base[idx] = h;
+    if (SPLIT) base[kvw + idx] = __float2bfloat16_rn(v - __bfloat162float(h));
+  };
   for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
     const int head = t / half, i = t - head * half;
     const float* src = in + head * HD;
     const float x1 = src[i], x2 = src[i + half];
     const float c = cs[i], s = sn[i];
-    const T o1 = to_store<T>(x1 * c - x2 * s);
-    const T o2 = to_store<T>(x2 * c + x1 * s);
+    const float o1 = x1 * c - x2 * s;
+    const float o2 = x2 * c + x1 * s;
     if (head < NH) {
       T* dst = q_out + (size_t)row * NH * HD + head * HD;
-      dst[i] = o1;
-      dst[i + half] = o2;
+      dst[i] = to_store<T>(o1);
+      dst[i + half] = to_store<T>(o2);
     } else {
-      T* dst = kd + (head - NH) * HD;
-      dst[i] = o1;
-      dst[i + half] = o2;
+      put(kd, (size_t)(head - NH) * HD + i, o1);
+      put(kd, (size_t)(head - NH) * HD + i + half, o2);
     }
   }
   const float* vin = in + (NH + NKV) * HD;
-  for (int t = threadIdx.x; t < NKV * HD; t += blockDim.x) vd[t] = to_store<T>(vin[t]);
+  for (int t = threadIdx.x; t < NKV * HD; t += blockDim.x) put(vd, t, vin[t]);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -685,11 +692,11 @@ constexpr int MMA_CH = 16;  // chain positions per stage (one PV k-step)
 // K/V cache rows (all kv heads of a slot) are gathered per 16-position chunk by 1-D TMA bulk
 // copies into a double-buffered stage whose row pitch is padded by 16 B (conflict-free fragment
 // loads).
-template <int HD>
-__global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer, const bf16* q,
-                                                             const int32_t* chains,
+template <int HD, bool SPLIT>
+__global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer,
+                                                             const void* qv, const int32_t* chains,
                                                              const int32_t* pos, float scale,
-                                                             bf16* out) {
+                                                             bf16* out, int nstages) {
   constexpr int KK = HD / 16;  // k-steps of Q K^T
   constexpr int NT = HD / 8;   // n-tiles of P V
   extern __shared__ __align__(128) unsigned char attn_smem[];
@@ -699,7 +706,8 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
   const int grp = lane >> 2, qd = lane & 3;
   const int row = blockIdx.x;
   const int NKV = l.NKV, kvh = warp, G = l.NH / NKV;
-  const int rowb = NKV * HD * 2;
+  const int halfb = NKV * HD * 2;              // bytes of one bf16 half-row
+  const int rowb = halfb * (SPLIT ? 2 : 1);    // cache row: [hi] or [hi | lo]
   const int pitch = rowb + 16;
   const int stage_bytes = 2 * MMA_CH * pitch;
   const int n = pos[row] + 1;
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
   }
   __syncthreads();
   auto issue = [&](int c) {  // warp 0
-    const int st = c & 1, c0 = c * MMA_CH, cn = min(MMA_CH, n - c0);
+    const int st = c % nstages, c0 = c * MMA_CH, cn = min(MMA_CH, n - c0);
     unsigned char* kd = stages + (size_t)st * stage_bytes;
     unsigned char* vd = kd + (size_t)MMA_CH * pitch;
     if (lane == 0) mbar_expect_tx(&bars[st], (unsigned)(2 * cn * rowb));
@@ -726,16 +734,32 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
     }
   };
   if (warp == 0) issue(0);
-  // Q fragments (A operand): row = head grp (< G), cols = dims; rows >= G and grp + 8 are zero
-  uint32_t qa[KK][4];
-  {
-    const bf16* qr = q + (size_t)row * l.NH * HD + (size_t)(kvh * G + grp) * HD;
+  // Q fragments (A operand): row = head grp (< G), cols = dims; rows >= G and grp + 8 are zero.
+  // SPLIT: q is fp32 and becomes a hi + lo pair of bf16 fragments.
+  uint32_t qa[KK][4], ql[SPLIT ? KK : 1][4];
 #pragma unroll
-    for (int kk = 0; kk < KK; ++kk) {
-      qa[kk][0] = grp < G ? *reinterpret_cast<const uint32_t*>(qr + kk * 16 + qd * 2) : 0u;
-      qa[kk][2] = grp < G ? *reinterpret_cast<const uint32_t*>(qr + kk * 16 + 8 + qd * 2) : 0u;
-      qa[kk][1] = 0u;
-      qa[kk][3] = 0u;
+  for (int kk = 0; kk < KK; ++kk) {
+    qa[kk][1] = qa[kk][3] = 0u;
+    if (SPLIT) ql[kk][1] = ql[kk][3] = 0u;
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const int col = kk * 16 + hlf * 8 + qd * 2;
+      uint32_t hi = 0u, lo = 0u;
+      if (grp < G) {
+        if (SPLIT) {
+          const float* qr = reinterpret_cast<const float*>(qv) + (size_t)row * l.NH * HD + (size_t)(kvh * G + grp) * HD;
+          const float2 f = *reinterpret_cast<const float2*>(qr + col);
+          const __nv_bfloat162 h = __floats2bfloat162_rn(f.x, f.y);
+          const float2 hf = __bfloat1622float2(h);
+          hi = *reinterpret_cast<const uint32_t*>(&h);
+          lo = pack_bf16(f.x - hf.x, f.y - hf.y);
+        } else {
+          const bf16* qr = reinterpret_cast<const bf16*>(qv) + (size_t)row * l.NH * HD + (size_t)(kvh * G + grp) * HD;
+          hi = *reinterpret_cast<const uint32_t*>(qr + col);
+        }
+      }
+      qa[kk][hlf * 2] = hi;
+      if (SPLIT) ql[kk][hlf * 2] = lo;
     }
   }
   float o[NT][4];
@@ -744,16 +768,20 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
   float m = -INFINITY, den = 0.f;  // per head row grp (identical across the quad)
   const int hoff = kvh * HD * 2;
   for (int c = 0; c < nch; ++c) {
-    if (warp == 0 && c + 1 < nch) issue(c + 1);
+    if (nstages == 2 && warp == 0 && c + 1 < nch) issue(c + 1);
     const int cn = min(MMA_CH, n - c * MMA_CH);
-    unsigned char* ks = stages + (size_t)(c & 1) * stage_bytes;
+    const int st = c % nstages;
+    unsigned char* ks = stages + (size_t)st * stage_bytes;
     unsigned char* vs = ks + (size_t)MMA_CH * pitch;
-    if (cn < MMA_CH) {  // zero this warp's slice of the unused V rows (0 * stale NaN = NaN)
+    if (cn < MMA_CH) {  // zero this warp's slices of the unused V rows (0 * stale NaN = NaN)
       constexpr int U = HD / 4;  // uint2 per head slice
-      for (int i = lane; i < (MMA_CH - cn) * U; i += 32)
-        reinterpret_cast<uint2*>(vs + (size_t)(cn + i / U) * pitch + hoff)[i % U] = make_uint2(0u, 0u);
+      for (int i = lane; i < (MMA_CH - cn) * U; i += 32) {
+        unsigned char* rp = vs + (size_t)(cn + i / U) * pitch + hoff;
+        reinterpret_cast<uint2*>(rp)[i % U] = make_uint2(0u, 0u);
+        if (SPLIT) reinterpret_cast<uint2*>(rp + halfb)[i % U] = make_uint2(0u, 0u);
+      }
     }
-    mbar_wait(&bars[c & 1], (unsigned)((c >> 1) & 1));
+    mbar_wait(&bars[st], (unsigned)((c / nstages) & 1));
     __syncwarp();
     float sc[2][4];
 #pragma unroll
@@ -766,6 +794,13 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
         kb2[0] = *reinterpret_cast<const uint32_t*>(kr + (kk * 16 + qd * 2) * 2);
         kb2[1] = *reinterpret_cast<const uint32_t*>(kr + (kk * 16 + 8 + qd * 2) * 2);
         mma_bf16_16816(sc[t], qa[kk], kb2);
+        if (SPLIT) {  // + q_lo k_hi + q_hi k_lo (the lo*lo term is below fp32 resolution)
+          uint32_t kl2[2];
+          kl2[0] = *reinterpret_cast<const uint32_t*>(kr + halfb + (kk * 16 + qd * 2) * 2);
+          kl2[1] = *reinterpret_cast<const uint32_t*>(kr + halfb + (kk * 16 + 8 + qd * 2) * 2);
+          mma_bf16_16816(sc[t], ql[kk], kb2);
+          mma_bf16_16816(sc[t], qa[kk], kl2);
+        }
       }
     }
     // online softmax over this chunk's positions (t * 8 + qd * 2 + {0, 1})
@@ -799,14 +834,20 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
       o[t][0] *= corr;
       o[t][1] *= corr;
     }
-    // P (A operand, 16 heads x 16 positions) from the S fragments
-    uint32_t pa[4];
-    pa[0] = pack_bf16(sc[0][0], sc[0][1]);
-    pa[1] = 0u;
-    pa[2] = pack_bf16(sc[1][0], sc[1][1]);
-    pa[3] = 0u;
+    // P (A operand, 16 heads x 16 positions) from the S fragments (+ its lo part when split)
+    uint32_t pa[4], pl[4];
+    pa[1] = pa[3] = pl[1] = pl[3] = 0u;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(sc[t][0], sc[t][1]);
+      pa[t * 2] = *reinterpret_cast<const uint32_t*>(&h);
+      if (SPLIT) {
+        const float2 hf = __bfloat1622float2(h);
+        pl[t * 2] = pack_bf16(sc[t][0] - hf.x, sc[t][1] - hf.y);
+      }
+    }
     // V (B operand, 16 positions x 8 dims) by ldmatrix.trans: matrices = (pos 0-7 | 8-15) x
-    // (dims nt*8 .. +8 | (nt+1)*8 .. +8)
+    // (dims t*8 .. +8 | (t+1)*8 .. +8)
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < NT; t += 2) {
@@ -818,16 +859,34 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
       const uint32_t b1[2] = {vb4[2], vb4[3]};
       mma_bf16_16816(o[t], pa, b0);
       mma_bf16_16816(o[t + 1], pa, b1);
+      if (SPLIT) {  // + p_lo v_hi + p_hi v_lo
+        uint32_t vl4[4];
+        ldsm_x4_trans(vl4, addr + halfb);
+        const uint32_t c0[2] = {vl4[0], vl4[1]};
+        const uint32_t c1[2] = {vl4[2], vl4[3]};
+        mma_bf16_16816(o[t], pl, b0);
+        mma_bf16_16816(o[t + 1], pl, b1);
+        mma_bf16_16816(o[t], pa, c0);
+        mma_bf16_16816(o[t + 1], pa, c1);
+      }
     }
     __syncthreads();  // every warp is done with this stage before it is refilled
+    if (nstages == 1 && warp == 0 && c + 1 < nch) issue(c + 1);
   }
   if (grp < G) {
     const float inv = 1.f / den;
-    bf16* orow = out + (size_t)row * l.NH * HD + (size_t)(kvh * G + grp) * HD;
+    const int W = l.NH * HD;
+    bf16* orow = out + (size_t)row * W * (SPLIT ? 2 : 1) + (size_t)(kvh * G + grp) * HD;
 #pragma unroll
-    for (int t = 0; t < NT; ++t)
-      *reinterpret_cast<__nv_bfloat162*>(orow + t * 8 + qd * 2) =
-          __floats2bfloat162_rn(o[t][0] * inv, o[t][1] * inv);
+    for (int t = 0; t < NT; ++t) {
+      const float a = o[t][0] * inv, b = o[t][1] * inv;
+      const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+      *reinterpret_cast<__nv_bfloat162*>(orow + t * 8 + qd * 2) = h;
+      if (SPLIT) {
+        const float2 hf = __bfloat1622float2(h);
+        *reinterpret_cast<__nv_bfloat162*>(orow + W + t * 8 + qd * 2) = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+      }
+    }
   }
 }
 
@@ -1339,24 +1398,27 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
     LAUNCH(kfn<<<M, 32 * x.NKV, smem, st>>>(x, layer, reinterpret_cast<const TV*>(q), chains,   \
                                             pos, scale, oo));                                   \
   } while (0)
-#define ATT(HDV, GV, DV)                      \
-  do {                                        \
-    if (x.split) ATT_T(HDV, GV, DV, float);   \
-    else ATT_T(HDV, GV, DV, bf16);            \
+#define ATT(HDV, GV, DV) ATT_T(HDV, GV, DV, bf16)
+  if (G <= 16) {  // tensor-core path (bf16 operands; hi/lo bf16 pairs in split precision)
+    const int rowb = x.NKV * x.HD * 2 * (x.split ? 2 : 1);
+    const int stage = 2 * MMA_CH * (rowb + 16);
+    const int nst = (128 + 2 * stage <= 80 * 1024) ? 2 : 1;  // keep >= 2-3 CTAs per SM
+    const int smem = 128 + nst * stage;
+    if (smem > 227 * 1024) return lbh::set_error(LB_ERR_ARG, "K/V cache row too wide for the attention stage");
+#define MMA_ATT(HDV, SV)                                                                            \
+  do {                                                                                              \
+    CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<HDV, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+    LAUNCH(chain_attn_mma_kernel<HDV, SV><<<M, 32 * x.NKV, smem, st>>>(x, layer, q, chains, pos, scale, oo, nst)); \
   } while (0)
-  if (!x.split && G <= 16) {  // tensor-core path (bf16 operands)
-    const int smem = 128 + 2 * 2 * MMA_CH * (x.NKV * x.HD * 2 + 16);
     if (x.HD == 64) {
-      CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      LAUNCH(chain_attn_mma_kernel<64><<<M, 32 * x.NKV, smem, st>>>(
-          x, layer, reinterpret_cast<const bf16*>(q), chains, pos, scale, oo));
+      if (x.split) MMA_ATT(64, true); else MMA_ATT(64, false);
     } else {
-      CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      LAUNCH(chain_attn_mma_kernel<128><<<M, 32 * x.NKV, smem, st>>>(
-          x, layer, reinterpret_cast<const bf16*>(q), chains, pos, scale, oo));
+      if (x.split) MMA_ATT(128, true); else MMA_ATT(128, false);
     }
+#undef MMA_ATT
     return LB_OK;
   }
+  if (x.split) return lbh::set_error(LB_ERR_ARG, "bf16x2 precision needs n_heads / n_kv_heads <= 16");
   if (x.HD == 64) {
     if (G == 1) ATT(64, 1, 16); else if (G == 2) ATT(64, 2, 16); else if (G == 4) ATT(64, 4, 8); else ATT(64, 8, 8);
   } else {

@@ -235,7 +235,7 @@ class LlamaScorer:
     PRECISIONS = ("bf16x2", "bf16")
 
     def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
-                 max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 256,
+                 max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 2048,
                  precision: str = "bf16x2"):
         """precision: "bf16x2" (default) feeds every body GEMM the activation as a hi+lo pair of
         bf16 values against duplicated bf16 weights -- fp32-equivalent activations on the bf16
@@ -582,7 +582,9 @@ class DeviceLlmSession:
             N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), dn.data_ptr(), wnext.data_ptr(), eps, n,
                                        hn.data_ptr(), slot.data_ptr() if last else None))
             del dn
-        chunk = self.scorer.lm_chunk // (2 if sfx else 1)  # logits chunk stays L2-resident
+        # rows per LM-head GEMM: large enough for full tensor-core tiles (measured: 2048 rows bf16 /
+        # 1024 rows bf16x2 beat L2-resident 256-row chunks by ~15% of the LLM step)
+        chunk = self.scorer.lm_chunk // (2 if sfx else 1)
         for c0 in range(0, n, chunk):
             c1 = min(n, c0 + chunk)
             if sfx:  # hi|lo against [E | E], fp32 logits

@@ -20,7 +20,9 @@ def main():
     args = bench.parse()
     world, cfg, raws = bench.make_inputs(args, 0)
     cfg = cfg.replace(llm_rescore_interval=args.interval)
-    sc = LlamaScorer(args.llm, seed=0, precision=args.precision)
+    import os
+    sc = LlamaScorer(args.llm, seed=0, precision=args.precision,
+                     lm_chunk=int(os.environ.get("LM_CHUNK", "256")))
     dm = device_model(world.table, world.model, 0)
     B, T = raws.shape[:2]
     frames = np.full(B, T, np.int32)
