@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-wer", action="store_true", help="skip the WER-parity check")
+    ap.add_argument("--wer-trials", type=int, default=64)
     ap.add_argument("--no-llm", action="store_true",
                     help="skip the BASELINE config-3 (LLM fusion) summary in the default line")
     ap.add_argument("--phases", action="store_true", help="add per-phase cycle breakdown of K2")
@@ -339,6 +341,7 @@ def run_ours(args):
         cpu = cpu_baseline(world, cfg, raws[: min(64, B)], args.cpu_seconds)
 
     clocks = clk.summary()
+    wer = wer_check(world, cfg, scorer, dev, args) if rank == 0 and not args.no_wer else None
     llm = None
     if not args.no_llm:  # BASELINE config 3 on the same utterances: + Llama-3.2-1B delayed fusion
         cfg3 = cfg.replace(llm_rescore_interval=args.interval)
@@ -394,6 +397,7 @@ def run_ours(args):
             "parity_check": check,
             "phase_cycles_per_frame": phases,
             "layout": batch.layout(),
+            "wer": wer,
             "llm_fusion": llm,
         }
         print(json.dumps(line))
@@ -645,6 +649,44 @@ def run_reference_llm(args):
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+_WER = {}
+
+
+def _wer_worker(i):
+    from oracle import lightbeam_oracle as O
+    from paper_2603_14002_b200 import StubScorer
+
+    w, cfg, logs = _WER["world"], _WER["cfg"], _WER["logs"]
+    d = O.log_softmax_scaled(logs[i], cfg.acoustic_scale)
+    sc = StubScorer(ngram_model=w.model, scale=cfg.ngram_weight / cfg.llm_weight)
+    return O.decode(d, cfg, w.table, w.model, sc, final_llm_only=True).text
+
+
+def wer_check(world, cfg, scorer, dev, args):
+    """WER parity (BASELINE metric): synthetic ground-truth trials (speech-shaped CTC logits
+    from LM-sampled sentences, ragged lengths), decoded on the GPU and by the CPU reference
+    restatement (fork pool); corpus WER of both and the count of identical transcripts."""
+    import multiprocessing as mp
+
+    from paper_2603_14002_b200 import decode_batch_raw, synth
+    from paper_2603_14002_b200.metrics import corpus_wer
+
+    sents, logs = synth.make_wer_trials(world, args.wer_trials)
+    res = decode_batch_raw(logs, cfg, world.table, world.model, scorer, final_llm_only=True,
+                           device=dev)
+    gpu = [r.text if not isinstance(r, Exception) else "" for r in res]
+    _WER.update(world=world, cfg=cfg, logs=logs)
+    with mp.get_context("fork").Pool(os.cpu_count() or 1) as pool:
+        cpu = pool.map(_wer_worker, range(len(logs)), chunksize=1)
+    same = sum(int(a == b) for a, b in zip(gpu, cpu))
+    return {"trials": len(logs), "frames": int(sum(len(x) for x in logs)),
+            "wer_gpu": corpus_wer(sents, [t.split() for t in gpu]),
+            "wer_cpu_reference": corpus_wer(sents, [t.split() for t in cpu]),
+            "identical_transcripts": f"{same}/{len(logs)}",
+            "data": "LM-sampled sentences -> lexicon phonemes -> CTC frames, N(0,2) + 10 on the "
+                    "true token, b2t25 profile, beam 64, n-gram fusion (config 2 settings)"}
 
 
 def batch_entry_sizes(batch):

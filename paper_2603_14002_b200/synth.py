@@ -178,3 +178,61 @@ def toy_world(n_words: int = 2000, seed: int = 7) -> World:
                            n_words, seed=seed + 1)
     model = parse_arpa_text(arpa_text_from_spec(spec))
     return World(vocab, lex, build_transition_table(lex, vocab), model)
+
+
+def _successors(model: NGramModel) -> dict:
+    """word -> (successor words, weights 10^log10p) from the listed bigrams (cached)."""
+    cache = getattr(model, "_synth_succ", None)
+    if cache is None:
+        tmp: dict = {}
+        for key, lp in model.probs.items():
+            if len(key) == 2:
+                tmp.setdefault(key[0], []).append((key[1], lp))
+        cache = {}
+        for w, lst in tmp.items():
+            words = [x for x, _ in lst]
+            p = np.exp(np.array([lp for _, lp in lst]))
+            cache[w] = (words, p / p.sum())
+        model._synth_succ = cache
+    return cache
+
+
+def make_wer_trials(world: World, n_trials: int, seed: int = 777, sigma: float = 2.0,
+                    mu: float = 10.0, min_words: int = 8, max_words: int = 20):
+    """Ground-truth sentences and CTC-shaped logits for WER measurement:
+    sentence = a walk over the LM's listed bigrams from `<s>` (uniform word when a history
+    has no listed continuation); each word -> its lexicon phonemes, each phoneme held
+    U{1..3} frames with U{0..2} blank frames before it, one `<sp>` frame after each word;
+    logits = N(0, sigma) + mu on the true token (mu = 10 puts the CPU reference's WER in the
+    5-25% band §8d asks for: 15% on the 2k-word world at beam 16).  Returns (list of word
+    lists, list of fp32 (T_i, 41) arrays)."""
+    rng = np.random.default_rng(seed)
+    succ = _successors(world.model)
+    pron = {e.surface: e.phonemes for e in world.lexicon.entries}
+    vocab_words = [e.surface for e in world.lexicon.entries]
+    sentences, logits = [], []
+    for _ in range(n_trials):
+        n_w = int(rng.integers(min_words, max_words + 1))
+        words, prev = [], SPECIAL_BOS
+        while len(words) < n_w:
+            cand = succ.get(prev)
+            if cand is not None and rng.random() < 0.8:
+                w = cand[0][int(rng.choice(len(cand[0]), p=cand[1]))]
+            else:
+                w = vocab_words[int(rng.integers(0, len(vocab_words)))]
+            if w not in pron:
+                continue
+            words.append(w)
+            prev = w
+        labels = []
+        for w in words:
+            for ph in pron[w]:
+                labels.extend([0] * int(rng.integers(0, 3)))
+                labels.extend([ph] * int(rng.integers(1, 4)))
+            labels.append(40)
+        lab = np.asarray(labels, dtype=np.int64)
+        x = rng.normal(scale=sigma, size=(len(lab), 41)).astype(np.float32)
+        x[np.arange(len(lab)), lab] += np.float32(mu)
+        sentences.append(words)
+        logits.append(x)
+    return sentences, logits
