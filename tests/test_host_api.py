@@ -241,3 +241,67 @@ def test_no_cpu_fallback_without_gpu():
     d = np.zeros((3, 41))
     with pytest.raises(DeviceError):
         decode(d, PROFILES["b2t25"].replace(beam_size=4), w.table, w.model, StubScorer(table={}))
+
+
+def _engine_files(tmp_path):
+    import json
+
+    from paper_2603_14002_b200 import save_vocab, synth
+    from paper_2603_14002_b200.synth import arpa_text_from_spec, make_ngram_spec
+
+    w = synth.toy_world(n_words=200, seed=5)
+    vp = tmp_path / "vocab.txt"
+    save_vocab(vp, w.vocab)
+    lp = tmp_path / "lexicon.txt"
+    lp.write_text("".join(f"{e.key}\t{' '.join(w.vocab.tokens[p] for p in e.phonemes)}\n"
+                          for e in w.lexicon.entries))
+    spec = make_ngram_spec([e.surface for e in w.lexicon.entries], 400, 200, 100, seed=6)
+    ap = tmp_path / "lm.arpa"
+    ap.write_text(arpa_text_from_spec(spec))
+    return vp, lp, ap
+
+
+def test_build_engine_argument_rules(tmp_path):
+    from paper_2603_14002_b200 import PROFILES, ConfigError, ScorerSpec, build_engine
+
+    vp, lp, ap = _engine_files(tmp_path)
+    with pytest.raises(ConfigError):
+        build_engine(vp, ap, ScorerSpec("stub_table"), config=PROFILES["b2t25"])
+    with pytest.raises(ConfigError):
+        build_engine(vp, ap, ScorerSpec("stub_table"), lexicon_path=lp)
+    with pytest.raises(ConfigError):
+        ScorerSpec("subprocess").build(None)
+    eng = build_engine(vp, ap, ScorerSpec("stub_ngram", scale=0.5), lexicon_path=lp,
+                       config=PROFILES["b2t25"], config_overrides={"beam_size": 8})
+    assert eng.config.beam_size == 8 and set(eng.components) == {"vocab", "lexicon", "arpa"}
+    assert eng.table.num_states > 1
+
+
+@pytest.mark.gpu
+def test_engine_decode_paths_matches_oracle(tmp_path):
+    import numpy as np
+
+    from oracle import lightbeam_oracle as O
+    from paper_2603_14002_b200 import PROFILES, RawLogits, ScorerSpec, build_engine, save_logits
+
+    vp, lp, ap = _engine_files(tmp_path)
+    eng = build_engine(vp, ap, ScorerSpec("stub_ngram", scale=0.5), lexicon_path=lp,
+                       config=PROFILES["b2t25"].replace(beam_size=16))
+    paths = []
+    for i in range(4):
+        x = np.random.default_rng(i).normal(scale=2.0, size=(60 + 10 * i, 41)).astype(np.float32)
+        p = tmp_path / f"u{i}.lblt"
+        save_logits(p, RawLogits(x, 80.0))
+        paths.append(p)
+    got = eng.decode_paths(paths)
+    for p, g in zip(paths, got):
+        res, sample = g
+        raw = eng.decode_path(p)[0]
+        assert (res.text, res.score, res.nbest) == (raw.text, raw.score, raw.nbest)
+        assert sample.utterance_duration_s == res.frame_count * 80.0 / 1000.0
+    from paper_2603_14002_b200 import load_logits
+
+    d = O.log_softmax_scaled(load_logits(paths[0], eng.vocab).frames, eng.config.acoustic_scale)
+    want = O.decode(d, eng.config, eng.table, eng.ngram_model, eng.scorer)
+    r = eng.decode_matrix(d)
+    assert (r.text, r.score, r.nbest) == (want.text, want.score, want.nbest)
