@@ -68,6 +68,34 @@ def parse():
     return ap.parse_args()
 
 
+def init_dist(local):
+    """One process per GPU over NCCL.  When more ranks than visible GPUs are launched (a
+    single-GPU smoke test of the multi-rank path), ranks share devices over gloo."""
+    import torch
+    import torch.distributed as dist
+
+    ngpu = torch.cuda.device_count()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+    if local_world <= ngpu:  # the same decision on every rank
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return local
+    dist.init_process_group("gloo")
+    dev = local % max(ngpu, 1)
+    torch.cuda.set_device(dev)
+    return dev
+
+
+def max_over_ranks(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+
+    dev = f"cuda:{torch.cuda.current_device()}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -200,12 +228,7 @@ def run_ours(args):
     import torch
 
     world_n, rank, local = dist_env()
-    if world_n > 1:
-        torch.cuda.set_device(local)
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
+    dev = init_dist(local) if world_n > 1 else local
     from paper_2603_14002_b200 import DeviceNgramScorer, decode_batch_raw
     from paper_2603_14002_b200.decoder import device_model, run_search
 
@@ -249,9 +272,7 @@ def run_ours(args):
     stats = batch.stats()
     total_ms = float(sum(ms_steps))
     if world_n > 1:
-        t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
     frames_per_step = float(frames.sum()) * world_n
     value = frames_per_step / (ms_per_step / 1e3)
@@ -326,9 +347,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / n_e2e
         if world_n > 1:
-            t = torch.tensor([e2e_s], device=f"cuda:{dev}", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t.item())
+            e2e_s = max_over_ranks(e2e_s)
         ne, nw = batch_entry_sizes(batch)
         h2d = raws.nbytes + frames.nbytes
         d2h = ne * (4 + 4 + 8 + 8 + 4) + nw * 4 + B * (4 + 4 + 4) + B * cfg.beam_size * 8 + 16 * B
@@ -468,9 +487,7 @@ def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1):
     sess.enable_timing(False)
     total_ms = float(sum(ms_steps))
     if world_n > 1:
-        t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / steps
     frames_per_step = float(frames.sum()) * world_n
     flops = rows * scorer.cfg.flops_per_token() * (2 if scorer.split else 1)
@@ -511,12 +528,7 @@ def run_llm(args):
     import torch
 
     world_n, rank, local = dist_env()
-    if world_n > 1:
-        torch.cuda.set_device(local)
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
+    dev = init_dist(local) if world_n > 1 else local
     torch.cuda.set_device(dev)
     from paper_2603_14002_b200 import decode_batch_raw
 
@@ -553,9 +565,7 @@ def run_llm(args):
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / n_e2e
         if world_n > 1:
-            t = torch.tensor([e2e_s], device=f"cuda:{dev}", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t.item())
+            e2e_s = max_over_ranks(e2e_s)
         e2e = {"value": frames_per_step / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": int(raws.nbytes + frames.nbytes),
                "d2h_bytes_per_step": None,
