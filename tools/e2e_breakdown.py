@@ -12,6 +12,10 @@ from paper_2603_14002_b200 import decoder as D
 w = synth.make_world()
 cfg = PROFILES["b2t25"].replace(beam_size=64)
 raws = synth.make_logits(256, 500, 41, base_seed=1000)
+from paper_2603_14002_b200._native import pinned_empty
+host = pinned_empty(raws.shape, np.float32)
+host[...] = raws
+raws = host
 frames = np.full(256, 500, dtype=np.int32)
 sc = DeviceNgramScorer(w.model, cfg.ngram_weight / cfg.llm_weight)
 dm = D.device_model(w.table, w.model)
@@ -23,5 +27,26 @@ for rep in range(3):
     st, ff = batch.status(); t.append(time.perf_counter())
     res = batch.results(); t.append(time.perf_counter())
     out = D._collect(batch, cfg, True, 0.0); t.append(time.perf_counter())
-    names = ["h2d+prologue", "search", "status", "results(gather+assemble+py)", "collect(again)"]
+    t0 = time.perf_counter()
+    D.decode_batch_raw((raws, frames), cfg, w.table, w.model, sc, final_llm_only=True)
+    t.append(time.perf_counter())
+    t[-2] = t0
+    names = ["h2d+prologue", "search", "status", "results(gather+assemble+py)", "collect(again)", "decode_batch_raw total"]
     print({n: round((b - a) * 1e3, 2) for n, a, b in zip(names, t, t[1:])})
+
+# split of results(): C side vs Python objects
+import ctypes as C
+from paper_2603_14002_b200 import _native as N
+for rep in range(2):
+    batch = dm.batch(cfg, 256, 500)
+    batch.load_logits(raws, frames)
+    D.run_search(batch, cfg, sc, w.model, True); batch.sync()
+    lib = N.lib()
+    t0 = time.perf_counter()
+    nbytes, ntot = C.c_int64(), C.c_int64()
+    N.check(lib.lb_batch_results_size(batch.h, C.byref(nbytes), C.byref(ntot)))
+    t1 = time.perf_counter()
+    res = batch.results()
+    t2 = time.perf_counter()
+    print("results_size (gather+D2H+assembly) ms", round((t1 - t0) * 1e3, 2), "full results() ms",
+          round((t2 - t1) * 1e3, 2), "nbest entries", ntot.value, "blob bytes", nbytes.value)
