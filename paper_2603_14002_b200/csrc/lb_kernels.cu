@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
         const double thr = xsub(M, c.theta);
         const int bthr =
             (int)fmin(fmax(xmul(xsub(U, thr), c.inv_binw), 0.0), (double)(NBINS - 1));
-        // ---- C: every warp scans the histogram; hcum[] written identically by all warps
+        // ---- C: every warp scans the histogram in registers; warp 0 publishes hcum[]
         int bstar = NBINS, cum_thr = 0, cum_bstar = 0;
         {
           constexpr int PB = NBINS / 32;
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
             if (lane >= o) incl += y;
           }
           const int excl = incl - ls;
-          {
+          if (warp == 0) {
             int run = excl;
 #pragma unroll
             for (int i = 0; i < PB; ++i) {
@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
               run += part[i];
             }
           }
+          bar_sync(1, NC);  // hcum[] visible to every compute warp
           __syncwarp();
           cum_thr = hcum[bthr] + (int)hist[bthr];
           const bool here = excl < c.k && incl >= c.k;
@@ -1326,7 +1327,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   extern __shared__ __align__(128) char sm[];
   __shared__ __align__(8) uint64_t dbar[2];
   __shared__ unsigned hist[NBINS];
-  __shared__ int hcum[NBINS];
+  __shared__ int hcum[NBINS];  // exclusive prefix of hist (published by warp 0)
   __shared__ int hfill[NBINS];
   __shared__ double wmax[NWC];
   __shared__ double s_maxs;
@@ -1639,7 +1640,7 @@ __global__ void __launch_bounds__(small::NT, 2)
             if (lane >= o) incl += y;
           }
           const int excl = incl - ls;
-          {
+          if (warp == 0) {
             int run = excl;
 #pragma unroll
             for (int i = 0; i < PB; ++i) {
@@ -1647,7 +1648,7 @@ __global__ void __launch_bounds__(small::NT, 2)
               run += part[i];
             }
           }
-          __syncwarp();
+          bar_sync(1, NC);  // hcum[] visible to every compute warp
           cum_thr = hcum[bthr] + (int)hist[bthr];
           const unsigned bl = __ballot_sync(FULLMASK, excl < c.k && incl >= c.k);
           if (bl) {
