@@ -58,8 +58,11 @@ def parse():
                     help="skip the BASELINE config-3 (LLM fusion) summary in the default line")
     ap.add_argument("--phases", action="store_true", help="add per-phase cycle breakdown of K2")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic: keep L2 warm between steps")
-    ap.add_argument("--config", type=int, choices=(2, 3), default=2,
-                    help="BASELINE config: 2 = n-gram only (headline), 3 = + Llama-3.2-1B delayed fusion")
+    ap.add_argument("--config", type=int, choices=(1, 2, 3, 5), default=2,
+                    help="BASELINE config: 2 = n-gram only (headline), 3 = + Llama-3.2-1B delayed "
+                         "fusion, 1 = one T=500 utterance, beam 10, toy LM + tiny LLM, 5 = 8192 "
+                         "utterances over the GPUs with an 8B-class LLM (sub-batches of 256)")
+    ap.add_argument("--sub-batch", type=int, default=0, help="utterances per device batch (0 = all)")
     ap.add_argument("--llm", default="llama-3.2-1b", help="LLM preset for --config 3")
     ap.add_argument("--interval", type=int, default=20, help="fusion interval (frames) for --config 3")
     ap.add_argument("--ref-trials", type=int, default=4, help="reference-arm sample (config 3)")
@@ -101,6 +104,24 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+CONFIG_PRESETS = {
+    # BASELINE.json configs[0]: single synthetic B2T'25-shaped trial, beam 10, toy 4-gram LM from
+    # a small lexicon, tiny random-init LLM, fusion every 20 frames
+    1: dict(trials=1, frames=500, beam=10, words=2000, ngrams="5000,3000,2000", llm="tiny",
+            interval=20),
+    # configs[4]: 8192 trials data-parallel over the GPUs, 8B-class LLM fusion (per-GPU trials =
+    # 8192 / N, decoded in device batches of 256 so the bf16x2 prefix cache fits in HBM)
+    5: dict(trials=8192, frames=500, beam=64, llm="llama-3.1-8b", interval=20, sub_batch=256),
+}
+
+
+def apply_preset(args, world_n):
+    for k, v in CONFIG_PRESETS.get(args.config, {}).items():
+        setattr(args, k, v)
+    if args.config == 5:
+        args.trials = max(1, 8192 // world_n)
 
 
 def make_inputs(args, rank):
@@ -364,7 +385,7 @@ def run_ours(args):
     llm = None
     if not args.no_llm:  # BASELINE config 3 on the same utterances: + Llama-3.2-1B delayed fusion
         cfg3 = cfg.replace(llm_rescore_interval=args.interval)
-        llm = {"workload": llm_workload(args, world, cfg3)["workload"]}
+        llm = {"workload": llm_workload(args, world, cfg3, config=3)["workload"]}
         for prec in ("bf16x2", "bf16"):
             core = llm_core(dev, world, cfg3, raws, args.llm, prec, max(1, min(args.steps, 3)), 1,
                             world_n)
@@ -426,13 +447,15 @@ def run_ours(args):
 
 
 # --------------------------------------------------------------------------- config 3
-def llm_workload(args, world, cfg):
+def llm_workload(args, world, cfg, config=None):
+    config = args.config if config is None else config
     return {
-        "workload": (f"BASELINE config 3: {args.trials} utterances/GPU x {args.frames} frames x 41 "
-                     f"classes, beam {args.beam}, {args.words}-word lexicon, "
-                     f"{len(world.model.probs)}-entry 4-gram + random-init {args.llm} delayed "
-                     f"fusion every {cfg.llm_rescore_interval} frames (bf16 body, prefix-trie KV "
-                     "cache), b2t25 profile"),
+        "workload": (f"BASELINE config {config}: {args.trials} utterances/GPU x "
+                     f"{args.frames} frames x 41 classes, beam {args.beam}, {args.words}-word "
+                     f"lexicon, {len(world.model.probs)}-entry 4-gram + random-init {args.llm} "
+                     f"delayed fusion every {cfg.llm_rescore_interval} frames ({args.precision} "
+                     "body on bf16 tensor cores, prefix-trie KV cache), b2t25 profile"
+                     + (f", device batches of {args.sub_batch}" if args.sub_batch else "")),
         "trials_per_gpu": args.trials, "frames": args.frames, "beam": args.beam, "vocab": 41,
         "lexicon_words": args.words, "ngrams": len(world.model.probs), "llm": args.llm,
         "fusion_interval": cfg.llm_rescore_interval,
@@ -440,7 +463,7 @@ def llm_workload(args, world, cfg):
     }
 
 
-def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1):
+def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1, sub_batch=0):
     """Device-timed BASELINE-config-3 steps: K1 + frames + every fusion event (LLM on the
     device) + closure + final fusion for the whole batch, L2 flushed between steps."""
     import torch
@@ -451,14 +474,30 @@ def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1):
     scorer = LlamaScorer(llm, seed=0, device=dev, precision=precision)
     dm = device_model(world.table, world.model, dev)
     B, T = raws.shape[0], raws.shape[1]
+    SB = sub_batch if 0 < sub_batch < B else B
     frames = np.full(B, T, dtype=np.int32)
     x_dev = torch.from_numpy(raws).to(f"cuda:{dev}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
-    batch = dm.batch(cfg, B, T)
+    batch = dm.batch(cfg, SB, T)
+    row_bytes = T * raws.shape[2] * 4
 
-    def step():
-        batch.load_logits(None, frames, on_device_ptr=x_dev.data_ptr())
-        run_search(batch, cfg, scorer, world.model, final_llm_only=False)
+    acc = {"llm_ms": 0.0, "rows": 0, "slots": 0, "events": 0, "waves": 0, "last_b0": 0}
+
+    def collect_now():
+        sess_ = batch._llm_session
+        acc["llm_ms"] += sess_.llm_ms()
+        st = sess_.stats()
+        for k in ("rows", "slots", "events", "waves"):
+            acc[k] += st["forward_rows" if k == "rows" else k]
+
+    def step(collect=False):  # every utterance of this GPU, in device batches of SB
+        for b0 in range(0, B, SB):
+            nb = min(SB, B - b0)
+            batch.load_logits(None, frames[b0:b0 + nb], on_device_ptr=x_dev.data_ptr() + b0 * row_bytes)
+            run_search(batch, cfg, scorer, world.model, final_llm_only=False)
+            acc["last_b0"] = b0
+            if collect and SB < B:  # several device batches: read each one's counters (syncs)
+                collect_now()
 
     for _ in range(warmup):
         flush.zero_()
@@ -468,22 +507,19 @@ def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1):
     if world_n > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    ms_steps, llm_ms, launches, rows, slots, events, waves = [], 0.0, 0, 0, 0, 0, 0
+    ms_steps, launches = [], 0
     with ClockSampler(dev) as clk:
         for _ in range(steps):
             flush.zero_()
             batch.mark_begin()
-            step()
+            step(collect=True)
             ms, nl = batch.mark_end()
             ms_steps.append(ms)
             launches += nl
-            llm_ms += sess.llm_ms()
-            st = sess.stats()
-            rows += st["forward_rows"]
-            slots += st["slots"]
-            events += st["events"]
-            waves += st["waves"]
+            if SB >= B:  # one device batch: counters read outside the timed region
+                collect_now()
         torch.cuda.synchronize()
+    llm_ms, rows, slots, events, waves = (acc[k] for k in ("llm_ms", "rows", "slots", "events", "waves"))
     sess.enable_timing(False)
     total_ms = float(sum(ms_steps))
     if world_n > 1:
@@ -504,7 +540,7 @@ def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1):
         "rows": rows, "slots": slots, "events": events, "waves": waves, "clocks": clk.summary(),
         "achieved_tf": achieved_tf, "peak_tf": peak_tf,
         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if pp.exists() else "fallback 1400 TFLOP/s",
-        "frames_per_step": frames_per_step,
+        "frames_per_step": frames_per_step, "last_b0": acc["last_b0"],
     }
 
 
@@ -514,10 +550,12 @@ def llm_replay_check(world, cfg, raws, core, n=2):
     from paper_2603_14002_b200 import ReplayScorer
 
     replay = ReplayScorer(core["sess"].replay_table())
-    got = core["batch"].results()
+    got = core["batch"].results()  # the last device batch of the step
+    b0 = core.get("last_b0", 0)
+    n = min(n, len(got))
     ok = 0
     for i in range(n):
-        want = O.decode(O.log_softmax_scaled(raws[i], cfg.acoustic_scale), cfg, world.table,
+        want = O.decode(O.log_softmax_scaled(raws[b0 + i], cfg.acoustic_scale), cfg, world.table,
                         world.model, replay)
         g = got[i]
         ok += int(g is not None and g[0] == want.text and g[1] == want.score)
@@ -536,7 +574,8 @@ def run_llm(args):
     world, cfg, raws = make_inputs(args, rank)
     cfg = cfg.replace(llm_rescore_interval=args.interval)
     setup_s = time.perf_counter() - t_setup
-    core = llm_core(dev, world, cfg, raws, args.llm, args.precision, args.steps, args.warmup, world_n)
+    core = llm_core(dev, world, cfg, raws, args.llm, args.precision, args.steps, args.warmup, world_n,
+                    args.sub_batch)
     scorer, batch, frames = core["scorer"], core["batch"], core["frames"]
     B, T = raws.shape[0], raws.shape[1]
     ms_per_step, total_ms, llm_ms = core["ms_per_step"], core["total_ms"], core["llm_ms"]
@@ -577,8 +616,8 @@ def run_llm(args):
 
     if rank == 0:
         line = {
-            "metric": f"decoded frames/s (BASELINE config 3, beam {args.beam}, {args.llm} fusion, "
-                      "1 x B200 per rank)",
+            "metric": f"decoded frames/s (BASELINE config {args.config}, beam {args.beam}, {args.llm} "
+                      "fusion, 1 x B200 per rank)",
             "value": value, "unit": "frames/s", "n_gpus": world_n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
@@ -650,8 +689,8 @@ def run_reference_llm(args):
     cpu["value"] = value
     print(json.dumps({
         "impl": "reference",
-        "metric": f"decoded frames/s (BASELINE config 3, beam {args.beam}, {args.llm} fusion, "
-                  "1 x B200 per rank)",
+        "metric": f"decoded frames/s (BASELINE config {args.config}, beam {args.beam}, {args.llm} "
+                  "fusion, 1 x B200 per rank)",
         "value": value, "unit": "frames/s", "n_gpus": world_n, "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 search + bf16 LLM", "data": "synthetic",
@@ -746,7 +785,8 @@ def run_reference(args):
 
 def main():
     args = parse()
-    if args.config == 3:
+    apply_preset(args, dist_env()[0])
+    if args.config in (1, 3, 5):
         if args.impl == "reference":
             run_reference_llm(args)
         else:
