@@ -109,7 +109,7 @@ def dist_env():
 CONFIG_PRESETS = {
     # BASELINE.json configs[0]: single synthetic B2T'25-shaped trial, beam 10, toy 4-gram LM from
     # a small lexicon, tiny random-init LLM, fusion every 20 frames
-    1: dict(trials=1, frames=500, beam=10, words=2000, ngrams="5000,3000,2000", llm="tiny",
+    1: dict(trials=1, frames=500, beam=10, words=2000, ngrams="5000,3000,2000", llm="tiny-gpt2",
             interval=20),
     # configs[4]: 8192 trials data-parallel over the GPUs, 8B-class LLM fusion (per-GPU trials =
     # 8192 / N, decoded in device batches of 256 so the bf16x2 prefix cache fits in HBM)

@@ -280,6 +280,12 @@ int lb_llm_finish(lb_llm* l, int32_t final_, int32_t min_frames);
  * later next-token log-probs). */
 int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float eps, int32_t M,
                    void* out, const int32_t* store_slots);
+/* LayerNorm variant (GPT-2 architecture): out = ((x - mean) * rsqrt(var + eps)) * w + b */
+int lb_llm_layernorm(lb_llm* l, float* x, const void* delta, const float* w, const float* b,
+                     float eps, int32_t M, void* out, const int32_t* store_slots);
+/* in fp32 [M][ffn] (+ bias [ffn] if non-NULL) -> out bf16 [M][ffn] = gelu_tanh(in) ([M][2 ffn]
+ * hi|lo pairs in bf16x2 precision) -- the GPT-2 MLP activation ("gelu_new") */
+int lb_llm_gelu(lb_llm* l, const float* in, const float* bias, int32_t M, int32_t ffn, void* out);
 /* qkv fp32 [M][(n_heads + 2 n_kv_heads) head_dim] -> q_out [M][n_heads head_dim] rotated (bf16;
  * fp32 in bf16x2 precision);
  * rotated K and V written to the rows' slots of layer `layer`.  cos/sin fp32 [pos][head_dim/2] */

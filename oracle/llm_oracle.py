@@ -9,8 +9,8 @@ empty text -> 0, `:130-137` scoreEos = best of text + ".", "?", "!" with strict 
 reference scorer protocol (`pkg/src/lightbeam/scorer.py:93-163`: `submit`/`next_request_id`,
 kinds "score" and "score_eos").  The sidecar's own model is a char-level TypeScript toy that
 cannot run here (no Node); the north star names random-init GPT-2/Llama-architecture models,
-so the model is transformers' `LlamaForCausalLM` in fp32 on the CPU, loaded with exactly the
-weights of the GPU scorer.  Tokens: one per word, FNV-1a-64 of the utf-8 word mod (V - 8) + 8,
+so the model is transformers' `LlamaForCausalLM` / `GPT2LMHeadModel` in fp32 on the CPU, loaded
+with exactly the weights of the GPU scorer.  Tokens: one per word, FNV-1a-64 of the utf-8 word mod (V - 8) + 8,
 BOS = 1, ".?!" = 2, 3, 4 (restated here independently of the product's tokenizer).
 
 Parity status: LLM numerics are "parity unpinned" (no reference test pins LLM
@@ -39,9 +39,23 @@ def tokens(text: str, vocab: int) -> list[int]:
 
 
 def hf_model(cfg, state_dict):
-    """transformers LlamaForCausalLM (fp32, CPU) with the given weights."""
+    """transformers LlamaForCausalLM / GPT2LMHeadModel (fp32, CPU) with the given weights."""
     import torch
     from transformers import LlamaConfig, LlamaForCausalLM
+
+    if getattr(cfg, "arch", "llama") == "gpt2":
+        from transformers import GPT2Config, GPT2LMHeadModel
+
+        g = GPT2Config(vocab_size=cfg.vocab_size, n_positions=state_dict["transformer.wpe.weight"].shape[0],
+                       n_embd=cfg.hidden, n_layer=cfg.layers, n_head=cfg.heads, n_inner=cfg.ffn,
+                       activation_function="gelu_new", layer_norm_epsilon=cfg.rms_eps,
+                       resid_pdrop=0.0, embd_pdrop=0.0, attn_pdrop=0.0, tie_word_embeddings=True)
+        m = GPT2LMHeadModel(g).float().eval()
+        missing, unexpected = m.load_state_dict(state_dict, strict=False)
+        assert not unexpected and all(k.endswith(".attn.bias") or k.endswith("masked_bias")
+                                      for k in missing), (missing, unexpected)
+        torch.set_grad_enabled(False)
+        return m
 
     kw = dict(vocab_size=cfg.vocab_size, hidden_size=cfg.hidden, intermediate_size=cfg.ffn,
               num_hidden_layers=cfg.layers, num_attention_heads=cfg.heads,

@@ -173,6 +173,8 @@ _SIGS = {
     "lb_llm_finish": (C.c_int, [_P, _I32, _I32]),
     "lb_llm_rmsnorm": (C.c_int, [_P, _P, _P, _P, C.c_float, _I32, _P, _P]),
     "lb_llm_rope_kv": (C.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _P, _P]),
+    "lb_llm_layernorm": (C.c_int, [_P, _P, _P, _P, _P, C.c_float, _I32, _P, _P]),
+    "lb_llm_gelu": (C.c_int, [_P, _P, _P, _I32, _I32, _P]),
     "lb_llm_attention": (C.c_int, [_P, _I32, _P, _I32, _P, _P, _P]),
     "lb_llm_swiglu": (C.c_int, [_P, _P, _I32, _I32, _P]),
     "lb_llm_lse": (C.c_int, [_P, _P, _I32, _I64, _P]),

@@ -356,10 +356,12 @@ __global__ void wave_rows_kernel(LlmDev l, int64_t row0, int n, int32_t* tok, in
 // ------------------------------------------------------------------ transformer body
 // x[M][H] fp32 residual (+= delta fp32 when given) -> out = bf16(x * rsqrt(mean(x^2) + eps) * w);
 // `store_slots` also keeps the fp32 row in the slot hidden-state table.
+// bias != nullptr: LayerNorm y = (x - mean) * rsqrt(var + eps) * w + bias (GPT-2), two-pass
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float* delta,
                                                           const float* w, float eps, int H,
                                                           bf16* out, const int32_t* store_slots,
-                                                          float* s_h, int split) {
+                                                          float* s_h, int split,
+                                                          const float* bias = nullptr) {
   const int row = blockIdx.x;
   float* xr = x + (size_t)row * H;
   const float* dr = delta ? delta + (size_t)row * H : nullptr;
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float*
       v.w += a.w;
       *reinterpret_cast<float4*>(xr + i) = v;
     }
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    ss += bias ? (v.x + v.y + v.z + v.w) : (v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w);
   }
   __shared__ float red[32];
   ss = warp_sum(ss);
@@ -386,13 +388,42 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float*
     if (threadIdx.x == 0) red[0] = t;
   }
   __syncthreads();
-  const float r = rsqrtf(red[0] / (float)H + eps);
+  float mean = 0.f, r;
+  if (bias) {  // LayerNorm: ss above is the plain sum; second pass for the centred variance
+    mean = red[0] / (float)H;
+    __syncthreads();
+    float vs = 0.f;
+    for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + i);
+      const float a = v.x - mean, b2 = v.y - mean, c2 = v.z - mean, d2 = v.w - mean;
+      vs += a * a + b2 * b2 + c2 * c2 + d2 * d2;
+    }
+    vs = warp_sum(vs);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = vs;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+      t = warp_sum(t);
+      if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    r = rsqrtf(red[0] / (float)H + eps);
+  } else {
+    r = rsqrtf(red[0] / (float)H + eps);
+  }
   bf16* orow = out + (size_t)row * H * (split ? 2 : 1);
   float* hrow = store_slots ? s_h + (size_t)store_slots[row] * H : nullptr;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
     const float4 v = *reinterpret_cast<const float4*>(xr + i);
     const float4 g = *reinterpret_cast<const float4*>(w + i);
-    const float4 y = make_float4(v.x * r * g.x, v.y * r * g.y, v.z * r * g.z, v.w * r * g.w);
+    float4 y;
+    if (bias) {
+      const float4 bb = *reinterpret_cast<const float4*>(bias + i);
+      y = make_float4((v.x - mean) * r * g.x + bb.x, (v.y - mean) * r * g.y + bb.y,
+                      (v.z - mean) * r * g.z + bb.z, (v.w - mean) * r * g.w + bb.w);
+    } else {
+      y = make_float4(v.x * r * g.x, v.y * r * g.y, v.z * r * g.z, v.w * r * g.w);
+    }
     __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(orow + i);
     const __nv_bfloat162 h0 = __floats2bfloat162_rn(y.x, y.y), h1 = __floats2bfloat162_rn(y.z, y.w);
     op[0] = h0;
@@ -917,6 +948,40 @@ __global__ void swiglu_kernel(const TI* gu, int F, bf16* out, int split) {
   if (split) *reinterpret_cast<uint4*>(orow + F + c) = lv;
 }
 
+// in[M][F] fp32 (+ bias[F]) -> out = bf16(gelu_tanh(in)) (GPT-2 "gelu_new"; split: hi|lo pairs
+// [M][2F]); 8 columns per thread
+__global__ void gelu_kernel(const float* in, const float* bias, int F, bf16* out, int split) {
+  const int row = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= F) return;
+  float g[8];
+  load_f<8>(in + (size_t)row * F + c, g);
+  if (bias) {
+    float bb[8];
+    load_f<8>(bias + c, bb);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) g[e] += bb[e];
+  }
+  uint4 ov, lv;
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&ov);
+  __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&lv);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float y[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float x = g[2 * e + k];
+      y[k] = 0.5f * x * (1.f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+    }
+    o2[e] = __floats2bfloat162_rn(y[0], y[1]);
+    const float2 h = __bfloat1622float2(o2[e]);
+    l2[e] = __floats2bfloat162_rn(y[0] - h.x, y[1] - h.y);
+  }
+  bf16* orow = out + (size_t)row * F * (split ? 2 : 1);
+  *reinterpret_cast<uint4*>(orow + c) = ov;
+  if (split) *reinterpret_cast<uint4*>(orow + F + c) = lv;
+}
+
 // K6a: log-sum-exp of one LM-head logit row per CTA (16-B loads, online max/sum merge)
 template <typename TL>
 __global__ void __launch_bounds__(512) lse_kernel(const TL* logits, int64_t ld, int V,
@@ -1360,6 +1425,26 @@ int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float
   LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
                                                       l->dev.H, reinterpret_cast<bf16*>(out),
                                                       store_slots, l->dev.s_h, l->dev.split));
+  return LB_OK;
+}
+
+int lb_llm_layernorm(lb_llm* l, float* x, const void* delta, const float* w, const float* b,
+                     float eps, int32_t M, void* out, const int32_t* store_slots) {
+  if (!l || !x || !w || !b || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (M <= 0) return LB_OK;
+  LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
+                                                      l->dev.H, reinterpret_cast<bf16*>(out),
+                                                      store_slots, l->dev.s_h, l->dev.split, b));
+  return LB_OK;
+}
+
+int lb_llm_gelu(lb_llm* l, const float* in, const float* bias, int32_t M, int32_t ffn, void* out) {
+  if (!l || !in || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (ffn % 8 != 0) return lbh::set_error(LB_ERR_ARG, "ffn must be a multiple of 8");
+  if (M <= 0) return LB_OK;
+  const dim3 grid((ffn / 8 + 127) / 128, M);
+  LAUNCH(gelu_kernel<<<grid, 128, 0, l->b->st>>>(in, bias, ffn, reinterpret_cast<bf16*>(out),
+                                                 l->dev.split));
   return LB_OK;
 }
 

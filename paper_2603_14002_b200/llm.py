@@ -56,11 +56,12 @@ class LlmConfig:
     rope_scaling: dict | None = None  # llama3 rope parameters
     rms_eps: float = 1e-5
     init_std: float = 0.02
+    arch: str = "llama"  # "llama" | "gpt2" (learned positions, LayerNorm, GELU, biases, MHA)
 
     def n_params(self) -> int:
         att = self.hidden * (self.heads + 2 * self.kv_heads) * self.head_dim
         att += self.heads * self.head_dim * self.hidden
-        mlp = 3 * self.hidden * self.ffn
+        mlp = (2 if self.arch == "gpt2" else 3) * self.hidden * self.ffn
         return self.vocab_size * self.hidden + self.layers * (att + mlp + 2 * self.hidden) + self.hidden
 
     def flops_per_token(self) -> float:
@@ -68,7 +69,8 @@ class LlmConfig:
         prefix excluded)."""
         att = self.hidden * (self.heads + 2 * self.kv_heads) * self.head_dim
         att += self.heads * self.head_dim * self.hidden
-        return 2.0 * (self.layers * (att + 3 * self.hidden * self.ffn) + self.vocab_size * self.hidden)
+        mlp = (2 if self.arch == "gpt2" else 3) * self.hidden * self.ffn
+        return 2.0 * (self.layers * (att + mlp) + self.vocab_size * self.hidden)
 
 
 _LLAMA3_1B_ROPE = {"factor": 32.0, "low_freq_factor": 1.0, "high_freq_factor": 4.0,
@@ -77,7 +79,9 @@ _LLAMA3_8B_ROPE = {"factor": 8.0, "low_freq_factor": 1.0, "high_freq_factor": 4.
                    "original_max_position_embeddings": 8192}
 
 PRESETS = {
-    # config 1 of BASELINE.json: a tiny model (Llama-architecture stand-in for the GPT-2-style toy)
+    # config 1 of BASELINE.json: the tiny GPT-2-style model (2 layers, d = 64)
+    "tiny-gpt2": LlmConfig("tiny-gpt2", 4096, 64, 2, 1, 1, 256, 64, arch="gpt2"),
+    # a tiny Llama-architecture model (fast tests of the Llama kernels)
     "tiny": LlmConfig("tiny", 4096, 128, 2, 2, 1, 512, 64),
     # config 3: Llama-3.2-1B architecture
     "llama-3.2-1b": LlmConfig("llama-3.2-1b", 128256, 2048, 16, 32, 8, 8192, 64,
@@ -181,6 +185,9 @@ class LlamaWeights:
         H, hd = cfg.hidden, cfg.head_dim
         self.emb = rnd(cfg.vocab_size, H)
         self.layers = []
+        if cfg.arch == "gpt2":
+            self._init_gpt2(rnd, max_pos)
+            return
         for _ in range(cfg.layers):
             wq = rnd(cfg.heads * hd, H)
             wk = rnd(cfg.kv_heads * hd, H)
@@ -205,9 +212,53 @@ class LlamaWeights:
         self.sin = freqs.sin().to(self.device).contiguous()
         self.max_pos = max_pos
 
+    def _init_gpt2(self, rnd, max_pos):
+        """GPT-2 layout: learned positions, pre-LayerNorm blocks, fused q/k/v with biases, GELU
+        MLP; every weight, bias and position row ~ N(0, init_std) (biases and LayerNorm shifts
+        random too, so the kernels' bias paths are exercised), LayerNorm gains 1."""
+        import torch
+
+        cfg, H, dev = self.cfg, self.cfg.hidden, self.device
+        f32 = lambda t: t.float().contiguous()  # noqa: E731  (bf16-valued fp32 vectors)
+        self.wpe = f32(rnd(max(max_pos, 1024), H))
+        for _ in range(cfg.layers):
+            self.layers.append({
+                "ln1": torch.ones(H, dtype=torch.float32, device=dev), "ln1b": f32(rnd(H)),
+                "wqkv": rnd(3 * H, H), "bqkv": f32(rnd(3 * H)),
+                "wo": rnd(H, H), "bo": f32(rnd(H)),
+                "ln2": torch.ones(H, dtype=torch.float32, device=dev), "ln2b": f32(rnd(H)),
+                "wfc": rnd(cfg.ffn, H), "bfc": f32(rnd(cfg.ffn)),
+                "wd": rnd(H, cfg.ffn), "bd": f32(rnd(H)),
+            })
+        self.norm = torch.ones(H, dtype=torch.float32, device=dev)
+        self.normb = f32(rnd(H))
+        half = cfg.head_dim // 2  # no rotary embedding: identity tables for the shared kernel
+        self.cos = torch.ones((max_pos, half), dtype=torch.float32, device=dev)
+        self.sin = torch.zeros((max_pos, half), dtype=torch.float32, device=dev)
+        self.max_pos = max_pos
+
     def hf_state_dict(self) -> dict:
-        """fp32 CPU tensors under transformers' LlamaForCausalLM names (for the test oracle)."""
+        """fp32 CPU tensors under transformers' LlamaForCausalLM / GPT2LMHeadModel names (for
+        the test oracle)."""
         cfg = self.cfg
+        if cfg.arch == "gpt2":
+            c = lambda t: t.float().cpu()  # noqa: E731
+            sd = {"transformer.wte.weight": c(self.emb), "transformer.wpe.weight": c(self.wpe),
+                  "transformer.ln_f.weight": c(self.norm), "transformer.ln_f.bias": c(self.normb),
+                  "lm_head.weight": c(self.emb)}
+            for i, L in enumerate(self.layers):
+                p = f"transformer.h.{i}."
+                sd[p + "ln_1.weight"], sd[p + "ln_1.bias"] = c(L["ln1"]), c(L["ln1b"])
+                sd[p + "ln_2.weight"], sd[p + "ln_2.bias"] = c(L["ln2"]), c(L["ln2b"])
+                sd[p + "attn.c_attn.weight"] = c(L["wqkv"]).t().contiguous()  # Conv1D: [in, out]
+                sd[p + "attn.c_attn.bias"] = c(L["bqkv"])
+                sd[p + "attn.c_proj.weight"] = c(L["wo"]).t().contiguous()
+                sd[p + "attn.c_proj.bias"] = c(L["bo"])
+                sd[p + "mlp.c_fc.weight"] = c(L["wfc"]).t().contiguous()
+                sd[p + "mlp.c_fc.bias"] = c(L["bfc"])
+                sd[p + "mlp.c_proj.weight"] = c(L["wd"]).t().contiguous()
+                sd[p + "mlp.c_proj.bias"] = c(L["bd"])
+            return sd
         qn, kn = cfg.heads * cfg.head_dim, cfg.kv_heads * cfg.head_dim
         sd = {"model.embed_tokens.weight": self.emb.float().cpu(),
               "model.norm.weight": self.norm.float().cpu(),
@@ -264,8 +315,9 @@ class LlamaScorer:
         self.split = precision == "bf16x2"
         if self.split:  # [W | W]: one GEMM computes hi @ W^T + lo @ W^T with fp32 accumulation
             for L in self.weights.layers:
-                for k in ("wqkv", "wo", "wgu", "wd"):
-                    L[k + "2"] = torch.cat([L[k], L[k]], 1).contiguous()
+                for k in ("wqkv", "wo", "wgu", "wfc", "wd"):
+                    if k in L:
+                        L[k + "2"] = torch.cat([L[k], L[k]], 1).contiguous()
             self.emb2 = torch.cat([self.weights.emb, self.weights.emb], 1).contiguous()
         self.device_llm_scorer = self  # the GPU decoder drives this scorer on the device
 
@@ -369,6 +421,8 @@ def dense_forward(W: LlamaWeights, ids, lens, eos: bool, exact_fp32: bool = Fals
             out = torch.mm(a2.to(torch.bfloat16), w.t(), out_dtype=torch.float32)
         return out.view(*a.shape[:-1], -1)
 
+    if cfg.arch == "gpt2":
+        return _dense_forward_gpt2(W, ids, lens, eos, exact_fp32, split)
     x = W.emb[ids].float()
     cos = W.cos[:S].repeat(1, 2)[None, None]
     sin = W.sin[:S].repeat(1, 2)[None, None]
@@ -408,6 +462,64 @@ def dense_forward(W: LlamaWeights, ids, lens, eos: bool, exact_fp32: bool = Fals
         tgt = ids[r, 1:n]
         total = 0.0
         for t, v in enumerate(lsm[: n - 1].gather(1, tgt[:, None])[:, 0].tolist()):
+            total += v
+        out_lp.append(total)
+        if eos:
+            out_p.append([float(lsm[n - 1, p]) for p in PUNCT_IDS])
+    return out_lp, out_p
+
+
+def _dense_forward_gpt2(W, ids, lens, eos, exact_fp32, split):
+    """GPT-2 block structure (transformers' GPT2LMHeadModel): x = wte + wpe; per layer
+    x += c_proj(attn(ln_1(x))) and x += mlp_proj(gelu_tanh(c_fc(ln_2(x)))); ln_f; tied head."""
+    import torch
+    import torch.nn.functional as F
+
+    cfg = W.cfg
+    B, S = ids.shape
+    hd, nh = cfg.head_dim, cfg.heads
+    opd = torch.float32 if exact_fp32 else torch.bfloat16
+
+    def mm(a, w, tag=None):
+        a2 = a.reshape(-1, a.shape[-1])
+        if exact_fp32:
+            out = a2.float() @ w.float().t()
+        elif tag in split:
+            hi = a2.float().to(torch.bfloat16)
+            lo = (a2.float() - hi.float()).to(torch.bfloat16)
+            out = torch.mm(hi, w.t(), out_dtype=torch.float32) + torch.mm(lo, w.t(), out_dtype=torch.float32)
+        else:
+            out = torch.mm(a2.to(torch.bfloat16), w.t(), out_dtype=torch.float32)
+        return out.view(*a.shape[:-1], -1)
+
+    def keep(tag):
+        return torch.float32 if (exact_fp32 or tag in split) else torch.bfloat16
+
+    def ln(v, w, b, tag=None):
+        return F.layer_norm(v, (v.shape[-1],), w, b, cfg.rms_eps).to(keep(tag))
+
+    attd = torch.float32 if ("attn" in split or exact_fp32) else opd
+    x = W.emb[ids].float() + W.wpe[:S][None]
+    for L in W.layers:
+        h = ln(x, L["ln1"], L["ln1b"], "qkv")
+        qkv = mm(h, L["wqkv"], "qkv") + L["bqkv"]
+        q, k, v = (qkv[..., i * nh * hd: (i + 1) * nh * hd].view(B, S, nh, hd).transpose(1, 2).to(attd)
+                   for i in range(3))
+        a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        x = x + mm(a.transpose(1, 2).reshape(B, S, nh * hd).to(keep("o")), L["wo"], "o") + L["bo"]
+        h = ln(x, L["ln2"], L["ln2b"], "gu")
+        f = mm(h, L["wfc"], "gu") + L["bfc"]
+        act = F.gelu(f.float(), approximate="tanh").to(keep("down"))
+        x = x + mm(act, L["wd"], "down") + L["bd"]
+    hn = F.layer_norm(x, (x.shape[-1],), W.norm, W.normb, cfg.rms_eps)
+    out_lp, out_p = [], []
+    for r in range(B):
+        n = lens[r]
+        logits = (mm(hn[r, :n], W.emb, "lm") if "lm" in split else mm(hn[r, :n].to(opd), W.emb)) \
+            if not exact_fp32 else hn[r, :n] @ W.emb.float().t()
+        lsm = torch.log_softmax(logits.float(), -1).double()
+        total = 0.0
+        for v in lsm[: n - 1].gather(1, ids[r, 1:n][:, None])[:, 0].tolist():
             total += v
         out_lp.append(total)
         if eos:
@@ -555,6 +667,8 @@ class DeviceLlmSession:
         tok, pos, slot, chain = ws["tok"][:n], ws["pos"][:n], ws["slot"][:n], ws["chain"][:n]
         N.check(lib.lb_llm_wave_rows(self.h, wave, row0, n, tok.data_ptr(), pos.data_ptr(),
                                      slot.data_ptr(), chain.data_ptr()))
+        if cfg.arch == "gpt2":
+            return self._forward_rows_gpt2(tok, pos, slot, chain, n)
         x = W.emb.index_select(0, tok.long()).float()
         hn, q, att, act = ws["hn"][:n], ws["q"][:n], ws["att"][:n], ws["act"][:n]
         eps = cfg.rms_eps
@@ -582,6 +696,15 @@ class DeviceLlmSession:
             N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), dn.data_ptr(), wnext.data_ptr(), eps, n,
                                        hn.data_ptr(), slot.data_ptr() if last else None))
             del dn
+        self._lm_head(hn, slot, n)
+
+    def _lm_head(self, hn, slot, n: int):
+        import torch
+
+        lib = N.lib()
+        W = self.scorer.weights
+        sfx = "2" if self.scorer.split else ""
+        f32 = torch.float32
         # rows per LM-head GEMM: large enough for full tensor-core tiles (measured: 2048 rows bf16 /
         # 1024 rows bf16x2 beat L2-resident 256-row chunks by ~15% of the LLM step)
         chunk = self.scorer.lm_chunk // (2 if sfx else 1)
@@ -593,6 +716,48 @@ class DeviceLlmSession:
                 logits = torch.mm(hn[c0:c1], W.emb.t())
             N.check(lib.lb_llm_lse(self.h, logits.data_ptr(), c1 - c0, logits.stride(0),
                                    slot[c0:].data_ptr()))
+
+    def _forward_rows_gpt2(self, tok, pos, slot, chain, n: int):
+        """GPT-2 blocks on the same kernels: LayerNorm (+bias), fused q/k/v GEMM + bias, identity
+        rotary tables (learned positions were added at the input), MHA chain attention, GELU."""
+        import torch
+
+        lib = N.lib()
+        cfg, W = self.scorer.cfg, self.scorer.weights
+        ws = self._work(n)
+        hn, q, att, act = ws["hn"][:n], ws["q"][:n], ws["att"][:n], ws["act"][:n]
+        eps, f32 = cfg.rms_eps, torch.float32
+        sfx = "2" if self.scorer.split else ""
+        x = W.emb.index_select(0, tok.long()).float() + W.wpe.index_select(0, pos.long())
+        L0 = W.layers[0]
+        N.check(lib.lb_llm_layernorm(self.h, x.data_ptr(), None, L0["ln1"].data_ptr(),
+                                     L0["ln1b"].data_ptr(), eps, n, hn.data_ptr(), None))
+        for li, L in enumerate(W.layers):
+            qkv = torch.mm(hn, L["wqkv" + sfx].t(), out_dtype=f32)
+            qkv += L["bqkv"]
+            N.check(lib.lb_llm_rope_kv(self.h, li, qkv.data_ptr(), n, pos.data_ptr(), slot.data_ptr(),
+                                       W.cos.data_ptr(), W.sin.data_ptr(), q.data_ptr()))
+            del qkv
+            N.check(lib.lb_llm_attention(self.h, li, q.data_ptr(), n, chain.data_ptr(), pos.data_ptr(),
+                                         att.data_ptr()))
+            o = torch.mm(att, L["wo" + sfx].t(), out_dtype=f32)
+            o += L["bo"]
+            N.check(lib.lb_llm_layernorm(self.h, x.data_ptr(), o.data_ptr(), L["ln2"].data_ptr(),
+                                         L["ln2b"].data_ptr(), eps, n, hn.data_ptr(), None))
+            del o
+            f = torch.mm(hn, L["wfc" + sfx].t(), out_dtype=f32)
+            N.check(lib.lb_llm_gelu(self.h, f.data_ptr(), L["bfc"].data_ptr(), n, cfg.ffn,
+                                    act.data_ptr()))
+            del f
+            dn = torch.mm(act, L["wd" + sfx].t(), out_dtype=f32)
+            dn += L["bd"]
+            last = li + 1 == cfg.layers
+            nw, nb = (W.norm, W.normb) if last else (W.layers[li + 1]["ln1"], W.layers[li + 1]["ln1b"])
+            N.check(lib.lb_llm_layernorm(self.h, x.data_ptr(), dn.data_ptr(), nw.data_ptr(),
+                                         nb.data_ptr(), eps, n, hn.data_ptr(),
+                                         slot.data_ptr() if last else None))
+            del dn
+        self._lm_head(hn, slot, n)
 
     def stats(self) -> dict:
         out = np.zeros(8, dtype=np.int64)

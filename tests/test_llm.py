@@ -207,12 +207,16 @@ def _peaky_tiny():
     return dataclasses.replace(PRESETS["tiny"], init_std=0.25, rope_theta=10000.0)
 
 
-def test_dense_fp32_forward_matches_transformers():
-    """The Llama body restated in plain torch (fp32) == transformers' LlamaForCausalLM."""
+@pytest.mark.parametrize("arch", ["llama", "gpt2"])
+def test_dense_fp32_forward_matches_transformers(arch):
+    """The Llama / GPT-2 bodies restated in plain torch (fp32) == transformers'
+    LlamaForCausalLM / GPT2LMHeadModel."""
     torch = pytest.importorskip("torch")
+    import dataclasses
+
     from paper_2603_14002_b200.llm import LlamaWeights, dense_forward
 
-    cfg = _peaky_tiny()
+    cfg = _peaky_tiny() if arch == "llama" else dataclasses.replace(PRESETS["tiny-gpt2"], init_std=0.25)
     W = LlamaWeights(cfg, seed=5, device="cpu", max_pos=64)
     oracle = LO.OracleLlmScorer(cfg, W.hf_state_dict())
     texts = ["w1 w2 w3 w4 w5 w6 w7 w8", "ant", "the ant at an ant the", "x" * 3 + " y"]
@@ -288,6 +292,50 @@ def test_llm_head_dim_128_gqa4_vs_oracle(precision):
     sc = LlamaScorer(cfg_llm, seed=9, precision=precision)
     w, cfg = _world_cfg()
     raws = synth.make_logits(3, 120, 41, base_seed=23)
+    ds, got, sess = _decode_with_session(sc, raws, cfg, w)
+    replay = ReplayScorer(sess.replay_table())
+    for i, d in enumerate(ds):
+        want = O.decode(d, cfg, w.table, w.model, replay)
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest)
+    ex = sess.export()
+    first = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._cap)}
+    mid = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._low)}
+    oracle = LO.OracleLlmScorer(sc.cfg, sc.weights.hf_state_dict())
+    texts, devs = [], []
+    for s in range(1, len(ex["parent"])):
+        if ex["parent"][s] < 0 or not ex["state"][s] & 2:
+            continue
+        words, cur = [], s
+        while cur != 0:
+            words.append(int(ex["token"][cur]))
+            cur = int(ex["parent"][cur])
+        words.reverse()
+        texts.append(" ".join([first[words[0]]] + [mid[t] for t in words[1:]]))
+        devs.append(ex["cum"][s])
+    texts, devs = texts[:150], devs[:150]
+    want = [oracle.score(t) for t in texts]
+    dense = sc.score_texts_dense(texts)
+    e_dev = max(abs(a - b) for a, b in zip(devs, want))
+    e_dense = max(abs(a - b) for a, b in zip(dense, want))
+    if precision == "bf16x2":
+        assert e_dev <= TOL, e_dev
+    else:
+        assert e_dev <= 2.0 * e_dense + 1e-4, (e_dev, e_dense)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["bf16", "bf16x2"])
+def test_llm_gpt2_tiny_device_vs_oracle(precision):
+    """BASELINE config 1's tiny GPT-2-style LLM (learned positions, LayerNorm + biases, GELU, MHA)
+    on the device kernels: replay parity and scores vs transformers' GPT2LMHeadModel in fp32."""
+    import dataclasses
+
+    from paper_2603_14002_b200 import LlamaScorer, ReplayScorer
+
+    cfg_llm = dataclasses.replace(PRESETS["tiny-gpt2"], init_std=0.1)
+    sc = LlamaScorer(cfg_llm, seed=4, precision=precision)
+    w, cfg = _world_cfg()
+    raws = synth.make_logits(3, 120, 41, base_seed=29)
     ds, got, sess = _decode_with_session(sc, raws, cfg, w)
     replay = ReplayScorer(sess.replay_table())
     for i, d in enumerate(ds):
