@@ -300,6 +300,11 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
 int lb_llm_swiglu(lb_llm* l, const void* gu, int32_t M, int32_t ffn, void* out);
 /* K6: log-sum-exp of LM-head logit rows (bf16 [M][ld], vocab columns) into the rows' slots */
 int lb_llm_lse(lb_llm* l, const void* logits, int32_t M, int64_t ld, const int32_t* slots);
+/* K6 fused on tcgen05: log-sum-exp of the LM-head logits h[M][K] . emb[N][K]^T (bf16, K-major,
+ * row pitches ldh / lde elements) into the rows' slots, without materialising logits.
+ * partial: device scratch of M * ceil(N / 256) float2. */
+int lb_llm_lmhead_lse(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t K, const void* emb,
+                      int64_t lde, int32_t N, const int32_t* slots, void* partial);
 /* out[8]: slots, events, waves, forwarded rows, widest wave, device bytes, scores computed
  * (next-token log-probs), 0 */
 int lb_llm_stats(lb_llm* l, int64_t* out);

@@ -38,8 +38,10 @@
 //   lp_kernel / cum_kernel  K6 gather: next-token log-prob and running text score
 //   punct_kernel          end-of-sentence punctuation log-probs of final texts
 //   llm_apply_kernel      K7: fusion into the ortho entries and beam scores
+#include <cuda.h>  // CUtensorMap (TMA descriptors; the encoder is fetched at run time)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -1186,6 +1188,232 @@ __global__ void root_slots_kernel(int32_t* node_slot, int B, int64_t ncap) {
     node_slot[(size_t)i * ncap] = 0;
 }
 
+// ---------------------------------------------------------------- K6 on tcgen05
+// Fused LM head + log-sum-exp: logits = H[M][K] . E[N][K]^T are never written.  A persistent
+// warp-specialised kernel: warp 0 (one lane) streams 128x64 A and 256x64 B tiles with 2-D TMA
+// (128-byte swizzle) through a 4-stage mbarrier ring; warp 1 (one lane) issues
+// tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16) into a double-buffered TMEM
+// accumulator (2 x 256 columns) and commits stage/accumulator barriers; warps 2-5 drain the
+// accumulator with tcgen05.ld (thread = row) and fold each 256-column slice into a per-row
+// (max, sum exp) partial.  lse_reduce_kernel combines the partials of a row.
+constexpr int LM_BM = 128, LM_BN = 256, LM_BK = 64, LM_ST = 4;
+constexpr int LM_A_BYTES = LM_BM * LM_BK * 2;
+constexpr int LM_B_BYTES = LM_BN * LM_BK * 2;
+constexpr int LM_STAGE_BYTES = LM_A_BYTES + LM_B_BYTES;
+constexpr int LM_SMEM = 1024 + LM_ST * LM_STAGE_BYTES + 256;
+constexpr int LM_THREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                         // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;               // stride byte offset
+  d |= (uint64_t)1 << 46;                         // version (sm_100)
+  d |= (uint64_t)2 << 61;                         // layout: SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: D f32, A/B bf16, K-major both, N = 256, M = 128
+constexpr uint32_t LM_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
+                              ((uint32_t)(LM_BM >> 4) << 24);
+
+__global__ void __launch_bounds__(LM_THREADS, 1)
+    lmhead_lse_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      int M, int N, int K, int MT, int NT, float2* partial) {
+  extern __shared__ __align__(1024) unsigned char lm_smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(lm_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + LM_ST * LM_STAGE_BYTES);
+  uint64_t* empty = full + LM_ST;
+  uint64_t* tfull = empty + LM_ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < LM_ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {  // 2 x 256 fp32 accumulator columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const int KB = K / LM_BK;
+  const int total = MT * NT;
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int m0 = (t % MT) * LM_BM, n0 = (t / MT) * LM_BN;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], LM_STAGE_BYTES);
+          unsigned char* sa = sm + stage * LM_STAGE_BYTES;
+          tma_2d(sa, &tmA, kb * LM_BK, m0, &full[stage]);
+          tma_2d(sa + LM_A_BYTES, &tmB, kb * LM_BK, n0, &full[stage]);
+          if (++stage == LM_ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(acc * LM_BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t sa = smem_u32(sm + stage * LM_STAGE_BYTES);
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + LM_A_BYTES);
+#pragma unroll
+          for (int k = 0; k < LM_BK / 16; ++k) {  // +32 B per K=16 step inside the swizzle atom
+            const uint32_t accum = (kb | k) ? 1u : 0u;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                "l"(da + (uint64_t)(k * 2)), "l"(db + (uint64_t)(k * 2)), "r"(LM_IDESC), "r"(accum));
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&empty[stage]))
+                       : "memory");
+          if (++stage == LM_ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&tfull[acc]))
+                     : "memory");
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else {  // ===== epilogue: warps 2..5, thread = accumulator row (TMEM lane)
+    const int q = warp & 3;  // the TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int m0 = (t % MT) * LM_BM, n = t / MT, n0 = n * LM_BN;
+      mbar_wait(&tfull[acc], aphase);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      float mrun = -INFINITY, srun = 0.f;
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * LM_BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < LM_BN; c0 += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(base + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const int valid = min(32, N - (n0 + c0));
+        float cm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < valid) cm = fmaxf(cm, __uint_as_float(v[j]));
+        if (cm > mrun) {
+          srun = (mrun == -INFINITY) ? 0.f : srun * __expf(mrun - cm);
+          mrun = cm;
+        }
+        float cs = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < valid) cs += __expf(__uint_as_float(v[j]) - mrun);
+        srun += cs;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(&tempty[acc]);
+      const int row = m0 + q * 32 + lane;
+      if (row < M) partial[(size_t)row * NT + n] = make_float2(mrun, srun);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
+// combine the per-tile (max, sum) partials of one row into its log-sum-exp
+__global__ void __launch_bounds__(128) lse_reduce_kernel(const float2* partial, int NT,
+                                                         const int32_t* slots, float* s_lse) {
+  const int row = blockIdx.x;
+  const float2* p = partial + (size_t)row * NT;
+  float m = -INFINITY, s = 0.f;
+  for (int i = threadIdx.x; i < NT; i += blockDim.x) {
+    const float2 v = p[i];
+    if (v.x == -INFINITY) continue;
+    const float nm = fmaxf(m, v.x);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + v.y * __expf(v.x - nm);
+    m = nm;
+  }
+  __shared__ float sm_m[4], sm_s[4];
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(FULLMASK, m, o), s2 = __shfl_xor_sync(FULLMASK, s, o);
+    const float nm = fmaxf(m, m2);
+    s = (nm == -INFINITY) ? 0.f : (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - nm));
+    m = nm;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sm_m[threadIdx.x >> 5] = m;
+    sm_s[threadIdx.x >> 5] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M2 = -INFINITY, S2 = 0.f;
+    for (int w = 0; w < 4; ++w) {
+      if (sm_m[w] == -INFINITY) continue;
+      const float nm = fmaxf(M2, sm_m[w]);
+      S2 = (M2 == -INFINITY ? 0.f : S2 * __expf(M2 - nm)) + sm_s[w] * __expf(sm_m[w] - nm);
+      M2 = nm;
+    }
+    s_lse[slots[row]] = M2 + logf(S2);
+  }
+}
+
 template <typename T>
 cudaError_t dalloc(T** p, size_t n) {
   if (n == 0) n = 1;
@@ -1539,6 +1767,63 @@ int lb_llm_lse(lb_llm* l, const void* logits, int32_t M, int64_t ld, const int32
   else
     LAUNCH(lse_kernel<bf16><<<M, 512, 0, l->b->st>>>(reinterpret_cast<const bf16*>(logits), ld,
                                                      l->dev.vocab, slots, l->dev.s_lse));
+  return LB_OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 K-major operand [rows][K] with row pitch `ld` elements, boxes of box_rows x 64
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return lbh::set_error(LB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)LM_BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return lbh::set_error(LB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return LB_OK;
+}
+
+int lb_llm_lmhead_lse(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t K, const void* emb,
+                      int64_t lde, int32_t N, const int32_t* slots, void* partial) {
+  if (!l || !h || !emb || !slots || !partial) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (K % LM_BK != 0) return lbh::set_error(LB_ERR_ARG, "K must be a multiple of 64");
+  if ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(emb)) & 15)
+    return lbh::set_error(LB_ERR_ARG, "operands must be 16-byte aligned");
+  if ((ldh * 2) % 16 || (lde * 2) % 16) return lbh::set_error(LB_ERR_ARG, "row pitch must be a multiple of 16 bytes");
+  if (M <= 0) return LB_OK;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, h, M, K, ldh, LM_BM);
+  if (rc) return rc;
+  rc = make_map(&mb, emb, N, K, lde, LM_BN);
+  if (rc) return rc;
+  const int MT = (M + LM_BM - 1) / LM_BM, NT = (N + LM_BN - 1) / LM_BN;
+  static int attr = 0;
+  if (!attr) {
+    CKL(cudaFuncSetAttribute(lmhead_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LM_SMEM));
+    attr = 1;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, l->b->m->device);
+  const int grid = std::min(MT * NT, nsm);
+  cudaStream_t st = l->b->st;
+  LAUNCH(lmhead_lse_kernel<<<grid, LM_THREADS, LM_SMEM, st>>>(ma, mb, M, N, K, MT, NT,
+                                                               reinterpret_cast<float2*>(partial)));
+  LAUNCH(lse_reduce_kernel<<<M, 128, 0, st>>>(reinterpret_cast<const float2*>(partial), NT, slots,
+                                               l->dev.s_lse));
   return LB_OK;
 }
 

@@ -287,7 +287,7 @@ class LlamaScorer:
 
     def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
                  max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 2048,
-                 precision: str = "bf16x2"):
+                 precision: str = "bf16x2", lm_head: str = "fused"):
         """precision: "bf16x2" (default) feeds every body GEMM the activation as a hi+lo pair of
         bf16 values against duplicated bf16 weights -- fp32-equivalent activations on the bf16
         tensor cores, scores within ~1e-3 of an fp32 forward even for 40-token texts -- and keeps
@@ -311,6 +311,9 @@ class LlamaScorer:
         self._ids = itertools.count(1)
         if precision not in self.PRECISIONS:
             raise ValueError(f"precision must be one of {self.PRECISIONS}")
+        if lm_head not in ("fused", "cublas"):
+            raise ValueError("lm_head must be 'fused' (tcgen05 GEMM + log-sum-exp) or 'cublas'")
+        self.lm_head = lm_head
         self.precision = precision
         self.split = precision == "bf16x2"
         if self.split:  # [W | W]: one GEMM computes hi @ W^T + lo @ W^T with fp32 accumulation
@@ -705,6 +708,14 @@ class DeviceLlmSession:
         W = self.scorer.weights
         sfx = "2" if self.scorer.split else ""
         f32 = torch.float32
+        if self.scorer.lm_head == "fused":  # K6 on tcgen05: logits never leave TMEM
+            E = self.scorer.emb2 if sfx else W.emb
+            nt = (E.shape[0] + 255) // 256
+            partial = torch.empty((n, nt, 2), dtype=torch.float32, device=hn.device)
+            N.check(lib.lb_llm_lmhead_lse(self.h, hn.data_ptr(), n, hn.stride(0), E.shape[1],
+                                          E.data_ptr(), E.stride(0), E.shape[0], slot.data_ptr(),
+                                          partial.data_ptr()))
+            return
         # rows per LM-head GEMM: large enough for full tensor-core tiles (measured: 2048 rows bf16 /
         # 1024 rows bf16x2 beat L2-resident 256-row chunks by ~15% of the LLM step)
         chunk = self.scorer.lm_chunk // (2 if sfx else 1)

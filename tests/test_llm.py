@@ -365,3 +365,60 @@ def test_llm_gpt2_tiny_device_vs_oracle(precision):
         assert e_dev <= TOL, e_dev
     else:
         assert e_dev <= 2.0 * e_dense + 1e-4, (e_dev, e_dense)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["bf16", "bf16x2"])
+def test_fused_lmhead_lse_matches_cublas_path(precision):
+    """K6 on tcgen05 (fused LM-head GEMM + log-sum-exp in TMEM) against cuBLAS logits + the
+    row LSE kernel: same decode, per-text scores within float rounding of the LSE."""
+    from paper_2603_14002_b200 import LlamaScorer
+
+    w, cfg = _world_cfg()
+    raws = synth.make_logits(3, 100, 41, base_seed=41)
+    outs = []
+    for mode in ("cublas", "fused"):
+        sc = LlamaScorer("tiny", seed=6, precision=precision, lm_head=mode)
+        _, got, sess = _decode_with_session(sc, raws, cfg, w)
+        outs.append((sess.export(), [(g.text, g.score) for g in got]))
+    (a, ga), (b, gb) = outs
+    pa, pb = _scores_by_path(a), _scores_by_path(b)  # slot ids depend on allocation order
+    assert pa.keys() == pb.keys()
+    d = max(abs(pa[k][0] - pb[k][0]) / max(pa[k][1], 1) for k in pa)
+    assert d < 2e-4, d
+    assert [t for t, _ in ga] == [t for t, _ in gb]
+
+
+def _scores_by_path(ex):
+    """token path -> (score, depth) of every scored slot of an export."""
+    out, memo = {}, {0: ()}
+
+    def path(s):
+        if s not in memo:
+            memo[s] = path(int(ex["parent"][s])) + (int(ex["token"][s]),)
+        return memo[s]
+
+    for s in range(1, len(ex["parent"])):
+        if ex["parent"][s] >= 0 and ex["state"][s] & 2:
+            out[path(s)] = (float(ex["cum"][s]), int(ex["depth"][s]))
+    return out
+
+
+@pytest.mark.gpu
+def test_fused_lmhead_1b_shapes():
+    """Llama-3.2-1B LM-head shapes (K = 2048 / 4096, N = 128256 = 501 x 256 tiles) through the
+    fused kernel vs cuBLAS, on ragged row counts."""
+    from paper_2603_14002_b200 import LlamaScorer
+
+    w, cfg = _world_cfg(r=10, k=8)
+    raws = synth.make_logits(2, 60, 41, base_seed=3)
+    res = []
+    for mode in ("cublas", "fused"):
+        sc = LlamaScorer("llama-3.2-1b", seed=2, lm_head=mode)
+        _, got, sess = _decode_with_session(sc, raws, cfg, w)
+        ex = sess.export()
+        res.append(ex)
+        del sc
+    pa, pb = _scores_by_path(res[0]), _scores_by_path(res[1])
+    assert pa.keys() == pb.keys()
+    assert max(abs(pa[k][0] - pb[k][0]) for k in pa) < 1e-3
