@@ -305,6 +305,12 @@ int lb_llm_lse(lb_llm* l, const void* logits, int32_t M, int64_t ld, const int32
  * partial: device scratch of M * ceil(N / 256) float2. */
 int lb_llm_lmhead_lse(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t K, const void* emb,
                       int64_t lde, int32_t N, const int32_t* slots, void* partial);
+/* Gate/up projection with the SwiGLU fused into the tcgen05 epilogue: act = silu(h W_g^T) *
+ * (h W_u^T) for h[M][K] bf16 (pitch ldh), weights interleaved in 128-row blocks
+ * [g 0:128 | u 0:128 | g 128:256 | u 128:256 | ...] ([2 ffn][K], pitch ldw); act bf16 [M][ffn]
+ * ([M][2 ffn] hi|lo pairs in bf16x2 precision).  ffn % 128 == 0. */
+int lb_llm_gateup_swiglu(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t K,
+                         const void* wgu_interleaved, int64_t ldw, int32_t ffn, void* act);
 /* out[8]: slots, events, waves, forwarded rows, widest wave, device bytes, scores computed
  * (next-token log-probs), 0 */
 int lb_llm_stats(lb_llm* l, int64_t* out);

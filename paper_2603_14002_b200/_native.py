@@ -179,6 +179,7 @@ _SIGS = {
     "lb_llm_swiglu": (C.c_int, [_P, _P, _I32, _I32, _P]),
     "lb_llm_lse": (C.c_int, [_P, _P, _I32, _I64, _P]),
     "lb_llm_lmhead_lse": (C.c_int, [_P, _P, _I32, _I64, _I32, _P, _I64, _I32, _P, _P]),
+    "lb_llm_gateup_swiglu": (C.c_int, [_P, _P, _I32, _I64, _I32, _P, _I64, _I32, _P]),
     "lb_llm_stats": (C.c_int, [_P, _P]),
     "lb_llm_export": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
 }

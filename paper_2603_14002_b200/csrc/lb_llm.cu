@@ -1225,13 +1225,27 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                         // layout: SWIZZLE_128B
   return d;
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 // instruction descriptor: D f32, A/B bf16, K-major both, N = 256, M = 128
 constexpr uint32_t LM_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
                               ((uint32_t)(LM_BM >> 4) << 24);
 
+// EPI 0: per-row (max, sum exp) partials of each 256-column slice (LM head, K6).
+// EPI 1: SwiGLU -- B rows are interleaved so tile n holds gate columns [n*128, +128) followed by
+//        the matching up columns; the epilogue writes act = silu(gate) * up (bf16, or hi|lo
+//        pairs when split) for its 128 output columns: the gate/up product never reaches HBM.
+constexpr int EPI_LSE = 0, EPI_SWIGLU = 1;
+
+template <int EPI>
 __global__ void __launch_bounds__(LM_THREADS, 1)
-    lmhead_lse_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      int M, int N, int K, int MT, int NT, float2* partial) {
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, int MT, int NT, void* out, int64_t ld_out, int F, int split) {
   extern __shared__ __align__(1024) unsigned char lm_smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(lm_smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -1330,8 +1344,46 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       const int m0 = (t % MT) * LM_BM, n = t / MT, n0 = n * LM_BN;
       mbar_wait(&tfull[acc], aphase);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      float mrun = -INFINITY, srun = 0.f;
       const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * LM_BN);
+      const int row = m0 + q * 32 + lane;
+      if constexpr (EPI == EPI_SWIGLU) {
+        bf16* orow = reinterpret_cast<bf16*>(out) + (size_t)row * ld_out + (size_t)n * (LM_BN / 2);
+#pragma unroll 1
+        for (int c0 = 0; c0 < LM_BN / 2; c0 += 16) {
+          uint32_t g[16], u[16];
+          tmem_ld16(base + (uint32_t)c0, g);
+          tmem_ld16(base + (uint32_t)(LM_BN / 2 + c0), u);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          uint4 hv[2], lv[2];
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hv);
+          __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float g0 = __uint_as_float(g[2 * e]), g1 = __uint_as_float(g[2 * e + 1]);
+            const float a = g0 / (1.f + __expf(-g0)) * __uint_as_float(u[2 * e]);
+            const float b = g1 / (1.f + __expf(-g1)) * __uint_as_float(u[2 * e + 1]);
+            h2[e] = __floats2bfloat162_rn(a, b);
+            const float2 hf = __bfloat1622float2(h2[e]);
+            l2[e] = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+          }
+          if (row < M && n * (LM_BN / 2) + c0 < F) {
+            reinterpret_cast<uint4*>(orow + c0)[0] = hv[0];
+            reinterpret_cast<uint4*>(orow + c0)[1] = hv[1];
+            if (split) {
+              reinterpret_cast<uint4*>(orow + F + c0)[0] = lv[0];
+              reinterpret_cast<uint4*>(orow + F + c0)[1] = lv[1];
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        mbar_arrive(&tempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+        continue;
+      }
+      float mrun = -INFINITY, srun = 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < LM_BN; c0 += 32) {
         uint32_t v[32];
@@ -1362,8 +1414,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       mbar_arrive(&tempty[acc]);
-      const int row = m0 + q * 32 + lane;
-      if (row < M) partial[(size_t)row * NT + n] = make_float2(mrun, srun);
+      if (row < M) reinterpret_cast<float2*>(out)[(size_t)row * NT + n] = make_float2(mrun, srun);
       if (++acc == 2) {
         acc = 0;
         aphase ^= 1;
@@ -1813,17 +1864,46 @@ int lb_llm_lmhead_lse(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t 
   const int MT = (M + LM_BM - 1) / LM_BM, NT = (N + LM_BN - 1) / LM_BN;
   static int attr = 0;
   if (!attr) {
-    CKL(cudaFuncSetAttribute(lmhead_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LM_SMEM));
+    CKL(cudaFuncSetAttribute(tc_gemm_kernel<EPI_LSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, LM_SMEM));
     attr = 1;
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, l->b->m->device);
   const int grid = std::min(MT * NT, nsm);
   cudaStream_t st = l->b->st;
-  LAUNCH(lmhead_lse_kernel<<<grid, LM_THREADS, LM_SMEM, st>>>(ma, mb, M, N, K, MT, NT,
-                                                               reinterpret_cast<float2*>(partial)));
+  LAUNCH(tc_gemm_kernel<EPI_LSE><<<grid, LM_THREADS, LM_SMEM, st>>>(ma, mb, M, N, K, MT, NT, partial,
+                                                                     0, 0, 0));
   LAUNCH(lse_reduce_kernel<<<M, 128, 0, st>>>(reinterpret_cast<const float2*>(partial), NT, slots,
                                                l->dev.s_lse));
+  return LB_OK;
+}
+
+int lb_llm_gateup_swiglu(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t K,
+                         const void* wgu_interleaved, int64_t ldw, int32_t ffn, void* act) {
+  if (!l || !h || !wgu_interleaved || !act) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (K % LM_BK != 0) return lbh::set_error(LB_ERR_ARG, "K must be a multiple of 64");
+  if (ffn % (LM_BN / 2) != 0) return lbh::set_error(LB_ERR_ARG, "ffn must be a multiple of 128");
+  if ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(wgu_interleaved) |
+       reinterpret_cast<uintptr_t>(act)) & 15)
+    return lbh::set_error(LB_ERR_ARG, "operands must be 16-byte aligned");
+  if (M <= 0) return LB_OK;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, h, M, K, ldh, LM_BM);
+  if (rc) return rc;
+  rc = make_map(&mb, wgu_interleaved, 2 * (int64_t)ffn, K, ldw, LM_BN);
+  if (rc) return rc;
+  const int MT = (M + LM_BM - 1) / LM_BM, NT = 2 * ffn / LM_BN;
+  static int attr = 0;
+  if (!attr) {
+    CKL(cudaFuncSetAttribute(tc_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, LM_SMEM));
+    attr = 1;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, l->b->m->device);
+  const int grid = std::min(MT * NT, nsm);
+  const int split = l->dev.split;
+  LAUNCH(tc_gemm_kernel<EPI_SWIGLU><<<grid, LM_THREADS, LM_SMEM, l->b->st>>>(
+      ma, mb, M, 2 * ffn, K, MT, NT, act, (int64_t)ffn * (split ? 2 : 1), ffn, split));
   return LB_OK;
 }
 

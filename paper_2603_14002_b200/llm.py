@@ -287,7 +287,7 @@ class LlamaScorer:
 
     def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
                  max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 2048,
-                 precision: str = "bf16x2", lm_head: str = "fused"):
+                 precision: str = "bf16x2", lm_head: str = "fused", fused_swiglu: bool = False):
         """precision: "bf16x2" (default) feeds every body GEMM the activation as a hi+lo pair of
         bf16 values against duplicated bf16 weights -- fp32-equivalent activations on the bf16
         tensor cores, scores within ~1e-3 of an fp32 forward even for 40-token texts -- and keeps
@@ -316,9 +316,18 @@ class LlamaScorer:
         self.lm_head = lm_head
         self.precision = precision
         self.split = precision == "bf16x2"
+        # gate/up rows interleaved in 128-row blocks for the tcgen05 GEMM with the SwiGLU epilogue
+        # (opt-in: measured 91 ms vs 70 ms for cuBLAS + the SwiGLU kernel per config-3 step in
+        # bf16x2 -- the 128x256 tile loses to cuBLAS's shape choice on these row counts)
+        self.fused_swiglu = fused_swiglu and self.cfg.arch == "llama" and self.cfg.ffn % 128 == 0
+        if self.fused_swiglu:
+            F, H = self.cfg.ffn, self.cfg.hidden
+            for L in self.weights.layers:
+                g, u = L["wgu"][:F].view(F // 128, 128, H), L["wgu"][F:].view(F // 128, 128, H)
+                L["wgui"] = torch.stack([g, u], 1).reshape(2 * F, H).contiguous()
         if self.split:  # [W | W]: one GEMM computes hi @ W^T + lo @ W^T with fp32 accumulation
             for L in self.weights.layers:
-                for k in ("wqkv", "wo", "wgu", "wfc", "wd"):
+                for k in ("wqkv", "wo", "wgu", "wgui", "wfc", "wd"):
                     if k in L:
                         L[k + "2"] = torch.cat([L[k], L[k]], 1).contiguous()
             self.emb2 = torch.cat([self.weights.emb, self.weights.emb], 1).contiguous()
@@ -690,9 +699,14 @@ class DeviceLlmSession:
             N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), o.data_ptr(), L["ln2"].data_ptr(), eps, n,
                                        hn.data_ptr(), None))
             del o
-            gu = torch.mm(hn, L["wgu" + sfx].t(), out_dtype=f32) if sfx else torch.mm(hn, L["wgu"].t())
-            N.check(lib.lb_llm_swiglu(self.h, gu.data_ptr(), n, cfg.ffn, act.data_ptr()))
-            del gu
+            if self.scorer.fused_swiglu:  # gate/up GEMM + SwiGLU in one tcgen05 kernel
+                wi = L["wgui" + sfx]
+                N.check(lib.lb_llm_gateup_swiglu(self.h, hn.data_ptr(), n, hn.stride(0), wi.shape[1],
+                                                 wi.data_ptr(), wi.stride(0), cfg.ffn, act.data_ptr()))
+            else:
+                gu = torch.mm(hn, L["wgu" + sfx].t(), out_dtype=f32) if sfx else torch.mm(hn, L["wgu"].t())
+                N.check(lib.lb_llm_swiglu(self.h, gu.data_ptr(), n, cfg.ffn, act.data_ptr()))
+                del gu
             dn = torch.mm(act, L["wd" + sfx].t(), out_dtype=f32)
             last = li + 1 == cfg.layers
             wnext = W.norm if last else W.layers[li + 1]["ln1"]

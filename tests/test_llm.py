@@ -377,7 +377,7 @@ def test_fused_lmhead_lse_matches_cublas_path(precision):
     w, cfg = _world_cfg()
     raws = synth.make_logits(3, 100, 41, base_seed=41)
     outs = []
-    for mode in ("cublas", "fused"):
+    for mode in ("cublas", "fused"):  # fused: tcgen05 LM head + LSE
         sc = LlamaScorer("tiny", seed=6, precision=precision, lm_head=mode)
         _, got, sess = _decode_with_session(sc, raws, cfg, w)
         outs.append((sess.export(), [(g.text, g.score) for g in got]))
@@ -422,3 +422,29 @@ def test_fused_lmhead_1b_shapes():
     pa, pb = _scores_by_path(res[0]), _scores_by_path(res[1])
     assert pa.keys() == pb.keys()
     assert max(abs(pa[k][0] - pb[k][0]) for k in pa) < 1e-3
+
+
+@pytest.mark.gpu
+def test_fused_gateup_swiglu_vs_oracle():
+    """Opt-in tcgen05 gate/up GEMM with the SwiGLU epilogue (bf16x2): replay parity and scores
+    within the north-star tolerance of the fp32 oracle."""
+    from paper_2603_14002_b200 import LlamaScorer, ReplayScorer
+
+    sc = LlamaScorer("tiny", seed=6, fused_swiglu=True)
+    assert sc.fused_swiglu
+    w, cfg = _world_cfg()
+    raws = synth.make_logits(3, 100, 41, base_seed=43)
+    ds, got, sess = _decode_with_session(sc, raws, cfg, w)
+    replay = ReplayScorer(sess.replay_table())
+    for i, d in enumerate(ds):
+        want = O.decode(d, cfg, w.table, w.model, replay)
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest)
+    oracle = LO.OracleLlmScorer(sc.cfg, sc.weights.hf_state_dict())
+    first = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._cap)}
+    mid = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._low)}
+    paths = _scores_by_path(sess.export())
+    errs = []
+    for path, (score, _) in list(paths.items())[:120]:
+        text = " ".join([first[path[0]]] + [mid[t] for t in path[1:]])
+        errs.append(abs(oracle.score(text) - score))
+    assert max(errs) <= TOL, max(errs)
