@@ -448,3 +448,38 @@ def test_fused_gateup_swiglu_vs_oracle():
         text = " ".join([first[path[0]]] + [mid[t] for t in path[1:]])
         errs.append(abs(oracle.score(text) - score))
     assert max(errs) <= TOL, max(errs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("final_only", [False, True])
+def test_llm_ragged_batch_replay_parity(tiny_scorer, final_only):
+    """Utterances of different lengths in one device batch: interval events skip finished
+    utterances (decoder.py:428 fires only for t < T_i), results bit-exact per utterance."""
+    from paper_2603_14002_b200 import ReplayScorer, decode_batch
+
+    w, cfg = _world_cfg(r=15)
+    lens = [31, 140, 15, 77, 200, 16, 90]
+    ds = [O.log_softmax_scaled(synth.make_logits(1, T, 41, base_seed=500 + T)[0], cfg.acoustic_scale)
+          for T in lens]
+    got = decode_batch(ds, cfg, w.table, w.model, tiny_scorer, final_llm_only=final_only)
+    from paper_2603_14002_b200.decoder import device_model
+
+    sess = device_model(w.table, w.model).batch(cfg, len(ds), max(lens))._llm_session
+    replay = ReplayScorer(sess.replay_table())
+    for d, g in zip(ds, got):
+        want = O.decode(d, cfg, w.table, w.model, replay, final_llm_only=final_only)
+        assert not isinstance(g, Exception), g
+        assert (g.text, g.score, g.nbest, g.llm_events, g.frame_count) == (
+            want.text, want.score, want.nbest, want.llm_events, want.frame_count)
+
+
+@pytest.mark.gpu
+def test_llm_capacity_error_is_loud():
+    """A prefix cache too small for the batch raises DeviceError (capacity), never a wrong result."""
+    from paper_2603_14002_b200 import DeviceError, LlamaScorer, decode_batch
+
+    sc = LlamaScorer("tiny", seed=1, max_slots=8)
+    w, cfg = _world_cfg()
+    ds = [O.log_softmax_scaled(x, cfg.acoustic_scale) for x in synth.make_logits(2, 120, 41, base_seed=8)]
+    with pytest.raises(DeviceError, match="prefix cache full"):
+        decode_batch(ds, cfg, w.table, w.model, sc)
