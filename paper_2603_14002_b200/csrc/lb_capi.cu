@@ -11,6 +11,7 @@
 #include <string>
 #include <string_view>
 #include <thread>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
@@ -383,6 +384,9 @@ int lb_batch_destroy(lb_batch* b) {
                   d.phase_cycles};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  void* hptrs[] = {b->h_beam, b->h_punct, b->h_woff, b->h_tot, b->h_words, b->h_misc, b->h_sc};
+  for (void* p : hptrs)
+    if (p) cudaFreeHost(p);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
   delete b;
@@ -670,25 +674,67 @@ int lb_batch_dump_frame(lb_batch* b, int32_t trial, int32_t t, int32_t* k, doubl
 }
 
 // ------------------------------------------------------------------ results (host assembly)
+extern "C++" {
+// Pinned host staging for the result gather (D2H at full link speed, reused across calls).
+template <typename T>
+static int pinned_reserve(T*& p, int64_t& cap, int64_t n) {
+  if (n <= cap) return LB_OK;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  const int64_t c = std::max<int64_t>(n, 2 * cap);
+  if (cudaHostAlloc(reinterpret_cast<void**>(&p), (size_t)std::max<int64_t>(c, 1) * sizeof(T),
+                    cudaHostAllocDefault) != cudaSuccess)
+    return fail(LB_ERR_CUDA, "cudaHostAlloc failed for result staging");
+  cap = c;
+  return LB_OK;
+}
+
+// Text of an entry = " ".join(surfaces) + punct.  When every surface is non-empty, unique, free
+// of ' ' and does not end in ".?!", (word ids, punct) -> text is injective, so the n-best text
+// dedupe (decoder.py:444-449) can compare word-id sequences and build strings only for the
+// entries that survive.
+static bool texts_injective(const lb_model* m) {
+  for (const auto& x : m->surfaces) {
+    if (x.empty() || x.find(' ') != std::string::npos) return false;
+    const char last = x.back();
+    if (last == '.' || last == '?' || last == '!') return false;
+  }
+  return true;
+}
+
+}  // extern "C++"
+
 int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest) {
   if (!b || b->n_trials < 1) return fail(LB_ERR_STATE, "no trials loaded");
   int rc = lb_batch_gather_entries(b, nullptr, nullptr);
   if (rc) return rc;
   const int B = b->n_trials;
   const int64_t ne = b->n_entries, nw = b->n_words;
-  std::vector<int32_t> e_beam(ne), words(nw), puncts(ne), nbeam(B), status(B);
-  std::vector<int64_t> woff(ne + 1);
-  std::vector<double> totals(ne), scores((size_t)B * b->K);
-  rc = lb_batch_copy_entries(b, nullptr, e_beam.data(), woff.data(), words.data(), totals.data(),
-                             puncts.data());
+  rc = pinned_reserve(b->h_beam, b->hcap_e1, ne);
+  if (!rc) rc = pinned_reserve(b->h_punct, b->hcap_e2, ne);
+  if (!rc) rc = pinned_reserve(b->h_woff, b->hcap_e3, ne + 1);
+  if (!rc) rc = pinned_reserve(b->h_tot, b->hcap_e4, ne);
+  if (!rc) rc = pinned_reserve(b->h_words, b->hcap_w, nw);
+  if (!rc) rc = pinned_reserve(b->h_misc, b->hcap_m, 2 * (int64_t)B);
+  if (!rc) rc = pinned_reserve(b->h_sc, b->hcap_s, (int64_t)B * b->K);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(nbeam.data(), b->dev.nbeam, B * 4, cudaMemcpyDeviceToHost, b->st));
-  CK(cudaMemcpyAsync(status.data(), b->dev.status, B * 4, cudaMemcpyDeviceToHost, b->st));
-  CK(cudaMemcpyAsync(scores.data(), b->dev.score, scores.size() * 8, cudaMemcpyDeviceToHost, b->st));
-  CK(cudaStreamSynchronize(b->st));
+  int32_t* e_beam = b->h_beam;
+  int32_t* puncts = b->h_punct;
+  int64_t* woff = b->h_woff;
+  double* totals = b->h_tot;
+  int32_t* words = b->h_words;
+  int32_t* nbeam = b->h_misc;
+  int32_t* status = b->h_misc + B;
+  double* scores = b->h_sc;
+  CK(cudaMemcpyAsync(nbeam, b->dev.nbeam, B * 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(status, b->dev.status, B * 4, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(scores, b->dev.score, (size_t)B * b->K * 8, cudaMemcpyDeviceToHost, b->st));
+  rc = lb_batch_copy_entries(b, nullptr, e_beam, woff, words, totals, puncts);  // synchronises
+  if (rc) return rc;
   static const char* PUN[4] = {"", ".", "?", "!"};
   const auto& surf = b->m->surfaces;
-  // per-trial assembly (decoder.py:433-460), trials spread over host threads
+  if (b->injective < 0) b->injective = texts_injective(b->m) ? 1 : 0;
+  const bool fast = b->injective == 1;
   struct TrialOut {
     std::string best;
     double best_score = 0.0;
@@ -696,6 +742,24 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
     std::vector<double> scores;
   };
   std::vector<TrialOut> outs(B);
+  auto text_of = [&](int64_t e) {
+    std::string s2;
+    size_t len = 1;
+    for (int64_t w = woff[e]; w < woff[e + 1]; ++w) len += surf[words[w]].size() + 1;
+    s2.reserve(len);
+    for (int64_t w = woff[e]; w < woff[e + 1]; ++w) {
+      if (w > woff[e]) s2.push_back(' ');
+      s2 += surf[words[w]];
+    }
+    s2 += PUN[puncts[e] & 3];
+    return s2;
+  };
+  auto same_words = [&](int64_t x, int64_t y) {
+    if ((puncts[x] & 3) != (puncts[y] & 3)) return false;
+    const int64_t nx = woff[x + 1] - woff[x];
+    if (nx != woff[y + 1] - woff[y]) return false;
+    return std::memcmp(words + woff[x], words + woff[y], (size_t)nx * 4) == 0;
+  };
   auto assemble = [&](int t) {
     if (status[t] != 0) return;
     TrialOut& to = outs[t];
@@ -706,42 +770,52 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
     first[K] = e1;
     for (int i = K - 1; i >= 0; --i)
       if (first[i] > first[i + 1]) first[i] = first[i + 1];
-    std::vector<std::string> texts(e1 - e0);
-    for (int64_t e = e0; e < e1; ++e) {
-      std::string& s2 = texts[e - e0];
-      size_t len = 1;
-      for (int64_t w = woff[e]; w < woff[e + 1]; ++w) len += surf[words[w]].size() + 1;
-      s2.reserve(len);
-      for (int64_t w = woff[e]; w < woff[e + 1]; ++w) {
-        if (w > woff[e]) s2.push_back(' ');
-        s2 += surf[words[w]];
-      }
-      s2 += PUN[puncts[e] & 3];
-    }
-    const double* sc = scores.data() + (size_t)t * b->K;
+    const double* sc = scores + (size_t)t * b->K;
     std::vector<int> order(K);
     for (int i = 0; i < K; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sc[x] > sc[y]; });
     struct Pair {
-      int text;
+      int64_t e;
       double score;
     };
     std::vector<Pair> pairs;
     pairs.reserve(e1 - e0);
     for (int i : order) {
       const double best_lm = totals[first[i]];
-      for (int64_t e = first[i]; e < first[i + 1]; ++e)
-        pairs.push_back({(int)(e - e0), (sc[i] - best_lm) + totals[e]});
+      for (int64_t e = first[i]; e < first[i + 1]; ++e) pairs.push_back({e, (sc[i] - best_lm) + totals[e]});
     }
     std::stable_sort(pairs.begin(), pairs.end(),
                      [](const Pair& x, const Pair& y) { return x.score > y.score; });
-    const int best = order[0];
-    to.best = texts[first[best] - e0];
-    to.best_score = sc[best];
+    to.best_score = sc[order[0]];
+    if (fast) {
+      // dedupe on (word ids, punct): FNV hash buckets, exact comparison on hash match
+      std::unordered_map<uint64_t, std::vector<int64_t>> seen;
+      seen.reserve(pairs.size() * 2);
+      for (const Pair& pr : pairs) {
+        uint64_t h = 0xCBF29CE484222325ull ^ (uint64_t)(puncts[pr.e] & 3);
+        for (int64_t w = woff[pr.e]; w < woff[pr.e + 1]; ++w) h = (h ^ (uint32_t)words[w]) * 0x100000001B3ull;
+        auto& bucket = seen[h];
+        bool dup = false;
+        for (int64_t o : bucket)
+          if (same_words(o, pr.e)) {
+            dup = true;
+            break;
+          }
+        if (dup) continue;
+        bucket.push_back(pr.e);
+        to.texts.push_back(text_of(pr.e));
+        to.scores.push_back(pr.score);
+      }
+      to.best = text_of(first[order[0]]);
+      return;
+    }
+    std::vector<std::string> texts(e1 - e0);
+    for (int64_t e = e0; e < e1; ++e) texts[e - e0] = text_of(e);
+    to.best = texts[first[order[0]] - e0];
     std::unordered_set<std::string_view> seen;
     seen.reserve(pairs.size() * 2);
     for (const Pair& pr : pairs) {
-      const std::string& tx = texts[pr.text];
+      const std::string& tx = texts[pr.e - e0];
       if (!seen.insert(std::string_view(tx)).second) continue;
       to.texts.push_back(tx);
       to.scores.push_back(pr.score);
@@ -759,6 +833,8 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
       });
     for (auto& th : pool) th.join();
   }
+  // blob: per successful trial its best text then its n-best texts, each followed by a NUL
+  // (offsets/lengths exclude the separators; the NULs let a caller split the blob in one call)
   b->blob.clear();
   b->best_off.assign(B, 0);
   b->best_len.assign(B, 0);
@@ -767,23 +843,29 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
   b->nb_off.clear();
   b->nb_len.clear();
   b->nb_score.clear();
-  size_t total = 0;
+  size_t total = 0, nn = 0;
   for (int t = 0; t < B; ++t) {
-    total += outs[t].best.size();
-    for (const auto& x : outs[t].texts) total += x.size();
+    total += outs[t].best.size() + 1;
+    for (const auto& x : outs[t].texts) total += x.size() + 1;
+    nn += outs[t].texts.size();
   }
   b->blob.reserve(total);
+  b->nb_off.reserve(nn);
+  b->nb_len.reserve(nn);
+  b->nb_score.reserve(nn);
   for (int t = 0; t < B; ++t) {
     if (status[t] != 0) continue;
     TrialOut& to = outs[t];
     b->best_off[t] = (int64_t)b->blob.size();
     b->blob += to.best;
+    b->blob.push_back('\0');
     b->best_len[t] = (int32_t)to.best.size();
     b->best_score[t] = to.best_score;
     b->nb_count[t] = (int32_t)to.texts.size();
     for (size_t i = 0; i < to.texts.size(); ++i) {
       b->nb_off.push_back((int64_t)b->blob.size());
       b->blob += to.texts[i];
+      b->blob.push_back('\0');
       b->nb_len.push_back((int32_t)to.texts[i].size());
       b->nb_score.push_back(to.scores[i]);
     }

@@ -57,6 +57,16 @@ struct lb_batch {
   std::vector<int64_t> best_off, nb_off;
   std::vector<int32_t> best_len, nb_count, nb_len;
   std::vector<double> best_score, nb_score;
+  // pinned result staging (lb_batch_results_size)
+  int32_t* h_beam = nullptr;
+  int32_t* h_punct = nullptr;
+  int64_t* h_woff = nullptr;
+  double* h_tot = nullptr;
+  int32_t* h_words = nullptr;
+  int32_t* h_misc = nullptr;
+  double* h_sc = nullptr;
+  int64_t hcap_e1 = 0, hcap_e2 = 0, hcap_e3 = 0, hcap_e4 = 0, hcap_w = 0, hcap_m = 0, hcap_s = 0;
+  int injective = -1;  // texts_injective(m), computed on first use
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   unsigned long long launch_mark = 0;

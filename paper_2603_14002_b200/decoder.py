@@ -340,28 +340,34 @@ class DeviceBatch:
         nsc = np.empty(m, dtype=np.float64)
         N.check(lib.lb_batch_results(self.h, blob, N.ptr(boff), N.ptr(blen), N.ptr(bsc),
                                      N.ptr(cnt), N.ptr(noff), N.ptr(nlen), N.ptr(nsc)))
+        # the blob holds, per successful trial, its best text and then its n-best texts, each
+        # NUL-terminated: one split() builds every Python string
         raw = blob.raw[: nbytes.value]
+        parts = raw.decode("utf-8").split("\x00")
         st, _ = self.status()
-        text_all = raw.decode("utf-8")
-        ascii_only = len(text_all) == len(raw)
-        boff_l, blen_l, bsc_l, cnt_l = boff.tolist(), blen.tolist(), bsc.tolist(), cnt.tolist()
-        noff_l, nlen_l, nsc_l = noff.tolist(), nlen.tolist(), nsc.tolist()
+        bsc_l, cnt_l, nsc_l = bsc.tolist(), cnt.tolist(), nsc.tolist()
+        if len(parts) != sum(cnt_l[i] + 1 for i in range(n) if st[i] == 0) + 1:
+            # a surface contains NUL: rebuild the texts from the offsets instead
+            parts = []
+            noff_l, nlen_l, boff_l, blen_l = noff.tolist(), nlen.tolist(), boff.tolist(), blen.tolist()
+            j = 0
+            for i in range(n):
+                if st[i] != 0:
+                    continue
+                parts.append(raw[boff_l[i]: boff_l[i] + blen_l[i]].decode("utf-8"))
+                for q in range(j, j + cnt_l[i]):
+                    parts.append(raw[noff_l[q]: noff_l[q] + nlen_l[q]].decode("utf-8"))
+                j += cnt_l[i]
         out = []
-        k = 0
+        k = j = 0
         for i in range(n):
             if st[i] != 0:
                 out.append(None)
                 continue
-            if ascii_only:
-                text = text_all[boff_l[i]: boff_l[i] + blen_l[i]]
-                nb = [(text_all[noff_l[j]: noff_l[j] + nlen_l[j]], nsc_l[j])
-                      for j in range(k, k + cnt_l[i])]
-            else:
-                text = raw[boff_l[i]: boff_l[i] + blen_l[i]].decode("utf-8")
-                nb = [(raw[noff_l[j]: noff_l[j] + nlen_l[j]].decode("utf-8"), nsc_l[j])
-                      for j in range(k, k + cnt_l[i])]
-            k += cnt_l[i]
-            out.append((text, bsc_l[i], nb))
+            c = cnt_l[i]
+            out.append((parts[k], bsc_l[i], list(zip(parts[k + 1: k + 1 + c], nsc_l[j: j + c]))))
+            k += c + 1
+            j += c
         return out
 
 
