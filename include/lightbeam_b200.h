@@ -204,6 +204,10 @@ int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* b
                      double* best_score, int32_t* nbest_count, int64_t* nbest_text_off,
                      int32_t* nbest_text_len, double* nbest_score);
 
+/* A non-blocking CUDA stream for lb_batch_create (pipelining batches on separate streams). */
+int lb_stream_create(int32_t device, void** out);
+int lb_stream_destroy(void* stream);
+
 /* Page-locked host memory (cudaHostAlloc) for input staging: H2D copies from it run at full
  * link speed and stay asynchronous. */
 int lb_host_alloc(int64_t bytes, void** out);

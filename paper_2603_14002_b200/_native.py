@@ -160,6 +160,8 @@ _SIGS = {
     "lb_batch_mark_begin": (C.c_int, [_P]),
     "lb_batch_mark_end": (C.c_int, [_P, _P, _P]),
     "lb_batch_sync": (C.c_int, [_P]),
+    "lb_stream_create": (C.c_int, [_I32, _P]),
+    "lb_stream_destroy": (C.c_int, [_P]),
     "lb_host_alloc": (C.c_int, [_I64, _P]),
     "lb_host_free": (C.c_int, [_P]),
     "lb_log_softmax_host": (C.c_int, [_P, _I64, _I32, _D, _P, _I32]),

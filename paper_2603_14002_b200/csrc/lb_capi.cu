@@ -896,6 +896,20 @@ int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* b
   return LB_OK;
 }
 
+int lb_stream_create(int32_t device, void** out) {
+  if (!out) return fail(LB_ERR_ARG, "null argument");
+  CK(cudaSetDevice(device));
+  cudaStream_t st = nullptr;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  *out = st;
+  return LB_OK;
+}
+
+int lb_stream_destroy(void* stream) {
+  if (stream) cudaStreamDestroy(reinterpret_cast<cudaStream_t>(stream));
+  return LB_OK;
+}
+
 int lb_host_alloc(int64_t bytes, void** out) {
   if (!out || bytes < 0) return fail(LB_ERR_ARG, "bad arguments");
   CK(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocPortable));

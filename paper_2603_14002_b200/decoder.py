@@ -106,6 +106,25 @@ class DeviceModel:
         self._batches[key] = got  # most recently used last
         return got
 
+    def pipeline_batch(self, cfg, slot: int, n_trials: int, n_frames: int) -> "DeviceBatch":
+        """One of the two DeviceBatch objects `decode_stream_raw` alternates between, each on its
+        own CUDA stream."""
+        key = (slot, cfg)
+        pipe = self.__dict__.setdefault("_pipe", {})
+        got = pipe.get(slot)
+        if got is not None and (got[0] != key or got[1].max_trials < n_trials
+                                or got[1].max_frames < n_frames):
+            got[1].destroy()
+            got = None
+        if got is None:
+            st = C.c_void_p()
+            N.check(N.lib().lb_stream_create(self.device, C.byref(st)))
+            b = DeviceBatch(self, cfg, max(n_trials, 1), max(n_frames, 1), stream=st.value)
+            b._own_stream = st
+            got = (key, b)
+            pipe[slot] = got
+        return got[1]
+
     def score_words(self, hist: list, words: list):
         """Device score_word for (history word ids, LM word id) pairs -- parity helper."""
         n = len(words)
@@ -181,6 +200,10 @@ class DeviceBatch:
         if getattr(self, "h", None):
             N.lib(False).lb_batch_destroy(self.h)
             self.h = None
+        st = getattr(self, "_own_stream", None)
+        if st is not None and st.value:
+            N.lib(False).lb_stream_destroy(st)
+            self._own_stream = None
 
     # ---- inputs
     def _frames(self, frames) -> np.ndarray:
@@ -504,6 +527,39 @@ def decode_batch_raw(raws, config, tt, lm, scorer, final_llm_only: bool = False,
     batch.load_logits(arr, frames)
     run_search(batch, cfg, scorer, model, final_llm_only)
     return _collect(batch, cfg, final_llm_only, time.perf_counter() - t0)
+
+
+def _raw_array(raws):
+    if isinstance(raws, tuple):
+        return np.asarray(raws[0], dtype=np.float32), np.asarray(raws[1], dtype=np.int32)
+    return _stack([np.asarray(getattr(r, "frames", r), dtype=np.float32) for r in raws], np.float32)
+
+
+def decode_stream_raw(batches, config, tt, lm, scorer, final_llm_only: bool = False,
+                      device: int = 0):
+    """Generator over many batches of raw logits (each a RawLogits list or `(array, frames)`):
+    yields each batch's list of DecodeResult / exception, in order.  Two device batches on two
+    CUDA streams alternate, so batch i+1's H2D copy and search run on the GPU while the host
+    assembles batch i's transcripts and n-best lists (with pinned host inputs the launches are
+    asynchronous).  Results are identical to `decode_batch_raw` per batch."""
+    cfg, model, dm = _prepare(config, tt, lm, device)
+    pending: list = []
+    slot = 0
+    for raws in batches:
+        arr, frames = _raw_array(raws)
+        if arr.ndim != 3 or arr.shape[2] != dm.vocab_size:
+            raise ShapeError(f"logit width must equal the table vocabulary ({dm.vocab_size})")
+        batch = dm.pipeline_batch(cfg, slot, arr.shape[0], max(arr.shape[1], 1))
+        t0 = time.perf_counter()
+        batch.load_logits(arr, frames)
+        run_search(batch, cfg, scorer, model, final_llm_only)
+        pending.append((batch, t0))
+        slot ^= 1
+        if len(pending) == 2:
+            b, t = pending.pop(0)
+            yield _collect(b, cfg, final_llm_only, time.perf_counter() - t)
+    for b, t in pending:
+        yield _collect(b, cfg, final_llm_only, time.perf_counter() - t)
 
 
 def decode(d, config, tt, lm, scorer, final_llm_only: bool = False) -> DecodeResult:

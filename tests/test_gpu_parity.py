@@ -223,3 +223,25 @@ def test_single_decode_api_and_errors():
         decode(bad, cfg1, tt, model, StubScorer(table={}))
     except EmptyBeamError:
         pass
+
+
+def test_decode_stream_raw_matches_batch_api():
+    """The two-stream pipelined API returns exactly decode_batch_raw's results, batch by batch
+    (ragged sizes, device n-gram scorer and a host stub scorer)."""
+    from paper_2603_14002_b200 import decode_stream_raw
+    from paper_2603_14002_b200._native import pinned_empty
+
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=16, llm_rescore_interval=20)
+    scale = cfg.ngram_weight / cfg.llm_weight
+    batches = []
+    for i, (n, T) in enumerate([(5, 90), (3, 140), (6, 60), (2, 110)]):
+        x = pinned_empty((n, T, 41), np.float32)
+        x[...] = synth.make_logits(n, T, 41, base_seed=900 + 10 * i)
+        batches.append((x, np.full(n, T, np.int32)))
+    for sc in (DeviceNgramScorer(w.model, scale), StubScorer(table={})):
+        want = [decode_batch_raw(b, cfg, w.table, w.model, sc) for b in batches]
+        got = list(decode_stream_raw(iter(batches), cfg, w.table, w.model, sc))
+        assert len(got) == len(want)
+        for gb, wb in zip(got, want):
+            assert [(r.text, r.score, r.nbest) for r in gb] == [(r.text, r.score, r.nbest) for r in wb]
