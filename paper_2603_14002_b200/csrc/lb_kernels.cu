@@ -2150,8 +2150,11 @@ __global__ void __launch_bounds__(small::NT, 2)
 // =====================================================================================
 // K3: end-of-utterance closure (decoder.py:375-405), one CTA per trial, warp per beam
 // =====================================================================================
-__global__ void __launch_bounds__(256) close_kernel(ModelDev m, CfgDev c, BatchDev b) {
-  constexpr int NT = 256, NW = NT / 32;
+__device__ int64_t block_excl_scan(int64_t v, int64_t* out_excl);
+
+constexpr int CLOSE_NT = 512;  // 16 warps: the open beams' closures are independent
+__global__ void __launch_bounds__(CLOSE_NT) close_kernel(ModelDev m, CfgDev c, BatchDev b) {
+  constexpr int NT = CLOSE_NT, NW = NT / 32;
   __shared__ WarpScratch wsc[NW];
   __shared__ int s_ncount, s_fail;
   __shared__ unsigned s_calls, s_probes;
@@ -2197,6 +2200,55 @@ __global__ void __launch_bounds__(256) close_kernel(ModelDev m, CfgDev c, BatchD
   atomicAdd(&s_calls, calls);
   atomicAdd(&s_probes, probes);
   __syncthreads();
+  if (K <= NT && O <= 4) {
+    // compact survivors in parallel, order preserved (decoder.py:397-405): every thread reads
+    // its beam into registers, a block scan gives its new index, then all write
+    const bool alive = tid < K && b.score[hb + tid] > GUARD;
+    double sc = 0.0;
+    uint64_t a1 = 0, a2 = 0;
+    int la = 0, pr = 0, ne = 0;
+    Ent e4[4];
+    if (alive) {
+      sc = b.score[hb + tid];
+      a1 = b.h1[hb + tid];
+      a2 = b.h2[hb + tid];
+      la = b.last[hb + tid];
+      pr = b.prefix[hb + tid];
+      ne = b.nent[hb + tid];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < O) e4[q] = b.ents[(hb + tid) * O + q];
+    }
+    int64_t excl;
+    const int64_t n = block_excl_scan(alive ? 1 : 0, &excl);  // ends with a barrier
+    if (alive) {
+      const size_t d = hb + (size_t)excl;
+      b.score[d] = sc;
+      b.h1[d] = a1;
+      b.h2[d] = a2;
+      b.last[d] = la;
+      b.prefix[d] = pr;
+      b.nent[d] = ne;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < O) b.ents[d * O + q] = e4[q];
+    }
+    if (tid == 0) {
+      b.nbeam[trial] = (int)n;
+      b.ncount[trial] = s_ncount;
+      if (s_fail) {
+        b.status[trial] = 4;
+        b.fail_frame[trial] = b.T[trial];
+      } else if (n == 0) {
+        b.status[trial] = 3;
+        b.fail_frame[trial] = b.T[trial];
+      }
+      unsigned long long* stt = b.stats + (size_t)trial * 8;
+      stt[3] += s_calls;
+      stt[4] += s_probes;
+    }
+    return;
+  }
   if (tid == 0) {
     // compact survivors, order preserved (decoder.py:397-405)
     int n = 0;
@@ -2695,8 +2747,8 @@ cudaError_t frames(const ModelDev& m, const CfgDev& c, const BatchDev& b, const 
 }
 
 cudaError_t close(const ModelDev& m, const CfgDev& c, const BatchDev& b, cudaStream_t st) {
-  const size_t sm = (size_t)8 * c.O * sizeof(Ent);
-  close_kernel<<<b.B, 256, sm, st>>>(m, c, b);
+  const size_t sm = (size_t)(CLOSE_NT / 32) * c.O * sizeof(Ent);
+  close_kernel<<<b.B, CLOSE_NT, sm, st>>>(m, c, b);
   ++g_launches;
   return cudaGetLastError();
 }
