@@ -446,7 +446,9 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "frames_kernel (K2)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel_ms": k_ms, "algorithmic_bytes": alg,
+                         "traffic": _profile_traffic("r1_frames_ncu.json"),
+                         "traffic_source": "profiles/r1_frames_ncu.json (ncu --set full, same launch)",
+                         "kernel_ms": k_ms, "algorithmic_bytes": alg,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pp.exists() else "fallback 6650 GB/s"},
             "cpu_baseline": cpu,
             "clocks": clocks,
@@ -653,7 +655,9 @@ def run_llm(args):
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "LLM body GEMMs + LM head (bf16 tensor cores)",
                          "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved_tf / peak_tf, "traffic": None,
+                         "frac": achieved_tf / peak_tf,
+                         "traffic": _profile_traffic("r1_tcgemm_ncu.json"),
+                         "traffic_source": "profiles/r1_tcgemm_ncu.json (LM-head tcgen05 kernel)",
                          "flops_per_row": scorer.cfg.flops_per_token() * (2 if scorer.split else 1),
                          "precision": args.precision,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"
@@ -754,6 +758,16 @@ def wer_check(world, cfg, scorer, dev, args):
             "identical_transcripts": f"{same}/{len(logs)}",
             "data": "LM-sampled sentences -> lexicon phonemes -> CTC frames, N(0,2) + 10 on the "
                     "true token, b2t25 profile, beam 64, n-gram fusion (config 2 settings)"}
+
+
+def _profile_traffic(name):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) recorded from an
+    `ncu --set full` capture of the same kernel in profiles/ (the bench cannot run ncu)."""
+    p = ROOT / "profiles" / name
+    try:
+        return int(json.loads(p.read_text())["traffic_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def batch_entry_sizes(batch):
