@@ -483,3 +483,28 @@ def test_llm_capacity_error_is_loud():
     ds = [O.log_softmax_scaled(x, cfg.acoustic_scale) for x in synth.make_logits(2, 120, 41, base_seed=8)]
     with pytest.raises(DeviceError, match="prefix cache full"):
         decode_batch(ds, cfg, w.table, w.model, sc)
+
+
+@pytest.mark.gpu
+def test_llm_batch_with_failing_utterance(tiny_scorer):
+    """An utterance that dies at closure (EmptyBeamError, decoder.py:394-395) inside a batch with
+    device LLM fusion: it raises the reference's error, the others stay bit-exact."""
+    from paper_2603_14002_b200 import EmptyBeamError, ReplayScorer, decode_batch
+    from paper_2603_14002_b200.decoder import device_model
+
+    w, cfg = _world_cfg()
+    first_ph = w.lexicon.entries[0].phonemes[0]
+    dead = np.full((1, 41), -40.0)
+    dead[0, first_ph] = 40.0  # one frame: a word-initial phoneme, nothing can close
+    dead = O.log_softmax_scaled(dead.astype(np.float32), cfg.acoustic_scale)
+    ok = [O.log_softmax_scaled(x, cfg.acoustic_scale) for x in synth.make_logits(2, 90, 41, base_seed=61)]
+    ds = [ok[0], dead, ok[1]]
+    got = decode_batch(ds, cfg, w.table, w.model, tiny_scorer)
+    assert isinstance(got[1], EmptyBeamError)
+    with pytest.raises(O.OracleEmptyBeam):
+        O.decode(dead, cfg, w.table, w.model, ReplayScorer(None))
+    sess = device_model(w.table, w.model).batch(cfg, 3, 90)._llm_session
+    replay = ReplayScorer(sess.replay_table())
+    for i in (0, 2):
+        want = O.decode(ds[i], cfg, w.table, w.model, replay)
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest)
