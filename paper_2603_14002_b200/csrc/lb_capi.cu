@@ -271,7 +271,7 @@ void plan_layout(lb_batch* b) {
   b->L.small = 0;
   const char* env = std::getenv("LB_KERNEL");
   const bool want_small = !(env && std::strcmp(env, "general") == 0);
-  if (want_small && K <= 64 && O <= 4 && b->m->dev.V <= 48 && b->m->dev.VP <= 56 && VPD <= 50) {
+  if (want_small && K <= 64 && O <= 3 && b->m->dev.V <= 48 && b->m->dev.VP <= 56 && VPD <= 50) {
     b->L.small = 1;
     b->L.smem_bytes = lbk::small_smem_bytes();
     b->L.gscratch_bytes = lbk::small_gscratch_bytes();

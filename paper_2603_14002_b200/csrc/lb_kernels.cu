@@ -1279,8 +1279,8 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
 // and word-boundary entries are built straight from the speculative pair results.
 // =====================================================================================
 namespace small {
-constexpr int KC = 64, OC = 4, VC = 48, VPC = 56, VPDC = 50;
-constexpr int LC = 320, PC = 256, TSC = 128;
+constexpr int KC = 64, OC = 3, VC = 48, VPC = 56, VPDC = 50;
+constexpr int LC = 320, PC = 160, TSC = 128;
 constexpr int NC = 256, NWC = NC / 32, NT = NC + NGT;
 constexpr int MAXI = (KC + (NC / VC) - 1) / (NC / VC);  // items per thread (13)
 constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8,
