@@ -695,10 +695,10 @@ class DeviceLlmSession:
             del qkv
             N.check(lib.lb_llm_attention(self.h, li, q.data_ptr(), n, chain.data_ptr(), pos.data_ptr(),
                                          att.data_ptr()))
-            o = torch.mm(att, L["wo" + sfx].t(), out_dtype=f32)
-            N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), o.data_ptr(), L["ln2"].data_ptr(), eps, n,
+            # residual add in the GEMM epilogue: x += att @ Wo^T (fp32 C/D, bf16 A/B)
+            torch.addmm(x, att, L["wo" + sfx].t(), out_dtype=f32, out=x)
+            N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), None, L["ln2"].data_ptr(), eps, n,
                                        hn.data_ptr(), None))
-            del o
             if self.scorer.fused_swiglu:  # gate/up GEMM + SwiGLU in one tcgen05 kernel
                 wi = L["wgui" + sfx]
                 N.check(lib.lb_llm_gateup_swiglu(self.h, hn.data_ptr(), n, hn.stride(0), wi.shape[1],
@@ -707,12 +707,11 @@ class DeviceLlmSession:
                 gu = torch.mm(hn, L["wgu" + sfx].t(), out_dtype=f32) if sfx else torch.mm(hn, L["wgu"].t())
                 N.check(lib.lb_llm_swiglu(self.h, gu.data_ptr(), n, cfg.ffn, act.data_ptr()))
                 del gu
-            dn = torch.mm(act, L["wd" + sfx].t(), out_dtype=f32)
+            torch.addmm(x, act, L["wd" + sfx].t(), out_dtype=f32, out=x)
             last = li + 1 == cfg.layers
             wnext = W.norm if last else W.layers[li + 1]["ln1"]
-            N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), dn.data_ptr(), wnext.data_ptr(), eps, n,
+            N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), None, wnext.data_ptr(), eps, n,
                                        hn.data_ptr(), slot.data_ptr() if last else None))
-            del dn
         self._lm_head(hn, slot, n)
 
     def _lm_head(self, hn, slot, n: int):
