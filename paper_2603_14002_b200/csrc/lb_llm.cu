@@ -725,11 +725,11 @@ constexpr int MMA_CH = 16;  // chain positions per stage (one PV k-step)
 // K/V cache rows (all kv heads of a slot) are gathered per 16-position chunk by 1-D TMA bulk
 // copies into a double-buffered stage whose row pitch is padded by 16 B (conflict-free fragment
 // loads).
-template <int HD, bool SPLIT>
+template <int HD, bool SPLIT, int nstages>
 __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer,
                                                              const void* qv, const int32_t* chains,
                                                              const int32_t* pos, float scale,
-                                                             bf16* out, int nstages) {
+                                                             bf16* out) {
   constexpr int KK = HD / 16;  // k-steps of Q K^T
   constexpr int NT = HD / 8;   // n-tiles of P V
   extern __shared__ __align__(128) unsigned char attn_smem[];
@@ -1769,10 +1769,15 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
     const int nst = (128 + 2 * stage <= 80 * 1024) ? 2 : 1;  // keep >= 2-3 CTAs per SM
     const int smem = 128 + nst * stage;
     if (smem > 227 * 1024) return lbh::set_error(LB_ERR_ARG, "K/V cache row too wide for the attention stage");
-#define MMA_ATT(HDV, SV)                                                                            \
+#define MMA_ATT_N(HDV, SV, NS)                                                                      \
   do {                                                                                              \
-    CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<HDV, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
-    LAUNCH(chain_attn_mma_kernel<HDV, SV><<<M, 32 * x.NKV, smem, st>>>(x, layer, q, chains, pos, scale, oo, nst)); \
+    CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<HDV, SV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+    LAUNCH(chain_attn_mma_kernel<HDV, SV, NS><<<M, 32 * x.NKV, smem, st>>>(x, layer, q, chains, pos, scale, oo)); \
+  } while (0)
+#define MMA_ATT(HDV, SV)               \
+  do {                                 \
+    if (nst == 2) MMA_ATT_N(HDV, SV, 2); \
+    else MMA_ATT_N(HDV, SV, 1);        \
   } while (0)
     if (x.HD == 64) {
       if (x.split) MMA_ATT(64, true); else MMA_ATT(64, false);
@@ -1780,6 +1785,7 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
       if (x.split) MMA_ATT(128, true); else MMA_ATT(128, false);
     }
 #undef MMA_ATT
+#undef MMA_ATT_N
     return LB_OK;
   }
   if (x.split) return lbh::set_error(LB_ERR_ARG, "bf16x2 precision needs n_heads / n_kv_heads <= 16");

@@ -22,7 +22,8 @@ def main():
     cfg = cfg.replace(llm_rescore_interval=args.interval)
     import os
     sc = LlamaScorer(args.llm, seed=0, precision=args.precision,
-                     lm_chunk=int(os.environ.get("LM_CHUNK", "2048")))
+                     lm_chunk=int(os.environ.get("LM_CHUNK", "2048")),
+                     lm_head=os.environ.get("LM_HEAD", "fused"))
     dm = device_model(world.table, world.model, 0)
     B, T = raws.shape[:2]
     frames = np.full(B, T, np.int32)
