@@ -450,16 +450,17 @@ __device__ __forceinline__ bf16 to_store<bf16>(float v) { return __float2bfloat1
 template <>
 __device__ __forceinline__ float to_store<float>(float v) { return v; }
 
-template <typename T>
+template <typename T, int HD>
 __global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, const int32_t* pos,
                                const int32_t* slots, const float* cosT, const float* sinT,
                                T* q_out) {
   const int row = blockIdx.x;
   if (row >= M) return;
-  const int HD = l.HD, half = HD / 2, NH = l.NH, NKV = l.NKV;
+  constexpr int half = HD / 2;
+  const int NH = l.NH, NKV = l.NKV;
   const int W = (NH + 2 * NKV) * HD;
   const float* in = qkv + (size_t)row * W;
-  const int p = pos[row];
+  const int p = pos[row];  // rotary tables: one row per position
   const size_t slot = (size_t)slots[row];
   const size_t kvw = (size_t)NKV * HD;
   // K/V cache rows: bf16 [NKV*HD]; split precision: [hi | lo] bf16 pairs [2*NKV*HD]
@@ -492,7 +493,13 @@ __global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, con
     }
   }
   const float* vin = in + (NH + NKV) * HD;
-  for (int t = threadIdx.x; t < NKV * HD; t += blockDim.x) put(vd, t, vin[t]);
+  for (int t = threadIdx.x * 4; t < NKV * HD; t += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(vin + t);
+    put(vd, t, v.x);
+    put(vd, t + 1, v.y);
+    put(vd, t + 2, v.z);
+    put(vd, t + 3, v.w);
+  }
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1733,12 +1740,16 @@ int lb_llm_rope_kv(lb_llm* l, int32_t layer, const void* qkv, int32_t M, const i
   if (layer < 0 || layer >= l->dev.L) return lbh::set_error(LB_ERR_ARG, "layer out of range");
   if (M <= 0) return LB_OK;
   const float* in = reinterpret_cast<const float*>(qkv);
-  if (l->dev.split)
-    LAUNCH(rope_kv_kernel<float><<<M, 128, 0, l->b->st>>>(l->dev, layer, in, M, pos, slots, cos_tab,
-                                                           sin_tab, reinterpret_cast<float*>(q_out)));
-  else
-    LAUNCH(rope_kv_kernel<bf16><<<M, 128, 0, l->b->st>>>(l->dev, layer, in, M, pos, slots, cos_tab,
-                                                          sin_tab, reinterpret_cast<bf16*>(q_out)));
+  cudaStream_t st = l->b->st;
+#define ROPE(TT, HDV) \
+  LAUNCH(rope_kv_kernel<TT, HDV><<<M, 128, 0, st>>>(l->dev, layer, in, M, pos, slots, cos_tab, sin_tab, \
+                                                     reinterpret_cast<TT*>(q_out)))
+  if (l->dev.split) {
+    if (l->dev.HD == 64) ROPE(float, 64); else ROPE(float, 128);
+  } else {
+    if (l->dev.HD == 64) ROPE(bf16, 64); else ROPE(bf16, 128);
+  }
+#undef ROPE
   return LB_OK;
 }
 
