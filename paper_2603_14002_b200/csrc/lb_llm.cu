@@ -359,72 +359,81 @@ __global__ void wave_rows_kernel(LlmDev l, int64_t row0, int n, int32_t* tok, in
 // x[M][H] fp32 residual (+= delta fp32 when given) -> out = bf16(x * rsqrt(mean(x^2) + eps) * w);
 // `store_slots` also keeps the fp32 row in the slot hidden-state table.
 // bias != nullptr: LayerNorm y = (x - mean) * rsqrt(var + eps) * w + bias (GPT-2), two-pass
+constexpr int NORM_NPT = 4;  // float4 per thread held in registers: hidden <= 256 * 4 * 4 = 4096
+
+__device__ __forceinline__ float block_sum256(float v, float* red) {
+  v = warp_sum(v);
+  __syncthreads();  // red[] may still be read by a previous reduction
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int w2 = 0; w2 < 8; ++w2) t += red[w2];
+  return t;
+}
+
+// bias != nullptr: LayerNorm y = (x - mean) * rsqrt(var + eps) * w + bias (GPT-2), two-pass
+// over the register-resident row; otherwise RMSNorm.  x is read once (+= delta, written back).
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float* delta,
                                                           const float* w, float eps, int H,
                                                           bf16* out, const int32_t* store_slots,
                                                           float* s_h, int split,
                                                           const float* bias = nullptr) {
+  __shared__ float red[8];
   const int row = blockIdx.x;
   float* xr = x + (size_t)row * H;
   const float* dr = delta ? delta + (size_t)row * H : nullptr;
+  float4 v[NORM_NPT];
   float ss = 0.f;
-  for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
-    if (dr) {
-      const float4 a = *reinterpret_cast<const float4*>(dr + i);
-      v.x += a.x;
-      v.y += a.y;
-      v.z += a.z;
-      v.w += a.w;
-      *reinterpret_cast<float4*>(xr + i) = v;
+#pragma unroll
+  for (int j = 0; j < NORM_NPT; ++j) {
+    const int i = (threadIdx.x + j * 256) * 4;
+    v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < H) {
+      v[j] = *reinterpret_cast<const float4*>(xr + i);
+      if (dr) {
+        const float4 a = *reinterpret_cast<const float4*>(dr + i);
+        v[j].x += a.x;
+        v[j].y += a.y;
+        v[j].z += a.z;
+        v[j].w += a.w;
+        *reinterpret_cast<float4*>(xr + i) = v[j];
+      }
+      ss += bias ? (v[j].x + v[j].y + v[j].z + v[j].w)
+                 : (v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w);
     }
-    ss += bias ? (v.x + v.y + v.z + v.w) : (v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w);
   }
-  __shared__ float red[32];
-  ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
+  const float tot = block_sum256(ss, red);
   float mean = 0.f, r;
-  if (bias) {  // LayerNorm: ss above is the plain sum; second pass for the centred variance
-    mean = red[0] / (float)H;
-    __syncthreads();
+  if (bias) {  // LayerNorm: tot is the plain sum; centred variance from the registers
+    mean = tot / (float)H;
     float vs = 0.f;
-    for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
-      const float4 v = *reinterpret_cast<const float4*>(xr + i);
-      const float a = v.x - mean, b2 = v.y - mean, c2 = v.z - mean, d2 = v.w - mean;
-      vs += a * a + b2 * b2 + c2 * c2 + d2 * d2;
+#pragma unroll
+    for (int j = 0; j < NORM_NPT; ++j) {
+      const int i = (threadIdx.x + j * 256) * 4;
+      if (i < H) {
+        const float a = v[j].x - mean, b2 = v[j].y - mean, c2 = v[j].z - mean, d2 = v[j].w - mean;
+        vs += a * a + b2 * b2 + c2 * c2 + d2 * d2;
+      }
     }
-    vs = warp_sum(vs);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = vs;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-      t = warp_sum(t);
-      if (threadIdx.x == 0) red[0] = t;
-    }
-    __syncthreads();
-    r = rsqrtf(red[0] / (float)H + eps);
+    r = rsqrtf(block_sum256(vs, red) / (float)H + eps);
   } else {
-    r = rsqrtf(red[0] / (float)H + eps);
+    r = rsqrtf(tot / (float)H + eps);
   }
   bf16* orow = out + (size_t)row * H * (split ? 2 : 1);
   float* hrow = store_slots ? s_h + (size_t)store_slots[row] * H : nullptr;
-  for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + i);
+#pragma unroll
+  for (int j = 0; j < NORM_NPT; ++j) {
+    const int i = (threadIdx.x + j * 256) * 4;
+    if (i >= H) continue;
     const float4 g = *reinterpret_cast<const float4*>(w + i);
     float4 y;
     if (bias) {
       const float4 bb = *reinterpret_cast<const float4*>(bias + i);
-      y = make_float4((v.x - mean) * r * g.x + bb.x, (v.y - mean) * r * g.y + bb.y,
-                      (v.z - mean) * r * g.z + bb.z, (v.w - mean) * r * g.w + bb.w);
+      y = make_float4((v[j].x - mean) * r * g.x + bb.x, (v[j].y - mean) * r * g.y + bb.y,
+                      (v[j].z - mean) * r * g.z + bb.z, (v[j].w - mean) * r * g.w + bb.w);
     } else {
-      y = make_float4(v.x * r * g.x, v.y * r * g.y, v.z * r * g.z, v.w * r * g.w);
+      y = make_float4(v[j].x * r * g.x, v[j].y * r * g.y, v[j].z * r * g.z, v[j].w * r * g.w);
     }
     __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(orow + i);
     const __nv_bfloat162 h0 = __floats2bfloat162_rn(y.x, y.y), h1 = __floats2bfloat162_rn(y.z, y.w);
@@ -440,9 +449,6 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float*
   }
 }
 
-// qkv[M][(NH + 2 NKV) HD] fp32 -> q_out[M][NH HD] bf16 rotated; rotated k and v stored (bf16)
-// at the row's slot.
-// rotate_half convention: (x1, x2) -> (x1 cos - x2 sin, x2 cos + x1 sin), x1/x2 = halves.
 template <typename T>
 __device__ __forceinline__ T to_store(float v);
 template <>
@@ -1707,6 +1713,7 @@ int lb_llm_finish(lb_llm* l, int32_t final_, int32_t min_frames) {
 int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float eps, int32_t M,
                    void* out, const int32_t* store_slots) {
   if (!l || !x || !w || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (l->dev.H > 256 * 4 * NORM_NPT) return lbh::set_error(LB_ERR_ARG, "hidden size > 4096");
   if (M <= 0) return LB_OK;
   LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
                                                       l->dev.H, reinterpret_cast<bf16*>(out),
@@ -1717,6 +1724,7 @@ int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float
 int lb_llm_layernorm(lb_llm* l, float* x, const void* delta, const float* w, const float* b,
                      float eps, int32_t M, void* out, const int32_t* store_slots) {
   if (!l || !x || !w || !b || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (l->dev.H > 256 * 4 * NORM_NPT) return lbh::set_error(LB_ERR_ARG, "hidden size > 4096");
   if (M <= 0) return LB_OK;
   LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
                                                       l->dev.H, reinterpret_cast<bf16*>(out),
