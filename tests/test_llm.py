@@ -2,7 +2,6 @@
 transformers oracle (1e-2 abs, BASELINE.json north star) and decode parity against the oracle
 decoder driven by a score-replay scorer on the GPU."""
 
-import math
 
 import numpy as np
 import pytest
