@@ -287,7 +287,8 @@ class LlamaScorer:
 
     def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
                  max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 2048,
-                 precision: str = "bf16x2", lm_head: str = "fused", fused_swiglu: bool = False):
+                 precision: str = "bf16x2", lm_head: str = "fused", fused_swiglu: bool = False,
+                 fused_swiglu_min_rows: int = 4096):
         """precision: "bf16x2" (default) feeds every body GEMM the activation as a hi+lo pair of
         bf16 values against duplicated bf16 weights -- fp32-equivalent activations on the bf16
         tensor cores, scores within ~1e-3 of an fp32 forward even for 40-token texts -- and keeps
@@ -317,9 +318,12 @@ class LlamaScorer:
         self.precision = precision
         self.split = precision == "bf16x2"
         # gate/up rows interleaved in 128-row blocks for the tcgen05 GEMM with the SwiGLU epilogue
-        # (opt-in: measured 91 ms vs 70 ms for cuBLAS + the SwiGLU kernel per config-3 step in
-        # bf16x2 -- the 128x256 tile loses to cuBLAS's shape choice on these row counts)
+        # (opt-in, for waves of >= fused_swiglu_min_rows rows).  On the 13.4k-row final wave of
+        # config 3 its 128x256 tiles keep the tensor pipe ~81% busy and the gate/up product never
+        # reaches HBM, but measured per step it only ties cuBLAS + the SwiGLU kernel (and loses
+        # on small waves to cuBLAS's per-shape tiles), so it is off by default.
         self.fused_swiglu = fused_swiglu and self.cfg.arch == "llama" and self.cfg.ffn % 128 == 0
+        self.fused_swiglu_min_rows = fused_swiglu_min_rows
         if self.fused_swiglu:
             F, H = self.cfg.ffn, self.cfg.hidden
             for L in self.weights.layers:
@@ -699,7 +703,8 @@ class DeviceLlmSession:
             torch.addmm(x, att, L["wo" + sfx].t(), out_dtype=f32, out=x)
             N.check(lib.lb_llm_rmsnorm(self.h, x.data_ptr(), None, L["ln2"].data_ptr(), eps, n,
                                        hn.data_ptr(), None))
-            if self.scorer.fused_swiglu:  # gate/up GEMM + SwiGLU in one tcgen05 kernel
+            if self.scorer.fused_swiglu and n >= self.scorer.fused_swiglu_min_rows:
+                # gate/up GEMM + SwiGLU in one tcgen05 kernel
                 wi = L["wgui" + sfx]
                 N.check(lib.lb_llm_gateup_swiglu(self.h, hn.data_ptr(), n, hn.stride(0), wi.shape[1],
                                                  wi.data_ptr(), wi.stride(0), cfg.ffn, act.data_ptr()))

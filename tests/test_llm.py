@@ -377,7 +377,7 @@ def test_fused_lmhead_lse_matches_cublas_path(precision):
     raws = synth.make_logits(3, 100, 41, base_seed=41)
     outs = []
     for mode in ("cublas", "fused"):  # fused: tcgen05 LM head + LSE
-        sc = LlamaScorer("tiny", seed=6, precision=precision, lm_head=mode)
+        sc = LlamaScorer("tiny", seed=6, precision=precision, lm_head=mode, fused_swiglu=False)
         _, got, sess = _decode_with_session(sc, raws, cfg, w)
         outs.append((sess.export(), [(g.text, g.score) for g in got]))
     (a, ga), (b, gb) = outs
@@ -429,7 +429,7 @@ def test_fused_gateup_swiglu_vs_oracle():
     within the north-star tolerance of the fp32 oracle."""
     from paper_2603_14002_b200 import LlamaScorer, ReplayScorer
 
-    sc = LlamaScorer("tiny", seed=6, fused_swiglu=True)
+    sc = LlamaScorer("tiny", seed=6, fused_swiglu=True, fused_swiglu_min_rows=1)
     assert sc.fused_swiglu
     w, cfg = _world_cfg()
     raws = synth.make_logits(3, 100, 41, base_seed=43)

@@ -23,7 +23,8 @@ def main():
     import os
     sc = LlamaScorer(args.llm, seed=0, precision=args.precision,
                      lm_chunk=int(os.environ.get("LM_CHUNK", "2048")),
-                     lm_head=os.environ.get("LM_HEAD", "fused"))
+                     lm_head=os.environ.get("LM_HEAD", "fused"),
+                     fused_swiglu=os.environ.get("FUSED_SWIGLU", "0") == "1")
     dm = device_model(world.table, world.model, 0)
     B, T = raws.shape[:2]
     frames = np.full(B, T, np.int32)
