@@ -28,7 +28,7 @@ from .config import DecodeConfig, config_from_dict, load_config
 from .decoder import DecodeResult, decode, decode_batch, decode_batch_raw
 from .errors import ConfigError
 from .lexicon import TransitionTable, build_transition_table, load_lexicon, load_table
-from .logits import LogProbMatrix, RawLogits, load_logits
+from .logits import LogProbMatrix, RawLogits, load_logits, load_logits_batch
 from .metrics import RtfSample, rtf
 from .ngram import LmSession, NGramModel, load_arpa
 from .scorer import DeviceNgramScorer, StubScorer
@@ -128,27 +128,27 @@ class Engine:
                                 final_llm_only=final_llm_only, device=self.device)
 
     def decode_paths(self, paths, final_llm_only: bool = False) -> list:
-        """[(DecodeResult, RtfSample) | exception] per file, decoded as one device batch."""
-        raws, out, slots = [], [], []
-        for p in paths:
-            try:
-                raws.append(load_logits(p, self.vocab))
-                slots.append(len(raws) - 1)
-            except Exception as exc:  # noqa: BLE001 -- per-utterance error record (cli.py:167-177)
-                slots.append(exc)
+        """[(DecodeResult, RtfSample) | exception] per file, decoded as one device batch; the
+        LBLT payloads are read straight into one page-locked staging array."""
+        paths = list(paths)
+        if not paths:
+            return []
+        arr, frames, frame_ms, errors = load_logits_batch(paths, self.vocab)
+        err = dict(errors)
+        ok = [i for i in range(len(paths)) if i not in err]
         t0 = time.perf_counter()
-        res = self.decode_batch_raw(raws, final_llm_only) if raws else []
+        if len(ok) == len(paths):  # keep the page-locked staging array (no gather copy)
+            res = self.decode_batch_raw((arr, frames), final_llm_only)
+        else:
+            res = self.decode_batch_raw((arr[ok], frames[ok]), final_llm_only) if ok else []
         wall = time.perf_counter() - t0
-        for s in slots:
-            if isinstance(s, Exception):
-                out.append(s)
-                continue
-            r = res[s]
-            if isinstance(r, Exception):
-                out.append(r)
-            else:
-                out.append((r, rtf(wall / max(len(raws), 1), r.frame_count,
-                                   raws[s].frame_duration_ms)))
+        out: list = [None] * len(paths)
+        for i, e in err.items():
+            out[i] = e
+        for j, i in enumerate(ok):
+            r = res[j]
+            out[i] = r if isinstance(r, Exception) else (
+                r, rtf(wall / max(len(ok), 1), r.frame_count, frame_ms[i]))
         return out
 
 

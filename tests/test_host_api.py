@@ -305,3 +305,25 @@ def test_engine_decode_paths_matches_oracle(tmp_path):
     want = O.decode(d, eng.config, eng.table, eng.ngram_model, eng.scorer)
     r = eng.decode_matrix(d)
     assert (r.text, r.score, r.nbest) == (want.text, want.score, want.nbest)
+
+
+def test_load_logits_batch_matches_single_loads(tmp_path):
+    import numpy as np
+
+    from paper_2603_14002_b200 import RawLogits, load_logits, save_logits, synth
+    from paper_2603_14002_b200.logits import load_logits_batch
+
+    vocab = synth.vocab41()
+    paths = []
+    for i, t in enumerate([5, 9, 3]):
+        p = tmp_path / f"u{i}.lblt"
+        save_logits(p, RawLogits(np.random.default_rng(i).normal(size=(t, 41)).astype(np.float32), 80.0))
+        paths.append(p)
+    bad = tmp_path / "bad.lblt"
+    bad.write_bytes(b"LBLT" + b"\\x00" * 4)
+    paths.insert(1, bad)
+    arr, frames, ms, errors = load_logits_batch(paths, vocab, pinned=False)
+    assert [i for i, _ in errors] == [1] and list(frames) == [5, 0, 9, 3]
+    for i in (0, 2, 3):
+        want = load_logits(paths[i], vocab).frames
+        assert np.array_equal(arr[i, : frames[i]], want) and ms[i] == 80.0
