@@ -402,6 +402,9 @@ class LlamaScorer:
 
     # ---- device path
     def session(self, batch) -> "DeviceLlmSession":
+        if batch.dm.device != self.device:
+            raise DeviceError(f"LlamaScorer lives on cuda:{self.device} but the decode runs on "
+                              f"cuda:{batch.dm.device}; build one scorer per device")
         sess = getattr(batch, "_llm_session", None)
         if sess is None or sess.scorer is not self:
             if sess is not None:
