@@ -633,9 +633,11 @@ def run_llm(args):
     cpu = None
     if rank == 0 and world_n == 1 and not args.no_cpu_baseline:
         cpu = reference_llm_sample(world, cfg, raws, scorer, args.ref_trials)
+    wer = llm_wer_check(world, cfg, scorer, dev, args) if rank == 0 and not args.no_wer else None
 
     if rank == 0:
         line = {
+            "wer": wer,
             "metric": f"decoded frames/s (BASELINE config {args.config}, beam {args.beam}, {args.llm} "
                       "fusion, 1 x B200 per rank)",
             "value": value, "unit": "frames/s", "n_gpus": world_n, "steps": args.steps,
@@ -690,6 +692,27 @@ def reference_llm_sample(world, cfg, raws, scorer, n):
     return {"value": frames / wall, "unit": "frames/s", "cores": 1, "kind": "port",
             "sample": f"{n} utterances (T={raws.shape[1]}): oracle/ decode on one host core + "
                       "LlamaScorer.submit full-sequence GPU forwards (no KV reuse)"}
+
+
+def llm_wer_check(world, cfg, scorer, dev, args, n=16):
+    """WER with LLM fusion: speech-shaped trials decoded on the GPU (device prefix-trie LLM) and
+    by the reference arm (oracle search on the host + the same LLM, full forward per text).
+    The two LLM paths round differently (kernels vs plain torch), so transcripts may differ on
+    fusion-score near-ties; `identical_transcripts` counts the ones that agree."""
+    from oracle import lightbeam_oracle as O
+    from paper_2603_14002_b200 import decode_batch_raw, synth
+    from paper_2603_14002_b200.metrics import corpus_wer
+
+    sents, logs = synth.make_wer_trials(world, n, seed=991)
+    got = decode_batch_raw(logs, cfg, world.table, world.model, scorer, device=dev)
+    gpu = [r.text if not isinstance(r, Exception) else "" for r in got]
+    ref = [O.decode(O.log_softmax_scaled(x, cfg.acoustic_scale), cfg, world.table, world.model,
+                    scorer).text for x in logs]
+    return {"trials": n, "wer_gpu": corpus_wer(sents, [t.split() for t in gpu]),
+            "wer_reference_arm": corpus_wer(sents, [t.split() for t in ref]),
+            "identical_transcripts": f"{sum(a == b for a, b in zip(gpu, ref))}/{n}",
+            "data": "LM-sampled sentences -> CTC frames (N(0,2) + 10 on the true token); config-3 "
+                    "settings with LLM fusion"}
 
 
 def run_reference_llm(args):
