@@ -184,6 +184,7 @@ class DeviceBatch:
         N.check(N.lib().lb_batch_create(dm.handle, C.byref(c), max_trials, max_frames,
                                         C.c_void_p(stream or 0), C.byref(h)))
         self.h = h
+        self.stream_ptr = int(stream or 0)  # the CUDA stream every kernel of this batch runs on
         self.n = 0
         self.frames = np.zeros(0, dtype=np.int32)
 

@@ -654,16 +654,23 @@ class DeviceLlmSession:
         return float(sum(a.elapsed_time(b) for a, b in self._timing))
 
     def event(self, final: bool, min_frames: int):
-        timing = getattr(self, "_timing", None)
-        if timing is not None:
-            import torch
+        import contextlib
 
-            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            ev[0].record()
-        self._event(final, min_frames)
-        if timing is not None:
-            ev[1].record()
-            timing.append(ev)
+        import torch
+
+        # torch's GEMMs must run on the batch's stream, in order with the lb_llm kernels
+        ptr = getattr(self.batch, "stream_ptr", 0)
+        ctx = (torch.cuda.stream(torch.cuda.ExternalStream(ptr, device=self.scorer.weights.device))
+               if ptr else contextlib.nullcontext())
+        with ctx:
+            timing = getattr(self, "_timing", None)
+            if timing is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+            self._event(final, min_frames)
+            if timing is not None:
+                ev[1].record()
+                timing.append(ev)
 
     def _event(self, final: bool, min_frames: int):
         lib = N.lib()

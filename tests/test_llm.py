@@ -507,3 +507,18 @@ def test_llm_batch_with_failing_utterance(tiny_scorer):
     for i in (0, 2):
         want = O.decode(ds[i], cfg, w.table, w.model, replay)
         assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest)
+
+
+@pytest.mark.gpu
+def test_llm_stream_api_matches_batch_api(tiny_scorer):
+    """decode_stream_raw (two device batches on two streams, each with its own prefix cache)
+    gives the LLM-fused results of decode_batch_raw, batch by batch."""
+    from paper_2603_14002_b200 import decode_batch_raw, decode_stream_raw
+
+    w, cfg = _world_cfg()
+    batches = [(synth.make_logits(n, T, 41, base_seed=700 + n), np.full(n, T, np.int32))
+               for n, T in [(3, 80), (2, 120), (4, 60)]]
+    want = [decode_batch_raw(b, cfg, w.table, w.model, tiny_scorer) for b in batches]
+    got = list(decode_stream_raw(iter(batches), cfg, w.table, w.model, tiny_scorer))
+    for gb, wb in zip(got, want):
+        assert [(r.text, r.score, r.nbest) for r in gb] == [(r.text, r.score, r.nbest) for r in wb]
