@@ -336,6 +336,9 @@ class LlamaScorer:
                         L[k + "2"] = torch.cat([L[k], L[k]], 1).contiguous()
             self.emb2 = torch.cat([self.weights.emb, self.weights.emb], 1).contiguous()
         self.device_llm_scorer = self  # the GPU decoder drives this scorer on the device
+        # the weights were built on the legacy default stream; decodes may run on non-blocking
+        # streams that do not order after it
+        torch.cuda.synchronize(device)
 
     # ---- reference protocol (host strings, one full forward per text, no KV reuse)
     def next_request_id(self) -> int:
