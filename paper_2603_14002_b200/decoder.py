@@ -542,7 +542,8 @@ def decode_stream_raw(batches, config, tt, lm, scorer, final_llm_only: bool = Fa
     yields each batch's list of DecodeResult / exception, in order.  Two device batches on two
     CUDA streams alternate, so batch i+1's H2D copy and search run on the GPU while the host
     assembles batch i's transcripts and n-best lists (with pinned host inputs the launches are
-    asynchronous).  Results are identical to `decode_batch_raw` per batch."""
+    asynchronous; a batch's host array must stay unmodified until its results are yielded).
+    Results are identical to `decode_batch_raw` per batch."""
     cfg, model, dm = _prepare(config, tt, lm, device)
     pending: list = []
     slot = 0
