@@ -1331,7 +1331,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   __shared__ int hfill[NBINS];
   __shared__ double wmax[NWC];
   __shared__ double s_maxs;
-  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_inr, s_cnt2;
+  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov, s_inr, s_cnt2;
   __shared__ int ngtot[2];
   __shared__ unsigned s_calls, s_probes;
 
@@ -1499,14 +1499,21 @@ __global__ void __launch_bounds__(small::NT, 2)
       if (gt == 0) {
         ppoff[K] = carry;
         s_ngP = carry;
+        if (carry <= PC) s_ngcov = carry;
       }
       const int P = carry;
-      if (P <= PC) {
-        // pair table: each parent writes its own (entry, surface) pairs -- no search
+      {
+        // pair table: each parent writes its own (entry, surface) pairs -- no search.  Parents
+        // are in score order; when the pairs exceed PC only the leading parents whose pairs all
+        // fit are speculated (s_ngcov = their pair count), the rest take the warp path after S4
         int4* qinfo = reinterpret_cast<int4*>(sm + O_QINFO);
         for (int p = gt; p < K; p += NGT) {
           // ppoff[K] is written by thread 0 without a barrier: use the scan total instead
           const int q0 = ppoff[p], q1 = p + 1 < K ? ppoff[p + 1] : P;
+          if (q1 > PC) {
+            if (q0 <= PC) s_ngcov = q0;  // the first parent that does not fit (unique)
+            continue;
+          }
           if (q0 == q1) continue;
           const CompHdr ch = comp_hdr(rows + p * VP, V);
           for (int q = q0; q < q1; ++q) {
@@ -1528,11 +1535,12 @@ __global__ void __launch_bounds__(small::NT, 2)
           }
         }
         bar_sync(3, NGT);
+        const int PCOV = s_ngcov;
         constexpr int NQ = NGT / 4;
         const int grp = gt >> 2, sub = lane & 3;
-        for (int q0 = 0; q0 < P; q0 += NQ) {
+        for (int q0 = 0; q0 < PCOV; q0 += NQ) {
           const int q = q0 + grp;
-          const bool act = q < P;
+          const bool act = q < PCOV;
           const int4 qi = act ? qinfo[q] : make_int4(0, -1, -1, 0);
           const Ent& E = C_ENTS[qi.x];
           uint32_t hh[MAXH] = {E.h[0], E.h[1], E.h[2]};
@@ -1814,7 +1822,9 @@ __global__ void __launch_bounds__(small::NT, 2)
       LB_PHASE(3);
 
       if (!dead) {
-        const bool ngover = s_ngP > PC;
+        const int ncov = s_ngcov;
+        const bool ngover = ncov < s_ngP;  // some parents' pairs were not speculated
+        if (timing && ngover) ph[15] += 1000;  // permille of frames past the speculative pair cap
         LB_PHASE(13);
         // ---- F: materialise survivors; new word boundaries pick their top-o pairs
         // selected beams spread over all compute warps (j = lane * NWC + warp), so the few
@@ -1838,7 +1848,7 @@ __global__ void __launch_bounds__(small::NT, 2)
           LB_PHASE(14);
           if (emit && tok == space) {
             blist[atomicAdd(&s_nb, 1)] = j;
-            if (ngover) {
+            if (ppoff[p + 1] > ncov) {
               bs.x = -2;
             } else {
               const int q0 = ppoff[p], q1 = ppoff[p + 1];
@@ -1900,6 +1910,7 @@ __global__ void __launch_bounds__(small::NT, 2)
         if (ngover && nb > 0) {
           for (int bi = warp; bi < nb; bi += NWC) {
             const int j = blist[bi];
+            if (bsel[j].x != -2) continue;  // speculated parent
             const int p = npar[j];
             int outn = -1;
             double sc = nscore[j];
@@ -1919,6 +1930,18 @@ __global__ void __launch_bounds__(small::NT, 2)
         // order, only the nb boundary beams need comparisons; hash groups via a smem table
         {
           const int n = nsel;
+          // beams outside blist are "regular": their score is sval[j], and sval is sorted
+          // (score desc, j asc), so a boundary beam counts the regular beams ahead of it by two
+          // binary searches over sval and a popcount of the regular mask (built per warp)
+          unsigned bm0 = 0, bm1 = 0;
+          for (int k2 = lane; k2 < nb; k2 += 32) {
+            const int j = blist[k2];
+            if (j < 32) bm0 |= 1u << j;
+            else bm1 |= 1u << (j - 32);
+          }
+          bm0 = __reduce_or_sync(FULLMASK, bm0);
+          bm1 = __reduce_or_sync(FULLMASK, bm1);
+          const uint64_t regm = ~(((uint64_t)bm1 << 32) | bm0) & (n >= 64 ? ~0ull : ((1ull << n) - 1));
           int G = 1;
           while (G < 32 && 2 * G * n <= NC) G <<= 1;
           const int groups = NC / G, g = tid / G, r = tid & (G - 1);
@@ -1926,8 +1949,7 @@ __global__ void __launch_bounds__(small::NT, 2)
             const int i = i0 + g;
             const bool act = i < n;
             const double si = act ? nscore[i] : 0.0;
-            const int bx = act ? bsel[i].x : -1;
-            const bool ib = act && (bx != -1 || si <= GUARD);
+            const bool ib = act && !((regm >> i) & 1ull);
             int cnt = 0;
             if (act) {
               for (int k2 = r; k2 < nb; k2 += G) {
@@ -1936,12 +1958,22 @@ __global__ void __launch_bounds__(small::NT, 2)
                 cnt += (sj > si) || (sj == si && j < i);
                 if (!ib) cnt -= (j < i);
               }
-              if (ib) {
-                for (int j = r; j < n; j += G) {
-                  if (bsel[j].x != -1 || nscore[j] <= GUARD) continue;
-                  const double sj = nscore[j];
-                  cnt += (sj > si) || (sj == si && j < i);
+              if (ib && r == 0) {
+                int lo = 0, hi = n;  // first j with sval[j] <= si
+                while (lo < hi) {
+                  const int mid = (lo + hi) >> 1;
+                  if (sval[mid] > si) lo = mid + 1;
+                  else hi = mid;
                 }
+                const int a = lo;
+                hi = n;  // first j with sval[j] < si
+                while (lo < hi) {
+                  const int mid = (lo + hi) >> 1;
+                  if (sval[mid] >= si) lo = mid + 1;
+                  else hi = mid;
+                }
+                const int e = max(a, min(lo, i));
+                cnt += __popcll(regm & (e >= 64 ? ~0ull : ((1ull << e) - 1)));
               }
             }
             for (int o = G >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULLMASK, cnt, o);

@@ -298,7 +298,7 @@ class DeviceBatch:
 
     PHASES = ("top_U", "cand_S1wait", "collect", "sort", "materialise", "ngram_G3", "recomb_rank",
               "recomb_keep", "scatter", "loop_tail", "fusion", "cand_loop", "F_work",
-              "F_start", "F_head", "p15")
+              "F_start", "F_head", "spec_overflow_permille")
 
     def enable_phase_timing(self, on: bool = True):
         N.check(N.lib().lb_batch_enable_phase_timing(self.h, int(on)))
