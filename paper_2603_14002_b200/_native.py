@@ -19,6 +19,9 @@ from .errors import DeviceError
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "_lightbeam_b200.so"
+# development A/B runs only (tools/ab_variants.py): load a variant build instead
+if os.environ.get("LB_LIB_VARIANT"):
+    LIB_PATH = PKG / f"_lightbeam_b200_{os.environ['LB_LIB_VARIANT']}.so"
 INCLUDE = PKG.parent / "include"
 
 NVCC_FLAGS = [

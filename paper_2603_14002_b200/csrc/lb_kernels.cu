@@ -115,6 +115,12 @@ __device__ __forceinline__ double cand_value(double s, double d, int v, int lp, 
 // bo(h0) + (bo(h1) + (... + p)), the successor = longest listed suffix of (h + w) capped at
 // order-1 words, and the successor's own suffix back-offs (the new entry's cache).  `w < 0`
 // is the OOV-without-<unk> kill: increment NEG_INF, successor ().
+// h[j] for a runtime j < MAXH without dynamic register indexing (no local-memory array)
+static_assert(MAXH == 3, "hist_at assumes three history slots");
+__device__ __forceinline__ uint32_t hist_at(const uint32_t h[MAXH], int j) {
+  return j == 0 ? h[0] : (j == 1 ? h[1] : h[2]);
+}
+
 struct WordScore {
   double inc;
   double sbo[MAXH];
@@ -131,10 +137,13 @@ __device__ void group_score_word(const ModelDev& m, bool act, const uint32_t h[M
   bool hit = false;
   double p = 0.0, bo = 0.0;
   if (valid && ki <= hl) {
-    uint32_t k[4] = {WPAD, WPAD, WPAD, WPAD};
-    int n = 0;
-    for (int j = ki; j < hl; ++j) k[n++] = h[j];
-    k[n] = (uint32_t)w;
+    // key = (h[ki..hl-1], w, pad...), built with static indices so it stays in registers
+    uint32_t k[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = ki + i;
+      k[i] = j < hl ? hist_at(h, j) : (j == hl ? (uint32_t)w : WPAD);
+    }
     uint32_t b1, b2;
     ng_buckets(ng_hash(k[0], k[1], k[2], k[3]), m.ng_nb, b1, b2);
     const uint4* bucket = reinterpret_cast<const uint4*>(m.ng + (size_t)(cb ? b2 : b1) * NG_WAYS);
@@ -175,7 +184,12 @@ __device__ void group_score_word(const ModelDev& m, bool act, const uint32_t h[M
       val = pk[j];
       hitk = j;
     }
-  for (int j = min(hitk, hl) - 1; j >= 0; --j) val = xadd(hbo[j], val);
+  {
+    const int lim = min(hitk, hl);  // right-nested back-off sum, j = lim-1 .. 0
+    if (lim > 2) val = xadd(hbo[2], val);
+    if (lim > 1) val = xadd(hbo[1], val);
+    if (lim > 0) val = xadd(hbo[0], val);
+  }
   out.inc = val;
   if (m.order > 1) {
     const int start = max(0, hl + 1 - (m.order - 1));
@@ -184,9 +198,12 @@ __device__ void group_score_word(const ModelDev& m, bool act, const uint32_t h[M
     for (int j = 3; j >= 0; --j)
       if (j >= start && j <= hl && fk[j] && prob_present(pk[j])) sk = j;
     if (sk >= 0) {
-      int n = 0;
-      for (int t = sk; t < hl; ++t) out.succ[n++] = h[t];
-      out.succ[n++] = (uint32_t)w;
+      const int n = hl - sk + 1;  // successor = (h[sk..hl-1], w)
+#pragma unroll
+      for (int t = 0; t < MAXH; ++t) {
+        const int j = sk + t;
+        out.succ[t] = j < hl ? hist_at(h, j) : (j == hl ? (uint32_t)w : 0u);
+      }
       out.slen = n;
 #pragma unroll
       for (int t = 0; t < MAXH; ++t) {
@@ -213,10 +230,13 @@ __device__ void quad_score_word(const ModelDev& m, bool act, const uint32_t h[MA
   bool hit = false;
   double p = 0.0, bo = 0.0;
   if (valid && ki <= hl) {
-    uint32_t k[4] = {WPAD, WPAD, WPAD, WPAD};
-    int n = 0;
-    for (int j = ki; j < hl; ++j) k[n++] = h[j];
-    k[n] = (uint32_t)w;
+    // key = (h[ki..hl-1], w, pad...), built with static indices so it stays in registers
+    uint32_t k[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = ki + i;
+      k[i] = j < hl ? hist_at(h, j) : (j == hl ? (uint32_t)w : WPAD);
+    }
     uint32_t b1, b2;
     ng_buckets(ng_hash(k[0], k[1], k[2], k[3]), m.ng_nb, b1, b2);
     const uint4* bk1 = reinterpret_cast<const uint4*>(m.ng + (size_t)b1 * NG_WAYS);
@@ -261,7 +281,12 @@ __device__ void quad_score_word(const ModelDev& m, bool act, const uint32_t h[MA
       val = pk[j];
       hitk = j;
     }
-  for (int j = min(hitk, hl) - 1; j >= 0; --j) val = xadd(hbo[j], val);
+  {
+    const int lim = min(hitk, hl);  // right-nested back-off sum, j = lim-1 .. 0
+    if (lim > 2) val = xadd(hbo[2], val);
+    if (lim > 1) val = xadd(hbo[1], val);
+    if (lim > 0) val = xadd(hbo[0], val);
+  }
   out.inc = val;
   if (m.order > 1) {
     const int start = max(0, hl + 1 - (m.order - 1));
@@ -270,9 +295,12 @@ __device__ void quad_score_word(const ModelDev& m, bool act, const uint32_t h[MA
     for (int j = 3; j >= 0; --j)
       if (j >= start && j <= hl && fk[j] && prob_present(pk[j])) sk = j;
     if (sk >= 0) {
-      int n = 0;
-      for (int t = sk; t < hl; ++t) out.succ[n++] = h[t];
-      out.succ[n++] = (uint32_t)w;
+      const int n = hl - sk + 1;  // successor = (h[sk..hl-1], w)
+#pragma unroll
+      for (int t = 0; t < MAXH; ++t) {
+        const int j = sk + t;
+        out.succ[t] = j < hl ? hist_at(h, j) : (j == hl ? (uint32_t)w : 0u);
+      }
       out.slen = n;
 #pragma unroll
       for (int t = 0; t < MAXH; ++t) {
@@ -1320,6 +1348,122 @@ constexpr int G_WARP = KC * OC * (int)sizeof(Ent);
 constexpr int GTOTAL = G_WARP + NWC * (int)sizeof(WarpScratch);
 }  // namespace small
 
+#ifdef LB_INLINE_FALLBACK
+#define LB_COLD __forceinline__
+#else
+#define LB_COLD __noinline__
+#endif
+// Exact radix-select fallback of frames_small_kernel (a histogram bin overflowed LC): compiled
+// out of line so its ~1300 instructions stay out of the frame loop's instruction-cache footprint.
+// Called by all NC compute threads; returns nsel with sval/skey in (value desc, index asc) order.
+__device__ LB_COLD int small_fallback_select(const CfgDev& c, int K, int V, int VP, double thr,
+                                             int blank, int space, int sink, const int32_t* rows,
+                                             const int32_t* C_LAST, const double* C_SCORE,
+                                             const double* drow, unsigned* hist, double* cval,
+                                             uint32_t* ckey, double* sval, uint32_t* skey,
+                                             int* s_inr, int* s_cnt2) {
+  using namespace small;
+  const int tid = threadIdx.x, lane = tid & 31;
+  int nsel;
+  // ---- fallback: exact radix select on the 96-bit key (ord64(value), ~flat index)
+  auto cval_at = [&](int f) -> double {
+    const int p = f / V, v = f - (f / V) * V;
+    const int lp = C_LAST[p];
+    const int nx = rows[p * VP + v];
+    if (!((nx != sink) || (v == blank) || (v == lp))) return -DBL_MAX;
+    const double x = cand_value(C_SCORE[p], drow[v], v, lp,
+                                FrameConsts{c.beta, c.gamma, blank, space});
+    return x > GUARD ? x : -DBL_MAX;
+  };
+  const int KV = K * V;
+  bar_sync(1, NC);
+  if (tid == 0) {
+    (*s_cnt2) = 0;
+    (*s_inr) = 0;
+  }
+  bar_sync(1, NC);
+  for (int f = tid; f < KV; f += NC)
+    if (cval_at(f) >= thr) atomicAdd(s_inr, 1);
+  bar_sync(1, NC);
+  nsel = min(c.k, (*s_inr));
+  uint64_t phi = 0, pmask_hi = 0;
+  uint32_t plo = 0, pmask_lo = 0;
+  int rem = nsel;
+  for (int pass = 0; pass < 12; ++pass) {
+    bar_sync(1, NC);
+    for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
+    bar_sync(1, NC);
+    for (int f = tid; f < KV; f += NC) {
+      const double x = cval_at(f);
+      if (!(x >= thr)) continue;
+      const uint64_t kh = ord64(x);
+      const uint32_t kl = ~(uint32_t)f;
+      if ((kh & pmask_hi) != phi || (kl & pmask_lo) != plo) continue;
+      const unsigned dg = pass < 8 ? (unsigned)((kh >> (56 - 8 * pass)) & 0xFF)
+                                   : (unsigned)((kl >> (24 - 8 * (pass - 8))) & 0xFF);
+      atomicAdd(&hist[dg], 1u);
+    }
+    bar_sync(1, NC);
+    int above = 0, dsel = 0;
+    for (int d = NBINS - 1; d >= 0; --d) {
+      const int h = (int)hist[d];
+      if (above + h >= rem) {
+        dsel = d;
+        break;
+      }
+      above += h;
+    }
+    rem -= above;
+    if (pass < 8) {
+      phi |= (uint64_t)dsel << (56 - 8 * pass);
+      pmask_hi |= 0xFFull << (56 - 8 * pass);
+    } else {
+      plo |= (uint32_t)dsel << (24 - 8 * (pass - 8));
+      pmask_lo |= 0xFFu << (24 - 8 * (pass - 8));
+    }
+  }
+  bar_sync(1, NC);
+  for (int f0 = 0; f0 < KV; f0 += NC) {
+    const int f = f0 + tid;
+    bool take = false;
+    double x = 0.0;
+    if (f < KV) {
+      x = cval_at(f);
+      if (x >= thr) {
+        const uint64_t kh = ord64(x);
+        const uint32_t kl = ~(uint32_t)f;
+        take = kh > phi || (kh == phi && kl >= plo);
+      }
+    }
+    const unsigned bl = __ballot_sync(FULLMASK, take);
+    if (bl) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(s_cnt2, __popc(bl));
+      base = __shfl_sync(FULLMASK, base, 0);
+      if (take) {
+        const int pos = base + __popc(bl & ((1u << lane) - 1u));
+        cval[pos] = x;
+        ckey[pos] = (uint32_t)f;
+      }
+    }
+  }
+  bar_sync(1, NC);
+  for (int i = tid; i < nsel; i += NC) {
+    const double vi = cval[i];
+    const uint32_t ki = ckey[i];
+    int cnt = 0;
+    for (int j = 0; j < nsel; ++j) {
+      const double vj = cval[j];
+      cnt += (vj > vi) || (vj == vi && ckey[j] < ki);
+    }
+    sval[cnt] = vi;
+    skey[cnt] = ki;
+  }
+  for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
+  return nsel;
+}
+
+template <bool TIMING>
 __global__ void __launch_bounds__(small::NT, 2)
     frames_small_kernel(ModelDev m, CfgDev c, BatchDev b, int t0, int t1, int fusion_mode,
                         double scale) {
@@ -1455,7 +1599,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
   unsigned calls_l = 0, probes_l = 0;
   int fail_t = -1;
-  const bool timing = b.phase_cycles != nullptr && tid == 0;
+  const bool timing = TIMING && b.phase_cycles != nullptr && tid == 0;
   unsigned long long ph[NPHASE];
   for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
   long long tprev = timing ? clock64() : 0;
@@ -1720,102 +1864,9 @@ __global__ void __launch_bounds__(small::NT, 2)
             }
           }
         } else {
-          // ---- fallback: exact radix select on the 96-bit key (ord64(value), ~flat index)
           ++st_fallback;
-          auto cval_at = [&](int f) -> double {
-            const int p = f / V, v = f - (f / V) * V;
-            const int lp = C_LAST[p];
-            const int nx = rows[p * VP + v];
-            if (!((nx != sink) || (v == blank) || (v == lp))) return -DBL_MAX;
-            const double x = cand_value(C_SCORE[p], drow[v], v, lp,
-                                        FrameConsts{c.beta, c.gamma, blank, space});
-            return x > GUARD ? x : -DBL_MAX;
-          };
-          const int KV = K * V;
-          bar_sync(1, NC);
-          if (tid == 0) {
-            s_cnt2 = 0;
-            s_inr = 0;
-          }
-          bar_sync(1, NC);
-          for (int f = tid; f < KV; f += NC)
-            if (cval_at(f) >= thr) atomicAdd(&s_inr, 1);
-          bar_sync(1, NC);
-          nsel = min(c.k, s_inr);
-          uint64_t phi = 0, pmask_hi = 0;
-          uint32_t plo = 0, pmask_lo = 0;
-          int rem = nsel;
-          for (int pass = 0; pass < 12; ++pass) {
-            bar_sync(1, NC);
-            for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
-            bar_sync(1, NC);
-            for (int f = tid; f < KV; f += NC) {
-              const double x = cval_at(f);
-              if (!(x >= thr)) continue;
-              const uint64_t kh = ord64(x);
-              const uint32_t kl = ~(uint32_t)f;
-              if ((kh & pmask_hi) != phi || (kl & pmask_lo) != plo) continue;
-              const unsigned dg = pass < 8 ? (unsigned)((kh >> (56 - 8 * pass)) & 0xFF)
-                                           : (unsigned)((kl >> (24 - 8 * (pass - 8))) & 0xFF);
-              atomicAdd(&hist[dg], 1u);
-            }
-            bar_sync(1, NC);
-            int above = 0, dsel = 0;
-            for (int d = NBINS - 1; d >= 0; --d) {
-              const int h = (int)hist[d];
-              if (above + h >= rem) {
-                dsel = d;
-                break;
-              }
-              above += h;
-            }
-            rem -= above;
-            if (pass < 8) {
-              phi |= (uint64_t)dsel << (56 - 8 * pass);
-              pmask_hi |= 0xFFull << (56 - 8 * pass);
-            } else {
-              plo |= (uint32_t)dsel << (24 - 8 * (pass - 8));
-              pmask_lo |= 0xFFu << (24 - 8 * (pass - 8));
-            }
-          }
-          bar_sync(1, NC);
-          for (int f0 = 0; f0 < KV; f0 += NC) {
-            const int f = f0 + tid;
-            bool take = false;
-            double x = 0.0;
-            if (f < KV) {
-              x = cval_at(f);
-              if (x >= thr) {
-                const uint64_t kh = ord64(x);
-                const uint32_t kl = ~(uint32_t)f;
-                take = kh > phi || (kh == phi && kl >= plo);
-              }
-            }
-            const unsigned bl = __ballot_sync(FULLMASK, take);
-            if (bl) {
-              int base = 0;
-              if (lane == 0) base = atomicAdd(&s_cnt2, __popc(bl));
-              base = __shfl_sync(FULLMASK, base, 0);
-              if (take) {
-                const int pos = base + __popc(bl & ((1u << lane) - 1u));
-                cval[pos] = x;
-                ckey[pos] = (uint32_t)f;
-              }
-            }
-          }
-          bar_sync(1, NC);
-          for (int i = tid; i < nsel; i += NC) {
-            const double vi = cval[i];
-            const uint32_t ki = ckey[i];
-            int cnt = 0;
-            for (int j = 0; j < nsel; ++j) {
-              const double vj = cval[j];
-              cnt += (vj > vi) || (vj == vi && ckey[j] < ki);
-            }
-            sval[cnt] = vi;
-            skey[cnt] = ki;
-          }
-          for (int i = tid; i < NBINS; i += NC) hist[i] = 0;
+          nsel = small_fallback_select(c, K, V, VP, thr, blank, space, sink, rows, C_LAST, C_SCORE,
+                                       drow, hist, cval, ckey, sval, skey, &s_inr, &s_cnt2);
         }
       }
       bar_sync(2, NT);  // S3: selection done + speculative n-gram results ready
@@ -1852,43 +1903,66 @@ __global__ void __launch_bounds__(small::NT, 2)
               bs.x = -2;
             } else {
               const int q0 = ppoff[p], q1 = ppoff[p + 1];
-              int top[OC];
+              // running top-O pair list (total desc, q asc) in three registers (OC == 3)
+              static_assert(OC == 3, "top-O registers");
+              int t0 = 0, t1 = 0, t2 = 0;
               int ntop = 0;
               for (int q = q0; q < q1; ++q) {
                 if (!pres[q].valid) continue;
                 const double tq = pres[q].total;
-                int pos = ntop;
-                for (int i = 0; i < ntop; ++i)
-                  if (tq > pres[top[i]].total) {
-                    pos = i;
-                    break;
-                  }
+                int pos = 0;
+                if (ntop > 0 && !(tq > pres[t0].total)) {
+                  pos = 1;
+                  if (ntop > 1 && !(tq > pres[t1].total)) pos = (ntop > 2 && !(tq > pres[t2].total)) ? 3 : 2;
+                }
                 if (pos >= O) continue;
-                for (int i = min(ntop, O - 1); i > pos; --i) top[i] = top[i - 1];
-                top[pos] = q;
+                if (pos == 0) {
+                  t2 = t1;
+                  t1 = t0;
+                  t0 = q;
+                } else if (pos == 1) {
+                  t2 = t1;
+                  t1 = q;
+                } else {
+                  t2 = q;
+                }
                 ntop = min(ntop + 1, O);
               }
               if (ntop == 0) {
                 sc = NEG_INF;  // decoder.py:223-225
               } else {
-                const double best = pres[top[0]].total;
+                const double best = pres[t0].total;
                 const double floor_ = xsub(best, c.lambda);
                 int kept = 0;
-                while (kept < ntop && pres[top[kept]].total >= floor_) ++kept;
+                if (pres[t0].total >= floor_) {
+                  kept = 1;
+                  if (ntop > 1 && pres[t1].total >= floor_) {
+                    kept = 2;
+                    if (ntop > 2 && pres[t2].total >= floor_) kept = 3;
+                  }
+                }
                 const int base = atomicAdd(&s_ncount, kept);
                 if (base + kept > b.ncap) {
                   s_fail = 1;
                   sc = NEG_INF;
                 } else {
                   const size_t nbase = (size_t)trial * b.ncap;
-                  for (int i = 0; i < kept; ++i) {
-                    b.nparent[nbase + base + i] = pres[top[i]].node;
-                    b.nsurf[nbase + base + i] = pres[top[i]].surf;
+                  if (kept > 0) {
+                    b.nparent[nbase + base] = pres[t0].node;
+                    b.nsurf[nbase + base] = pres[t0].surf;
+                  }
+                  if (kept > 1) {
+                    b.nparent[nbase + base + 1] = pres[t1].node;
+                    b.nsurf[nbase + base + 1] = pres[t1].surf;
+                  }
+                  if (kept > 2) {
+                    b.nparent[nbase + base + 2] = pres[t2].node;
+                    b.nsurf[nbase + base + 2] = pres[t2].surf;
                   }
                   bs.x = kept;
                   bs.y = base;
-                  bs.z = (top[0] & 0xFFFF) | ((kept > 1 ? top[1] : 0) << 16);
-                  bs.w = (kept > 2 ? top[2] : 0) | ((kept > 3 ? top[3] : 0) << 16);
+                  bs.z = (t0 & 0xFFFF) | ((kept > 1 ? t1 : 0) << 16);
+                  bs.w = kept > 2 ? t2 : 0;
                   sc = xadd(x, xsub(best, C_ENTS[p * OC].total));
                 }
               }
@@ -2692,7 +2766,10 @@ int small_gscratch_bytes() { return small::GTOTAL; }
 
 cudaError_t set_smem_limit(int nthreads, int64_t bytes) {
   cudaError_t e = cudaSuccess;
-  e = cudaFuncSetAttribute(frames_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(frames_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           small::TOTAL);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(frames_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            small::TOTAL);
   if (e != cudaSuccess) return e;
 #define LB_SET(NCV)                                                                          \
@@ -2748,7 +2825,12 @@ cudaError_t frames(const ModelDev& m, const CfgDev& c, const BatchDev& b, const 
                    int t1, int fusion_mode, double scale, cudaStream_t st) {
   const size_t sm = (size_t)L.smem_bytes;
   if (L.small) {
-    frames_small_kernel<<<b.B, small::NT, sm, st>>>(m, c, b, t0, t1, fusion_mode, scale);
+    // the phase-timer build is a separate instantiation: the production kernel carries no
+    // timer state (it would cost registers at the 96-register cap)
+    if (b.phase_cycles != nullptr)
+      frames_small_kernel<true><<<b.B, small::NT, sm, st>>>(m, c, b, t0, t1, fusion_mode, scale);
+    else
+      frames_small_kernel<false><<<b.B, small::NT, sm, st>>>(m, c, b, t0, t1, fusion_mode, scale);
     ++g_launches;
     return cudaGetLastError();
   }

@@ -245,3 +245,30 @@ def test_decode_stream_raw_matches_batch_api():
         assert len(got) == len(want)
         for gb, wb in zip(got, want):
             assert [(r.text, r.score, r.nbest) for r in gb] == [(r.text, r.score, r.nbest) for r in wb]
+
+
+def test_selection_fallback_on_flat_frames():
+    """Flat / tied log-prob rows pile hundreds of candidates into one histogram bin, so the
+    kernels take the exact radix-select fallback; beams must still equal the oracle frame by
+    frame (ties resolved by flat index as in the reference's stable sort)."""
+    g, w = _world_runs()
+    rng = np.random.default_rng(5)
+    T = 40
+    ds = [np.full((T, 41), -np.log(41.0)),
+          -np.log(41.0) + 0.25 * rng.integers(0, 2, size=(T, 41)).astype(np.float64)]
+    for k in (64, 200):
+        cfg = PROFILES["b2t25"].replace(beam_size=k, llm_rescore_interval=1000)
+        dm = device_model(w.table, w.model)
+        batch = dm.batch(cfg, len(ds), T)
+        batch.enable_dump(True)
+        batch.clear_stats()
+        batch.load_logprobs(np.stack(ds), np.full(len(ds), T, dtype=np.int32))
+        batch.reset()
+        batch.run(0, T)
+        assert batch.stats()["fallback_selects"] > 0, k
+        for i, d in enumerate(ds):
+            s = O.OracleSearch(cfg, w.table, w.model, StubScorer(table={}))
+            for t in range(T):
+                s.frame(d[t], t)
+                assert batch.dump_frame(i, t) == s.snapshot(), (k, i, t)
+        batch.enable_dump(False)
