@@ -204,6 +204,26 @@ int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* b
                      double* best_score, int32_t* nbest_count, int64_t* nbest_text_off,
                      int32_t* nbest_text_len, double* nbest_score);
 
+/* Zero-copy view of the results assembled by the last lb_batch_results_size call: pointers
+ * into library-owned host buffers, valid until the next results call or lb_batch_destroy.
+ * Same content as lb_batch_results plus the per-trial status (0 = decoded).  Lets a binding
+ * build its result objects straight from the library's buffers (no blob copy). */
+typedef struct lb_results_view {
+  int32_t n_trials;
+  int64_t total_nbest;
+  int64_t blob_bytes;
+  const char* blob;
+  const int32_t* status;
+  const int64_t* best_text_off;
+  const int32_t* best_text_len;
+  const double* best_score;
+  const int32_t* nbest_count;
+  const int64_t* nbest_text_off;
+  const int32_t* nbest_text_len;
+  const double* nbest_score;
+} lb_results_view;
+int lb_batch_results_view(lb_batch* b, lb_results_view* out);
+
 /* A non-blocking CUDA stream for lb_batch_create (pipelining batches on separate streams). */
 int lb_stream_create(int32_t device, void** out);
 int lb_stream_destroy(void* stream);

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sysconfig
 import subprocess
 from pathlib import Path
 
@@ -34,8 +35,46 @@ NVCC_FLAGS = [
 SOURCES = ["lb_kernels.cu", "lb_capi.cu", "lb_llm.cu"]
 
 
+PYRES_PATH = PKG / f"_lb_results{sysconfig.get_config_var('EXT_SUFFIX')}"
+
+
+def build_pyresults(force: bool = False) -> Path:
+    """gcc -> the CPython result binding (csrc/lb_pyresults.c), skipped when up to date."""
+    src = CSRC / "lb_pyresults.c"
+    deps = [src, INCLUDE / "lightbeam_b200.h"]
+    if not force and PYRES_PATH.exists() and PYRES_PATH.stat().st_mtime >= max(
+            p.stat().st_mtime for p in deps):
+        return PYRES_PATH
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-std=c11",
+           f"-I{sysconfig.get_paths()['include']}", f"-I{INCLUDE}", "-o", str(PYRES_PATH), str(src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise DeviceError(f"result binding build failed ({' '.join(cmd)}):\n{res.stderr}")
+    return PYRES_PATH
+
+
+_PYRES = None
+
+
+def pyresults():
+    """The CPython result binding (built by build(); no pure-Python stand-in)."""
+    global _PYRES
+    if _PYRES is None:
+        if not PYRES_PATH.exists():
+            raise DeviceError(f"{PYRES_PATH.name} is missing: run __graft_entry__.build()")
+        import importlib.util
+
+        spec = importlib.util.spec_from_file_location("_lb_results", PYRES_PATH)
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        _PYRES = mod
+    return _PYRES
+
+
 def build(verbose: bool = False, force: bool = False) -> Path:
-    """nvcc -> paper_2603_14002_b200/_lightbeam_b200.so (skipped when up to date)."""
+    """nvcc -> paper_2603_14002_b200/_lightbeam_b200.so (skipped when up to date), plus the
+    CPython result binding."""
+    build_pyresults(force)
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
     deps.append(INCLUDE / "lightbeam_b200.h")
     if not force and LIB_PATH.exists():
@@ -52,6 +91,24 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if verbose:
         print(res.stderr)
     return LIB_PATH
+
+
+class LbResultsView(C.Structure):
+    """lb_results_view (include/lightbeam_b200.h)."""
+    _fields_ = [
+        ("n_trials", C.c_int32),
+        ("total_nbest", C.c_int64),
+        ("blob_bytes", C.c_int64),
+        ("blob", C.c_void_p),
+        ("status", C.c_void_p),
+        ("best_text_off", C.c_void_p),
+        ("best_text_len", C.c_void_p),
+        ("best_score", C.c_void_p),
+        ("nbest_count", C.c_void_p),
+        ("nbest_text_off", C.c_void_p),
+        ("nbest_text_len", C.c_void_p),
+        ("nbest_score", C.c_void_p),
+    ]
 
 
 class LbConfig(C.Structure):
@@ -160,6 +217,7 @@ _SIGS = {
     "lb_batch_dump_frame": (C.c_int, [_P, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "lb_batch_results_size": (C.c_int, [_P, _P, _P]),
     "lb_batch_results": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lb_batch_results_view": (C.c_int, [_P, _P]),
     "lb_batch_mark_begin": (C.c_int, [_P]),
     "lb_batch_mark_end": (C.c_int, [_P, _P, _P]),
     "lb_batch_sync": (C.c_int, [_P]),

@@ -5,6 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -689,6 +693,71 @@ static int pinned_reserve(T*& p, int64_t& cap, int64_t n) {
   return LB_OK;
 }
 
+// Persistent worker pool for the host-side result assembly (spawning threads per call cost
+// ~1 ms per config-2 batch).  run(n, f) calls f(0..n-1) on the workers and the caller.
+class HostPool {
+ public:
+  explicit HostPool(int nw) {
+    for (int w = 0; w < nw; ++w) th_.emplace_back([this] { loop(); });
+  }
+  template <typename F>
+  void run(int n, F&& f) {
+    if (n <= 0) return;
+    std::function<void(int)> fn(f);
+    if (th_.empty() || n == 1) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &fn;
+      n_ = n;
+      next_.store(0);
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (int i; (i = next_.fetch_add(1)) < n;) fn(i);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return active_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      int n;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        f = job_;
+        n = n_;
+        if (!f) continue;
+        ++active_;
+      }
+      for (int i; (i = next_.fetch_add(1)) < n;) (*f)(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--active_ == 0) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, active_ = 0;
+  uint64_t gen_ = 0;
+  std::atomic<int> next_{0};
+};
+
+static HostPool& host_pool() {
+  // never destroyed: workers block on the condition variable until process exit
+  static HostPool* pool = new HostPool(
+      std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 1)));
+  return *pool;
+}
+
 // Text of an entry = " ".join(surfaces) + punct.  When every surface is non-empty, unique, free
 // of ' ' and does not end in ".?!", (word ids, punct) -> text is injective, so the n-best text
 // dedupe (decoder.py:444-449) can compare word-id sequences and build strings only for the
@@ -732,26 +801,42 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
   rc = lb_batch_copy_entries(b, nullptr, e_beam, woff, words, totals, puncts);  // synchronises
   if (rc) return rc;
   static const char* PUN[4] = {"", ".", "?", "!"};
+  static const int PUNLEN[4] = {0, 1, 1, 1};
   const auto& surf = b->m->surfaces;
   if (b->injective < 0) b->injective = texts_injective(b->m) ? 1 : 0;
   const bool fast = b->injective == 1;
+  // phase A (parallel over trials): ranking + n-best dedupe -> selected entries, scores and
+  // text byte lengths; no strings are built on the injective path
   struct TrialOut {
-    std::string best;
+    int64_t best_e = -1;
     double best_score = 0.0;
-    std::vector<std::string> texts;
+    std::vector<int64_t> ents;
     std::vector<double> scores;
+    std::vector<int32_t> lens;
+    int32_t best_len = 0;
+    size_t bytes = 0;
   };
   std::vector<TrialOut> outs(B);
-  auto text_of = [&](int64_t e) {
-    std::string s2;
-    size_t len = 1;
-    for (int64_t w = woff[e]; w < woff[e + 1]; ++w) len += surf[words[w]].size() + 1;
-    s2.reserve(len);
+  auto text_len = [&](int64_t e) {
+    int64_t len = PUNLEN[puncts[e] & 3];
+    for (int64_t w = woff[e]; w < woff[e + 1]; ++w) len += (int64_t)surf[words[w]].size() + (w > woff[e]);
+    return (int32_t)len;
+  };
+  auto write_text = [&](int64_t e, char* dst) {
     for (int64_t w = woff[e]; w < woff[e + 1]; ++w) {
-      if (w > woff[e]) s2.push_back(' ');
-      s2 += surf[words[w]];
+      if (w > woff[e]) *dst++ = ' ';
+      const std::string& x = surf[words[w]];
+      std::memcpy(dst, x.data(), x.size());
+      dst += x.size();
     }
-    s2 += PUN[puncts[e] & 3];
+    const int pl = PUNLEN[puncts[e] & 3];
+    if (pl) *dst++ = PUN[puncts[e] & 3][0];
+    *dst = '\0';
+  };
+  auto text_of = [&](int64_t e) {
+    std::string s2((size_t)text_len(e) + 1, '\0');
+    write_text(e, &s2[0]);
+    s2.pop_back();
     return s2;
   };
   auto same_words = [&](int64_t x, int64_t y) {
@@ -787,6 +872,17 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
     std::stable_sort(pairs.begin(), pairs.end(),
                      [](const Pair& x, const Pair& y) { return x.score > y.score; });
     to.best_score = sc[order[0]];
+    to.best_e = first[order[0]];
+    to.best_len = text_len(to.best_e);
+    to.bytes = (size_t)to.best_len + 1;
+    to.ents.reserve(pairs.size());
+    auto keep = [&](const Pair& pr) {
+      const int32_t len = text_len(pr.e);
+      to.ents.push_back(pr.e);
+      to.scores.push_back(pr.score);
+      to.lens.push_back(len);
+      to.bytes += (size_t)len + 1;
+    };
     if (fast) {
       // dedupe on (word ids, punct): FNV hash buckets, exact comparison on hash match
       std::unordered_map<uint64_t, std::vector<int64_t>> seen;
@@ -803,75 +899,63 @@ int lb_batch_results_size(lb_batch* b, int64_t* blob_bytes, int64_t* total_nbest
           }
         if (dup) continue;
         bucket.push_back(pr.e);
-        to.texts.push_back(text_of(pr.e));
-        to.scores.push_back(pr.score);
+        keep(pr);
       }
-      to.best = text_of(first[order[0]]);
       return;
     }
     std::vector<std::string> texts(e1 - e0);
     for (int64_t e = e0; e < e1; ++e) texts[e - e0] = text_of(e);
-    to.best = texts[first[order[0]] - e0];
     std::unordered_set<std::string_view> seen;
     seen.reserve(pairs.size() * 2);
-    for (const Pair& pr : pairs) {
-      const std::string& tx = texts[pr.e - e0];
-      if (!seen.insert(std::string_view(tx)).second) continue;
-      to.texts.push_back(tx);
-      to.scores.push_back(pr.score);
-    }
+    for (const Pair& pr : pairs)
+      if (seen.insert(std::string_view(texts[pr.e - e0])).second) keep(pr);
   };
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  const int nthr = std::min(std::min(hw, 32), std::max(1, B / 8));
-  if (nthr <= 1) {
-    for (int t = 0; t < B; ++t) assemble(t);
-  } else {
-    std::vector<std::thread> pool;
-    for (int w = 0; w < nthr; ++w)
-      pool.emplace_back([&, w]() {
-        for (int t = w; t < B; t += nthr) assemble(t);
-      });
-    for (auto& th : pool) th.join();
+  host_pool().run(B, assemble);
+  // phase B (serial): blob layout -- per successful trial its best text then its n-best texts,
+  // each followed by a NUL (offsets/lengths exclude the separators)
+  std::vector<size_t> tb(B + 1, 0);
+  std::vector<int64_t> tn(B + 1, 0);
+  for (int t = 0; t < B; ++t) {
+    tb[t + 1] = tb[t] + outs[t].bytes;
+    tn[t + 1] = tn[t] + (int64_t)outs[t].ents.size();
   }
-  // blob: per successful trial its best text then its n-best texts, each followed by a NUL
-  // (offsets/lengths exclude the separators; the NULs let a caller split the blob in one call)
-  b->blob.clear();
+  const size_t total = tb[B];
+  const int64_t nn = tn[B];
+  if (total > b->blob_cap) {
+    b->blob_cap = std::max(total, 2 * b->blob_cap);
+    b->blob.reset(new char[b->blob_cap]);
+  }
+  b->blob_len = total;
   b->best_off.assign(B, 0);
   b->best_len.assign(B, 0);
   b->best_score.assign(B, 0.0);
   b->nb_count.assign(B, 0);
-  b->nb_off.clear();
-  b->nb_len.clear();
-  b->nb_score.clear();
-  size_t total = 0, nn = 0;
-  for (int t = 0; t < B; ++t) {
-    total += outs[t].best.size() + 1;
-    for (const auto& x : outs[t].texts) total += x.size() + 1;
-    nn += outs[t].texts.size();
-  }
-  b->blob.reserve(total);
-  b->nb_off.reserve(nn);
-  b->nb_len.reserve(nn);
-  b->nb_score.reserve(nn);
-  for (int t = 0; t < B; ++t) {
-    if (status[t] != 0) continue;
-    TrialOut& to = outs[t];
-    b->best_off[t] = (int64_t)b->blob.size();
-    b->blob += to.best;
-    b->blob.push_back('\0');
-    b->best_len[t] = (int32_t)to.best.size();
+  b->nb_off.resize(nn);
+  b->nb_len.resize(nn);
+  b->nb_score.resize(nn);
+  // phase C (parallel over trials): texts written in place
+  char* blob = b->blob.get();
+  host_pool().run(B, [&](int t) {
+    if (status[t] != 0) return;
+    const TrialOut& to = outs[t];
+    size_t at = tb[t];
+    b->best_off[t] = (int64_t)at;
+    b->best_len[t] = to.best_len;
     b->best_score[t] = to.best_score;
-    b->nb_count[t] = (int32_t)to.texts.size();
-    for (size_t i = 0; i < to.texts.size(); ++i) {
-      b->nb_off.push_back((int64_t)b->blob.size());
-      b->blob += to.texts[i];
-      b->blob.push_back('\0');
-      b->nb_len.push_back((int32_t)to.texts[i].size());
-      b->nb_score.push_back(to.scores[i]);
+    write_text(to.best_e, blob + at);
+    at += (size_t)to.best_len + 1;
+    const int64_t q0 = tn[t];
+    b->nb_count[t] = (int32_t)to.ents.size();
+    for (size_t i = 0; i < to.ents.size(); ++i) {
+      b->nb_off[q0 + i] = (int64_t)at;
+      b->nb_len[q0 + i] = to.lens[i];
+      b->nb_score[q0 + i] = to.scores[i];
+      write_text(to.ents[i], blob + at);
+      at += (size_t)to.lens[i] + 1;
     }
-  }
-  *blob_bytes = (int64_t)b->blob.size();
-  *total_nbest = (int64_t)b->nb_score.size();
+  });
+  *blob_bytes = (int64_t)total;
+  *total_nbest = nn;
   return LB_OK;
 }
 
@@ -880,7 +964,7 @@ int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* b
                      int32_t* nbest_text_len, double* nbest_score) {
   if (!b) return fail(LB_ERR_ARG, "null argument");
   const int B = b->n_trials;
-  if (blob && !b->blob.empty()) std::memcpy(blob, b->blob.data(), b->blob.size());
+  if (blob && b->blob_len) std::memcpy(blob, b->blob.get(), b->blob_len);
   for (int t = 0; t < B; ++t) {
     if (best_text_off) best_text_off[t] = b->best_off[t];
     if (best_text_len) best_text_len[t] = b->best_len[t];
@@ -893,6 +977,25 @@ int lb_batch_results(lb_batch* b, char* blob, int64_t* best_text_off, int32_t* b
     if (nbest_text_len) nbest_text_len[i] = b->nb_len[i];
     if (nbest_score) nbest_score[i] = b->nb_score[i];
   }
+  return LB_OK;
+}
+
+int lb_batch_results_view(lb_batch* b, lb_results_view* out) {
+  if (!b || !out) return fail(LB_ERR_ARG, "null argument");
+  const int B = b->n_trials;
+  if ((int)b->best_off.size() != B || !b->h_misc) return fail(LB_ERR_STATE, "call lb_batch_results_size first");
+  out->n_trials = B;
+  out->total_nbest = (int64_t)b->nb_score.size();
+  out->blob_bytes = (int64_t)b->blob_len;
+  out->blob = b->blob.get();
+  out->status = b->h_misc + B;
+  out->best_text_off = b->best_off.data();
+  out->best_text_len = b->best_len.data();
+  out->best_score = b->best_score.data();
+  out->nbest_count = b->nb_count.data();
+  out->nbest_text_off = b->nb_off.data();
+  out->nbest_text_len = b->nb_len.data();
+  out->nbest_score = b->nb_score.data();
   return LB_OK;
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/lightbeam_b200.h"
@@ -53,7 +54,8 @@ struct lb_batch {
   int64_t n_entries = 0, n_words = 0;
   std::vector<int64_t> h_entry_off, h_word_off;
   // results cache
-  std::string blob;
+  std::unique_ptr<char[]> blob;  // result texts (uninitialised growth buffer)
+  size_t blob_len = 0, blob_cap = 0;
   std::vector<int64_t> best_off, nb_off;
   std::vector<int32_t> best_len, nb_count, nb_len;
   std::vector<double> best_score, nb_score;

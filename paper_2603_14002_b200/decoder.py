@@ -348,51 +348,15 @@ class DeviceBatch:
         N.check(N.lib().lb_batch_sync(self.h))
 
     def results(self):
-        """[(text, score, nbest)] per trial (None for failed trials)."""
+        """[(text, score, nbest)] per trial (None for failed trials).  The library ranks and
+        dedupes on the host (lb_batch_results_size); the CPython binding `_lb_results` builds the
+        Python objects straight from the library's buffers (lb_batch_results_view)."""
         lib = N.lib()
         nbytes, ntot = C.c_int64(), C.c_int64()
         N.check(lib.lb_batch_results_size(self.h, C.byref(nbytes), C.byref(ntot)))
-        n = self.n
-        blob = C.create_string_buffer(max(nbytes.value, 1))
-        boff = np.empty(n, dtype=np.int64)
-        blen = np.empty(n, dtype=np.int32)
-        bsc = np.empty(n, dtype=np.float64)
-        cnt = np.empty(n, dtype=np.int32)
-        m = max(ntot.value, 1)
-        noff = np.empty(m, dtype=np.int64)
-        nlen = np.empty(m, dtype=np.int32)
-        nsc = np.empty(m, dtype=np.float64)
-        N.check(lib.lb_batch_results(self.h, blob, N.ptr(boff), N.ptr(blen), N.ptr(bsc),
-                                     N.ptr(cnt), N.ptr(noff), N.ptr(nlen), N.ptr(nsc)))
-        # the blob holds, per successful trial, its best text and then its n-best texts, each
-        # NUL-terminated: one split() builds every Python string
-        raw = blob.raw[: nbytes.value]
-        parts = raw.decode("utf-8").split("\x00")
-        st, _ = self.status()
-        bsc_l, cnt_l, nsc_l = bsc.tolist(), cnt.tolist(), nsc.tolist()
-        if len(parts) != sum(cnt_l[i] + 1 for i in range(n) if st[i] == 0) + 1:
-            # a surface contains NUL: rebuild the texts from the offsets instead
-            parts = []
-            noff_l, nlen_l, boff_l, blen_l = noff.tolist(), nlen.tolist(), boff.tolist(), blen.tolist()
-            j = 0
-            for i in range(n):
-                if st[i] != 0:
-                    continue
-                parts.append(raw[boff_l[i]: boff_l[i] + blen_l[i]].decode("utf-8"))
-                for q in range(j, j + cnt_l[i]):
-                    parts.append(raw[noff_l[q]: noff_l[q] + nlen_l[q]].decode("utf-8"))
-                j += cnt_l[i]
-        out = []
-        k = j = 0
-        for i in range(n):
-            if st[i] != 0:
-                out.append(None)
-                continue
-            c = cnt_l[i]
-            out.append((parts[k], bsc_l[i], list(zip(parts[k + 1: k + 1 + c], nsc_l[j: j + c]))))
-            k += c + 1
-            j += c
-        return out
+        view = N.LbResultsView()
+        N.check(lib.lb_batch_results_view(self.h, C.byref(view)))
+        return N.pyresults().assemble(C.addressof(view))
 
 
 def _host_fusion(batch: DeviceBatch, scorer, cfg, final: bool, min_frames: int):

@@ -327,3 +327,33 @@ def test_load_logits_batch_matches_single_loads(tmp_path):
     for i in (0, 2, 3):
         want = load_logits(paths[i], vocab).frames
         assert np.array_equal(arr[i, : frames[i]], want) and ms[i] == 80.0
+
+
+def test_results_binding_builds_objects_from_a_view():
+    """The CPython result binding (csrc/lb_pyresults.c) on a hand-made lb_results_view: texts by
+    offset (utf-8, no separators needed), None for failed trials, n-best pairs in order."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2603_14002_b200 import _native as N
+
+    texts = ["héllo world", "héllo word.", "hello", "x y z?"]
+    blob = b"".join(t.encode() for t in texts)
+    offs = np.cumsum([0] + [len(t.encode()) for t in texts])[:-1].astype(np.int64)
+    lens = np.array([len(t.encode()) for t in texts], dtype=np.int32)
+    buf = C.create_string_buffer(blob, len(blob))
+    status = np.array([0, 2, 0], dtype=np.int32)
+    best_off = np.array([offs[0], 0, offs[3]], dtype=np.int64)
+    best_len = np.array([lens[0], 0, lens[3]], dtype=np.int32)
+    best_sc = np.array([-1.5, 0.0, -7.25])
+    cnt = np.array([2, 0, 1], dtype=np.int32)
+    nb_off = np.array([offs[1], offs[2], offs[3]], dtype=np.int64)
+    nb_len = np.array([lens[1], lens[2], lens[3]], dtype=np.int32)
+    nb_sc = np.array([-1.5, -2.0, -7.25])
+    v = N.LbResultsView(3, 3, len(blob), C.addressof(buf), status.ctypes.data, best_off.ctypes.data,
+                        best_len.ctypes.data, best_sc.ctypes.data, cnt.ctypes.data,
+                        nb_off.ctypes.data, nb_len.ctypes.data, nb_sc.ctypes.data)
+    got = N.pyresults().assemble(C.addressof(v))
+    assert got == [("héllo world", -1.5, [("héllo word.", -1.5), ("hello", -2.0)]), None,
+                   ("x y z?", -7.25, [("x y z?", -7.25)])]

@@ -50,3 +50,24 @@ for rep in range(2):
     t2 = time.perf_counter()
     print("results_size (gather+D2H+assembly) ms", round((t1 - t0) * 1e3, 2), "full results() ms",
           round((t2 - t1) * 1e3, 2), "nbest entries", ntot.value, "blob bytes", nbytes.value)
+
+# split of _collect: status, results_size (C), binding, DecodeResult loop
+for rep in range(3):
+    batch = dm.batch(cfg, 256, 500)
+    batch.load_logits(raws, frames)
+    D.run_search(batch, cfg, sc, w.model, True); batch.sync()
+    lib = N.lib()
+    t0 = time.perf_counter()
+    st, ff = batch.status()
+    t1 = time.perf_counter()
+    nbytes, ntot = C.c_int64(), C.c_int64()
+    N.check(lib.lb_batch_results_size(batch.h, C.byref(nbytes), C.byref(ntot)))
+    t2 = time.perf_counter()
+    view = N.LbResultsView()
+    N.check(lib.lb_batch_results_view(batch.h, C.byref(view)))
+    res = N.pyresults().assemble(C.addressof(view))
+    t3 = time.perf_counter()
+    out = [D.DecodeResult(r[0], r[1], r[2], int(batch.frames[i]), 0.0, 0) for i, r in enumerate(res)]
+    t4 = time.perf_counter()
+    print("status %.2f results_size %.2f binding %.2f DecodeResult loop %.2f ms" %
+          tuple(1e3 * x for x in (t1 - t0, t2 - t1, t3 - t2, t4 - t3)))
