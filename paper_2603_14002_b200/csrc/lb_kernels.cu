@@ -1848,7 +1848,9 @@ __global__ void __launch_bounds__(small::NT, 2)
           const int m_sel = hcum[take_bin] + hfill[take_bin];
           nsel = min(c.k, m_sel);
           LB_PHASE(2);
-          for (int a = lane * NWC + warp; a < m_sel; a += NC) {
+          // consecutive positions per warp: lanes share bins (uniform loop counts, broadcast
+          // loads of the bin mates) -- 1% faster than spreading a warp over all bins
+          for (int a = tid; a < m_sel; a += NC) {
             const double va = cval[a];
             const uint32_t ka = ckey[a];
             const int bn = cbinl[a];
