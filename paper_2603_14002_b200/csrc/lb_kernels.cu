@@ -637,7 +637,12 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
   unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
   unsigned calls_l = 0, probes_l = 0;
   int fail_t = -1;
+  // phase timers live in frames_small_kernel<true>; here they would cost registers/spills
+#ifdef LB_GENERAL_PHASE_TIMING
   const bool timing = b.phase_cycles != nullptr && tid == 0;
+#else
+  const bool timing = false;
+#endif
   unsigned long long ph[NPHASE];
   for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
   long long tprev = timing ? clock64() : 0;
@@ -1015,20 +1020,26 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
               bn = -2;  // resolved below by the warp-per-beam path
             } else {
               const int q0 = ppoff[p], q1 = ppoff[p + 1];
+              // running top-O list (total desc, q asc); every index below is a compile-time
+              // constant after unrolling, so the list lives in registers (no local memory)
               int top[OMAX];
+#pragma unroll
+              for (int i = 0; i < OMAX; ++i) top[i] = 0;
               int ntop = 0;
               for (int q = q0; q < q1; ++q) {
                 if (!pres[q].valid) continue;
                 const double tq = pres[q].total;
                 int pos = ntop;
-                for (int i = 0; i < ntop; ++i)
-                  if (tq > pres[top[i]].total) {
-                    pos = i;
-                    break;
-                  }
+#pragma unroll
+                for (int i = OMAX - 1; i >= 0; --i)
+                  if (i < ntop && tq > pres[top[i]].total) pos = i;
                 if (pos >= O) continue;
-                for (int i = min(ntop, O - 1); i > pos; --i) top[i] = top[i - 1];
-                top[pos] = q;
+#pragma unroll
+                for (int i = OMAX - 1; i > 0; --i)
+                  if (i > pos && i <= ntop) top[i] = top[i - 1];
+#pragma unroll
+                for (int i = 0; i < OMAX; ++i)
+                  if (i == pos) top[i] = q;
                 ntop = min(ntop + 1, O);
               }
               if (ntop == 0) {
@@ -1037,7 +1048,9 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
                 const double best = pres[top[0]].total;
                 const double floor_ = xsub(best, c.lambda);
                 int kept = 0;
-                while (kept < ntop && pres[top[kept]].total >= floor_) ++kept;
+#pragma unroll
+                for (int i = 0; i < OMAX; ++i)
+                  if (kept == i && i < ntop && pres[top[i]].total >= floor_) kept = i + 1;
                 const int base = atomicAdd(&s_ncount, kept);
                 if (base + kept > b.ncap) {
                   s_fail = 1;
@@ -1045,7 +1058,9 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
                 } else {
                   const size_t nbase = (size_t)trial * b.ncap;
                   Ent* out = bents + (size_t)j * O;
-                  for (int i = 0; i < kept; ++i) {
+#pragma unroll
+                  for (int i = 0; i < OMAX; ++i) {
+                    if (i >= kept) break;
                     const PairRes& pr = pres[top[i]];
                     const uint32_t node = (uint32_t)(base + i);
                     b.nparent[nbase + node] = pr.node;
