@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
   __shared__ int hfill[NBINS];  // counting-sort fill pointers
   __shared__ double wmax[NWC];
   __shared__ double s_maxs;     // max beam score entering the frame
-  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP;
+  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov;
   __shared__ int ngtot[2];
   __shared__ unsigned s_calls, s_probes;
 
@@ -690,14 +690,23 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
       if (gt == 0) {
         ppoff[K] = carry;
         s_ngP = carry;
+        if (carry <= L.pcap) s_ngcov = carry;
       }
       const int P = carry;
-      if (P <= L.pcap) {
+      // parents are in score order: when the pairs exceed the cap, speculate the leading
+      // parents whose pairs all fit (s_ngcov pairs); the rest take the warp path after S4
+      for (int p = gt; p < K; p += NGT) {
+        const int q0 = ppoff[p], q1 = p + 1 < K ? ppoff[p + 1] : P;
+        if (q1 > L.pcap && q0 <= L.pcap) s_ngcov = q0;  // the first parent that does not fit
+      }
+      bar_sync(3, NGT);
+      const int PCOV = s_ngcov;
+      {
         constexpr int NG = NGT / 8;
         const int grp = gt >> 3, sub = lane & 7;
-        for (int q0 = 0; q0 < P; q0 += NG) {
+        for (int q0 = 0; q0 < PCOV; q0 += NG) {
           const int q = q0 + grp;
-          const bool act = q < P;
+          const bool act = q < PCOV;
           int w = -1, surf = -1, p = 0, e = 0;
           if (act) {
             int lo = 0, hi = K - 1;  // last parent with ppoff[p] <= q
@@ -995,7 +1004,8 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
       LB_PHASE(3);
 
       if (!dead) {
-        const bool ngover = s_ngP > L.pcap;
+        const int ncov = s_ngcov;
+        const bool ngover = ncov < s_ngP;  // some parents' pairs were not speculated
         // ---- F: materialise survivors (decoder.py:272-291); a new word-boundary emitter merges
         // its parent's precomputed (entry, surface) pairs (decoder.py:208-235) right here
         for (int j = tid; j < nsel; j += NC) {
@@ -1016,7 +1026,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
           int bn = -1;
           if (emit && tok == m.space) {
             blist[atomicAdd(&s_nb, 1)] = j;
-            if (ngover) {
+            if (ppoff[p + 1] > ncov) {
               bn = -2;  // resolved below by the warp-per-beam path
             } else {
               const int q0 = ppoff[p], q1 = ppoff[p + 1];
@@ -1096,6 +1106,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
           // rare: more pairs than the speculative round holds -> one warp per boundary beam
           for (int bi = warp; bi < nb; bi += NWC) {
             const int j = blist[bi];
+            if (bnent[j] != -2) continue;  // speculated parent
             const int p = npar[j];
             int outn = -1;
             double sc = nscore[j];
@@ -1126,21 +1137,34 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
         const bool ib = act && (bnent[i] != -1 || si <= GUARD);  // crossed a boundary
         int cnt = 0;
         if (act) {
+          // regular beams keep sval order (score desc, j asc): those beating a boundary beam
+          // are the regular indices below e (two binary searches over sval); the boundary
+          // beams below e are subtracted in the loop that compares the boundary beams
+          int e = 0;
+          if (ib) {
+            int lo = 0, hi = n;  // first j with sval[j] <= si
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (sval[mid] > si) lo = mid + 1;
+              else hi = mid;
+            }
+            const int a = lo;
+            hi = n;  // first j with sval[j] < si
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (sval[mid] >= si) lo = mid + 1;
+              else hi = mid;
+            }
+            e = max(a, min(lo, i));
+          }
           // boundary beams beating i (+ count of boundary beams before i when i is regular)
           for (int k2 = r; k2 < nb; k2 += G) {
             const int j = blist[k2];
             const double sj = nscore[j];
             cnt += (sj > si) || (sj == si && j < i);
-            if (!ib) cnt -= (j < i);
+            cnt -= ib ? (j < e) : (j < i);
           }
-          if (ib) {
-            // regular beams beating a boundary beam: scan (they are the non-boundary indices)
-            for (int j = r; j < n; j += G) {
-              if (bnent[j] != -1 || nscore[j] <= GUARD) continue;
-              const double sj = nscore[j];
-              cnt += (sj > si) || (sj == si && j < i);
-            }
-          }
+          if (ib && r == 0) cnt += e;
         }
         for (int o = G >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULLMASK, cnt, o);
         if (act && r == 0) {

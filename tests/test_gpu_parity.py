@@ -272,3 +272,18 @@ def test_selection_fallback_on_flat_frames():
                 s.frame(d[t], t)
                 assert batch.dump_frame(i, t) == s.snapshot(), (k, i, t)
         batch.enable_dump(False)
+
+
+def test_wide_beam_general_kernel_device_ngram():
+    """Beam 200 runs the general frames kernel (speculated + warp-path n-gram pairs, binary-search
+    recombination ranking): transcripts, scores and n-best lists equal the oracle."""
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=200)
+    raws = synth.make_logits(6, 160, 41, base_seed=2024)
+    ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+    scale = cfg.ngram_weight / cfg.llm_weight
+    got = decode_batch(ds, cfg, w.table, w.model, DeviceNgramScorer(w.model, scale), final_llm_only=True)
+    for i, d in enumerate(ds):
+        want = O.decode(d, cfg, w.table, w.model, StubScorer(ngram_model=w.model, scale=scale),
+                        final_llm_only=True)
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest), i
