@@ -23,8 +23,11 @@ def main():
     with torch.no_grad():
         ref, _ = dense_forward(W, ids, lens, False, exact_fp32=True)
         ref = np.array(ref)
-        for split in [(), ("lm",), ("attn",), ("attn", "lm"), ("qkv", "o", "gu", "down", "attn"),
-                      ("qkv", "o", "gu", "down", "attn", "lm")]:
+        full = ("qkv", "o", "gu", "down", "attn", "lm")
+        variants = [(), full] + [tuple(x for x in full if x != drop) for drop in full]
+        if len(sys.argv) > 2:
+            variants = [tuple(v.split("+")) if v else () for v in sys.argv[2].split(",")]
+        for split in variants:
             got, _ = dense_forward(W, ids, lens, False, split=frozenset(split))
             err = np.abs(np.array(got) - ref) / (S - 1)
             tot = np.abs(np.array(got) - ref)
