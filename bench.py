@@ -239,9 +239,14 @@ class ClockSampler:
 def algorithmic_bytes(stats, V=41, VP=44):
     """SURVEY.md §8(d) per-frame bytes, from the run's own counters:
     logit/log-prob row (8 B x V fp64 as the kernel reads it) + lexicon rows gathered for the
-    mask (4 B x V per beam entering the frame) + n-gram probes (one 32-B record each)
-    + word-history node writes (20 B) + completion CSR reads (8 B per boundary beam)."""
-    return (8 * V * stats["frames"] + 4 * V * stats["beams_in"] + 32 * stats["ngram_probes"]
+    mask (4 B x V per beam entering the frame) + n-gram probes (one 32-B record each) of the
+    pairs the word-boundary beams consume (the reference's score_word calls; the kernel's
+    speculative pairs for beams that are not selected do not count) + word-history node
+    writes (20 B) + completion CSR reads (8 B per boundary beam)."""
+    probes = stats["ngram_probes"]
+    if stats.get("ngram_calls") and stats.get("ngram_pairs_used") is not None:
+        probes = probes * stats["ngram_pairs_used"] / stats["ngram_calls"]
+    return (8 * V * stats["frames"] + 4 * V * stats["beams_in"] + 32 * probes
             + 20 * stats["history_nodes"] + 8 * stats["boundary_beams"])
 
 

@@ -111,6 +111,8 @@ typedef struct {
   uint64_t boundary_beams;
   uint64_t history_nodes;
   uint64_t fallback_selects; /* frames that needed the radix fallback */
+  uint64_t ngram_pairs_used; /* (entry, surface) pairs the word-boundary beams consume: the
+                                reference's score_word calls (ngram_calls adds speculation) */
 } lb_stats;
 
 const char* lb_last_error(void);

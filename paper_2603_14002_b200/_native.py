@@ -161,7 +161,7 @@ class LbNgramDesc(C.Structure):
 class LbStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "frames", "beams_in", "beams_out", "ngram_calls", "ngram_probes", "boundary_beams",
-        "history_nodes", "fallback_selects")]
+        "history_nodes", "fallback_selects", "ngram_pairs_used")]
 
 
 class LbLlmDesc(C.Structure):

@@ -580,6 +580,7 @@ int lb_batch_stats(lb_batch* b, lb_stats* out) {
     out->ngram_probes += s[8 * i + 4];
     out->boundary_beams += s[8 * i + 5];
     out->fallback_selects += s[8 * i + 7];
+    out->ngram_pairs_used += s[8 * i + 6];
     out->history_nodes += (uint64_t)std::max(0, nc[i] - 1);
   }
   return LB_OK;

@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
   __shared__ double s_maxs;     // max beam score entering the frame
   __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov;
   __shared__ int ngtot[2];
-  __shared__ unsigned s_calls, s_probes;
+  __shared__ unsigned s_calls, s_probes, s_pairs;
 
   const int trial = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -606,6 +606,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
     s_fail = 0;
     s_status = 0;
     s_calls = 0;
+    s_pairs = 0;
     s_probes = 0;
     s_K = K;
     mbar_init(&dbar[0], 1);
@@ -635,7 +636,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
   if (tid == 0) issue_chunk(0);
 
   unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
-  unsigned calls_l = 0, probes_l = 0;
+  unsigned calls_l = 0, probes_l = 0, pairs_l = 0;
   int fail_t = -1;
   // phase timers live in frames_small_kernel<true>; here they would cost registers/spills
 #ifdef LB_GENERAL_PHASE_TIMING
@@ -1026,6 +1027,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
           int bn = -1;
           if (emit && tok == m.space) {
             blist[atomicAdd(&s_nb, 1)] = j;
+            pairs_l += (unsigned)(ppoff[p + 1] - ppoff[p]);
             if (ppoff[p + 1] > ncov) {
               bn = -2;  // resolved below by the warp-per-beam path
             } else {
@@ -1324,6 +1326,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
     for (int i = tid; i < K * O * ENT_U4; i += NT) dst[i] = src[i];
   }
   atomicAdd(&s_calls, calls_l);
+  if (pairs_l) atomicAdd(&s_pairs, pairs_l);
   atomicAdd(&s_probes, probes_l);
   __syncthreads();
   if (tid == 0) {
@@ -1334,6 +1337,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
     stt[3] += s_calls;
     stt[4] += s_probes;
     stt[5] += st_bound;
+    stt[6] += s_pairs;  // (entry, surface) pairs the boundary beams consume (reference score_word calls)
     stt[7] += st_fallback;
   }
 }
@@ -1516,7 +1520,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   __shared__ double s_maxs;
   __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov, s_inr, s_cnt2;
   __shared__ int ngtot[2];
-  __shared__ unsigned s_calls, s_probes;
+  __shared__ unsigned s_calls, s_probes, s_pairs;
 
   const int trial = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1607,6 +1611,7 @@ __global__ void __launch_bounds__(small::NT, 2)
     s_fail = 0;
     s_status = 0;
     s_calls = 0;
+    s_pairs = 0;
     s_probes = 0;
     s_K = K;
     mbar_init(&dbar[0], 1);
@@ -1636,7 +1641,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   if (tid == 0) issue_chunk(0);
 
   unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
-  unsigned calls_l = 0, probes_l = 0;
+  unsigned calls_l = 0, probes_l = 0, pairs_l = 0;
   int fail_t = -1;
   const bool timing = TIMING && b.phase_cycles != nullptr && tid == 0;
   unsigned long long ph[NPHASE];
@@ -1940,6 +1945,7 @@ __global__ void __launch_bounds__(small::NT, 2)
           LB_PHASE(14);
           if (emit && tok == space) {
             blist[atomicAdd(&s_nb, 1)] = j;
+            pairs_l += (unsigned)(ppoff[p + 1] - ppoff[p]);
             if (ppoff[p + 1] > ncov) {
               bs.x = -2;
             } else {
@@ -2265,6 +2271,7 @@ __global__ void __launch_bounds__(small::NT, 2)
     }
   }
   atomicAdd(&s_calls, calls_l);
+  if (pairs_l) atomicAdd(&s_pairs, pairs_l);
   atomicAdd(&s_probes, probes_l);
   __syncthreads();
   if (tid == 0) {
@@ -2275,6 +2282,7 @@ __global__ void __launch_bounds__(small::NT, 2)
     stt[3] += s_calls;
     stt[4] += s_probes;
     stt[5] += st_bound;
+    stt[6] += s_pairs;  // (entry, surface) pairs the boundary beams consume (reference score_word calls)
     stt[7] += st_fallback;
   }
 #undef BUF
@@ -2304,7 +2312,7 @@ __global__ void __launch_bounds__(CLOSE_NT) close_kernel(ModelDev m, CfgDev c, B
   constexpr int NT = CLOSE_NT, NW = NT / 32;
   __shared__ WarpScratch wsc[NW];
   __shared__ int s_ncount, s_fail;
-  __shared__ unsigned s_calls, s_probes;
+  __shared__ unsigned s_calls, s_probes, s_pairs;
   extern __shared__ __align__(16) Ent close_tmp[];
   const int trial = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2317,6 +2325,7 @@ __global__ void __launch_bounds__(CLOSE_NT) close_kernel(ModelDev m, CfgDev c, B
     s_ncount = b.ncount[trial];
     s_fail = 0;
     s_calls = 0;
+    s_pairs = 0;
     s_probes = 0;
   }
   __syncthreads();
