@@ -705,7 +705,10 @@ class HostPool {
   void run(int n, F&& f) {
     if (n <= 0) return;
     std::function<void(int)> fn(f);
-    if (th_.empty() || n == 1) {
+    // one job at a time: batches driven from different host threads share the pool, and a
+    // caller that finds it busy runs its job inline instead of waiting
+    std::unique_lock<std::mutex> owner(run_mu_, std::try_to_lock);
+    if (!owner.owns_lock() || th_.empty() || n == 1) {
       for (int i = 0; i < n; ++i) fn(i);
       return;
     }
@@ -744,7 +747,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> th_;
-  std::mutex mu_;
+  std::mutex run_mu_, mu_;
   std::condition_variable cv_, done_;
   const std::function<void(int)>* job_ = nullptr;
   int n_ = 0, active_ = 0;

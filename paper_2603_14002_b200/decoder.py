@@ -25,6 +25,7 @@ kernel reads the scores from the cache.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import time
 import weakref
 from dataclasses import dataclass
@@ -83,7 +84,15 @@ class DeviceModel:
         handle = C.c_void_p()
         N.check(lib.lb_model_create(C.byref(td), C.byref(nd), device, C.byref(handle)))
         self.handle = handle
-        self._batches: dict = {}
+        # per host thread: batch handles are not thread-safe (SURVEY §8b threading row), so each
+        # thread gets its own LRU of batches and its own pipeline pair
+        self._per_thread: dict = {}
+        self._lock = threading.Lock()
+
+    def _mine(self) -> dict:
+        tid = threading.get_ident()
+        with self._lock:
+            return self._per_thread.setdefault(tid, {"lru": {}, "pipe": {}})
 
     def footprint(self) -> int:
         out = C.c_int64()
@@ -95,22 +104,23 @@ class DeviceModel:
             "acoustic_scale", "beam_prune_threshold", "homophone_prune_threshold",
             "token_insertion_bonus", "word_boundary_bonus", "ngram_weight", "llm_weight",
             "beam_size", "ortho_beams", "llm_rescore_interval", "llm_chunk_size"))
-        got = self._batches.pop(key, None)
+        lru = self._mine()["lru"]
+        got = lru.pop(key, None)
         if got is None or got.max_trials < n_trials or got.max_frames < n_frames:
             if got is not None:
                 got.destroy()
-            while len(self._batches) >= self.MAX_CACHED_BATCHES:  # evict the least recently used
-                old = self._batches.pop(next(iter(self._batches)))
+            while len(lru) >= self.MAX_CACHED_BATCHES:  # evict the least recently used
+                old = lru.pop(next(iter(lru)))
                 old.destroy()
             got = DeviceBatch(self, cfg, max(n_trials, 1), max(n_frames, 1))
-        self._batches[key] = got  # most recently used last
+        lru[key] = got  # most recently used last
         return got
 
     def pipeline_batch(self, cfg, slot: int, n_trials: int, n_frames: int) -> "DeviceBatch":
         """One of the two DeviceBatch objects `decode_stream_raw` alternates between, each on its
         own CUDA stream."""
         key = (slot, cfg)
-        pipe = self.__dict__.setdefault("_pipe", {})
+        pipe = self._mine()["pipe"]
         got = pipe.get(slot)
         if got is not None and (got[0] != key or got[1].max_trials < n_trials
                                 or got[1].max_frames < n_frames):
@@ -143,8 +153,9 @@ class DeviceModel:
 
     def __del__(self):
         try:
-            for b in self._batches.values():
-                b.destroy()
+            for per in self._per_thread.values():
+                for b in list(per["lru"].values()) + [x[1] for x in per["pipe"].values()]:
+                    b.destroy()
             if getattr(self, "handle", None):
                 N.lib(False).lb_model_destroy(self.handle)
                 self.handle = None

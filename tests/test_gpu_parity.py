@@ -287,3 +287,41 @@ def test_wide_beam_general_kernel_device_ngram():
         want = O.decode(d, cfg, w.table, w.model, StubScorer(ngram_model=w.model, scale=scale),
                         final_llm_only=True)
         assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest), i
+
+
+def test_concurrent_host_threads():
+    """Two host threads decoding through the same components at once (each gets its own batch
+    handles and streams; the library's host worker pool is shared) return the single-thread
+    results."""
+    import threading
+
+    from paper_2603_14002_b200 import decode_stream_raw
+
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=64)
+    scale = cfg.ngram_weight / cfg.llm_weight
+    sc = DeviceNgramScorer(w.model, scale)
+    inputs = [synth.make_logits(12, 120, 41, base_seed=500 + i) for i in range(2)]
+    want = [[(r.text, r.score, r.nbest) for r in decode_batch_raw(list(x), cfg, w.table, w.model, sc)]
+            for x in inputs]
+    got: dict = {}
+
+    def work(i):
+        outs = []
+        for _ in range(3):
+            outs.append([(r.text, r.score, r.nbest)
+                         for r in decode_batch_raw(list(inputs[i]), cfg, w.table, w.model, sc)])
+        frames = np.full(12, 120, dtype=np.int32)
+        for res in decode_stream_raw([(inputs[i], frames)] * 2, cfg, w.table, w.model, sc):
+            outs.append([(r.text, r.score, r.nbest) for r in res])
+        got[i] = outs
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(2):
+        assert len(got[i]) == 5
+        for o in got[i]:
+            assert o == want[i]
