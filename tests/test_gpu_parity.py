@@ -325,3 +325,44 @@ def test_concurrent_host_threads():
         assert len(got[i]) == 5
         for o in got[i]:
             assert o == want[i]
+
+
+def test_profile_default_beam_900():
+    """The b2t25 profile's own beam (900 -> the 960-thread frames kernel): per-frame beams for
+    one utterance and final results with device n-gram fusion equal the oracle."""
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"]
+    assert cfg.beam_size == 900
+    raws = synth.make_logits(3, 90, 41, base_seed=77)
+    ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+    scale = cfg.ngram_weight / cfg.llm_weight
+    got = decode_batch(ds, cfg, w.table, w.model, DeviceNgramScorer(w.model, scale), final_llm_only=True)
+    for i, d in enumerate(ds):
+        want = O.decode(d, cfg, w.table, w.model, StubScorer(ngram_model=w.model, scale=scale),
+                        final_llm_only=True)
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest), i
+    cfg_t = cfg.replace(llm_rescore_interval=1000)
+    dm = device_model(w.table, w.model)
+    batch = dm.batch(cfg_t, 1, 60)
+    batch.enable_dump(True)
+    batch.load_logprobs(ds[0][None, :60], np.array([60], dtype=np.int32))
+    batch.reset()
+    batch.run(0, 60)
+    s = O.OracleSearch(cfg_t, w.table, w.model, StubScorer(table={}))
+    for t in range(60):
+        s.frame(ds[0][t], t)
+        assert batch.dump_frame(0, t) == s.snapshot(), t
+    batch.enable_dump(False)
+
+
+def test_max_beam_4096():
+    """beam_size at the C-ABI maximum (4096): every working-set region but the log-prob stage
+    lives in global scratch; results equal the oracle."""
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=4096)
+    raws = synth.make_logits(2, 30, 41, base_seed=91)
+    ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+    got = decode_batch(ds, cfg, w.table, w.model, StubScorer(table={}))
+    for i, d in enumerate(ds):
+        want = O.decode(d, cfg, w.table, w.model, StubScorer(table={}))
+        assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest), i
