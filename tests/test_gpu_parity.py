@@ -366,3 +366,48 @@ def test_max_beam_4096():
     for i, d in enumerate(ds):
         want = O.decode(d, cfg, w.table, w.model, StubScorer(table={}))
         assert (got[i].text, got[i].score, got[i].nbest) == (want.text, want.score, want.nbest), i
+
+
+def _wide_vocab_world(seed=3):
+    """64-token vocabulary (the kernel maximum; wider than the small-kernel path's 48)."""
+    from paper_2603_14002_b200.ngram import parse_arpa_text
+
+    rng = np.random.default_rng(seed)
+    toks = ["<blank>"] + [f"P{i}" for i in range(62)] + ["<sp>"]
+    vocab = G.vocab_of({"tokens": toks, "blank": 0, "space": 63})
+    rows, words = [], []
+    for i in range(300):
+        n = int(rng.integers(2, 6))
+        ph = [int(rng.integers(1, 63)) for _ in range(n)]
+        surf = f"w{i}" if i % 17 else f"w{i - 1}"  # a few homophones
+        rows.append([f"k{i}", surf, ph])
+        words.append(surf)
+    uni = sorted(set(words))
+    lines = ["\\data\\", f"ngram 1={len(uni) + 3}", "ngram 2=200", "", "\\1-grams:"]
+    for w in ["<s>", "</s>", "<unk>"] + uni:
+        lines.append(f"{-rng.uniform(1, 4):.4f}\t{w}\t{-rng.uniform(0, 1):.4f}")
+    lines += ["", "\\2-grams:"]
+    for _ in range(200):
+        a, b = rng.choice(uni, 2)
+        lines.append(f"{-rng.uniform(0.2, 2):.4f}\t{a} {b}")
+    lines += ["", "\\end\\", ""]
+    model = parse_arpa_text("\n".join(lines))
+    tt = G.build_transition_table(G.lexicon_of(rows), vocab)
+    return tt, model
+
+
+def test_vocab_64_general_kernel():
+    """V = 64 runs the general kernel for every beam; host (interval) and device n-gram fusion
+    both equal the oracle."""
+    tt, model = _wide_vocab_world()
+    raws = synth.make_logits(4, 80, 64, base_seed=640)
+    for k in (16, 64):
+        cfg = PROFILES["b2t25"].replace(beam_size=k, llm_rescore_interval=10)
+        scale = cfg.ngram_weight / cfg.llm_weight
+        ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+        for sc in (StubScorer(ngram_model=model, scale=scale), DeviceNgramScorer(model, scale)):
+            got = decode_batch(ds, cfg, tt, model, sc)
+            for i, d in enumerate(ds):
+                want = O.decode(d, cfg, tt, model, StubScorer(ngram_model=model, scale=scale))
+                assert (got[i].text, got[i].score, got[i].nbest) == \
+                    (want.text, want.score, want.nbest), (k, type(sc).__name__, i)
