@@ -23,6 +23,7 @@ def main():
     from paper_2603_14002_b200 import (PROFILES, DeviceNgramScorer, LlamaScorer, ReplayScorer,
                                        StubScorer, synth)
     from paper_2603_14002_b200.decoder import device_model, run_search
+    from paper_2603_14002_b200.errors import DeviceError
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--llm", default="llama-3.2-1b")
@@ -56,11 +57,18 @@ def main():
                     batch.load_logits(None, frames, on_device_ptr=x.data_ptr())
                     run_search(batch, cfg, scorer, world.model, final_llm_only=final_only)
 
-                step()
-                torch.cuda.synchronize()
-                batch.mark_begin()
-                step()
-                ms, launches = batch.mark_end()
+                try:
+                    step()
+                    torch.cuda.synchronize()
+                    batch.mark_begin()
+                    step()
+                    ms, launches = batch.mark_end()
+                except DeviceError as e:  # e.g. the LLM prefix cache is full: record, go on
+                    point = {"T": T, "beam": k, "interval": r, "trials": args.trials, "error": str(e)}
+                    print(json.dumps(point), flush=True)
+                    results.append(point)
+                    dm = device_model(world.table, world.model, 0)
+                    continue
                 point = {"T": T, "beam": k, "interval": r, "trials": args.trials,
                          "ms": ms, "frames_per_s": args.trials * T / (ms / 1e3),
                          "rtf": (ms / 1e3) / (args.trials * T * 0.08), "launches": launches}
