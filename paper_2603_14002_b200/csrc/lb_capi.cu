@@ -339,6 +339,8 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
   ncap = std::min<int64_t>(ncap, std::max<int64_t>(4096, budget_nodes));
   ncap = std::min<int64_t>(ncap, (int64_t)1 << 30);
   BatchDev& d = b->dev;
+  d.spec_cap = 1 << 30;  // frames_small_kernel clamps to its shared-memory pair cap
+  if (const char* e = std::getenv("LB_SPEC_CAP")) d.spec_cap = std::max(0, std::atoi(e));
   d.Tmax = max_frames;
   d.K = b->K;
   d.O = b->O;

@@ -113,6 +113,8 @@ struct BatchDev {
   int32_t* dump_k;  // [B][Tmax]
   // optional per-phase cycle counters of the frames kernel: [B][NPHASE] (thread 0, clock64)
   unsigned long long* phase_cycles;
+  // speculative n-gram pair budget of frames_small_kernel per frame (<= its shared-memory cap)
+  int32_t spec_cap;
 };
 constexpr int NPHASE = 16;
 

@@ -1684,10 +1684,11 @@ __global__ void __launch_bounds__(small::NT, 2)
         carry += tot;
         bar_sync(3, NGT);
       }
+      const int SCAP = min(PC, b.spec_cap);
       if (gt == 0) {
         ppoff[K] = carry;
         s_ngP = carry;
-        if (carry <= PC) s_ngcov = carry;
+        if (carry <= SCAP) s_ngcov = carry;
       }
       const int P = carry;
       {
@@ -1698,8 +1699,8 @@ __global__ void __launch_bounds__(small::NT, 2)
         for (int p = gt; p < K; p += NGT) {
           // ppoff[K] is written by thread 0 without a barrier: use the scan total instead
           const int q0 = ppoff[p], q1 = p + 1 < K ? ppoff[p + 1] : P;
-          if (q1 > PC) {
-            if (q0 <= PC) s_ngcov = q0;  // the first parent that does not fit (unique)
+          if (q1 > SCAP) {
+            if (q0 <= SCAP) s_ngcov = q0;  // the first parent that does not fit (unique)
             continue;
           }
           if (q0 == q1) continue;
