@@ -1351,7 +1351,11 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
 // =====================================================================================
 namespace small {
 constexpr int KC = 64, OC = 3, VC = 48, VPC = 56, VPDC = 50;
-constexpr int LC = 320, PC = 160, TSC = 128;
+// PC: speculative (entry, surface) pairs per frame -- 64..80 measured best at config 2 (7.23 ms
+// at 160 -> 7.13 ms; the n-gram warps are the critical path up to S3 and the uncovered parents'
+// few selected boundary beams take the warp path); LC 280 and 4-frame D chunks keep two CTAs
+// inside the 132 KB shared-memory carve-out (124 KB of L1 for the lexicon / n-gram probes)
+constexpr int LC = 280, PC = 80, TSC = 128, SCHUNK = 4;
 constexpr int NC = 256, NWC = NC / 32, NT = NC + NGT;
 constexpr int MAXI = (KC + (NC / VC) - 1) / (NC / VC);  // items per thread (13)
 constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8,
@@ -1359,7 +1363,7 @@ constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8
               B_ENTS = 3 * KC * 8 + 3 * KC * 4;
 constexpr int BEAM_BYTES = B_ENTS + KC * OC * (int)sizeof(Ent);
 constexpr int O_DBUF = 0;
-constexpr int O_ROWS = O_DBUF + 2 * CHUNK * VPDC * 8;
+constexpr int O_ROWS = O_DBUF + 2 * SCHUNK * VPDC * 8;
 constexpr int O_BEAM = O_ROWS + KC * VPC * 4;
 constexpr int O_CVAL = O_BEAM + 2 * BEAM_BYTES;
 constexpr int O_CKEY = O_CVAL + LC * 8;
@@ -1630,12 +1634,12 @@ __global__ void __launch_bounds__(small::NT, 2)
 
   const double* Dtrial = b.D + (size_t)trial * b.Tmax * VPD;
   auto issue_chunk = [&](int ci) {
-    const int f0 = tb + ci * CHUNK;
+    const int f0 = tb + ci * SCHUNK;
     if (f0 >= te) return;
-    const int nf = min(CHUNK, te - f0);
+    const int nf = min(SCHUNK, te - f0);
     const unsigned bytes = (unsigned)(nf * VPD * sizeof(double));
     mbar_expect_tx(&dbar[ci & 1], bytes);
-    tma_bulk_g2s(dbuf + (size_t)(ci & 1) * CHUNK * VPDC, Dtrial + (size_t)f0 * VPD, bytes,
+    tma_bulk_g2s(dbuf + (size_t)(ci & 1) * SCHUNK * VPDC, Dtrial + (size_t)f0 * VPD, bytes,
                  &dbar[ci & 1]);
   };
   if (tid == 0) issue_chunk(0);
@@ -1656,8 +1660,8 @@ __global__ void __launch_bounds__(small::NT, 2)
 
   for (int t = tb; t < te; ++t) {
     const int rel = t - tb;
-    const int ci = rel / CHUNK;
-    const int cr = rel - ci * CHUNK;
+    const int ci = rel / SCHUNK;
+    const int cr = rel - ci * SCHUNK;
     st_beams_in += K;
 
     if (warp >= NWC) {
@@ -1761,7 +1765,7 @@ __global__ void __launch_bounds__(small::NT, 2)
         mbar_wait(&dbar[ci & 1], (unsigned)((ci >> 1) & 1));
         if (tid == 0) issue_chunk(ci + 1);
       }
-      const double* drow = dbuf + (size_t)(ci & 1) * CHUNK * VPDC + (size_t)cr * VPD;
+      const double* drow = dbuf + (size_t)(ci & 1) * SCHUNK * VPDC + (size_t)cr * VPD;
       const double U = __dadd_ru(__dadd_ru(__dadd_ru(s_maxs, drow[V]), fmax(c.beta, 0.0)),
                                  fmax(c.gamma, 0.0));
       // per-thread token constants
