@@ -339,7 +339,10 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
   ncap = std::min<int64_t>(ncap, std::max<int64_t>(4096, budget_nodes));
   ncap = std::min<int64_t>(ncap, (int64_t)1 << 30);
   BatchDev& d = b->dev;
-  d.spec_cap = 1 << 30;  // frames_small_kernel clamps to its shared-memory pair cap
+  // speculative n-gram pairs per frame (leading parents in score order; the rest of the
+  // selected word-boundary beams take the warp path).  Measured: config 2 (k = 64) flat at
+  // 64..80 (7.13 ms vs 7.23 at 160); k = 256: 42.7 ms at 64 vs 56.0 ms at 256 (full).
+  d.spec_cap = 64;
   if (const char* e = std::getenv("LB_SPEC_CAP")) d.spec_cap = std::max(0, std::atoi(e));
   d.Tmax = max_frames;
   d.K = b->K;

@@ -691,14 +691,15 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
       if (gt == 0) {
         ppoff[K] = carry;
         s_ngP = carry;
-        if (carry <= L.pcap) s_ngcov = carry;
+        if (carry <= min(L.pcap, b.spec_cap)) s_ngcov = carry;
       }
       const int P = carry;
       // parents are in score order: when the pairs exceed the cap, speculate the leading
       // parents whose pairs all fit (s_ngcov pairs); the rest take the warp path after S4
       for (int p = gt; p < K; p += NGT) {
         const int q0 = ppoff[p], q1 = p + 1 < K ? ppoff[p + 1] : P;
-        if (q1 > L.pcap && q0 <= L.pcap) s_ngcov = q0;  // the first parent that does not fit
+        const int scap = min(L.pcap, b.spec_cap);
+        if (q1 > scap && q0 <= scap) s_ngcov = q0;  // the first parent that does not fit
       }
       bar_sync(3, NGT);
       const int PCOV = s_ngcov;
