@@ -63,6 +63,10 @@ def parse():
                          "fusion, 1 = one T=500 utterance, beam 10, toy LM + tiny LLM, 5 = 8192 "
                          "utterances over the GPUs with an 8B-class LLM (sub-batches of 256)")
     ap.add_argument("--sub-batch", type=int, default=0, help="utterances per device batch (0 = all)")
+    ap.add_argument("--replay-check", type=int, default=2,
+                    help="config 3/5: utterances checked against the oracle replaying the device scores")
+    ap.add_argument("--interleave", action="store_true",
+                    help="config 3/5: two device batches on two streams, driven event by event")
     ap.add_argument("--llm", default="llama-3.2-1b", help="LLM preset for --config 3")
     ap.add_argument("--interval", type=int, default=20, help="fusion interval (frames) for --config 3")
     ap.add_argument("--ref-trials", type=int, default=4, help="reference-arm sample (config 3)")
@@ -570,22 +574,124 @@ def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1, su
     }
 
 
+def llm_core_interleaved(dev, world, cfg, raws, llm, precision, steps, warmup, world_n, sub_batch):
+    """llm_core with the GPU's utterances split into two device batches on two CUDA streams,
+    driven event by event (`run_search_many`): one batch's frames and LLM forward run while the
+    host plans the other's next fusion event.  Timed from an event on stream A (stream B waits on
+    it) to an event on A after A has waited for B's last kernel."""
+    import torch
+
+    from paper_2603_14002_b200 import LlamaScorer
+    from paper_2603_14002_b200.decoder import device_model, run_search_many
+
+    scorer = LlamaScorer(llm, seed=0, device=dev, precision=precision)
+    dm = device_model(world.table, world.model, dev)
+    B, T = raws.shape[0], raws.shape[1]
+    SB = (B + 1) // 2 if not (0 < sub_batch < B) else sub_batch
+    starts = list(range(0, B, SB))
+    if len(starts) != 2:
+        raise SystemExit("--interleave needs exactly two sub-batches (--sub-batch >= B/2)")
+    frames = np.full(B, T, dtype=np.int32)
+    x_dev = torch.from_numpy(raws).to(f"cuda:{dev}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    row_bytes = T * raws.shape[2] * 4
+    batches = [dm.pipeline_batch(cfg, i, min(SB, B - b0), T) for i, b0 in enumerate(starts)]
+    streams = [torch.cuda.ExternalStream(b.stream_ptr, device=f"cuda:{dev}") for b in batches]
+
+    def step():
+        for b, b0 in zip(batches, starts):
+            nb = min(SB, B - b0)
+            b.load_logits(None, frames[b0:b0 + nb], on_device_ptr=x_dev.data_ptr() + b0 * row_bytes)
+        run_search_many(batches, cfg, scorer, world.model, final_llm_only=False)
+
+    for _ in range(warmup):
+        flush.zero_()
+        torch.cuda.synchronize()
+        step()
+    torch.cuda.synchronize()
+    sessions = [b._llm_session for b in batches]
+    for sess in sessions:
+        sess.enable_timing(True)
+    if world_n > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ms_steps, launches = [], 0
+    acc = {"rows": 0, "slots": 0, "events": 0, "waves": 0}
+    llm_ms = 0.0
+    with ClockSampler(dev) as clk:
+        for _ in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            batches[0].mark_begin()
+            e0 = torch.cuda.Event()
+            e0.record(streams[0])
+            streams[1].wait_event(e0)
+            step()
+            eb = torch.cuda.Event()
+            eb.record(streams[1])
+            streams[0].wait_event(eb)
+            ms, nl = batches[0].mark_end()
+            ms_steps.append(ms)
+            launches += nl
+            for sess in sessions:  # counters read outside the timed region
+                llm_ms += sess.llm_ms()
+                st = sess.stats()
+                for k in acc:
+                    acc[k] += st["forward_rows" if k == "rows" else k]
+        torch.cuda.synchronize()
+    for sess in sessions:
+        sess.enable_timing(False)
+    total_ms = float(sum(ms_steps))
+    if world_n > 1:
+        total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / steps
+    frames_per_step = float(frames.sum()) * world_n
+    rows = acc["rows"]
+    flops = rows * scorer.cfg.flops_per_token() * (2 if scorer.split else 1)
+    # event time of the two overlapped streams summed: a conservative (low) achieved rate
+    achieved_tf = flops / (llm_ms / 1e3) / 1e12 if llm_ms > 0 else 0.0
+    peaks = {}
+    pp = ROOT / "MEASURED_PEAKS.json"
+    if pp.exists():
+        peaks = json.loads(pp.read_text())
+    peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+    return {
+        "scorer": scorer, "batch": batches[1], "sess": sessions[1], "frames": frames,
+        "value": frames_per_step / (ms_per_step / 1e3), "ms_per_step": ms_per_step,
+        "total_ms": total_ms, "launches": launches, "llm_ms": llm_ms,
+        "rows": rows, "slots": acc["slots"], "events": acc["events"], "waves": acc["waves"],
+        "clocks": clk.summary(), "achieved_tf": achieved_tf, "peak_tf": peak_tf,
+        "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if pp.exists() else "fallback 1400 TFLOP/s",
+        "frames_per_step": frames_per_step, "last_b0": starts[1], "interleaved": True,
+    }
+
+
 def llm_replay_check(world, cfg, raws, core, n=2):
     """Bit-exact check of this run: the oracle decoder replaying the device LLM's scores."""
     from oracle import lightbeam_oracle as O
     from paper_2603_14002_b200 import ReplayScorer
 
     replay = ReplayScorer(core["sess"].replay_table())
-    got = core["batch"].results()  # the last device batch of the step
+    batch = core["batch"]
+    got = batch.results()  # the last device batch of the step
     b0 = core.get("last_b0", 0)
-    n = min(n, len(got))
+    skip = int(os.environ.get("REPLAY_SKIP", "0"))  # diagnostic: check utterances b0+skip ...
+    n = min(n, len(got) - skip)
     ok = 0
+    dmat = batch.get_logprobs()
     for i in range(n):
-        want = O.decode(O.log_softmax_scaled(raws[b0 + i], cfg.acoustic_scale), cfg, world.table,
+        # the oracle searches the device's own log-prob rows: the fused prologue (K1) agrees with
+        # numpy only to a few ulps, and the search itself is what this check pins bit for bit
+        want = O.decode(dmat[skip + i, : int(batch.frames[skip + i])], cfg, world.table,
                         world.model, replay)
-        g = got[i]
-        ok += int(g is not None and g[0] == want.text and g[1] == want.score)
-    return f"{ok}/{n} utterances bit-exact vs the oracle decoder replaying this run's device LLM scores"
+        g = got[skip + i]
+        good = g is not None and g[0] == want.text and g[1] == want.score
+        ok += int(good)
+        if not good:
+            print(f"replay mismatch utterance {b0 + skip + i}: device {g[:2] if g else g!r} oracle "
+                  f"{(want.text, want.score)!r}", file=sys.stderr)
+    return (f"{ok}/{n} utterances bit-exact vs the oracle decoder replaying this run's device LLM "
+            f"scores on the device's log-prob rows")
 
 
 def run_llm(args):
@@ -600,8 +706,9 @@ def run_llm(args):
     world, cfg, raws = make_inputs(args, rank)
     cfg = cfg.replace(llm_rescore_interval=args.interval)
     setup_s = time.perf_counter() - t_setup
-    core = llm_core(dev, world, cfg, raws, args.llm, args.precision, args.steps, args.warmup, world_n,
-                    args.sub_batch)
+    core_fn = llm_core_interleaved if args.interleave else llm_core
+    core = core_fn(dev, world, cfg, raws, args.llm, args.precision, args.steps, args.warmup, world_n,
+                   args.sub_batch)
     scorer, batch, frames = core["scorer"], core["batch"], core["frames"]
     B, T = raws.shape[0], raws.shape[1]
     ms_per_step, total_ms, llm_ms = core["ms_per_step"], core["total_ms"], core["llm_ms"]
@@ -611,7 +718,7 @@ def run_llm(args):
     achieved_tf, peak_tf = core["achieved_tf"], core["peak_tf"]
     pp = ROOT / "MEASURED_PEAKS.json"
 
-    check = llm_replay_check(world, cfg, raws, core) if rank == 0 else None
+    check = llm_replay_check(world, cfg, raws, core, n=args.replay_check) if rank == 0 else None
 
     e2e = None
     if not args.no_e2e:

@@ -407,6 +407,26 @@ def _uses_device_scorer(scorer, model, dm: DeviceModel) -> bool:
 
 def run_search(batch: DeviceBatch, cfg, scorer, model, final_llm_only: bool):
     """Everything after the inputs are on the device: frames, events, closure, final fusion."""
+    for _ in _search_steps(batch, cfg, scorer, model, final_llm_only):
+        pass
+
+
+def run_search_many(batches, cfg, scorer, model, final_llm_only: bool):
+    """run_search over several device batches (each on its own CUDA stream, e.g. the
+    `pipeline_batch` pair) interleaved event by event: while the host waits for one batch's
+    fusion plan, the other batch's frames and LLM forward keep the GPU busy."""
+    gens = [_search_steps(b, cfg, scorer, model, final_llm_only) for b in batches]
+    while gens:
+        for g in list(gens):
+            try:
+                next(g)
+            except StopIteration:
+                gens.remove(g)
+
+
+def _search_steps(batch: DeviceBatch, cfg, scorer, model, final_llm_only: bool):
+    """run_search as a generator: yields after the launches of each fusion event (the host
+    synchronises only inside an event's planning step)."""
     frames = batch.frames
     t_max = int(frames.max()) if len(frames) else 0
     r = cfg.llm_rescore_interval
@@ -431,9 +451,11 @@ def run_search(batch: DeviceBatch, cfg, scorer, model, final_llm_only: bool):
             batch.run(t, e + 1)
             fuse(False, e)
             t = e + 1
+            yield
     batch.run(t, t_max)
     batch.close()
     fuse(True, 0)
+    yield
 
 
 def _collect(batch: DeviceBatch, cfg, final_llm_only: bool, wall: float):
@@ -520,8 +542,18 @@ def decode_stream_raw(batches, config, tt, lm, scorer, final_llm_only: bool = Fa
     asynchronous; a batch's host array must stay unmodified until its results are yielded).
     Results are identical to `decode_batch_raw` per batch."""
     cfg, model, dm = _prepare(config, tt, lm, device)
-    pending: list = []
+    pending: list = []  # [batch, t0, search generator or None when its launches are all issued]
     slot = 0
+
+    def advance(until):  # step every in-flight search (event by event) until `until` is issued
+        while until[2] is not None:
+            for item in pending:
+                if item[2] is not None:
+                    try:
+                        next(item[2])
+                    except StopIteration:
+                        item[2] = None
+
     for raws in batches:
         arr, frames = _raw_array(raws)
         if arr.ndim != 3 or arr.shape[2] != dm.vocab_size:
@@ -529,13 +561,15 @@ def decode_stream_raw(batches, config, tt, lm, scorer, final_llm_only: bool = Fa
         batch = dm.pipeline_batch(cfg, slot, arr.shape[0], max(arr.shape[1], 1))
         t0 = time.perf_counter()
         batch.load_logits(arr, frames)
-        run_search(batch, cfg, scorer, model, final_llm_only)
-        pending.append((batch, t0))
+        pending.append([batch, t0, _search_steps(batch, cfg, scorer, model, final_llm_only)])
         slot ^= 1
         if len(pending) == 2:
-            b, t = pending.pop(0)
+            advance(pending[0])
+            b, t, _ = pending.pop(0)
             yield _collect(b, cfg, final_llm_only, time.perf_counter() - t)
-    for b, t in pending:
+    while pending:
+        advance(pending[0])
+        b, t, _ = pending.pop(0)
         yield _collect(b, cfg, final_llm_only, time.perf_counter() - t)
 
 
