@@ -411,3 +411,26 @@ def test_vocab_64_general_kernel():
                 want = O.decode(d, cfg, tt, model, StubScorer(ngram_model=model, scale=scale))
                 assert (got[i].text, got[i].score, got[i].nbest) == \
                     (want.text, want.score, want.nbest), (k, type(sc).__name__, i)
+
+
+@pytest.mark.parametrize("k,o,r", [(1, 1, 1), (5, 8, 3), (64, 1, 7), (64, 8, 5), (300, 2, 11)])
+def test_ortho_interval_edges(k, o, r):
+    """Ortho beams 1 and 8 (both kernels), fusion every frame, ragged lengths down to one frame,
+    host n-gram stub fusion: results equal the oracle."""
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=k, ortho_beams=o, llm_rescore_interval=r)
+    scale = cfg.ngram_weight / cfg.llm_weight
+    lens = [1, 2, 37, 64]
+    raws = synth.make_logits(len(lens), max(lens), 41, base_seed=300 + k + o)
+    ds = [O.log_softmax_scaled(x[:n], cfg.acoustic_scale) for x, n in zip(raws, lens)]
+    got = decode_batch(ds, cfg, w.table, w.model, StubScorer(ngram_model=w.model, scale=scale))
+    for i, d in enumerate(ds):
+        try:
+            want = O.decode(d, cfg, w.table, w.model, StubScorer(ngram_model=w.model, scale=scale))
+        except Exception as e:  # the reference raises (e.g. EmptyBeamError): so must we
+            assert isinstance(got[i], Exception), (i, e, got[i])
+            assert str(got[i]) == str(e) or type(got[i]).__name__ == type(e).__name__, (got[i], e)
+            continue
+        assert not isinstance(got[i], Exception), (i, got[i])
+        assert (got[i].text, got[i].score, got[i].nbest, got[i].llm_events) == \
+            (want.text, want.score, want.nbest, want.llm_events), (k, o, r, i)
