@@ -12,7 +12,9 @@ from paper_2603_14002_b200 import (PROFILES, DeviceNgramScorer, LlamaScorer, Stu
 
 w = synth.toy_world(n_words=2000, seed=7)
 raws = synth.make_logits(3, 60, 41, base_seed=11)
-for k in (16, 64, 96):
+import os  # noqa: E402
+
+for k in (16, 64, 96, 300) + ((900,) if os.environ.get("SAN_WIDE") else ()):
     cfg = PROFILES["b2t25"].replace(beam_size=k, llm_rescore_interval=20)
     ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
     scale = cfg.ngram_weight / cfg.llm_weight
