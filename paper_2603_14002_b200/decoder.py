@@ -561,7 +561,12 @@ def decode_stream_raw(batches, config, tt, lm, scorer, final_llm_only: bool = Fa
         batch = dm.pipeline_batch(cfg, slot, arr.shape[0], max(arr.shape[1], 1))
         t0 = time.perf_counter()
         batch.load_logits(arr, frames)
-        pending.append([batch, t0, _search_steps(batch, cfg, scorer, model, final_llm_only)])
+        item = [batch, t0, _search_steps(batch, cfg, scorer, model, final_llm_only)]
+        pending.append(item)
+        try:  # launch right away (up to its first fusion event): the GPU never waits on the host
+            next(item[2])
+        except StopIteration:
+            item[2] = None
         slot ^= 1
         if len(pending) == 2:
             advance(pending[0])
