@@ -434,3 +434,25 @@ def test_ortho_interval_edges(k, o, r):
         assert not isinstance(got[i], Exception), (i, got[i])
         assert (got[i].text, got[i].score, got[i].nbest, got[i].llm_events) == \
             (want.text, want.score, want.nbest, want.llm_events), (k, o, r, i)
+
+
+def test_run_search_many_interleaves_host_fusion_batches():
+    """Two device batches on two streams advanced event by event (host scorer: every event is a
+    device->host->device round trip) give the results of decoding each batch alone."""
+    from paper_2603_14002_b200.decoder import _collect, device_model, run_search_many
+
+    w = synth.toy_world(n_words=2000, seed=7)
+    cfg = PROFILES["b2t25"].replace(beam_size=16, llm_rescore_interval=9)
+    scale = cfg.ngram_weight / cfg.llm_weight
+    raws = [synth.make_logits(3, 70, 41, base_seed=900 + i) for i in range(2)]
+    want = [[(r.text, r.score, r.nbest) for r in
+             decode_batch_raw(list(x), cfg, w.table, w.model, StubScorer(ngram_model=w.model, scale=scale))]
+            for x in raws]
+    dm = device_model(w.table, w.model)
+    batches = [dm.pipeline_batch(cfg, i, 3, 70) for i in range(2)]
+    for b, x in zip(batches, raws):
+        b.load_logits(x, np.full(3, 70, np.int32))
+    run_search_many(batches, cfg, StubScorer(ngram_model=w.model, scale=scale), w.model, False)
+    for b, wv in zip(batches, want):
+        got = [(r.text, r.score, r.nbest) for r in _collect(b, cfg, False, 0.0)]
+        assert got == wv
