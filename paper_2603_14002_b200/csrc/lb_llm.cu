@@ -374,11 +374,16 @@ __device__ __forceinline__ float block_sum256(float v, float* red) {
 
 // bias != nullptr: LayerNorm y = (x - mean) * rsqrt(var + eps) * w + bias (GPT-2), two-pass
 // over the register-resident row; otherwise RMSNorm.  x is read once (+= delta, written back).
+// Programmatic dependent launch: the body kernels below may be launched before their
+// predecessor finishes (launch latency hidden); they wait for its memory here first.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* x, const float* delta,
                                                           const float* w, float eps, int H,
                                                           bf16* out, const int32_t* store_slots,
                                                           float* s_h, int split,
                                                           const float* bias = nullptr) {
+  pdl_wait();
   __shared__ float red[8];
   const int row = blockIdx.x;
   float* xr = x + (size_t)row * H;
@@ -460,6 +465,7 @@ template <typename T, int HD>
 __global__ void rope_kv_kernel(LlmDev l, int layer, const float* qkv, int M, const int32_t* pos,
                                const int32_t* slots, const float* cosT, const float* sinT,
                                T* q_out) {
+  pdl_wait();
   const int row = blockIdx.x;
   if (row >= M) return;
   constexpr int half = HD / 2;
@@ -743,6 +749,7 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
                                                              const void* qv, const int32_t* chains,
                                                              const int32_t* pos, float scale,
                                                              bf16* out) {
+  pdl_wait();
   constexpr int KK = HD / 16;  // k-steps of Q K^T
   constexpr int NT = HD / 8;   // n-tiles of P V
   extern __shared__ __align__(128) unsigned char attn_smem[];
@@ -940,6 +947,7 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
 // (split: hi|lo pairs [M][2F]); 8 columns per thread
 template <typename TI>
 __global__ void swiglu_kernel(const TI* gu, int F, bf16* out, int split) {
+  pdl_wait();
   const int row = blockIdx.y;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c >= F) return;
@@ -1519,6 +1527,36 @@ static int launched(cudaError_t e) {
     if (_rc) return _rc;            \
   } while (0)
 
+// Launch with programmatic stream serialization (LB_PDL=0 disables): the kernel's launch
+// overlaps the tail of its predecessor on the stream; the kernel itself starts with pdl_wait().
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+#define LAUNCH_PDL(...)                       \
+  do {                                        \
+    int _rc = launched(launch_pdl(__VA_ARGS__)); \
+    if (_rc) return _rc;                      \
+  } while (0)
+
 static int check_err_flags(lb_llm* l) {
   int32_t err = 0;
   CKL(cudaMemcpyAsync(&err, l->dev.ctr + C_ERR, 4, cudaMemcpyDeviceToHost, l->b->st));
@@ -1715,9 +1753,9 @@ int lb_llm_rmsnorm(lb_llm* l, float* x, const void* delta, const float* w, float
   if (!l || !x || !w || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
   if (l->dev.H > 256 * 4 * NORM_NPT) return lbh::set_error(LB_ERR_ARG, "hidden size > 4096");
   if (M <= 0) return LB_OK;
-  LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
-                                                      l->dev.H, reinterpret_cast<bf16*>(out),
-                                                      store_slots, l->dev.s_h, l->dev.split));
+  LAUNCH_PDL(add_rmsnorm_kernel, dim3(M), dim3(256), 0, l->b->st, x,
+             reinterpret_cast<const float*>(delta), w, eps, l->dev.H, reinterpret_cast<bf16*>(out),
+             store_slots, l->dev.s_h, l->dev.split, static_cast<const float*>(nullptr));
   return LB_OK;
 }
 
@@ -1726,9 +1764,9 @@ int lb_llm_layernorm(lb_llm* l, float* x, const void* delta, const float* w, con
   if (!l || !x || !w || !b || !out) return lbh::set_error(LB_ERR_ARG, "null argument");
   if (l->dev.H > 256 * 4 * NORM_NPT) return lbh::set_error(LB_ERR_ARG, "hidden size > 4096");
   if (M <= 0) return LB_OK;
-  LAUNCH(add_rmsnorm_kernel<<<M, 256, 0, l->b->st>>>(x, reinterpret_cast<const float*>(delta), w, eps,
-                                                      l->dev.H, reinterpret_cast<bf16*>(out),
-                                                      store_slots, l->dev.s_h, l->dev.split, b));
+  LAUNCH_PDL(add_rmsnorm_kernel, dim3(M), dim3(256), 0, l->b->st, x,
+             reinterpret_cast<const float*>(delta), w, eps, l->dev.H, reinterpret_cast<bf16*>(out),
+             store_slots, l->dev.s_h, l->dev.split, b);
   return LB_OK;
 }
 
@@ -1749,9 +1787,13 @@ int lb_llm_rope_kv(lb_llm* l, int32_t layer, const void* qkv, int32_t M, const i
   if (M <= 0) return LB_OK;
   const float* in = reinterpret_cast<const float*>(qkv);
   cudaStream_t st = l->b->st;
-#define ROPE(TT, HDV) \
-  LAUNCH(rope_kv_kernel<TT, HDV><<<M, 128, 0, st>>>(l->dev, layer, in, M, pos, slots, cos_tab, sin_tab, \
-                                                     reinterpret_cast<TT*>(q_out)))
+#define ROPE(TT, HDV)                                                                          \
+  do {                                                                                         \
+    void (*kfn)(LlmDev, int, const float*, int, const int32_t*, const int32_t*, const float*,  \
+                const float*, TT*) = rope_kv_kernel<TT, HDV>;                                  \
+    LAUNCH_PDL(kfn, dim3(M), dim3(128), 0, st, l->dev, layer, in, M, pos, slots, cos_tab, sin_tab, \
+               reinterpret_cast<TT*>(q_out));                                                  \
+  } while (0)
   if (l->dev.split) {
     if (l->dev.HD == 64) ROPE(float, 64); else ROPE(float, 128);
   } else {
@@ -1791,7 +1833,7 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
 #define MMA_ATT_N(HDV, SV, NS)                                                                      \
   do {                                                                                              \
     CKL(cudaFuncSetAttribute(chain_attn_mma_kernel<HDV, SV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
-    LAUNCH(chain_attn_mma_kernel<HDV, SV, NS><<<M, 32 * x.NKV, smem, st>>>(x, layer, q, chains, pos, scale, oo)); \
+    LAUNCH_PDL((chain_attn_mma_kernel<HDV, SV, NS>), dim3(M), dim3(32 * x.NKV), smem, st, x, layer, q, chains, pos, scale, oo); \
   } while (0)
 #define MMA_ATT(HDV, SV)               \
   do {                                 \
@@ -1824,12 +1866,15 @@ int lb_llm_swiglu(lb_llm* l, const void* gu, int32_t M, int32_t ffn, void* out) 
   if (M <= 0) return LB_OK;
   if (ffn % 8 != 0) return lbh::set_error(LB_ERR_ARG, "ffn must be a multiple of 8");
   const dim3 grid((ffn / 8 + 127) / 128, M);
-  if (l->dev.split)
-    LAUNCH(swiglu_kernel<float><<<grid, 128, 0, l->b->st>>>(reinterpret_cast<const float*>(gu), ffn,
-                                                            reinterpret_cast<bf16*>(out), 1));
-  else
-    LAUNCH(swiglu_kernel<bf16><<<grid, 128, 0, l->b->st>>>(reinterpret_cast<const bf16*>(gu), ffn,
-                                                           reinterpret_cast<bf16*>(out), 0));
+  if (l->dev.split) {
+    void (*kfn)(const float*, int, bf16*, int) = swiglu_kernel<float>;
+    LAUNCH_PDL(kfn, grid, dim3(128), 0, l->b->st, reinterpret_cast<const float*>(gu), ffn,
+               reinterpret_cast<bf16*>(out), 1);
+  } else {
+    void (*kfn)(const bf16*, int, bf16*, int) = swiglu_kernel<bf16>;
+    LAUNCH_PDL(kfn, grid, dim3(128), 0, l->b->st, reinterpret_cast<const bf16*>(gu), ffn,
+               reinterpret_cast<bf16*>(out), 0);
+  }
   return LB_OK;
 }
 
