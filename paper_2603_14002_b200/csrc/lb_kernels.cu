@@ -2318,7 +2318,7 @@ __global__ void __launch_bounds__(CLOSE_NT) close_kernel(ModelDev m, CfgDev c, B
   constexpr int NT = CLOSE_NT, NW = NT / 32;
   __shared__ WarpScratch wsc[NW];
   __shared__ int s_ncount, s_fail;
-  __shared__ unsigned s_calls, s_probes, s_pairs;
+  __shared__ unsigned s_calls, s_probes;
   extern __shared__ __align__(16) Ent close_tmp[];
   const int trial = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2331,7 +2331,6 @@ __global__ void __launch_bounds__(CLOSE_NT) close_kernel(ModelDev m, CfgDev c, B
     s_ncount = b.ncount[trial];
     s_fail = 0;
     s_calls = 0;
-    s_pairs = 0;
     s_probes = 0;
   }
   __syncthreads();
