@@ -357,3 +357,18 @@ def test_results_binding_builds_objects_from_a_view():
     got = N.pyresults().assemble(C.addressof(v))
     assert got == [("héllo world", -1.5, [("héllo word.", -1.5), ("hello", -2.0)]), None,
                    ("x y z?", -7.25, [("x y z?", -7.25)])]
+
+
+def test_bench_algorithmic_bytes_counts_consumed_pairs_only():
+    """bench.algorithmic_bytes: n-gram probe bytes scale with the pairs the
+    word-boundary beams consume, not with the kernel's speculative pairs."""
+    import bench
+
+    base = dict(frames=100, beams_in=5000, ngram_probes=4000, ngram_calls=1000,
+                ngram_pairs_used=500, history_nodes=300, boundary_beams=80)
+    got = bench.algorithmic_bytes(base)
+    want = 8 * 41 * 100 + 4 * 41 * 5000 + 32 * 4000 * 500 / 1000 + 20 * 300 + 8 * 80
+    assert got == want
+    # without speculation (every computed pair consumed) the probe term is the raw count
+    full = dict(base, ngram_pairs_used=1000)
+    assert bench.algorithmic_bytes(full) - got == 32 * 2000
