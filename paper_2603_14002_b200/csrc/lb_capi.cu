@@ -309,6 +309,8 @@ void fill_cfg(lb_batch* b) {
 
 extern "C" {
 
+static int batch_alloc(lb_batch* b, int32_t max_trials, int32_t max_frames);
+
 int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32_t max_frames,
                     void* stream, lb_batch** out) {
   if (!m || !cfg || !out) return fail(LB_ERR_ARG, "null argument");
@@ -332,6 +334,18 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
     delete b;
     return fail(LB_ERR_ARG, "beam_size too wide for the per-CTA shared-memory layout");
   }
+  // every failure after this point frees what was allocated so far (lb_batch_destroy skips
+  // null pointers), so an OOM during creation does not leak device memory
+  const int rc = batch_alloc(b, max_trials, max_frames);
+  if (rc != LB_OK) {
+    lb_batch_destroy(b);
+    return rc;
+  }
+  *out = b;
+  return LB_OK;
+}
+
+static int batch_alloc(lb_batch* b, int32_t max_trials, int32_t max_frames) {
   CK(lbk::set_smem_limit(b->L.nthreads, b->L.smem_bytes));
   const size_t B = (size_t)max_trials, K = (size_t)b->K, O = (size_t)b->O;
   int64_t ncap = (int64_t)max_frames * b->K * b->O + 1;
@@ -376,7 +390,6 @@ int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32
   CK(cudaEventCreate(&b->ev0));
   CK(cudaEventCreate(&b->ev1));
   b->T_host.assign(B, 0);
-  *out = b;
   return LB_OK;
 }
 

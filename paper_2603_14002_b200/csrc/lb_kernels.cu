@@ -1358,7 +1358,8 @@ constexpr int KC = 64, OC = 3, VC = 48, VPC = 56, VPDC = 50;
 // inside the 132 KB shared-memory carve-out (124 KB of L1 for the lexicon / n-gram probes)
 constexpr int LC = 280, PC = 80, TSC = 128, SCHUNK = 4;
 constexpr int NC = 256, NWC = NC / 32, NT = NC + NGT;
-constexpr int MAXI = (KC + (NC / VC) - 1) / (NC / VC);  // items per thread (13)
+constexpr int TBK = VC / 4;  // candidate tokens per thread: 4 threads per parent
+static_assert(KC * 4 == NC && TBK % 4 == 0, "candidate mapping: one parent per 4 threads");
 constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8,
               B_PRE = 3 * KC * 8 + KC * 4, B_NENT = 3 * KC * 8 + 2 * KC * 4,
               B_ENTS = 3 * KC * 8 + 3 * KC * 4;
@@ -1404,7 +1405,8 @@ constexpr int GTOTAL = G_WARP + NWC * (int)sizeof(WarpScratch);
 // Exact radix-select fallback of frames_small_kernel (a histogram bin overflowed LC): compiled
 // out of line so its ~1300 instructions stay out of the frame loop's instruction-cache footprint.
 // Called by all NC compute threads; returns nsel with sval/skey in (value desc, index asc) order.
-__device__ LB_COLD int small_fallback_select(const CfgDev& c, int K, int V, int VP, double thr,
+__device__ LB_COLD int small_fallback_select(const int ck, const double cbeta, const double cgamma,
+                                             int K, int V, int VP, double thr,
                                              int blank, int space, int sink, const int32_t* rows,
                                              const int32_t* C_LAST, const double* C_SCORE,
                                              const double* drow, unsigned* hist, double* cval,
@@ -1420,7 +1422,7 @@ __device__ LB_COLD int small_fallback_select(const CfgDev& c, int K, int V, int 
     const int nx = rows[p * VP + v];
     if (!((nx != sink) || (v == blank) || (v == lp))) return -DBL_MAX;
     const double x = cand_value(C_SCORE[p], drow[v], v, lp,
-                                FrameConsts{c.beta, c.gamma, blank, space});
+                                FrameConsts{cbeta, cgamma, blank, space});
     return x > GUARD ? x : -DBL_MAX;
   };
   const int KV = K * V;
@@ -1433,7 +1435,7 @@ __device__ LB_COLD int small_fallback_select(const CfgDev& c, int K, int V, int 
   for (int f = tid; f < KV; f += NC)
     if (cval_at(f) >= thr) atomicAdd(s_inr, 1);
   bar_sync(1, NC);
-  nsel = min(c.k, (*s_inr));
+  nsel = min(ck, (*s_inr));
   uint64_t phi = 0, pmask_hi = 0;
   uint32_t plo = 0, pmask_lo = 0;
   int rem = nsel;
@@ -1518,7 +1520,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   using namespace small;
   extern __shared__ __align__(128) char sm[];
   __shared__ __align__(8) uint64_t dbar[2];
-  __shared__ unsigned hist[NBINS];
+  __shared__ unsigned hist[NBINS + 1];  // + a spare bin for rejected candidates (never read)
   __shared__ int hcum[NBINS];  // exclusive prefix of hist (published by warp 0)
   __shared__ int hfill[NBINS];
   __shared__ double wmax[NWC];
@@ -1580,12 +1582,23 @@ __global__ void __launch_bounds__(small::NT, 2)
 
   const int V = m.V, VP = m.VP, VPD = b.VPD, O = c.O, KC_ = b.K;
   const int TS = TSC;
+  const double ibw = c.inv_binw;
   const double b_on = c.beta, b_off = xmul(c.beta, 0.0);
   const double g_on = c.gamma, g_off = xmul(c.gamma, 0.0);
   const int blank = m.blank, space = m.space, sink = m.sink;
-  // transposed candidate mapping: thread -> token tv, parents tg, tg + ngrp, ...
-  const int ngrp = NC / V;
-  const int tv = tid % V, tg = tid / V;
+  // candidate mapping: thread -> parent cp = tid / 4 and its token block of TBK tokens, with
+  // the block's static token classes as bit masks (bit i = token cv0 + i)
+  const int cp = tid >> 2, cv0 = (tid & 3) * TBK;
+  unsigned tk_inv = 0, tk_phon = 0, tk_blank = 0;
+  int tk_sidx = -1;
+  for (int i = 0; i < TBK; ++i) {
+    const int v = cv0 + i;
+    if (v >= V) continue;
+    tk_inv |= 1u << i;
+    if (v == blank) tk_blank |= 1u << i;
+    else if (v == space) tk_sidx = i;
+    else tk_phon |= 1u << i;
+  }
 
   // ---- load the home beam state and gather the first frame's lexicon rows
   int K = b.nbeam[trial];
@@ -1769,35 +1782,51 @@ __global__ void __launch_bounds__(small::NT, 2)
       const double* drow = dbuf + (size_t)(ci & 1) * SCHUNK * VPDC + (size_t)cr * VPD;
       const double U = __dadd_ru(__dadd_ru(__dadd_ru(s_maxs, drow[V]), fmax(c.beta, 0.0)),
                                  fmax(c.gamma, 0.0));
-      // per-thread token constants
-      const bool tact = tg < ngrp;
-      const double dv = drow[tv];
-      const bool tph = (tv != blank) && (tv != space);
+      // per-thread parent constants (thread -> parent cp, tokens cv0 .. cv0 + TBK - 1)
+      const bool pin = cp < K;
+      const int pcl = pin ? cp : 0;
+      const int lp = C_LAST[pcl];
+      const double sp = C_SCORE[pcl];
+      const double gsel = lp != space ? g_on : g_off;
+      // token classes of this frame: bonus bits (phoneme, not a repeat of lp) and the tokens
+      // that are always allowed (blank, the repeat of lp; lexicon.py:124-137)
+      const unsigned lpb = (unsigned)(lp - cv0) < (unsigned)TBK ? 1u << (lp - cv0) : 0u;
+      const unsigned bbits = tk_phon & ~lpb;
+      const unsigned abits = tk_blank | (lpb & tk_inv);
       LB_PHASE(0);
 
-      // ---- A: candidates of token tv for parents tg, tg+ngrp, ... ; bins kept in registers
-      uint16_t bins[MAXI];
+      // ---- A: candidates of parent cp for its TBK tokens; bins kept in registers.  Branch-free
+      // (predicated) so the unrolled items' fp64 chains overlap; the lexicon row segment arrives
+      // as int4 loads.  x = (s + d) + addend, addend = beta*[phoneme, no repeat] or, on the
+      // space column, gamma*[last != space]: the reference's ((s + d) + beta*mask) + gamma*m
+      // (decoder.py:252-256) adds beta*0 = +-0.0 to the space column, an exact identity.  The
+      // bin is trunc((U - x) / binw) clamped to NBINS-1: x <= U (U rounds up), so no lower
+      // clamp; monotone in x, identical to the clamped double form.  Rejected candidates count
+      // into the spare bin NBINS (never scanned).
+      uint16_t bins[TBK];
       double wm = -DBL_MAX;
+      if (__any_sync(FULLMASK, pin)) {
+        const int4* rseg = reinterpret_cast<const int4*>(rows + pcl * VP + cv0);
 #pragma unroll
-      for (int i = 0; i < MAXI; ++i) {
-        bins[i] = 0xFFFF;
-        const int p = tg + i * ngrp;
-        if (tact && p < K) {
-          const int lp = C_LAST[p];
-          const int nx = rows[p * VP + tv];
-          if ((nx != sink) || (tv == blank) || (tv == lp)) {
-            double x = xadd(C_SCORE[p], dv);
-            x = xadd(x, (tph && tv != lp) ? b_on : b_off);
-            if (tv == space) x = xadd(x, lp != space ? g_on : g_off);
-            if (x > GUARD) {
-              const double fb =
-                  fmin(fmax(xmul(xsub(U, x), c.inv_binw), 0.0), (double)(NBINS - 1));
-              bins[i] = (uint16_t)(int)fb;
-              atomicAdd(&hist[bins[i]], 1u);
-              wm = fmax(wm, x);
-            }
+        for (int q = 0; q < TBK / 4; ++q) {
+          const int4 n4 = rseg[q];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = 4 * q + u;
+            const int nx = u == 0 ? n4.x : u == 1 ? n4.y : u == 2 ? n4.z : n4.w;
+            const double add = (i == tk_sidx) ? gsel : (((bbits >> i) & 1u) ? b_on : b_off);
+            const double x = xadd(xadd(sp, drow[cv0 + i]), add);
+            const bool al = (nx != sink) ? ((tk_inv >> i) & 1u) : ((abits >> i) & 1u);
+            const bool ok = pin && al && (x > GUARD);
+            const int bn = min(__double2int_rz(xmul(xsub(U, x), ibw)), NBINS - 1);
+            bins[i] = ok ? (uint16_t)bn : (uint16_t)0xFFFF;
+            atomicAdd(&hist[ok ? bn : NBINS], 1u);
+            wm = (ok && x > wm) ? x : wm;
           }
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < TBK; ++i) bins[i] = 0xFFFF;
       }
       wm = warp_max(wm);
       LB_PHASE(11);
@@ -1825,7 +1854,7 @@ __global__ void __launch_bounds__(small::NT, 2)
       } else {
         const double thr = xsub(M, c.theta);
         const int bthr =
-            (int)fmin(fmax(xmul(xsub(U, thr), c.inv_binw), 0.0), (double)(NBINS - 1));
+            (int)fmin(fmax(xmul(xsub(U, thr), ibw), 0.0), (double)(NBINS - 1));
         int bstar = NBINS, cum_thr = 0, cum_bstar = 0;
         {
           constexpr int PB = NBINS / 32;
@@ -1878,18 +1907,16 @@ __global__ void __launch_bounds__(small::NT, 2)
         if (bound <= LC) {
           // ---- D: counting-sort collect from the register bins
 #pragma unroll
-          for (int i = 0; i < MAXI; ++i) {
+          for (int i = 0; i < TBK; ++i) {
             const int bn = bins[i];
             if (bn <= take_bin) {
-              const int p = tg + i * ngrp;
-              const int lp = C_LAST[p];
-              double x = xadd(C_SCORE[p], dv);
-              x = xadd(x, (tph && tv != lp) ? b_on : b_off);
-              if (tv == space) x = xadd(x, lp != space ? g_on : g_off);
+              const int v = cv0 + i;
+              const double add = (i == tk_sidx) ? gsel : (((bbits >> i) & 1u) ? b_on : b_off);
+              const double x = xadd(xadd(sp, drow[v]), add);
               if (sure || x >= thr) {
                 const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
                 cval[pos] = x;
-                ckey[pos] = (uint32_t)(p * V + tv);
+                ckey[pos] = (uint32_t)(cp * V + v);
                 cbinl[pos] = (uint16_t)bn;
               }
             }
@@ -1917,7 +1944,7 @@ __global__ void __launch_bounds__(small::NT, 2)
           }
         } else {
           ++st_fallback;
-          nsel = small_fallback_select(c, K, V, VP, thr, blank, space, sink, rows, C_LAST, C_SCORE,
+          nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, VP, thr, blank, space, sink, rows, C_LAST, C_SCORE,
                                        drow, hist, cval, ckey, sval, skey, &s_inr, &s_cnt2);
         }
       }

@@ -72,7 +72,6 @@ class DeviceModel:
         self.vocab_size = tab.table.shape[1]
         self.blank_id, self.space_id = tab.blank_id, tab.space_id
         self.device = device
-        self.model = model
         soff = tab.surface_off.astype(np.int64)
         td = N.LbTableDesc(
             N.ptr(tab.table), tab.table.shape[0], tab.table.shape[1], tab.sink, tab.blank_id,
@@ -92,7 +91,31 @@ class DeviceModel:
     def _mine(self) -> dict:
         tid = threading.get_ident()
         with self._lock:
-            return self._per_thread.setdefault(tid, {"lru": {}, "pipe": {}})
+            mine = self._per_thread.get(tid)
+            if mine is None:
+                # a new thread: first release the batches of threads that have exited
+                alive = {t.ident for t in threading.enumerate()}
+                for dead in [k for k in self._per_thread if k not in alive]:
+                    self._destroy_batches(self._per_thread.pop(dead))
+                mine = self._per_thread[tid] = {"lru": {}, "pipe": {}}
+            return mine
+
+    @staticmethod
+    def _destroy_batches(per: dict):
+        for b in list(per["lru"].values()) + [x[1] for x in per["pipe"].values()]:
+            b.destroy()
+        per["lru"].clear()
+        per["pipe"].clear()
+
+    def release(self):
+        """Free every device batch (all threads) and the device images; idempotent."""
+        with self._lock:
+            per_all, self._per_thread = list(self._per_thread.values()), {}
+        for per in per_all:
+            self._destroy_batches(per)
+        if getattr(self, "handle", None):
+            N.lib(False).lb_model_destroy(self.handle)
+            self.handle = None
 
     def footprint(self) -> int:
         out = C.c_int64()
@@ -153,31 +176,47 @@ class DeviceModel:
 
     def __del__(self):
         try:
-            for per in self._per_thread.values():
-                for b in list(per["lru"].values()) + [x[1] for x in per["pipe"].values()]:
-                    b.destroy()
-            if getattr(self, "handle", None):
-                N.lib(False).lb_model_destroy(self.handle)
-                self.handle = None
+            self.release()
         except Exception:
             pass
 
 
 _MODELS: dict = {}
+_MODELS_LOCK = threading.Lock()
+
+
+def _drop_model(key):
+    with _MODELS_LOCK:
+        hit = _MODELS.pop(key, None)
+    if hit is not None:
+        hit[2].release()
 
 
 def device_model(tt, lm, device: int = 0) -> DeviceModel:
-    """Cached DeviceModel for (tt, lm-model, device); entries die with their components."""
+    """Cached DeviceModel for (tt, lm-model, device).  The cache holds its components only
+    weakly: when the table or the n-gram model is collected, the entry is dropped and its
+    device memory freed (`weakref.finalize`); `release_device_model` frees it explicitly."""
     model = getattr(lm, "model", lm)
     key = (id(tt), id(model), device)
-    hit = _MODELS.get(key)
+    with _MODELS_LOCK:
+        hit = _MODELS.get(key)
     if hit is not None:
         wt, wm, dm = hit
-        if wt() is tt and wm() is model:
+        if wt() is tt and wm() is model and dm.handle:
             return dm
+        _drop_model(key)  # an id() reused by a new object, or a released entry
     dm = DeviceModel(tt, model, device)
-    _MODELS[key] = (weakref.ref(tt), weakref.ref(model), dm)
+    with _MODELS_LOCK:
+        _MODELS[key] = (weakref.ref(tt), weakref.ref(model), dm)
+    weakref.finalize(tt, _drop_model, key)
+    weakref.finalize(model, _drop_model, key)
     return dm
+
+
+def release_device_model(tt, lm, device: int = 0) -> None:
+    """Free the cached device images and batches of (tt, lm-model, device), if any."""
+    model = getattr(lm, "model", lm)
+    _drop_model((id(tt), id(model), device))
 
 
 class DeviceBatch:
@@ -463,6 +502,9 @@ def _collect(batch: DeviceBatch, cfg, final_llm_only: bool, wall: float):
     res = batch.results()
     out = []
     for i in range(batch.n):
+        if batch.frames[i] == 0:  # decoder.py:421-422 (per item, so one bad item keeps the batch)
+            out.append(DataValueError("cannot decode an empty log-probability matrix"))
+            continue
         if st[i] != 0:
             if st[i] == 4:
                 out.append(DeviceError("device word-history arena exhausted"))
