@@ -338,7 +338,7 @@ def run_ours(args):
         n_cta_frames = B * T
         phases = {k: v / n_cta_frames for k, v in cyc.items() if v}
         phases["total_cycles_per_frame"] = sum(v for k, v in phases.items()
-                                               if not k.endswith("permille"))
+                                               if k.endswith("_work") or k.endswith("_sync"))
         batch.enable_phase_timing(False)
 
     # correctness spot check of this very run against the oracle (2 utterances)

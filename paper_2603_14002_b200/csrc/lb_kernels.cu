@@ -48,6 +48,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -1493,7 +1497,7 @@ __device__ LB_COLD int small_fallback_select(const int ck, const double cbeta, c
       if (take) {
         const int pos = base + __popc(bl & ((1u << lane) - 1u));
         cval[pos] = x;
-        ckey[pos] = (uint32_t)f;
+        ckey[pos] = ((uint32_t)(f / V) << 8) | (uint32_t)(f % V);  // (parent, token) key
       }
     }
   }
@@ -1528,6 +1532,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov, s_inr, s_cnt2;
   __shared__ int ngtot[2];
   __shared__ unsigned s_calls, s_probes, s_pairs;
+  __shared__ unsigned s_tarr[NBAR_EV], s_tbase;  // TIMING only
 
   const int trial = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1632,6 +1637,8 @@ __global__ void __launch_bounds__(small::NT, 2)
     s_pairs = 0;
     s_probes = 0;
     s_K = K;
+    s_tbase = (unsigned)clock();
+    for (int e = 0; e < NBAR_EV; ++e) s_tarr[e] = 0;
     mbar_init(&dbar[0], 1);
     mbar_init(&dbar[1], 1);
     fence_mbar_init();
@@ -1661,16 +1668,25 @@ __global__ void __launch_bounds__(small::NT, 2)
   unsigned long long st_beams_in = 0, st_beams_out = 0, st_bound = 0, st_fallback = 0;
   unsigned calls_l = 0, probes_l = 0, pairs_l = 0;
   int fail_t = -1;
-  const bool timing = TIMING && b.phase_cycles != nullptr && tid == 0;
+  // TIMING: critical-path accounting per barrier event e (SM clock, 32-bit wrap-safe): every
+  // arriving warp records its arrival (atomicMax), thread 0 after the release adds
+  // work[e] = last arrival - previous release and sync[e] = release - last arrival.
+  const bool timing = TIMING && b.phase_cycles != nullptr;
   unsigned long long ph[NPHASE];
   for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
-  long long tprev = timing ? clock64() : 0;
-#define LB_PHASE(i)                                \
-  if (timing) {                                    \
-    const long long tnow = clock64();              \
-    ph[i] += (unsigned long long)(tnow - tprev);   \
-    tprev = tnow;                                  \
+  unsigned trel = timing ? (unsigned)clock() : 0u, tfs = trel;
+#define LB_ARR(e)                                              \
+  if (timing && lane == 0) atomicMax(&s_tarr[e], (unsigned)clock() - s_tbase);
+#define LB_REL(e)                                              \
+  if (timing && tid == 0) {                                    \
+    const unsigned tnow = (unsigned)clock();                   \
+    const unsigned ta = s_tarr[e] + s_tbase;                   \
+    ph[2 * (e)] += ta - trel;                                  \
+    ph[2 * (e) + 1] += tnow - ta;                              \
+    trel = tnow;                                               \
+    s_tarr[e] = 0;                                             \
   }
+#define LB_PHASE(i)
 
   for (int t = tb; t < te; ++t) {
     const int rel = t - tb;
@@ -1772,6 +1788,8 @@ __global__ void __launch_bounds__(small::NT, 2)
           }
         }
       }
+      LB_ARR(3);
+      LB_ARR(8);
       bar_arrive(2, NT);
     } else {
       // ============================== compute warps ==============================
@@ -1837,7 +1855,9 @@ __global__ void __launch_bounds__(small::NT, 2)
         slotb[i] = -1;
         slotm[i] = 0x7FFFFFFF;
       }
+      LB_ARR(0);
       bar_sync(1, NC);  // S1
+      LB_REL(0);
       LB_PHASE(1);
 
       double M = -DBL_MAX;
@@ -1879,7 +1899,9 @@ __global__ void __launch_bounds__(small::NT, 2)
               run += part[i];
             }
           }
+          LB_ARR(1);
           bar_sync(1, NC);  // hcum[] visible to every compute warp
+          LB_REL(1);
           cum_thr = hcum[bthr] + (int)hist[bthr];
           const unsigned bl = __ballot_sync(FULLMASK, excl < c.k && incl >= c.k);
           if (bl) {
@@ -1916,12 +1938,14 @@ __global__ void __launch_bounds__(small::NT, 2)
               if (sure || x >= thr) {
                 const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
                 cval[pos] = x;
-                ckey[pos] = (uint32_t)(cp * V + v);
+                ckey[pos] = ((uint32_t)cp << 8) | (uint32_t)v;  // orders like cp * V + v
                 cbinl[pos] = (uint16_t)bn;
               }
             }
           }
+          LB_ARR(2);
           bar_sync(1, NC);  // S2
+          LB_REL(2);
           const int m_sel = hcum[take_bin] + hfill[take_bin];
           nsel = min(c.k, m_sel);
           LB_PHASE(2);
@@ -1948,13 +1972,22 @@ __global__ void __launch_bounds__(small::NT, 2)
                                        drow, hist, cval, ckey, sval, skey, &s_inr, &s_cnt2);
         }
       }
+      LB_ARR(3);
+      LB_ARR(9);
       bar_sync(2, NT);  // S3: selection done + speculative n-gram results ready
+      if (timing && tid == 0) {  // n-gram warps' and compute warps' arrival since frame start
+        ph[17] += s_tarr[8] + s_tbase - tfs;
+        ph[18] += s_tarr[9] + s_tbase - tfs;
+        s_tarr[8] = 0;
+        s_tarr[9] = 0;
+      }
+      LB_REL(3);
       LB_PHASE(3);
 
       if (!dead) {
         const int ncov = s_ngcov;
         const bool ngover = ncov < s_ngP;  // some parents' pairs were not speculated
-        if (timing && ngover) ph[15] += 1000;  // permille of frames past the speculative pair cap
+        if (timing && tid == 0 && ngover) ph[16] += 1000;  // permille of frames past the speculative pair cap
         LB_PHASE(13);
         // ---- F: materialise survivors; new word boundaries pick their top-o pairs
         // selected beams spread over all compute warps (j = lane * NWC + warp), so the few
@@ -1962,8 +1995,8 @@ __global__ void __launch_bounds__(small::NT, 2)
         for (int j = lane * NWC + warp; j < nsel; j += NC) {
           const double x = sval[j];
           const uint32_t f = skey[j];
-          const int p = (int)f / V;
-          const int tok = (int)f - p * V;
+          const int p = (int)(f >> 8);
+          const int tok = (int)(f & 0xFFu);
           const int lp = C_LAST[p], pp = C_PRE[p];
           const bool emit = (tok != blank) && (tok != lp);
           uint64_t a1 = C_H1[p], a2 = C_H2[p];
@@ -1972,6 +2005,14 @@ __global__ void __launch_bounds__(small::NT, 2)
             a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
             a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
             np = rows[p * VP + tok];
+          }
+          {  // warm L1 with the next frame's lexicon row (gathered by cp.async.ca at the scatter)
+            const char* r0 = reinterpret_cast<const char*>(m.table + (size_t)np * VP);
+            const char* r1 = r0 + VP * 4 - 1;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(r0));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(r1));
+            if ((((uintptr_t)r1 >> 7) - ((uintptr_t)r0 >> 7)) > 1)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(r0 + 128));
           }
           double sc = x;
           int4 bs = make_int4(-1, 0, 0, 0);
@@ -2057,7 +2098,9 @@ __global__ void __launch_bounds__(small::NT, 2)
           bsel[j] = bs;
         }
         LB_PHASE(12);
+        LB_ARR(4);
         bar_sync(1, NC);  // S4
+        LB_REL(4);
         LB_PHASE(4);
         const int nb = s_nb;
         st_bound += nb;
@@ -2076,6 +2119,7 @@ __global__ void __launch_bounds__(small::NT, 2)
               bsel[j] = make_int4(outn >= 0 ? -2 - outn : -1, 0, 0, 0);  // -2-n: n entries in gbents
             }
           }
+          if (timing && tid == 0) ph[19] += (unsigned)clock() - trel;
           bar_sync(1, NC);
         }
         LB_PHASE(5);
@@ -2148,13 +2192,17 @@ __global__ void __launch_bounds__(small::NT, 2)
             }
           }
         }
+        LB_ARR(5);
         bar_sync(1, NC);  // S5
+        LB_REL(5);
         LB_PHASE(6);
         for (int i = tid; i < nsel; i += NC) {
           if (nscore[i] > GUARD && slotm[myslot[i]] == rankv[i])
             atomicOr(&keep[rankv[i] >> 5], 1u << (rankv[i] & 31));
         }
+        LB_ARR(6);
         bar_sync(1, NC);  // S6
+        LB_REL(6);
         LB_PHASE(7);
 
         // ---- scatter in rank order; boundary entries built from the chosen pairs;
@@ -2223,7 +2271,7 @@ __global__ void __launch_bounds__(small::NT, 2)
               }
             }
             const int32_t* srow = m.table + (size_t)npre[i] * VP;
-            for (int u = r; u < (VP >> 2); u += G) cp_async16(rows + pos * VP + u * 4, srow + u * 4);
+            for (int u = r; u < (VP >> 2); u += G) cp_async16_ca(rows + pos * VP + u * 4, srow + u * 4);
           }
           cp_async_commit();
           cp_async_wait_all();
@@ -2237,7 +2285,10 @@ __global__ void __launch_bounds__(small::NT, 2)
         if (s_fail || newK == 0) fail_t = t;
       }  // !dead
     }  // compute warps
+    LB_ARR(7);
     __syncthreads();  // frame end (whole CTA)
+    LB_REL(7);
+    tfs = trel;
     LB_PHASE(8);
     par ^= 1;
     K = s_K;
@@ -2276,9 +2327,11 @@ __global__ void __launch_bounds__(small::NT, 2)
 
   // ---- write back
   __syncthreads();
-  if (timing)
+  if (timing && tid == 0)
     for (int i = 0; i < NPHASE; ++i) b.phase_cycles[(size_t)trial * NPHASE + i] += ph[i];
 #undef LB_PHASE
+#undef LB_ARR
+#undef LB_REL
   const int status = s_status;
   if (tid == 0) {
     if (status != 0) {

@@ -346,15 +346,18 @@ class DeviceBatch:
     def clear_stats(self):
         N.check(N.lib().lb_batch_clear_stats(self.h))
 
-    PHASES = ("top_U", "cand_S1wait", "collect", "sort", "materialise", "ngram_G3", "recomb_rank",
-              "recomb_keep", "scatter", "loop_tail", "fusion", "cand_loop", "F_work",
-              "F_start", "F_head", "spec_overflow_permille")
+    # frames_small_kernel (k <= 64) TIMING build: per barrier event, the critical (last-arriving)
+    # warp's work since the previous release and the barrier's own release latency
+    PHASES = ("A_work", "S1_sync", "scan_work", "hcum_sync", "collect_work", "S2_sync",
+              "rank_work", "S3_sync", "F_work", "S4_sync", "recomb_work", "S5_sync",
+              "keep_work", "S6_sync", "scatter_work", "frame_sync", "spec_overflow_permille",
+              "ngram_warps_to_S3", "compute_to_S3", "ngover_work")
 
     def enable_phase_timing(self, on: bool = True):
         N.check(N.lib().lb_batch_enable_phase_timing(self.h, int(on)))
 
     def phase_cycles(self) -> dict:
-        out = np.zeros(16, dtype=np.uint64)
+        out = np.zeros(len(self.PHASES), dtype=np.uint64)
         N.check(N.lib().lb_batch_phase_cycles(self.h, N.ptr(out)))
         return {name: int(v) for name, v in zip(self.PHASES, out)}
 
