@@ -159,37 +159,62 @@ _CPU = {}
 
 
 def _cpu_worker(i):
+    w, cfg, raws, rw = _CPU["world"], _CPU["cfg"], _CPU["raws"], _CPU["ref"]
+    scale = cfg.ngram_weight / cfg.llm_weight
+    if rw is not None:  # the unmodified reference: lightbeam.decoder.decode (decoder.py:408-460)
+        d = rw.scale_log_softmax(raws[i % len(raws)], cfg)
+        t0 = time.perf_counter()
+        rw.decode(d, _CPU["ref_cfg"], rw.stub(scale), final_llm_only=True)
+        return d.shape[0], time.perf_counter() - t0
     from oracle import lightbeam_oracle as O
     from paper_2603_14002_b200 import StubScorer
 
-    w, cfg, raws = _CPU["world"], _CPU["cfg"], _CPU["raws"]
     d = O.log_softmax_scaled(raws[i % len(raws)], cfg.acoustic_scale)
-    sc = StubScorer(ngram_model=w.model, scale=cfg.ngram_weight / cfg.llm_weight)
+    sc = StubScorer(ngram_model=w.model, scale=scale)
     t0 = time.perf_counter()
     O.decode(d, cfg, w.table, w.model, sc, final_llm_only=True)
     return d.shape[0], time.perf_counter() - t0
 
 
+def reference_world(world):
+    """The unmodified reference's objects for `world` (oracle/refbridge.py; the package is
+    installed under baseline/_ref), or None when it is not available on this host."""
+    from oracle import refbridge
+
+    if refbridge.reference() is None:
+        return None
+    if _CPU.get("ref_of") is not world:
+        _CPU.update(ref_of=world, ref_world=refbridge.RefWorld(world))
+    return _CPU["ref_world"]
+
+
 def cpu_baseline(world, cfg, raws, budget_s):
-    """The oracle port (numpy/Python restatement of the reference decode) on all host cores:
-    a fork pool of os.cpu_count() workers decoding trials of the same workload for ~budget_s."""
+    """The reference decoder on all host cores: a fork pool of os.cpu_count() workers, each
+    decoding distinct utterances of the same workload for ~budget_s.  The unmodified reference
+    (`lightbeam.decoder.decode` from baseline/_ref, kind "reference") when it is installed,
+    else the oracle/ restatement (kind "port")."""
     import multiprocessing as mp
 
-    _CPU.update(world=world, cfg=cfg, raws=raws)
+    rw = reference_world(world)
+    _CPU.update(world=world, cfg=cfg, raws=raws, ref=rw,
+                ref_cfg=rw.config(cfg) if rw is not None else None)
     cores = os.cpu_count() or 1
     # probe one trial to size the sample
     frames0, dt0 = _cpu_worker(0)
     per_core = max(1, int(budget_s / max(dt0, 1e-3)))
-    n = max(cores, min(per_core * cores, 4 * len(raws)))
+    n = max(cores, min(per_core * cores, len(raws)))
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(cores) as pool:
         out = pool.map(_cpu_worker, range(n), chunksize=1)
     wall = time.perf_counter() - t0
     frames = sum(f for f, _ in out)
-    return {"value": frames / wall, "unit": "frames/s", "cores": cores, "kind": "port",
-            "sample": f"{n} of the workload's utterances (T={raws.shape[1]}), oracle/ restatement "
-                      f"of lightbeam.decoder.decode, fork pool x{cores}, {wall:.1f} s wall",
+    what = ("lightbeam.decoder.decode (the unmodified reference, baseline/_ref)" if rw is not None
+            else "oracle/ restatement of lightbeam.decoder.decode")
+    return {"value": frames / wall, "unit": "frames/s", "cores": cores,
+            "kind": "reference" if rw is not None else "port",
+            "sample": f"{n} distinct utterances of the workload (T={raws.shape[1]}), {what}, "
+                      f"fork pool x{cores}, {wall:.1f} s wall",
             "single_core_frames_per_s": frames0 / dt0}
 
 
@@ -404,9 +429,11 @@ def run_ours(args):
                "single_call": {"value": frames_per_step / single_s, "unit": "frames/s",
                                "api": "decode_batch_raw, one call per step"}}
 
+    gather = gather_check(raws, frames, cfg, world, scorer, dev, rank, world_n) if world_n > 1 else None
+
     cpu = None
     if rank == 0 and world_n == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(world, cfg, raws[: min(64, B)], args.cpu_seconds)
+        cpu = cpu_baseline(world, cfg, raws, args.cpu_seconds)
 
     clocks = clk.summary()
     wer = wer_check(world, cfg, scorer, dev, args) if rank == 0 and not args.no_wer else None
@@ -469,6 +496,7 @@ def run_ours(args):
             "layout": batch.layout(),
             "wer": wer,
             "llm_fusion": llm,
+            "gather": gather,
         }
         print(json.dumps(line))
     if world_n > 1:
@@ -903,6 +931,43 @@ def wer_check(world, cfg, scorer, dev, args):
                     "true token, b2t25 profile, beam 64, n-gram fusion (config 2 settings)"}
 
 
+def results_digest(items):
+    """sha256 over the ordered (text, score bits) of a result list (errors by message)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for it in items:
+        h.update(repr(it).encode())
+    return h.hexdigest()
+
+
+def result_key(r):
+    return ("error", type(r).__name__, str(r)) if isinstance(r, Exception) else (r.text, r.score.hex())
+
+
+def gather_check(raws, frames, cfg, world, scorer, dev, rank, world_n):
+    """Multi-rank runs: every rank decodes its own utterances once more through the public API
+    (untimed), the (text, score) results travel host-side to every rank (all_gather_object, the
+    only cross-rank data movement) in global utterance order, and rank 0 reports their count,
+    the distinct devices used and a digest a single-rank decode of the same utterances must
+    reproduce (tests/test_multiproc.py)."""
+    import socket
+
+    import torch
+
+    from paper_2603_14002_b200 import decode_batch_raw
+    from paper_2603_14002_b200.shard import gather_results
+
+    res = decode_batch_raw((raws, frames), cfg, world.table, world.model, scorer,
+                           final_llm_only=True, device=dev)
+    B = len(res)
+    merged = gather_results([result_key(r) for r in res], np.arange(B) + rank * B, world_n)
+    uuid = getattr(torch.cuda.get_device_properties(dev), "uuid", dev)
+    devs = gather_results([(socket.gethostname(), str(uuid))], np.array([rank]), world_n)
+    return {"utterances": len(merged), "ranks": world_n, "devices": len({str(d) for d in devs}),
+            "errors": sum(1 for m in merged if m[0] == "error"), "digest": results_digest(merged)}
+
+
 def _profile_traffic(name):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) recorded from an
     `ncu --set full` capture of the same kernel in profiles/ (the bench cannot run ncu)."""
@@ -934,7 +999,7 @@ def run_reference(args):
         pass
     budget = max(2.0, args.cpu_seconds / max(1, args.steps))
     for _ in range(args.steps):
-        cpu = cpu_baseline(world, cfg, raws[: min(64, len(raws))], budget)
+        cpu = cpu_baseline(world, cfg, raws, budget)
         vals.append(cpu["value"])
     value = statistics.median(vals)
     cpu["value"] = value
@@ -958,8 +1023,33 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` started without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (one per GPU; ranks beyond the visible GPUs
+    share devices over gloo, see init_dist) and return its exit code.  Rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args.gpus))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}; "
+              "using WORLD_SIZE", file=sys.stderr)
     apply_preset(args, dist_env()[0])
     if args.config in (1, 3, 5):
         if args.impl == "reference":

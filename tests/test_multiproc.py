@@ -96,3 +96,41 @@ def test_two_rank_gloo_shard_decode_gather():
     for i in range(8):
         assert m0[i] == _decode_one(O, w, cfg, raws[i, : lengths[i]], StubScorer)
     assert sum(1 for r in m0 if r[0] != "error") >= 1
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_gpu_gather_matches_single_rank():
+    """`bench.py --gpus 2` without a launcher spawns two ranks itself (on a one-GPU box they
+    share cuda:0 over gloo); both ranks' utterances are decoded on the device, gathered
+    host-side, and the gathered (text, score) list equals one single-process decode of the same
+    16 utterances (rank r decodes seeds 1000 + 8r ...)."""
+    import json
+    import subprocess
+    import sys
+
+    from paper_2603_14002_b200 import PROFILES, DeviceNgramScorer, decode_batch_raw, synth
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run(
+        [sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--trials", "8",
+         "--frames", "120", "--words", "2000", "--ngrams", "5000,3000,2000", "--steps", "2",
+         "--warmup", "3", "--no-llm", "--no-wer", "--no-cpu-baseline", "--no-e2e"],
+        capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["gather"]["ranks"] == 2
+    assert line["gather"]["utterances"] == 16
+    assert line["value"] > 0 and line["gpu_launches"] > 0
+
+    sys.path.insert(0, root)
+    import bench
+
+    world = synth.make_world(n_words=2000, n2=5000, n3=3000, n4=2000, seed=12345)
+    cfg = PROFILES["b2t25"].replace(beam_size=64)
+    raws = synth.make_logits(16, 120, 41, base_seed=1000)
+    scorer = DeviceNgramScorer(world.model, cfg.ngram_weight / cfg.llm_weight)
+    res = decode_batch_raw((raws, np.full(16, 120, np.int32)), cfg, world.table, world.model,
+                           scorer, final_llm_only=True)
+    assert line["gather"]["digest"] == bench.results_digest([bench.result_key(r) for r in res])
