@@ -38,10 +38,16 @@ def tokens(text: str, vocab: int) -> list[int]:
     return [1] + [8 + fnv1a64(w.encode("utf-8")) % (vocab - 8) for w in sc.split()]
 
 
-def hf_model(cfg, state_dict):
-    """transformers LlamaForCausalLM / GPT2LMHeadModel (fp32, CPU) with the given weights."""
+def hf_model(cfg, state_dict, device="cpu"):
+    """transformers LlamaForCausalLM / GPT2LMHeadModel (fp32) with the given weights.  `device`
+    "cuda" builds it on the GPU (TF32 off: plain fp32 FMA GEMMs) for the 8B-class shape, which
+    does not fit a CPU-speed test budget."""
     import torch
     from transformers import LlamaConfig, LlamaForCausalLM
+
+    if device != "cpu":
+        torch.backends.cuda.matmul.allow_tf32 = False
+        torch.backends.cudnn.allow_tf32 = False
 
     if getattr(cfg, "arch", "llama") == "gpt2":
         from transformers import GPT2Config, GPT2LMHeadModel
@@ -64,8 +70,9 @@ def hf_model(cfg, state_dict):
               attention_bias=False, mlp_bias=False)
     if cfg.rope_scaling:
         kw["rope_scaling"] = dict(rope_type="llama3", **cfg.rope_scaling)
-    m = LlamaForCausalLM(LlamaConfig(**kw)).float().eval()
-    missing, unexpected = m.load_state_dict(state_dict, strict=False)
+    with torch.device(device):
+        m = LlamaForCausalLM(LlamaConfig(**kw)).float().eval()
+    missing, unexpected = m.load_state_dict(state_dict, strict=False, assign=device != "cpu")
     assert not unexpected and all("rotary" in k for k in missing), (missing, unexpected)
     torch.set_grad_enabled(False)
     return m
@@ -74,9 +81,10 @@ def hf_model(cfg, state_dict):
 class OracleLlmScorer:
     """Reference-protocol scorer over a CPU fp32 transformers Llama."""
 
-    def __init__(self, cfg, state_dict):
+    def __init__(self, cfg, state_dict, device="cpu"):
         self.cfg = cfg
-        self.model = hf_model(cfg, state_dict)
+        self.device = device
+        self.model = hf_model(cfg, state_dict, device)
         self._ids = itertools.count(1)
         self.evaluations = 0
 
@@ -87,8 +95,8 @@ class OracleLlmScorer:
         import torch
 
         ids = tokens(text, self.cfg.vocab_size)
-        out = self.model(torch.tensor([ids])).logits[0].float()
-        return ids, torch.log_softmax(out, -1).double()
+        out = self.model(torch.tensor([ids], device=self.device)).logits[0].float()
+        return ids, torch.log_softmax(out, -1).double().cpu()
 
     def score(self, text: str) -> float:
         if not text:

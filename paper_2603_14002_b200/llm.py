@@ -237,12 +237,12 @@ class LlamaWeights:
         self.sin = torch.zeros((max_pos, half), dtype=torch.float32, device=dev)
         self.max_pos = max_pos
 
-    def hf_state_dict(self) -> dict:
-        """fp32 CPU tensors under transformers' LlamaForCausalLM / GPT2LMHeadModel names (for
-        the test oracle)."""
+    def hf_state_dict(self, device="cpu") -> dict:
+        """fp32 tensors (on `device`) under transformers' LlamaForCausalLM / GPT2LMHeadModel
+        names (for the test oracle)."""
         cfg = self.cfg
         if cfg.arch == "gpt2":
-            c = lambda t: t.float().cpu()  # noqa: E731
+            c = lambda t: t.float().to(device)  # noqa: E731
             sd = {"transformer.wte.weight": c(self.emb), "transformer.wpe.weight": c(self.wpe),
                   "transformer.ln_f.weight": c(self.norm), "transformer.ln_f.bias": c(self.normb),
                   "lm_head.weight": c(self.emb)}
@@ -260,22 +260,22 @@ class LlamaWeights:
                 sd[p + "mlp.c_proj.bias"] = c(L["bd"])
             return sd
         qn, kn = cfg.heads * cfg.head_dim, cfg.kv_heads * cfg.head_dim
-        sd = {"model.embed_tokens.weight": self.emb.float().cpu(),
-              "model.norm.weight": self.norm.float().cpu(),
-              "lm_head.weight": self.emb.float().cpu()}
+        sd = {"model.embed_tokens.weight": self.emb.float().to(device),
+              "model.norm.weight": self.norm.float().to(device),
+              "lm_head.weight": self.emb.float().to(device)}
         for i, L in enumerate(self.layers):
             p = f"model.layers.{i}."
-            w = L["wqkv"].float().cpu()
+            w = L["wqkv"].float().to(device)
             sd[p + "self_attn.q_proj.weight"] = w[:qn]
             sd[p + "self_attn.k_proj.weight"] = w[qn: qn + kn]
             sd[p + "self_attn.v_proj.weight"] = w[qn + kn:]
-            sd[p + "self_attn.o_proj.weight"] = L["wo"].float().cpu()
-            gu = L["wgu"].float().cpu()
+            sd[p + "self_attn.o_proj.weight"] = L["wo"].float().to(device)
+            gu = L["wgu"].float().to(device)
             sd[p + "mlp.gate_proj.weight"] = gu[: cfg.ffn]
             sd[p + "mlp.up_proj.weight"] = gu[cfg.ffn:]
-            sd[p + "mlp.down_proj.weight"] = L["wd"].float().cpu()
-            sd[p + "input_layernorm.weight"] = L["ln1"].float().cpu()
-            sd[p + "post_attention_layernorm.weight"] = L["ln2"].float().cpu()
+            sd[p + "mlp.down_proj.weight"] = L["wd"].float().to(device)
+            sd[p + "input_layernorm.weight"] = L["ln1"].float().to(device)
+            sd[p + "post_attention_layernorm.weight"] = L["ln2"].float().to(device)
         return sd
 
 
