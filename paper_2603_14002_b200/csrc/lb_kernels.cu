@@ -1533,6 +1533,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   __shared__ int ngtot[2];
   __shared__ unsigned s_calls, s_probes, s_pairs;
   __shared__ unsigned s_tarr[NBAR_EV], s_tbase;  // TIMING only
+  __shared__ unsigned long long ph[NPHASE];       // TIMING only (thread 0): no register cost
 
   const int trial = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1672,8 +1673,8 @@ __global__ void __launch_bounds__(small::NT, 2)
   // arriving warp records its arrival (atomicMax), thread 0 after the release adds
   // work[e] = last arrival - previous release and sync[e] = release - last arrival.
   const bool timing = TIMING && b.phase_cycles != nullptr;
-  unsigned long long ph[NPHASE];
-  for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
+  if (timing && tid == 0)
+    for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
   unsigned trel = timing ? (unsigned)clock() : 0u, tfs = trel;
 #define LB_ARR(e)                                              \
   if (timing && lane == 0) atomicMax(&s_tarr[e], (unsigned)clock() - s_tbase);
@@ -1838,7 +1839,11 @@ __global__ void __launch_bounds__(small::NT, 2)
             const bool ok = pin && al && (x > GUARD);
             const int bn = min(__double2int_rz(xmul(xsub(U, x), ibw)), NBINS - 1);
             bins[i] = ok ? (uint16_t)bn : (uint16_t)0xFFFF;
+#ifdef LB_E1
+            if (ok) atomicAdd(&hist[bn], 1u);
+#else
             atomicAdd(&hist[ok ? bn : NBINS], 1u);
+#endif
             wm = (ok && x > wm) ? x : wm;
           }
         }
@@ -2142,6 +2147,9 @@ __global__ void __launch_bounds__(small::NT, 2)
           const uint64_t regm = ~(((uint64_t)bm1 << 32) | bm0) & (n >= 64 ? ~0ull : ((1ull << n) - 1));
           int G = 1;
           while (G < 32 && 2 * G * n <= NC) G <<= 1;
+#ifdef LB_G4R
+          if (G < 4 && n <= NC / 4) G = 4;
+#endif
           const int groups = NC / G, g = tid / G, r = tid & (G - 1);
           for (int i0 = 0; i0 < n; i0 += groups) {
             const int i = i0 + g;
@@ -2215,6 +2223,9 @@ __global__ void __launch_bounds__(small::NT, 2)
         {
           int G = 1;
           while (G < 32 && 2 * G * nsel <= NC) G <<= 1;
+#ifdef LB_G4S
+          if (G < 4 && nsel <= NC / 4) G = 4;
+#endif
           const int groups = NC / G, g = tid / G, r = tid & (G - 1);
           for (int i0 = 0; i0 < nsel; i0 += groups) {
             const int i = i0 + g;
