@@ -357,8 +357,15 @@ def run_ours(args):
     scale = cfg.ngram_weight / cfg.llm_weight
     scorer = DeviceNgramScorer(world.model, scale)
     torch.cuda.set_device(dev)
+    world_s = time.perf_counter() - t_setup
+    setup = image_setup(world, dev)
     dm = device_model(world.table, world.model, dev)
     setup_s = time.perf_counter() - t_setup
+    setup["world_s"] = world_s
+    if world_n > 1:
+        from paper_2603_14002_b200.shard import gather_results
+
+        setup["per_rank"] = gather_results([dict(setup)], np.array([rank]), world_n)
     B, T = raws.shape[0], raws.shape[1]
     frames = np.full(B, T, dtype=np.int32)
     x_dev = torch.from_numpy(raws).to(f"cuda:{dev}")
@@ -545,6 +552,7 @@ def run_ours(args):
             "clocks": clocks,
             "counters": stats,
             "setup_s": setup_s,
+            "setup": setup,
             "parity_check": check,
             "phase_cycles_per_frame": phases,
             "layout": batch.layout(),
@@ -1107,6 +1115,34 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def image_setup(world, dev):
+    """Device-image setup of this rank: cold = compile the lexicon and n-gram
+    images from the components and upload them (written to a persisted .npz on the way), warm =
+    a fresh DeviceModel of the same components loading that file instead of compiling."""
+    import shutil
+    import tempfile
+
+    from paper_2603_14002_b200.decoder import (device_model, register_image_path,
+                                               release_device_model)
+
+    d = tempfile.mkdtemp(prefix="lb_images_")
+    try:
+        register_image_path(world.table, world.model, os.path.join(d, "images.npz"))
+        t0 = time.perf_counter()
+        dm = device_model(world.table, world.model, dev)
+        cold = (time.perf_counter() - t0, dm.image_source)
+        release_device_model(world.table, world.model, dev)
+        t0 = time.perf_counter()
+        dm = device_model(world.table, world.model, dev)
+        warm = (time.perf_counter() - t0, dm.image_source)
+        size = os.path.getsize(os.path.join(d, "images.npz"))
+    finally:
+        register_image_path(world.table, world.model, None)
+        shutil.rmtree(d, ignore_errors=True)
+    return {"images_cold_s": cold[0], "images_cold": cold[1], "images_warm_s": warm[0],
+            "images_warm": warm[1], "image_file_bytes": size}
 
 
 def _free_port():

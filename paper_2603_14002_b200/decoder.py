@@ -79,10 +79,26 @@ class DeviceModel:
 
     MAX_CACHED_BATCHES = 2
 
-    def __init__(self, tt, model, device: int = 0):
+    def __init__(self, tt, model, device: int = 0, image_path=None):
+        """Compile the images from (tt, model), or -- with `image_path` -- load them from that
+        file when it exists (skipping the compile) and write them there when it does not."""
+        import os
+
         lib = N.lib()
-        ng = images.compile_ngram(model)
-        tab = images.compile_table(tt, model, ng)
+        t0 = time.perf_counter()
+        if image_path is not None and os.path.exists(image_path):
+            tab, ng, bos_bo = images.load_images(image_path)
+            self.image_source = "loaded"
+        else:
+            ng = images.compile_ngram(model)
+            tab = images.compile_table(tt, model, ng)
+            bos_bo = float(model.backoffs.get(("<s>",), 0.0))
+            self.image_source = "compiled"
+            if image_path is not None:
+                tmp = f"{image_path}.{os.getpid()}.tmp"
+                images.save_images(tmp, tab, ng, bos_bo)
+                os.replace(tmp, image_path)  # atomic: concurrent ranks never read a partial file
+        self.image_s = time.perf_counter() - t0
         self.ngram_image, self.table_image = ng, tab
         self.surfaces = tab.surfaces
         self.whitespace_free = tab.whitespace_free
@@ -94,9 +110,8 @@ class DeviceModel:
             N.ptr(tab.table), tab.table.shape[0], tab.table.shape[1], tab.sink, tab.blank_id,
             tab.space_id, N.ptr(tab.comp_off), N.ptr(tab.comp_surface), N.ptr(tab.comp_lmword),
             len(tab.comp_surface), tab.surface_blob, N.ptr(soff), len(tab.surfaces))
-        nd = N.LbNgramDesc(model.order, len(ng.probs), N.ptr(ng.words), N.ptr(ng.probs),
-                           N.ptr(ng.backoffs), ng.bos_id, ng.eos_eff,
-                           float(model.backoffs.get(("<s>",), 0.0)))
+        nd = N.LbNgramDesc(ng.order, len(ng.probs), N.ptr(ng.words), N.ptr(ng.probs),
+                           N.ptr(ng.backoffs), ng.bos_id, ng.eos_eff, bos_bo)
         handle = C.c_void_p()
         N.check(lib.lb_model_create(C.byref(td), C.byref(nd), device, C.byref(handle)))
         self.handle = handle
@@ -209,6 +224,23 @@ def _drop_model(key):
         hit[2].release()
 
 
+_IMAGE_PATHS: dict = {}
+
+
+def register_image_path(tt, lm, path) -> None:
+    """Persist / reuse the device images of (tt, lm-model) at `path` (an .npz written by
+    images.save_images): the next DeviceModel built for these components loads the file when
+    it exists instead of compiling, and writes it when it does not.  `build_engine(...,
+    image_cache=dir)` registers a path keyed by the component files' sha256."""
+    model = getattr(lm, "model", lm)
+    key = (id(tt), id(model))
+    if path is None:  # unregister
+        _IMAGE_PATHS.pop(key, None)
+        return
+    _IMAGE_PATHS[key] = str(path)
+    weakref.finalize(tt, _IMAGE_PATHS.pop, key, None)
+
+
 def device_model(tt, lm, device: int = 0) -> DeviceModel:
     """Cached DeviceModel for (tt, lm-model, device).  The cache holds its components only
     weakly: when the table or the n-gram model is collected, the entry is dropped and its
@@ -222,7 +254,7 @@ def device_model(tt, lm, device: int = 0) -> DeviceModel:
         if wt() is tt and wm() is model and dm.handle:
             return dm
         _drop_model(key)  # an id() reused by a new object, or a released entry
-    dm = DeviceModel(tt, model, device)
+    dm = DeviceModel(tt, model, device, _IMAGE_PATHS.get((id(tt), id(model))))
     with _MODELS_LOCK:
         _MODELS[key] = (weakref.ref(tt), weakref.ref(model), dm)
     weakref.finalize(tt, _drop_model, key)

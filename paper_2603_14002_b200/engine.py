@@ -186,10 +186,13 @@ def _resolve_config(config, config_path, overrides) -> DecodeConfig:
 
 def build_engine(vocab_path, arpa_path, scorer_spec: ScorerSpec, lexicon_path=None,
                  table_path=None, config: DecodeConfig | None = None, config_path=None,
-                 config_overrides: dict | None = None, device: int = 0) -> Engine:
+                 config_overrides: dict | None = None, device: int = 0,
+                 image_cache=None) -> Engine:
     """Load the component set (the argument rules of the reference's `build_engine`,
     engine.py:132-177: exactly one of lexicon/table; a config object, file or overrides) and
-    record every component file's path and sha256."""
+    record every component file's path and sha256.  `image_cache` (a directory): the compiled
+    device images are kept there under the components' combined sha256, so the next engine
+    over the same files uploads them instead of compiling."""
     if (lexicon_path is None) == (table_path is None):
         raise ConfigError("provide exactly one of lexicon_path or table_path")
     cfg = _resolve_config(config, config_path, config_overrides)
@@ -203,5 +206,15 @@ def build_engine(vocab_path, arpa_path, scorer_spec: ScorerSpec, lexicon_path=No
              "arpa": arpa_path, "stub_table": scorer_spec.table_path}
     components = {name: {"path": str(p), "sha256": sha256_of(p)}
                   for name, p in files.items() if p}
+    if image_cache is not None:
+        from .decoder import register_image_path
+
+        digest = hashlib.sha256("".join(
+            f"{n}={components[n]['sha256']};" for n in ("vocab", "lexicon", "table", "arpa")
+            if n in components).encode()).hexdigest()
+        Path(image_cache).mkdir(parents=True, exist_ok=True)
+        path = Path(image_cache) / f"lb_images_{digest[:32]}.npz"
+        register_image_path(table, ngram_model, path)
+        components["device_images"] = {"path": str(path), "sha256_of_components": digest}
     return Engine(vocab, table, ngram_model, cfg, scorer_spec.build(ngram_model), components,
                   device)

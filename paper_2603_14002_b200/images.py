@@ -132,3 +132,56 @@ def compile_table(tt, model, img: NgramImage) -> TableImage:
         surface_off=soff,
         whitespace_free=ws_free,
     )
+
+
+# ------------------------------------------------------------------ persisted images
+IMAGE_FORMAT = 1
+
+
+def save_images(path, tab: TableImage, ng: NgramImage, bos_backoff: float) -> None:
+    """Write both compiled images to one uncompressed .npz (plain arrays + a small header), so
+    a later process uploads them without re-parsing or re-compiling the components.  The
+    reference builders this replaces run per process: `load_arpa` (ngram.py:90-174, 2.4 s for
+    1M n-grams) and `build_transition_table` (lexicon.py:149-209), plus compile_ngram /
+    compile_table here."""
+    import json
+
+    names = [None] * len(ng.word_id)
+    for w, i in ng.word_id.items():
+        names[i] = w
+    header = {"format": IMAGE_FORMAT, "sink": tab.sink, "blank_id": tab.blank_id,
+              "space_id": tab.space_id, "whitespace_free": tab.whitespace_free,
+              "order": ng.order, "bos_id": ng.bos_id, "eos_eff": ng.eos_eff, "unk_id": ng.unk_id,
+              "bos_backoff": bos_backoff}
+    lm_blob = "\n".join(names).encode("utf-8")
+    with open(path, "wb") as fh:
+        np.savez(fh, header=np.frombuffer(json.dumps(header).encode(), dtype=np.uint8),
+                 table=tab.table, comp_off=tab.comp_off, comp_surface=tab.comp_surface,
+                 comp_lmword=tab.comp_lmword,
+                 surface_blob=np.frombuffer(tab.surface_blob, dtype=np.uint8),
+                 surface_off=tab.surface_off, words=ng.words, probs=ng.probs,
+                 backoffs=ng.backoffs, lm_names=np.frombuffer(lm_blob, dtype=np.uint8))
+
+
+def load_images(path) -> tuple[TableImage, NgramImage, float]:
+    """Inverse of save_images: (TableImage, NgramImage, back-off of `<s>`)."""
+    import json
+
+    with np.load(path, allow_pickle=False) as z:
+        header = json.loads(bytes(z["header"]).decode())
+        if header.get("format") != IMAGE_FORMAT:
+            raise FormatError(f"{path}: image format {header.get('format')} != {IMAGE_FORMAT}")
+        blob = bytes(z["surface_blob"])
+        soff = z["surface_off"].astype(np.int64)
+        surfaces = [blob[soff[i]:soff[i + 1]].decode("utf-8") for i in range(len(soff) - 1)]
+        tab = TableImage(table=np.ascontiguousarray(z["table"], dtype=np.int32),
+                         sink=header["sink"], blank_id=header["blank_id"],
+                         space_id=header["space_id"], comp_off=z["comp_off"],
+                         comp_surface=z["comp_surface"], comp_lmword=z["comp_lmword"],
+                         surfaces=surfaces, surface_blob=blob, surface_off=soff,
+                         whitespace_free=bool(header["whitespace_free"]))
+        names = bytes(z["lm_names"]).decode("utf-8").split("\n")
+        ng = NgramImage(order=header["order"], words=z["words"], probs=z["probs"],
+                        backoffs=z["backoffs"], word_id={w: i for i, w in enumerate(names)},
+                        bos_id=header["bos_id"], eos_eff=header["eos_eff"], unk_id=header["unk_id"])
+    return tab, ng, float(header["bos_backoff"])

@@ -372,3 +372,49 @@ def test_bench_algorithmic_bytes_counts_consumed_pairs_only():
     # without speculation (every computed pair consumed) the probe term is the raw count
     full = dict(base, ngram_pairs_used=1000)
     assert bench.algorithmic_bytes(full) - got == 32 * 2000
+
+
+def test_device_image_file_round_trip(tmp_path):
+    """Persisted device images: save -> load reproduces every array and field
+    bit for bit (absent-prob NaN payloads included)."""
+    import dataclasses
+
+    from paper_2603_14002_b200 import images
+
+    w = synth.toy_world(n_words=1500, seed=3)
+    ng = images.compile_ngram(w.model)
+    tab = images.compile_table(w.table, w.model, ng)
+    p = tmp_path / "img.npz"
+    images.save_images(p, tab, ng, -0.25)
+    t2, n2, bo = images.load_images(p)
+    assert bo == -0.25
+    for a, b in ((tab, t2), (ng, n2)):
+        for f in dataclasses.fields(a):
+            x, y = getattr(a, f.name), getattr(b, f.name)
+            if isinstance(x, np.ndarray):
+                assert x.dtype == y.dtype and x.tobytes() == y.tobytes(), f.name
+            else:
+                assert x == y, f.name
+
+
+@pytest.mark.gpu
+def test_engine_image_cache_reuses_images(tmp_path):
+    """build_engine(image_cache=dir): the first engine compiles and writes the images, a second
+    engine over the same files loads them, and both decode identically."""
+    from paper_2603_14002_b200 import ScorerSpec, build_engine
+    from paper_2603_14002_b200.decoder import device_model
+
+    vp, lp, ap = _engine_files(tmp_path)
+    raws = synth.make_logits(4, 80, 41, base_seed=31)
+    outs, sources = [], []
+    for _ in range(2):
+        eng = build_engine(vp, ap, ScorerSpec(kind="device_ngram", scale=0.8), lexicon_path=lp,
+                           config=PROFILES["b2t25"].replace(beam_size=16),
+                           image_cache=tmp_path / "cache")
+        res = eng.decode_batch_raw(list(raws))
+        sources.append(device_model(eng.table, eng.ngram_model).image_source)
+        outs.append([(r.text, r.score, r.nbest) for r in res])
+        eng.close()
+    assert sources == ["compiled", "loaded"]
+    assert outs[0] == outs[1]
+    assert len(list((tmp_path / "cache").glob("lb_images_*.npz"))) == 1
