@@ -114,7 +114,7 @@ def dist_env():
 CONFIG_PRESETS = {
     # BASELINE.json configs[0]: single synthetic B2T'25-shaped trial, beam 10, toy 4-gram LM from
     # a small lexicon, tiny random-init LLM, fusion every 20 frames
-    1: dict(trials=1, frames=500, beam=10, words=2000, ngrams="5000,3000,2000", llm="tiny-gpt2",
+    1: dict(trials=1, frames=500, beam=10, words=2000, ngrams="5000,3000,2000", llm="tiny-char-lm",
             interval=20),
     # configs[4]: 8192 trials data-parallel over the GPUs, 8B-class LLM fusion (per-GPU trials =
     # 8192 / N, decoded in device batches of 256 so the bf16x2 prefix cache fits in HBM)
@@ -923,16 +923,24 @@ def reference_llm_sample(world, cfg, raws, scorer, n):
     scoring every unique text with a full forward pass (no KV reuse)."""
     from oracle import lightbeam_oracle as O
 
+    rw = reference_world(world)
     n = max(1, min(n, len(raws)))
     t0 = time.perf_counter()
     frames = 0
     for i in range(n):
-        d = O.log_softmax_scaled(raws[i], cfg.acoustic_scale)
-        O.decode(d, cfg, world.table, world.model, scorer)
+        if rw is not None:  # the unmodified reference decoder (baseline/_ref)
+            d = rw.scale_log_softmax(raws[i], cfg)
+            rw.decode(d, cfg, scorer)
+        else:
+            d = O.log_softmax_scaled(raws[i], cfg.acoustic_scale)
+            O.decode(d, cfg, world.table, world.model, scorer)
         frames += d.shape[0]
     wall = time.perf_counter() - t0
-    return {"value": frames / wall, "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": f"{n} utterances (T={raws.shape[1]}): oracle/ decode on one host core + "
+    who = ("lightbeam.decoder.decode (unmodified reference, baseline/_ref)" if rw is not None
+           else "oracle/ restatement of lightbeam.decoder.decode")
+    return {"value": frames / wall, "unit": "frames/s", "cores": 1,
+            "kind": "reference" if rw is not None else "port",
+            "sample": f"{n} utterances (T={raws.shape[1]}): {who} on one host core + "
                       "LlamaScorer.submit full-sequence GPU forwards (no KV reuse)"}
 
 

@@ -278,10 +278,17 @@ typedef struct {
   int32_t max_depth;   /* longest text in tokens after BOS (<= 4095) */
   int32_t bos_token;
   int32_t punct_tokens[3];             /* ".", "?", "!" */
-  const int32_t* surface_tokens;       /* host [n_surfaces]: token of each lexicon surface */
-  const int32_t* surface_tokens_first; /* host [n_surfaces]: token of the sentence-cased surface */
+  const int32_t* surface_tokens;       /* host: tokens of each lexicon surface after an earlier
+                                        * word (word-level: one per surface; char-level: " w o r d") */
+  const int32_t* surface_tokens_first; /* host: tokens of the surface as the sentence-cased first word */
   int32_t n_surfaces;
-  const void* embedding; /* device bf16 [vocab][hidden]; tied LM head; caller-owned */
+  const int32_t* surface_token_off;       /* host [n_surfaces + 1] CSR offsets into surface_tokens,
+                                           * or NULL: exactly one token per surface */
+  const int32_t* surface_token_off_first; /* same for surface_tokens_first */
+  const void* embedding; /* device bf16 [vocab][hidden]: the LM head (tied or not); caller-owned */
+  const float* head_f32; /* device fp32 [vocab][hidden] or NULL: next-token / punctuation dot
+                          * products read this copy of the LM head (weights that are not
+                          * bf16-exact, e.g. the sidecar's TinyCausalLM, model.ts:93-117) */
   int32_t precision;     /* 0 = bf16: one bf16 GEMM operand per activation, bf16 q/K/V;
                           * 1 = bf16x2: activations as hi+lo bf16 pairs ([M][2K] GEMM operands
                           *     against [W | W]), fp32 q/K/V -- fp32-equivalent activations on

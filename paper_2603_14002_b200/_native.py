@@ -179,7 +179,10 @@ class LbLlmDesc(C.Structure):
         ("surface_tokens", C.c_void_p),
         ("surface_tokens_first", C.c_void_p),
         ("n_surfaces", C.c_int32),
+        ("surface_token_off", C.c_void_p),
+        ("surface_token_off_first", C.c_void_p),
         ("embedding", C.c_void_p),
+        ("head_f32", C.c_void_p),
         ("precision", C.c_int32),
     ]
 

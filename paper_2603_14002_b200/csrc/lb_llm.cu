@@ -92,12 +92,15 @@ struct LlmDev {
   int32_t* cum_list;
   int32_t* wave_slots;
   int32_t* blk;        // [ceil(cap / 1024)] compaction block offsets
-  const int32_t* tok_low;
-  const int32_t* tok_cap;
+  const int32_t* tok_low;  // surface tokens after an earlier word, CSR over tok_low_off
+  const int32_t* tok_cap;  // surface tokens as the sentence-cased first word, CSR over tok_cap_off
+  const int32_t* tok_low_off;
+  const int32_t* tok_cap_off;
   int32_t n_surf;
   int32_t bos_tok;
   int32_t punct_tok[3];
   const bf16* emb;
+  const float* head32;  // fp32 LM head for the lp / punct dot products (nullptr: emb)
 };
 
 enum {
@@ -225,13 +228,21 @@ __global__ void __launch_bounds__(256) map_nodes_kernel(BatchDev b, LlmDev l, in
         continue;
       }
       const int d = l.nlist_depth[lb + j];
-      int s = -1;
-      if (d > l.max_depth) {
-        atomicOr(l.ctr + C_ERR, 4);
-      } else {
-        const int surf = (int)b.nsurf[nb + n];
-        const int tok = (d == 1 ? l.tok_cap : l.tok_low)[surf];
-        s = hashcons(l, ps, tok, d);
+      // the word's tokens hang below its parent's slot one slot per token (word-level
+      // tokenizers: one; char-level: " w o r d"); the node maps to the last one
+      const int surf = (int)b.nsurf[nb + n];
+      const int32_t* toff = d == 1 ? l.tok_cap_off : l.tok_low_off;
+      const int32_t* toks = d == 1 ? l.tok_cap : l.tok_low;
+      int s = ps;
+      for (int k = toff[surf]; k < toff[surf + 1]; ++k) {
+        const int dep = ld_vol(l.s_depth + s) + 1;
+        if (dep > l.max_depth) {
+          atomicOr(l.ctr + C_ERR, 4);
+          s = -1;
+          break;
+        }
+        s = hashcons(l, s, toks[k], dep);
+        if (s < 0) break;
       }
       ns[n] = s < 0 ? 0 : s;  // on error map to the root so the walk terminates
     }
@@ -1059,6 +1070,12 @@ __global__ void __launch_bounds__(512) lse_kernel(const TL* logits, int64_t ld, 
 
 // fp32 dot of an fp32 hidden row and a bf16 embedding row of length H by one warp (fixed
 // order: lane stride, xor tree)
+__device__ __forceinline__ float warp_dot32(const float* a, const float* b, int H) {
+  float acc = 0.f;
+  for (int i = threadIdx.x % 32; i < H; i += 32) acc += a[i] * b[i];
+  return warp_sum(acc);
+}
+
 __device__ __forceinline__ float warp_dot(const float* a, const bf16* b, int H) {
   float acc = 0.f;
   for (int i = threadIdx.x % 32 * 8; i < H; i += 256) {
@@ -1087,7 +1104,9 @@ __global__ void lp_kernel(LlmDev l) {
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
     const int s = l.cum_list[w];
     const int p = l.s_parent[s];
-    const float dot = warp_dot(l.s_h + (size_t)p * l.H, l.emb + (size_t)l.s_token[s] * l.H, l.H);
+    const int tk = l.s_token[s];
+    const float dot = l.head32 ? warp_dot32(l.s_h + (size_t)p * l.H, l.head32 + (size_t)tk * l.H, l.H)
+                               : warp_dot(l.s_h + (size_t)p * l.H, l.emb + (size_t)tk * l.H, l.H);
     if (lane == 0) l.s_lp[s] = (double)dot - (double)l.s_lse[p];
   }
 }
@@ -1147,7 +1166,9 @@ __global__ void __launch_bounds__(256) punct_kernel(BatchDev b, LlmDev l, int mi
     if (lane == 0) claim = atomicCAS(l.s_pun + s, 0, 1) == 0;
     if (!__shfl_sync(FULLMASK, claim, 0)) continue;
     for (int j = 0; j < 3; ++j) {
-      const float dot = warp_dot(l.s_h + (size_t)s * l.H, l.emb + (size_t)l.punct_tok[j] * l.H, l.H);
+      const int tk = l.punct_tok[j];
+      const float dot = l.head32 ? warp_dot32(l.s_h + (size_t)s * l.H, l.head32 + (size_t)tk * l.H, l.H)
+                                 : warp_dot(l.s_h + (size_t)s * l.H, l.emb + (size_t)tk * l.H, l.H);
       if (lane == 0) l.s_plp[(size_t)s * 3 + j] = (double)dot - (double)l.s_lse[s];
     }
   }
@@ -1499,6 +1520,8 @@ struct lb_llm {
   LlmDev dev{};
   int32_t* d_tok_low = nullptr;
   int32_t* d_tok_cap = nullptr;
+  int32_t* d_tok_low_off = nullptr;
+  int32_t* d_tok_cap_off = nullptr;
   int64_t node_slot_elems = 0;
   int64_t bytes = 0;
   // stats
@@ -1578,11 +1601,22 @@ int lb_llm_create(lb_batch* b, const lb_llm_desc* d, lb_llm** out) {
     return lbh::set_error(LB_ERR_ARG, "n_heads must be a multiple of n_kv_heads");
   const int G = d->n_heads / d->n_kv_heads;
   if (G != 1 && G != 2 && G != 4 && G != 8) return lbh::set_error(LB_ERR_ARG, "GQA group must be 1, 2, 4 or 8");
-  if (d->hidden % 8 != 0 || d->vocab % 8 != 0) return lbh::set_error(LB_ERR_ARG, "hidden and vocab must be multiples of 8");
+  if (d->hidden % 8 != 0) return lbh::set_error(LB_ERR_ARG, "hidden must be a multiple of 8");
   if (d->max_slots < 2 || d->max_slots > ((int64_t)1 << 30)) return lbh::set_error(LB_ERR_ARG, "max_slots out of range");
   if (d->max_depth < 1 || d->max_depth > 4095) return lbh::set_error(LB_ERR_ARG, "max_depth out of range");
   if (d->n_surfaces != (int32_t)b->m->surfaces.size())
     return lbh::set_error(LB_ERR_ARG, "surface token table does not match the model's surfaces");
+  for (int v = 0; v < 2; ++v) {  // surface token CSR (NULL offsets: one token per surface)
+    const int32_t* off = v ? d->surface_token_off_first : d->surface_token_off;
+    const int32_t* tk = v ? d->surface_tokens_first : d->surface_tokens;
+    if (off && off[0] != 0) return lbh::set_error(LB_ERR_ARG, "surface token offsets must start at 0");
+    for (int i = 0; i < d->n_surfaces; ++i) {
+      const int32_t a = off ? off[i] : i, e = off ? off[i + 1] : i + 1;
+      if (e <= a) return lbh::set_error(LB_ERR_ARG, "every surface needs at least one token");
+      for (int k = a; k < e; ++k)
+        if (tk[k] < 0 || tk[k] >= d->vocab) return lbh::set_error(LB_ERR_ARG, "surface token out of range");
+    }
+  }
   CKL(cudaSetDevice(b->m->device));
   lb_llm* l = new lb_llm();
   l->b = b;
@@ -1598,6 +1632,7 @@ int lb_llm_create(lb_batch* b, const lb_llm_desc* d, lb_llm** out) {
   x.bos_tok = d->bos_token;
   for (int j = 0; j < 3; ++j) x.punct_tok[j] = d->punct_tokens[j];
   x.emb = reinterpret_cast<const bf16*>(d->embedding);
+  x.head32 = d->head_f32;
   if (d->precision != 0 && d->precision != 1) return lbh::set_error(LB_ERR_ARG, "precision must be 0 (bf16) or 1 (bf16x2)");
   x.split = d->precision;
   x.n_surf = d->n_surfaces;
@@ -1633,12 +1668,26 @@ int lb_llm_create(lb_batch* b, const lb_llm_desc* d, lb_llm** out) {
   CKL(dalloc(&x.cum_list, cap));
   CKL(dalloc(&x.wave_slots, cap));
   CKL(dalloc(&x.blk, (cap + CB - 1) / CB));
-  CKL(dalloc(&l->d_tok_low, x.n_surf));
-  CKL(dalloc(&l->d_tok_cap, x.n_surf));
-  CKL(cudaMemcpy(l->d_tok_low, d->surface_tokens, x.n_surf * 4, cudaMemcpyHostToDevice));
-  CKL(cudaMemcpy(l->d_tok_cap, d->surface_tokens_first, x.n_surf * 4, cudaMemcpyHostToDevice));
+  {  // surface token tables as CSR (one token per surface when no offsets are given)
+    std::vector<int32_t> ident(x.n_surf + 1);
+    for (int i = 0; i <= x.n_surf; ++i) ident[i] = i;
+    const int32_t* offs[2] = {d->surface_token_off ? d->surface_token_off : ident.data(),
+                              d->surface_token_off_first ? d->surface_token_off_first : ident.data()};
+    const int32_t* toks[2] = {d->surface_tokens, d->surface_tokens_first};
+    int32_t** dtok[2] = {&l->d_tok_low, &l->d_tok_cap};
+    int32_t** doff[2] = {&l->d_tok_low_off, &l->d_tok_cap_off};
+    for (int v = 0; v < 2; ++v) {
+      const int32_t nt = offs[v][x.n_surf];
+      CKL(dalloc(dtok[v], (size_t)std::max(nt, 1)));
+      CKL(dalloc(doff[v], (size_t)x.n_surf + 1));
+      CKL(cudaMemcpy(*dtok[v], toks[v], (size_t)nt * 4, cudaMemcpyHostToDevice));
+      CKL(cudaMemcpy(*doff[v], offs[v], ((size_t)x.n_surf + 1) * 4, cudaMemcpyHostToDevice));
+    }
+  }
   x.tok_low = l->d_tok_low;
   x.tok_cap = l->d_tok_cap;
+  x.tok_low_off = l->d_tok_low_off;
+  x.tok_cap_off = l->d_tok_cap_off;
   l->bytes = (int64_t)cap * (4 * 6 + 8 * 5 + 4 + 4 * x.H + 4 * 4) + (int64_t)2 * x.L * cap * kvw * esz +
              (int64_t)hsz * 4 + l->node_slot_elems * 4 + (int64_t)B * x.nlist_cap * 8;
   *out = l;
@@ -1652,7 +1701,7 @@ int lb_llm_destroy(lb_llm* l) {
   void* ptrs[] = {x.s_parent, x.s_token, x.s_depth, x.s_fwd, x.s_cum, x.s_pun, x.s_lp, x.s_cumv,
                   x.s_plp, x.s_lse, x.s_h, x.kc, x.vc, x.htab, x.ctr, x.node_slot, x.nlist,
                   x.nlist_depth, x.fwd_list, x.cum_list, x.wave_slots, x.blk,
-                  l->d_tok_low, l->d_tok_cap};
+                  l->d_tok_low, l->d_tok_cap, l->d_tok_low_off, l->d_tok_cap_off};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete l;

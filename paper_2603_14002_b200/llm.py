@@ -57,11 +57,13 @@ class LlmConfig:
     rms_eps: float = 1e-5
     init_std: float = 0.02
     arch: str = "llama"  # "llama" | "gpt2" (learned positions, LayerNorm, GELU, biases, MHA)
+    #                      | "tinychar" (the reference sidecar's TinyCausalLM, charlm.py)
+    identifier: str = ""  # tinychar: the model identifier its weights derive from (model.ts:93)
 
     def n_params(self) -> int:
         att = self.hidden * (self.heads + 2 * self.kv_heads) * self.head_dim
         att += self.heads * self.head_dim * self.hidden
-        mlp = (2 if self.arch == "gpt2" else 3) * self.hidden * self.ffn
+        mlp = (3 if self.arch == "llama" else 2) * self.hidden * self.ffn
         return self.vocab_size * self.hidden + self.layers * (att + mlp + 2 * self.hidden) + self.hidden
 
     def flops_per_token(self) -> float:
@@ -69,7 +71,7 @@ class LlmConfig:
         prefix excluded)."""
         att = self.hidden * (self.heads + 2 * self.kv_heads) * self.head_dim
         att += self.heads * self.head_dim * self.hidden
-        mlp = (2 if self.arch == "gpt2" else 3) * self.hidden * self.ffn
+        mlp = (3 if self.arch == "llama" else 2) * self.hidden * self.ffn
         return 2.0 * (self.layers * (att + mlp) + self.vocab_size * self.hidden)
 
 
@@ -83,6 +85,11 @@ PRESETS = {
     "tiny-gpt2": LlmConfig("tiny-gpt2", 4096, 64, 2, 1, 1, 256, 64, arch="gpt2"),
     # a tiny Llama-architecture model (fast tests of the Llama kernels)
     "tiny": LlmConfig("tiny", 4096, 128, 2, 2, 1, 512, 64),
+    # config 1 with the reference's own scorer model: the sidecar's TinyCausalLM (model.ts:20-26:
+    # char-level, dim 32, 2 heads of 16 -- padded to 64 on the device, q pre-scaled by 2 so the
+    # 1/sqrt(64) softmax scale equals model.ts's 1/sqrt(16) exactly -- 2 layers, untied head)
+    "tiny-char-lm": LlmConfig("tiny-char-lm", 97, 32, 2, 2, 2, 128, 64, rms_eps=1e-5,
+                              arch="tinychar", identifier="tiny-char-lm-v1"),
     # config 3: Llama-3.2-1B architecture
     "llama-3.2-1b": LlmConfig("llama-3.2-1b", 128256, 2048, 16, 32, 8, 8192, 64,
                               rope_scaling=_LLAMA3_1B_ROPE),
@@ -183,8 +190,11 @@ class LlamaWeights:
             return w.to(torch.bfloat16)
 
         H, hd = cfg.hidden, cfg.head_dim
-        self.emb = rnd(cfg.vocab_size, H)
         self.layers = []
+        if cfg.arch == "tinychar":
+            self._init_tinychar(max_pos)
+            return
+        self.emb = rnd(cfg.vocab_size, H)
         if cfg.arch == "gpt2":
             self._init_gpt2(rnd, max_pos)
             return
@@ -235,6 +245,59 @@ class LlamaWeights:
         half = cfg.head_dim // 2  # no rotary embedding: identity tables for the shared kernel
         self.cos = torch.ones((max_pos, half), dtype=torch.float32, device=dev)
         self.sin = torch.zeros((max_pos, half), dtype=torch.float32, device=dev)
+        self.max_pos = max_pos
+
+    def _init_tinychar(self, max_pos):
+        """TinyCausalLM (charlm.tiny_char_weights, model.ts:93-117) on the GPT-2-style kernels:
+        LayerNorm gain 1 / shift 0 (model.ts:220-236 has no affine), no biases, tanh GELU,
+        learned positions, MHA with head_dim padded 16 -> 64 (zero rows / columns; q x 2 so the
+        kernel's 1/sqrt(64) scale is model.ts's 1/sqrt(16)), untied LM head.  The float64
+        weights are not bf16-exact, so every GEMM weight is a bf16 hi + lo pair (the lo term is
+        one more GEMM against the hi half of the activation), the input rows are fp32 and the
+        next-token dot products read an fp32 copy of the head."""
+        import torch
+
+        from .charlm import VOCAB, tiny_char_weights
+
+        cfg, H, dev = self.cfg, self.cfg.hidden, self.device
+        nh, hdp = cfg.heads, cfg.head_dim
+        w = tiny_char_weights(cfg.identifier or "tiny-char-lm-v1", H, nh, cfg.layers, 1024)
+        hd = H // nh
+        self.f64 = w
+
+        def hilo(a):
+            t = torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+            hi = t.to(torch.bfloat16)
+            return hi.contiguous(), (t - hi.double()).to(torch.bfloat16).contiguous()
+
+        f32 = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32, device=dev)  # noqa: E731
+        self.emb_in = f32(w["embed"])
+        self.wpe = f32(w["pos"])
+        vpad = (VOCAB + 7) // 8 * 8  # GEMM row pitch; the log-sum-exp reads the first VOCAB
+        head = np.zeros((vpad, H))
+        head[:VOCAB] = w["wout"].T
+        self.emb, self.head_lo = hilo(head)
+        self.head32 = f32(w["wout"].T)
+        ones = lambda n: torch.ones(n, dtype=torch.float32, device=dev)  # noqa: E731
+        zeros = lambda n: torch.zeros(n, dtype=torch.float32, device=dev)  # noqa: E731
+        for li in range(cfg.layers):
+            wqkv = np.zeros((3 * nh * hdp, H))
+            for h in range(nh):
+                for part, name, sc in ((0, "wq", 2.0), (1, "wk", 1.0), (2, "wv", 1.0)):
+                    r0 = part * nh * hdp + h * hdp
+                    wqkv[r0:r0 + hd] = sc * w[f"{name}.{li}"][:, h * hd:(h + 1) * hd].T
+            wo = np.zeros((H, nh * hdp))
+            for h in range(nh):
+                wo[:, h * hdp:h * hdp + hd] = w[f"wo.{li}"][h * hd:(h + 1) * hd, :].T
+            L = {"ln1": ones(H), "ln1b": zeros(H), "ln2": ones(H), "ln2b": zeros(H),
+                 "bqkv": None, "bo": None, "bfc": None, "bd": None}
+            for k, m in (("wqkv", wqkv), ("wo", wo), ("wfc", w[f"w1.{li}"].T),
+                         ("wd", w[f"w2.{li}"].T)):
+                L[k], L[k + "_lo"] = hilo(m)
+            self.layers.append(L)
+        self.norm, self.normb = ones(H), zeros(H)
+        self.cos = torch.ones((max_pos, hdp // 2), dtype=torch.float32, device=dev)
+        self.sin = torch.zeros((max_pos, hdp // 2), dtype=torch.float32, device=dev)
         self.max_pos = max_pos
 
     def hf_state_dict(self, device="cpu") -> dict:
@@ -302,8 +365,16 @@ class LlamaScorer:
         self.cfg = get_config(config)
         self.device = device
         self.seed = seed
+        if self.cfg.arch == "tinychar":
+            max_depth = min(max_depth, 1023)  # model.ts:25 maxContext 1024 positions
+            lm_head = "cublas"  # untied 97-token head: hi/lo GEMM + log-sum-exp kernel
         self.weights = LlamaWeights(self.cfg, seed, f"cuda:{device}", max_pos=max(max_depth + 2, 1100))
-        self.tokenizer = WordTokenizer(self.cfg.vocab_size)
+        if self.cfg.arch == "tinychar":
+            from .charlm import CharTokenizer
+
+            self.tokenizer = CharTokenizer()
+        else:
+            self.tokenizer = WordTokenizer(self.cfg.vocab_size)
         self.max_slots = max_slots
         self.max_depth = max_depth
         self.row_chunk = row_chunk
@@ -312,6 +383,8 @@ class LlamaScorer:
         self._ids = itertools.count(1)
         if precision not in self.PRECISIONS:
             raise ValueError(f"precision must be one of {self.PRECISIONS}")
+        if self.cfg.arch == "tinychar" and precision != "bf16x2":
+            raise ValueError("the TinyCausalLM runs in bf16x2 only (float64 weights as hi+lo)")
         if lm_head not in ("fused", "cublas"):
             raise ValueError("lm_head must be 'fused' (tcgen05 GEMM + log-sum-exp) or 'cublas'")
         self.lm_head = lm_head
@@ -374,6 +447,8 @@ class LlamaScorer:
         """Full-sequence forward per text (plain torch: bf16 GEMMs, SDPA, fp32 log-softmax)."""
         import torch
 
+        if self.cfg.arch == "tinychar":  # float64, as the sidecar computes (model.ts:119-209)
+            return self._dense_tinychar(texts, eos)
         res: list = [None] * len(texts)
         toks = [self.tokenizer.encode(t) for t in texts]
         order = sorted(range(len(texts)), key=lambda i: len(toks[i]))
@@ -398,6 +473,11 @@ class LlamaScorer:
                 res[k] = (lp_all[r], plp[r] if eos else None)
             i = j
         return res
+
+    def _dense_tinychar(self, texts, eos):
+        from .charlm import dense_scores
+
+        return dense_scores(self.weights.f64, texts, self.weights.device, eos)
 
     def _dense_forward(self, ids, lens, eos):
         split = frozenset(("qkv", "o", "gu", "down", "attn", "lm")) if self.split else frozenset()
@@ -549,8 +629,10 @@ def _dense_forward_gpt2(W, ids, lens, eos, exact_fp32, split):
     return out_lp, out_p
 
 
-def _surface_tokens(dm, tok: WordTokenizer):
-    key = ("llm_tokens", tok.vocab_size)
+def _surface_tokens(dm, tok):
+    """Per-surface token tables of the tokenizer: (low, cap) one token each (word level) or
+    (low, low_off, cap, cap_off) CSR (char level), cached on the device model."""
+    key = ("llm_tokens", type(tok).__name__, tok.vocab_size)
     cache = dm.__dict__.setdefault("_tok_cache", {})
     if key not in cache:
         cache[key] = tok.surface_tables(dm.surfaces)
@@ -566,8 +648,14 @@ class DeviceLlmSession:
         self.scorer = scorer
         self.batch = batch
         cfg, W = scorer.cfg, scorer.weights
-        low, cap = _surface_tokens(batch.dm, scorer.tokenizer)
-        self._low, self._cap = low, cap
+        tabs = _surface_tokens(batch.dm, scorer.tokenizer)
+        if len(tabs) == 2:
+            low, cap = tabs
+            low_off = cap_off = None
+        else:
+            low, low_off, cap, cap_off = tabs
+        self._low, self._cap = low, cap  # (word level: token per surface)
+        self._tabs = tabs
         esz = 4 if scorer.split else 2
         per_slot = cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * esz + cfg.hidden * 4 + 96
         if scorer.max_slots:
@@ -587,13 +675,19 @@ class DeviceLlmSession:
         d.head_dim, d.hidden, d.vocab = cfg.head_dim, cfg.hidden, cfg.vocab_size
         d.max_slots = max_slots
         d.max_depth = scorer.max_depth
-        d.bos_token = BOS_ID
+        tok = scorer.tokenizer
+        d.bos_token = tok.bos
+        pids = getattr(tok, "punct_ids", PUNCT_IDS)
         for j in range(3):
-            d.punct_tokens[j] = PUNCT_IDS[j]
+            d.punct_tokens[j] = pids[j]
         d.surface_tokens = low.ctypes.data
         d.surface_tokens_first = cap.ctypes.data
-        d.n_surfaces = len(low)
+        d.n_surfaces = len(batch.dm.surfaces)
+        d.surface_token_off = low_off.ctypes.data if low_off is not None else None
+        d.surface_token_off_first = cap_off.ctypes.data if cap_off is not None else None
         d.embedding = W.emb.data_ptr()
+        head32 = getattr(W, "head32", None)
+        d.head_f32 = head32.data_ptr() if head32 is not None else None
         d.precision = 1 if scorer.split else 0
         h = C.c_void_p()
         N.check(N.lib().lb_llm_create(batch.h, C.byref(d), C.byref(h)))
@@ -696,7 +790,7 @@ class DeviceLlmSession:
         tok, pos, slot, chain = ws["tok"][:n], ws["pos"][:n], ws["slot"][:n], ws["chain"][:n]
         N.check(lib.lb_llm_wave_rows(self.h, wave, row0, n, tok.data_ptr(), pos.data_ptr(),
                                      slot.data_ptr(), chain.data_ptr()))
-        if cfg.arch == "gpt2":
+        if cfg.arch in ("gpt2", "tinychar"):
             return self._forward_rows_gpt2(tok, pos, slot, chain, n)
         x = W.emb.index_select(0, tok.long()).float()
         hn, q, att, act = ws["hn"][:n], ws["q"][:n], ws["att"][:n], ws["act"][:n]
@@ -752,8 +846,13 @@ class DeviceLlmSession:
         chunk = self.scorer.lm_chunk // (2 if sfx else 1)
         for c0 in range(0, n, chunk):
             c1 = min(n, c0 + chunk)
-            if sfx:  # hi|lo against [E | E], fp32 logits
-                logits = torch.mm(hn[c0:c1], self.scorer.emb2.t(), out_dtype=f32)
+            head_lo = getattr(W, "head_lo", None)
+            if sfx or head_lo is not None:  # hi|lo against [E | E], fp32 logits
+                logits = (torch.mm(hn[c0:c1], self.scorer.emb2.t(), out_dtype=f32) if sfx
+                          else torch.mm(hn[c0:c1], W.emb.t(), out_dtype=f32))
+                if head_lo is not None:  # + hi @ E_lo^T (head weights not bf16-exact)
+                    torch.addmm(logits, hn[c0:c1, : head_lo.shape[1]], head_lo.t(), out_dtype=f32,
+                                out=logits)
             else:
                 logits = torch.mm(hn[c0:c1], W.emb.t())
             N.check(lib.lb_llm_lse(self.h, logits.data_ptr(), c1 - c0, logits.stride(0),
@@ -770,29 +869,45 @@ class DeviceLlmSession:
         hn, q, att, act = ws["hn"][:n], ws["q"][:n], ws["att"][:n], ws["act"][:n]
         eps, f32 = cfg.rms_eps, torch.float32
         sfx = "2" if self.scorer.split else ""
-        x = W.emb.index_select(0, tok.long()).float() + W.wpe.index_select(0, pos.long())
+        emb_in = getattr(W, "emb_in", None)  # tinychar: fp32 input rows
+        x = (emb_in.index_select(0, tok.long()) if emb_in is not None
+             else W.emb.index_select(0, tok.long()).float()) + W.wpe.index_select(0, pos.long())
+
+        def lo_fix(out, a, L, k):  # weights that are bf16 hi + lo pairs: out += a_hi @ W_lo^T
+            wl = L.get(k + "_lo")
+            if wl is not None:
+                torch.addmm(out, a[:, : wl.shape[1]], wl.t(), out_dtype=f32, out=out)
+
         L0 = W.layers[0]
         N.check(lib.lb_llm_layernorm(self.h, x.data_ptr(), None, L0["ln1"].data_ptr(),
                                      L0["ln1b"].data_ptr(), eps, n, hn.data_ptr(), None))
         for li, L in enumerate(W.layers):
             qkv = torch.mm(hn, L["wqkv" + sfx].t(), out_dtype=f32)
-            qkv += L["bqkv"]
+            lo_fix(qkv, hn, L, "wqkv")
+            if L["bqkv"] is not None:
+                qkv += L["bqkv"]
             N.check(lib.lb_llm_rope_kv(self.h, li, qkv.data_ptr(), n, pos.data_ptr(), slot.data_ptr(),
                                        W.cos.data_ptr(), W.sin.data_ptr(), q.data_ptr()))
             del qkv
             N.check(lib.lb_llm_attention(self.h, li, q.data_ptr(), n, chain.data_ptr(), pos.data_ptr(),
                                          att.data_ptr()))
             o = torch.mm(att, L["wo" + sfx].t(), out_dtype=f32)
-            o += L["bo"]
+            lo_fix(o, att, L, "wo")
+            if L["bo"] is not None:
+                o += L["bo"]
             N.check(lib.lb_llm_layernorm(self.h, x.data_ptr(), o.data_ptr(), L["ln2"].data_ptr(),
                                          L["ln2b"].data_ptr(), eps, n, hn.data_ptr(), None))
             del o
             f = torch.mm(hn, L["wfc" + sfx].t(), out_dtype=f32)
-            N.check(lib.lb_llm_gelu(self.h, f.data_ptr(), L["bfc"].data_ptr(), n, cfg.ffn,
-                                    act.data_ptr()))
+            lo_fix(f, hn, L, "wfc")
+            N.check(lib.lb_llm_gelu(self.h, f.data_ptr(),
+                                    L["bfc"].data_ptr() if L["bfc"] is not None else None, n,
+                                    cfg.ffn, act.data_ptr()))
             del f
             dn = torch.mm(act, L["wd" + sfx].t(), out_dtype=f32)
-            dn += L["bd"]
+            lo_fix(dn, act, L, "wd")
+            if L["bd"] is not None:
+                dn += L["bd"]
             last = li + 1 == cfg.layers
             nw, nb = (W.norm, W.normb) if last else (W.layers[li + 1]["ln1"], W.layers[li + 1]["ln1b"])
             N.check(lib.lb_llm_layernorm(self.h, x.data_ptr(), dn.data_ptr(), nw.data_ptr(),
