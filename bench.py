@@ -598,7 +598,7 @@ def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1, su
     frames = np.full(B, T, dtype=np.int32)
     x_dev = torch.from_numpy(raws).to(f"cuda:{dev}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
-    batch = dm.batch(cfg, SB, T)
+    batch = dm.batch(cfg, SB, T, own_stream=bool(getattr(scorer, "graphs", False)))
     row_bytes = T * raws.shape[2] * 4
 
     acc = {"llm_ms": 0.0, "rows": 0, "slots": 0, "events": 0, "waves": 0, "last_b0": 0}
@@ -893,6 +893,7 @@ def run_llm(args):
                     "ms_per_step": llm_ms / args.steps},
             "e2e": e2e,
             "gpu_launches": launches,
+            "llm_graph_mode": bool(getattr(scorer, "graphs", False)),
             "roofline": {"bound": "tensor", "kernel": "LLM body GEMMs + LM head (bf16 tensor cores)",
                          "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_tf,

@@ -237,6 +237,8 @@ int lb_host_free(void* p);
 
 /* Device-side timing of everything enqueued between mark_begin and mark_end (CUDA events on
  * the batch stream); also the number of kernels this library launched in between. */
+/* kernels this library has launched so far (all batches; CUDA-graph replays not included) */
+int lb_launch_count(uint64_t* out);
 int lb_batch_mark_begin(lb_batch* b);
 int lb_batch_mark_end(lb_batch* b, float* ms, int64_t* launches);
 int lb_batch_sync(lb_batch* b);
@@ -300,6 +302,10 @@ int lb_llm_destroy(lb_llm* l);
 int lb_llm_footprint(lb_llm* l, int64_t* bytes);
 /* forget every cached prefix (start of a batch decode; the BOS row joins the next plan) */
 int lb_llm_reset(lb_llm* l);
+/* the two halves of lb_llm_reset: the device state (stream-ordered kernels, CUDA-graph
+ * capturable) and the host-side event statistics (run before each graph replay) */
+int lb_llm_reset_device(lb_llm* l);
+int lb_llm_reset_stats(lb_llm* l);
 /* wave_rows: caller array of LB_LLM_MAX_WAVES.  Synchronises the batch stream once. */
 int lb_llm_plan(lb_llm* l, int32_t final_, int32_t min_frames, int32_t* n_waves,
                 int64_t* wave_rows);
@@ -307,6 +313,15 @@ int lb_llm_plan(lb_llm* l, int32_t final_, int32_t min_frames, int32_t* n_waves,
 int lb_llm_wave_rows(lb_llm* l, int32_t wave, int64_t row0, int32_t n, int32_t* tokens,
                      int32_t* positions, int32_t* slots, int32_t* chains);
 int lb_llm_finish(lb_llm* l, int32_t final_, int32_t min_frames);
+/* Graph-capturable event (no host synchronisation, for CUDA-graph replay of whole decodes):
+ * the planning kernels of lb_llm_plan with the row count left on the device; the forward then
+ * always runs rows_cap rows (lb_llm_wave_rows_async pads past the event's rows with BOS-only
+ * rows that write a scratch slot).  An event with more than rows_cap rows sets a device flag
+ * that lb_llm_check (synchronises) reports as LB_ERR_CAPACITY: the caller re-decodes eagerly. */
+int lb_llm_plan_async(lb_llm* l, int32_t final_, int32_t min_frames, int32_t rows_cap);
+int lb_llm_wave_rows_async(lb_llm* l, int32_t rows_cap, int32_t* tokens, int32_t* positions,
+                           int32_t* slots, int32_t* chains);
+int lb_llm_check(lb_llm* l);
 /* x[M][hidden] fp32 residual (+= delta fp32 [M][hidden] if non-NULL); out bf16 = RMSNorm(x)*w
  * ([M][2 hidden] hi|lo pairs in bf16x2 precision).
  * store_slots != NULL: the rows are the final hidden states of those slots (kept in fp32 for

@@ -237,6 +237,12 @@ _SIGS = {
     "lb_llm_plan": (C.c_int, [_P, _I32, _I32, _P, _P]),
     "lb_llm_wave_rows": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
     "lb_llm_finish": (C.c_int, [_P, _I32, _I32]),
+    "lb_llm_plan_async": (C.c_int, [_P, _I32, _I32, _I32]),
+    "lb_llm_wave_rows_async": (C.c_int, [_P, _I32, _P, _P, _P, _P]),
+    "lb_llm_check": (C.c_int, [_P]),
+    "lb_llm_reset_stats": (C.c_int, [_P]),
+    "lb_llm_reset_device": (C.c_int, [_P]),
+    "lb_launch_count": (C.c_int, [_P]),
     "lb_llm_rmsnorm": (C.c_int, [_P, _P, _P, _P, C.c_float, _I32, _P, _P]),
     "lb_llm_rope_kv": (C.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _P, _P]),
     "lb_llm_layernorm": (C.c_int, [_P, _P, _P, _P, _P, C.c_float, _I32, _P, _P]),

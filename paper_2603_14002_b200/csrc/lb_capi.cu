@@ -1056,6 +1056,12 @@ int lb_host_free(void* p) {
   return LB_OK;
 }
 
+int lb_launch_count(uint64_t* out) {
+  if (!out) return fail(LB_ERR_ARG, "null argument");
+  *out = lbk::g_launches;
+  return LB_OK;
+}
+
 int lb_batch_mark_begin(lb_batch* b) {
   if (!b) return fail(LB_ERR_ARG, "null argument");
   b->launch_mark = lbk::g_launches;

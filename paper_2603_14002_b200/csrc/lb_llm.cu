@@ -109,6 +109,9 @@ enum {
   C_NFWD = 2,    // forward-set size of this event
   C_NCUM = 3,    // cum-needed slots of this event
   C_BOS = 4,     // 1: BOS slot still to be forwarded
+  C_EVENTS = 5,  // graph-mode (async) events, forward rows, largest event: device-side stats
+  C_ROWS = 6,
+  C_MAXROWS = 7,
   C_NCTR = 8
 };
 
@@ -152,7 +155,7 @@ __device__ int hashcons(const LlmDev& l, int ps, int tok, int depth) {
     if (v < 0) {
       if (mine < 0) {
         mine = atomicAdd(l.ctr + C_SLOTS, 1);
-        if (mine >= l.cap) {
+        if (mine >= l.cap - 1) {  // slot cap-1: scratch row of padded graph-mode rows
           atomicOr(l.ctr + C_ERR, 1);
           return -1;
         }
@@ -346,6 +349,46 @@ __global__ void __launch_bounds__(CB) compact_kernel(LlmDev l, const int32_t* bl
   }
   __syncthreads();
   if (f) l.wave_slots[blk_off[blockIdx.x] + wsum[warp] + __popc(bal & ((1u << lane) - 1))] = s;
+}
+
+// Graph-mode events: the host never reads the row count.  plan_async_kernel flags an event
+// with more rows than the captured capacity (the caller re-runs the decode eagerly) and keeps
+// the device-side stats; wave_rows_async_kernel fills all `cap_rows` rows, the ones past the
+// event's count as BOS-only padding whose K/V, hidden state and LSE land in the scratch slot.
+__global__ void plan_async_kernel(LlmDev l, int cap_rows) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int n = l.ctr[C_NFWD];
+    if (n > cap_rows) l.ctr[C_ERR] |= 8;
+    l.ctr[C_EVENTS] += 1;
+    l.ctr[C_ROWS] += min(n, cap_rows);
+    l.ctr[C_MAXROWS] = max(l.ctr[C_MAXROWS], n);
+  }
+}
+
+__global__ void wave_rows_async_kernel(LlmDev l, int cap_rows, int32_t* tok, int32_t* pos,
+                                       int32_t* slots, int32_t* chains) {
+  const int pitch = l.max_depth + 1;
+  const int n = min(l.ctr[C_NFWD], cap_rows);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < cap_rows; r += gridDim.x * blockDim.x) {
+    int32_t* ch = chains + (size_t)r * pitch;
+    if (r >= n) {
+      tok[r] = l.bos_tok;
+      pos[r] = 0;
+      slots[r] = (int32_t)(l.cap - 1);
+      ch[0] = 0;
+      continue;
+    }
+    const int s = l.wave_slots[r];
+    const int d = l.s_depth[s];
+    tok[r] = l.s_token[s];
+    pos[r] = d;
+    slots[r] = s;
+    int cur = s;
+    for (int j = d; j >= 0; --j) {
+      ch[j] = cur;
+      cur = l.s_parent[cur];
+    }
+  }
 }
 
 __global__ void wave_rows_kernel(LlmDev l, int64_t row0, int n, int32_t* tok, int32_t* pos,
@@ -1215,6 +1258,9 @@ __global__ void llm_apply_kernel(CfgDev c, BatchDev b, LlmDev l, int final_, int
 
 __global__ void llm_reset_kernel(LlmDev l) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int i = 0; i < C_NCTR; ++i) l.ctr[i] = 0;  // (a kernel, not a host copy: capturable)
+    l.ctr[C_SLOTS] = 1;
+    l.ctr[C_BOS] = 1;
     l.s_parent[0] = -1;
     l.s_token[0] = l.bos_tok;
     l.s_depth[0] = 0;
@@ -1715,16 +1761,24 @@ int lb_llm_footprint(lb_llm* l, int64_t* bytes) {
 }
 
 int lb_llm_reset(lb_llm* l) {
+  const int rc = lb_llm_reset_device(l);
+  return rc ? rc : lb_llm_reset_stats(l);
+}
+
+int lb_llm_reset_device(lb_llm* l) {
   if (!l) return lbh::set_error(LB_ERR_ARG, "null argument");
   LlmDev& x = l->dev;
   cudaStream_t st = l->b->st;
   CKL(cudaMemsetAsync(x.htab, 0xFF, ((size_t)x.hmask + 1) * 4, st));
   CKL(cudaMemsetAsync(x.node_slot, 0xFF, (size_t)l->node_slot_elems * 4, st));
-  int32_t c[C_NCTR] = {1, 0, 0, 0, 1, 0, 0, 0};
-  CKL(cudaMemcpyAsync(x.ctr, c, sizeof(c), cudaMemcpyHostToDevice, st));
   LAUNCH(llm_reset_kernel<<<1, 32, 0, st>>>(x));
   const int B = l->b->Bmax;
   LAUNCH(root_slots_kernel<<<(B + 127) / 128, 128, 0, st>>>(x.node_slot, B, l->b->dev.ncap));
+  return LB_OK;
+}
+
+int lb_llm_reset_stats(lb_llm* l) {
+  if (!l) return lbh::set_error(LB_ERR_ARG, "null argument");
   l->events = l->waves = l->rows = l->cum = l->max_wave_rows = 0;
   return LB_OK;
 }
@@ -1769,6 +1823,44 @@ int lb_llm_plan(lb_llm* l, int32_t final_, int32_t min_frames, int32_t* n_waves,
   l->waves += nw;
   l->rows += total;
   return LB_OK;
+}
+
+int lb_llm_plan_async(lb_llm* l, int32_t final_, int32_t min_frames, int32_t rows_cap) {
+  if (!l) return lbh::set_error(LB_ERR_ARG, "null argument");
+  lb_batch* b = l->b;
+  if (b->n_trials < 1) return lbh::set_error(LB_ERR_STATE, "no trials loaded");
+  if (rows_cap < 1) return lbh::set_error(LB_ERR_ARG, "rows_cap must be >= 1");
+  LlmDev& x = l->dev;
+  cudaStream_t st = b->st;
+  CKL(cudaMemsetAsync(x.ctr + C_NFWD, 0, 8, st));  // C_NFWD, C_NCUM
+  const int B = b->n_trials;
+  const int nblk = (int)((x.cap + CB - 1) / CB);
+  LAUNCH(map_nodes_kernel<<<B, 256, 0, st>>>(b->dev, x, min_frames));
+  LAUNCH(schedule_kernel<<<B, 128, 0, st>>>(b->dev, x, min_frames, final_));
+  LAUNCH(flag_count_kernel<<<nblk, CB, 0, st>>>(x, x.blk));
+  LAUNCH(blk_scan_kernel<<<1, CB, 0, st>>>(x.blk, nblk));
+  LAUNCH(compact_kernel<<<nblk, CB, 0, st>>>(x, x.blk));
+  LAUNCH(plan_async_kernel<<<1, 32, 0, st>>>(x, rows_cap));
+  return LB_OK;
+}
+
+int lb_llm_wave_rows_async(lb_llm* l, int32_t rows_cap, int32_t* tokens, int32_t* positions,
+                           int32_t* slots, int32_t* chains) {
+  if (!l || !tokens || !positions || !slots || !chains) return lbh::set_error(LB_ERR_ARG, "null argument");
+  if (rows_cap < 1) return lbh::set_error(LB_ERR_ARG, "rows_cap must be >= 1");
+  const int grid = std::min(4 * 148, (rows_cap + 127) / 128);
+  LAUNCH(wave_rows_async_kernel<<<grid, 128, 0, l->b->st>>>(l->dev, rows_cap, tokens, positions,
+                                                            slots, chains));
+  return LB_OK;
+}
+
+int lb_llm_check(lb_llm* l) {
+  if (!l) return lbh::set_error(LB_ERR_ARG, "null argument");
+  int32_t err = 0;
+  CKL(cudaMemcpyAsync(&err, l->dev.ctr + C_ERR, 4, cudaMemcpyDeviceToHost, l->b->st));
+  CKL(cudaStreamSynchronize(l->b->st));
+  if (err & 8) return lbh::set_error(LB_ERR_CAPACITY, "fusion event larger than the captured graph rows");
+  return check_err_flags(l);
 }
 
 int lb_llm_wave_rows(lb_llm* l, int32_t wave, int64_t row0, int32_t n, int32_t* tokens,
@@ -2031,11 +2123,14 @@ int lb_llm_stats(lb_llm* l, int64_t* out) {
   int32_t slots = 0;
   CKL(cudaMemcpyAsync(&slots, l->dev.ctr + C_SLOTS, 4, cudaMemcpyDeviceToHost, l->b->st));
   CKL(cudaStreamSynchronize(l->b->st));
+  int32_t dev[3] = {0, 0, 0};  // graph-mode events / rows / largest event
+  CKL(cudaMemcpyAsync(dev, l->dev.ctr + C_EVENTS, 12, cudaMemcpyDeviceToHost, l->b->st));
+  CKL(cudaStreamSynchronize(l->b->st));
   out[0] = slots;
-  out[1] = l->events;
-  out[2] = l->waves;
-  out[3] = l->rows;
-  out[4] = l->max_wave_rows;
+  out[1] = l->events + dev[0];
+  out[2] = l->waves + dev[0];
+  out[3] = l->rows + dev[1];
+  out[4] = std::max<int64_t>(l->max_wave_rows, dev[2]);
   out[5] = l->bytes;
   out[6] = l->cum;
   out[7] = 0;

@@ -154,12 +154,18 @@ class DeviceModel:
         N.check(N.lib().lb_model_footprint(self.handle, C.byref(out)))
         return out.value
 
-    def batch(self, cfg, n_trials: int, n_frames: int) -> "DeviceBatch":
-        key = tuple(getattr(cfg, f) for f in (
+    def batch(self, cfg, n_trials: int, n_frames: int, own_stream: bool | None = None) -> "DeviceBatch":
+        """A cached DeviceBatch for this config.  `own_stream`: the batch runs on its own CUDA
+        stream (needed to capture whole decodes as CUDA graphs, LLM graph mode) instead of the
+        legacy default stream; None = whichever batch the last decode of this config used."""
+        base = tuple(getattr(cfg, f) for f in (
             "acoustic_scale", "beam_prune_threshold", "homophone_prune_threshold",
             "token_insertion_bonus", "word_boundary_bonus", "ngram_weight", "llm_weight",
             "beam_size", "ortho_beams", "llm_rescore_interval", "llm_chunk_size"))
         lru = self._mine()["lru"]
+        if own_stream is None:
+            own_stream = next((k[-1] for k in reversed(list(lru)) if k[:-1] == base), False)
+        key = base + (own_stream,)
         got = lru.pop(key, None)
         if got is None or got.max_trials < n_trials or got.max_frames < n_frames:
             if got is not None:
@@ -167,7 +173,14 @@ class DeviceModel:
             while len(lru) >= self.MAX_CACHED_BATCHES:  # evict the least recently used
                 old = lru.pop(next(iter(lru)))
                 old.destroy()
-            got = DeviceBatch(self, cfg, max(n_trials, 1), max(n_frames, 1))
+            stream = None
+            if own_stream:
+                import torch
+
+                stream = torch.cuda.Stream(device=self.device)
+            got = DeviceBatch(self, cfg, max(n_trials, 1), max(n_frames, 1),
+                              stream=stream.cuda_stream if stream is not None else None)
+            got._torch_stream = stream  # keep the stream alive with the batch
         lru[key] = got  # most recently used last
         return got
 
@@ -284,6 +297,7 @@ class DeviceBatch:
                                         C.c_void_p(stream or 0), C.byref(h)))
         self.h = h
         self.stream_ptr = int(stream or 0)  # the CUDA stream every kernel of this batch runs on
+        self.graph_launches = 0  # library kernels run inside CUDA-graph replays (LLM graph mode)
         self.n = 0
         self.frames = np.zeros(0, dtype=np.int32)
 
@@ -314,9 +328,17 @@ class DeviceBatch:
         self.frames = fr
         return fr
 
+    def _after_torch(self):
+        """Inputs produced by torch on its current stream: order this batch's stream after it."""
+        if self.stream_ptr and getattr(self, "_torch_stream", None) is not None:
+            import torch
+
+            self._torch_stream.wait_stream(torch.cuda.current_stream(self.dm.device))
+
     def load_logprobs(self, d: np.ndarray, frames, on_device_ptr: int | None = None):
         fr = self._frames(frames)
         if on_device_ptr is not None:
+            self._after_torch()
             N.check(N.lib().lb_batch_set_logprobs(self.h, len(fr), C.c_void_p(on_device_ptr),
                                                   N.ptr(fr), 1))
             return
@@ -330,6 +352,7 @@ class DeviceBatch:
     def load_logits(self, x: np.ndarray | None, frames, on_device_ptr: int | None = None):
         fr = self._frames(frames)
         if on_device_ptr is not None:
+            self._after_torch()
             N.check(N.lib().lb_batch_set_logits(self.h, len(fr), C.c_void_p(on_device_ptr),
                                                 N.ptr(fr), 1))
             return
@@ -440,11 +463,14 @@ class DeviceBatch:
 
     def mark_begin(self):
         N.check(N.lib().lb_batch_mark_begin(self.h))
+        self._graph_mark = self.graph_launches
 
     def mark_end(self):
+        """(device ms since mark_begin, kernels launched since: by the library directly plus
+        the library kernels inside CUDA-graph replays of whole decodes)."""
         ms, launches = C.c_float(), C.c_int64()
         N.check(N.lib().lb_batch_mark_end(self.h, C.byref(ms), C.byref(launches)))
-        return ms.value, launches.value
+        return ms.value, launches.value + self.graph_launches - getattr(self, "_graph_mark", 0)
 
     def sync(self):
         N.check(N.lib().lb_batch_sync(self.h))
@@ -492,6 +518,11 @@ def _host_fusion(batch: DeviceBatch, scorer, cfg, final: bool, min_frames: int):
     batch.apply_scores(scores, puncts, has, final, min_frames)
 
 
+def _graph_mode(scorer) -> bool:
+    """The scorer's decodes run as CUDA-graph replays (device LLM in graph mode)."""
+    return bool(getattr(getattr(scorer, "device_llm_scorer", None), "graphs", False))
+
+
 def _uses_device_scorer(scorer, model, dm: DeviceModel) -> bool:
     return getattr(scorer, "device_ngram_model", None) is model and dm.whitespace_free
 
@@ -531,6 +562,10 @@ def _search_steps(batch: DeviceBatch, cfg, scorer, model, final_llm_only: bool):
     llm = getattr(scorer, "device_llm_scorer", None)
     if llm is not None and batch.dm.whitespace_free:
         sess = llm.session(batch)
+        if getattr(llm, "graphs", False) and batch.stream_ptr:
+            _graph_search(batch, cfg, sess, final_llm_only, t_max)
+            yield
+            return
         sess.reset()
         fuse = sess.event
     else:
@@ -547,6 +582,74 @@ def _search_steps(batch: DeviceBatch, cfg, scorer, model, final_llm_only: bool):
     batch.close()
     fuse(True, 0)
     yield
+
+
+def _event_frames(t_max: int, r: int, final_llm_only: bool) -> list:
+    """Interval fusion events after frames e = r, 2r, ... < the longest T (decoder.py:428)."""
+    return [] if final_llm_only else list(range(r, t_max, r))
+
+
+def _graph_search(batch: DeviceBatch, cfg, sess, final_llm_only: bool, t_max: int):
+    """The whole decode of a batch with a device LLM scorer as ONE CUDA-graph replay: frames
+    intervals, every fusion event (planning, a forward over a fixed row capacity, fusion),
+    closure and the final pass, with no host synchronisation between events.  The first decode
+    of a shape runs eagerly (it also measures the largest event) and captures the graph for the
+    next ones; a replay whose event outgrows the captured rows is detected on the device
+    (lb_llm_check) and the batch is decoded again eagerly, then re-captured with more rows."""
+    import torch
+
+    from .errors import DeviceError
+
+    events = _event_frames(t_max, cfg.llm_rescore_interval, final_llm_only)
+    key = (batch.n, tuple(int(x) for x in batch.frames), cfg.llm_rescore_interval,
+           bool(final_llm_only))
+    ent = sess.graphs.get(key)
+    stream = torch.cuda.ExternalStream(batch.stream_ptr, device=sess.scorer.weights.device)
+    if ent is not None:
+        N.check(N.lib().lb_llm_reset_stats(sess.h))  # host half of the captured reset
+        sess.waves_log = []
+        with torch.cuda.stream(stream):  # replay on the batch's stream (ordered, timed there)
+            ent["graph"].replay()
+        batch.graph_launches += ent["kernels"]
+        try:
+            sess.check()
+            return
+        except DeviceError:  # an event had more rows than captured: redo eagerly, re-capture
+            sess.graphs.pop(key, None)
+    # eager decode (the result of this call) -- also sizes the graph's row capacity
+    batch.reset()
+    sess.reset()
+    t = 0
+    for e in events:
+        batch.run(t, e + 1)
+        sess.event(False, e)
+        t = e + 1
+    batch.run(t, t_max)
+    batch.close()
+    sess.event(True, 0)
+    rows = max([max(w) if w else 0 for w in sess.waves_log] + [1])
+    R = 64
+    while R < 2 * rows:
+        R *= 2
+    if R > sess.scorer.row_chunk:
+        return  # too large to pad every event: stay eager
+    ws = sess.graph_workspace(R)
+    c0, c1 = C.c_uint64(), C.c_uint64()
+    N.check(N.lib().lb_launch_count(C.byref(c0)))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        batch.reset()
+        N.check(N.lib().lb_llm_reset_device(sess.h))  # the host statistics stay this decode's
+        t = 0
+        for e in events:
+            batch.run(t, e + 1)
+            sess.event_async(False, e, R, ws)
+            t = e + 1
+        batch.run(t, t_max)
+        batch.close()
+        sess.event_async(True, 0, R, ws)
+    N.check(N.lib().lb_launch_count(C.byref(c1)))
+    sess.graphs[key] = {"graph": g, "rows": R, "ws": ws, "kernels": int(c1.value - c0.value)}
 
 
 def _collect(batch: DeviceBatch, cfg, final_llm_only: bool, wall: float):
@@ -597,7 +700,7 @@ def decode_batch(ds, config, tt, lm, scorer, final_llm_only: bool = False, devic
     if arr.ndim != 3 or arr.shape[2] != dm.vocab_size:
         raise ShapeError(f"log-prob width must equal the table vocabulary ({dm.vocab_size})")
     t0 = time.perf_counter()
-    batch = dm.batch(cfg, arr.shape[0], max(arr.shape[1], 1))
+    batch = dm.batch(cfg, arr.shape[0], max(arr.shape[1], 1), own_stream=_graph_mode(scorer))
     batch.load_logprobs(arr, frames)
     run_search(batch, cfg, scorer, model, final_llm_only)
     return _collect(batch, cfg, final_llm_only, time.perf_counter() - t0)
@@ -615,7 +718,7 @@ def decode_batch_raw(raws, config, tt, lm, scorer, final_llm_only: bool = False,
     if arr.ndim != 3 or arr.shape[2] != dm.vocab_size:
         raise ShapeError(f"logit width must equal the table vocabulary ({dm.vocab_size})")
     t0 = time.perf_counter()
-    batch = dm.batch(cfg, arr.shape[0], max(arr.shape[1], 1))
+    batch = dm.batch(cfg, arr.shape[0], max(arr.shape[1], 1), own_stream=_graph_mode(scorer))
     batch.load_logits(arr, frames)
     run_search(batch, cfg, scorer, model, final_llm_only)
     return _collect(batch, cfg, final_llm_only, time.perf_counter() - t0)

@@ -351,7 +351,7 @@ class LlamaScorer:
     def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
                  max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 2048,
                  precision: str = "bf16x2", lm_head: str = "fused", fused_swiglu: bool = False,
-                 fused_swiglu_min_rows: int = 4096):
+                 fused_swiglu_min_rows: int = 4096, graphs: bool | None = None):
         """precision: "bf16x2" (default) feeds every body GEMM the activation as a hi+lo pair of
         bf16 values against duplicated bf16 weights -- fp32-equivalent activations on the bf16
         tensor cores, scores within ~1e-3 of an fp32 forward even for 40-token texts -- and keeps
@@ -409,6 +409,10 @@ class LlamaScorer:
                         L[k + "2"] = torch.cat([L[k], L[k]], 1).contiguous()
             self.emb2 = torch.cat([self.weights.emb, self.weights.emb], 1).contiguous()
         self.device_llm_scorer = self  # the GPU decoder drives this scorer on the device
+        # graph mode: whole decodes replay as one CUDA graph (events padded to a fixed row
+        # capacity, no host round trip per event) -- for small models, where an event is
+        # launch-bound; big models keep the eager path (exact row counts, large GEMMs)
+        self.graphs = (self.cfg.hidden <= 256) if graphs is None else bool(graphs)
         # the weights were built on the legacy default stream; decodes may run on non-blocking
         # streams that do not order after it
         torch.cuda.synchronize(device)
@@ -694,8 +698,10 @@ class DeviceLlmSession:
         self.h = h
         self._ws = {}
         self.waves_log: list = []
+        self.graphs: dict = {}  # decode shape -> captured CUDA graph (LLM graph mode)
 
     def destroy(self):
+        getattr(self, "graphs", {}).clear()  # captured graphs point into this session's buffers
         if getattr(self, "h", None):
             N.lib(False).lb_llm_destroy(self.h)
             self.h = None
@@ -713,18 +719,26 @@ class DeviceLlmSession:
             self._timing = []
 
     def _work(self, n: int):
-        import torch
-
         cap = self._ws.get("n", 0)
         if cap < n:
+            self._ws = {}  # free the old buffers first
+            self._ws = self._alloc_work(max(n, 256))
+        return self._ws
+
+    def graph_workspace(self, n: int) -> dict:
+        """Buffers owned by one captured graph (never reallocated under it)."""
+        return self._alloc_work(n)
+
+    def _alloc_work(self, cap: int) -> dict:
+        import torch
+
+        if True:
             dev = self.scorer.weights.device
             cfg = self.scorer.cfg
             k = 2 if self.scorer.split else 1
-            cap = max(n, 256)
             i32 = dict(dtype=torch.int32, device=dev)
             bf = dict(dtype=torch.bfloat16, device=dev)
-            self._ws = {}  # free the old buffers first
-            self._ws = {
+            return {
                 "n": cap,
                 "tok": torch.empty(cap, **i32),
                 "pos": torch.empty(cap, **i32),
@@ -736,7 +750,6 @@ class DeviceLlmSession:
                 "hn": torch.empty((cap, k * cfg.hidden), **bf),
                 "act": torch.empty((cap, k * cfg.ffn), **bf),
             }
-        return self._ws
 
     def enable_timing(self, on: bool = True):
         """Record CUDA events around every fusion event (device ms spent in the LLM step)."""
@@ -781,17 +794,35 @@ class DeviceLlmSession:
                 self._forward_rows(w, r0, min(self.scorer.row_chunk, m - r0))
         N.check(lib.lb_llm_finish(self.h, int(final), int(min_frames)))
 
-    def _forward_rows(self, wave: int, row0: int, n: int):
+    def event_async(self, final: bool, min_frames: int, rows_cap: int, ws: dict):
+        """One fusion event without host synchronisation (CUDA-graph capturable): planning
+        kernels, a forward over `rows_cap` rows (the event's rows + BOS-only padding), the
+        fusion kernels.  Overflow is flagged on the device (`check`)."""
+        lib = N.lib()
+        N.check(lib.lb_llm_plan_async(self.h, int(final), int(min_frames), int(rows_cap)))
+        self._forward_rows(0, 0, rows_cap, ws=ws)
+        N.check(lib.lb_llm_finish(self.h, int(final), int(min_frames)))
+
+    def check(self):
+        """Synchronise and raise DeviceError if a graph-mode event overflowed its rows."""
+        N.check(N.lib().lb_llm_check(self.h))
+
+    def _forward_rows(self, wave: int, row0: int, n: int, ws: dict | None = None):
         import torch
 
         lib = N.lib()
         cfg, W = self.scorer.cfg, self.scorer.weights
-        ws = self._work(n)
+        graph_rows = ws is not None
+        ws = ws if graph_rows else self._work(n)
         tok, pos, slot, chain = ws["tok"][:n], ws["pos"][:n], ws["slot"][:n], ws["chain"][:n]
-        N.check(lib.lb_llm_wave_rows(self.h, wave, row0, n, tok.data_ptr(), pos.data_ptr(),
-                                     slot.data_ptr(), chain.data_ptr()))
+        if graph_rows:
+            N.check(lib.lb_llm_wave_rows_async(self.h, n, tok.data_ptr(), pos.data_ptr(),
+                                               slot.data_ptr(), chain.data_ptr()))
+        else:
+            N.check(lib.lb_llm_wave_rows(self.h, wave, row0, n, tok.data_ptr(), pos.data_ptr(),
+                                         slot.data_ptr(), chain.data_ptr()))
         if cfg.arch in ("gpt2", "tinychar"):
-            return self._forward_rows_gpt2(tok, pos, slot, chain, n)
+            return self._forward_rows_gpt2(tok, pos, slot, chain, n, ws)
         x = W.emb.index_select(0, tok.long()).float()
         hn, q, att, act = ws["hn"][:n], ws["q"][:n], ws["att"][:n], ws["act"][:n]
         eps = cfg.rms_eps
@@ -858,14 +889,13 @@ class DeviceLlmSession:
             N.check(lib.lb_llm_lse(self.h, logits.data_ptr(), c1 - c0, logits.stride(0),
                                    slot[c0:].data_ptr()))
 
-    def _forward_rows_gpt2(self, tok, pos, slot, chain, n: int):
+    def _forward_rows_gpt2(self, tok, pos, slot, chain, n: int, ws: dict):
         """GPT-2 blocks on the same kernels: LayerNorm (+bias), fused q/k/v GEMM + bias, identity
         rotary tables (learned positions were added at the input), MHA chain attention, GELU."""
         import torch
 
         lib = N.lib()
         cfg, W = self.scorer.cfg, self.scorer.weights
-        ws = self._work(n)
         hn, q, att, act = ws["hn"][:n], ws["q"][:n], ws["att"][:n], ws["act"][:n]
         eps, f32 = cfg.rms_eps, torch.float32
         sfx = "2" if self.scorer.split else ""
