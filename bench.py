@@ -544,8 +544,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "frames_kernel (K2)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": _profile_traffic("r1_frames_ncu.json"),
-                         "traffic_source": "profiles/r1_frames_ncu.json (ncu --set full, same launch)",
+                         "traffic": _profile_traffic("r2_frames_ncu.json"),
+                         "traffic_source": "profiles/r2_frames_ncu.json (ncu --set full, same launch)",
                          "kernel_ms": k_ms, "algorithmic_bytes": alg,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pp.exists() else "fallback 6650 GB/s"},
             "cpu_baseline": cpu,
@@ -957,8 +957,14 @@ def llm_wer_check(world, cfg, scorer, dev, args, n=16):
     sents, logs = synth.make_wer_trials(world, n, seed=991)
     got = decode_batch_raw(logs, cfg, world.table, world.model, scorer, device=dev)
     gpu = [r.text if not isinstance(r, Exception) else "" for r in got]
-    ref = [O.decode(O.log_softmax_scaled(x, cfg.acoustic_scale), cfg, world.table, world.model,
-                    scorer).text for x in logs]
+    def ref_text(x):  # an utterance whose beam dies decodes to "" on both sides
+        try:
+            return O.decode(O.log_softmax_scaled(x, cfg.acoustic_scale), cfg, world.table,
+                            world.model, scorer).text
+        except O.OracleEmptyBeam:
+            return ""
+
+    ref = [ref_text(x) for x in logs]
     return {"trials": n, "wer_gpu": corpus_wer(sents, [t.split() for t in gpu]),
             "wer_reference_arm": corpus_wer(sents, [t.split() for t in ref]),
             "identical_transcripts": f"{sum(a == b for a, b in zip(gpu, ref))}/{n}",
@@ -1006,7 +1012,10 @@ def _wer_worker(i):
     w, cfg, logs = _WER["world"], _WER["cfg"], _WER["logs"]
     d = O.log_softmax_scaled(logs[i], cfg.acoustic_scale)
     sc = StubScorer(ngram_model=w.model, scale=cfg.ngram_weight / cfg.llm_weight)
-    return O.decode(d, cfg, w.table, w.model, sc, final_llm_only=True).text
+    try:
+        return O.decode(d, cfg, w.table, w.model, sc, final_llm_only=True).text
+    except O.OracleEmptyBeam:  # a dead beam decodes to "" on both sides
+        return ""
 
 
 def wer_check(world, cfg, scorer, dev, args):
