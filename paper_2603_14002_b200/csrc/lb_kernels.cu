@@ -1839,11 +1839,7 @@ __global__ void __launch_bounds__(small::NT, 2)
             const bool ok = pin && al && (x > GUARD);
             const int bn = min(__double2int_rz(xmul(xsub(U, x), ibw)), NBINS - 1);
             bins[i] = ok ? (uint16_t)bn : (uint16_t)0xFFFF;
-#ifdef LB_E1
-            if (ok) atomicAdd(&hist[bn], 1u);
-#else
             atomicAdd(&hist[ok ? bn : NBINS], 1u);
-#endif
             wm = (ok && x > wm) ? x : wm;
           }
         }
@@ -1933,19 +1929,23 @@ __global__ void __launch_bounds__(small::NT, 2)
         const int bound = sure ? cum_bstar : cum_thr;
         if (bound <= LC) {
           // ---- D: counting-sort collect from the register bins
+          // only the (typically 0-2) items inside the take window are revisited: a bit mask of
+          // them, then one pass per set bit (value and bin recomputed exactly as in A)
+          unsigned cm = 0;
 #pragma unroll
-          for (int i = 0; i < TBK; ++i) {
-            const int bn = bins[i];
-            if (bn <= take_bin) {
-              const int v = cv0 + i;
-              const double add = (i == tk_sidx) ? gsel : (((bbits >> i) & 1u) ? b_on : b_off);
-              const double x = xadd(xadd(sp, drow[v]), add);
-              if (sure || x >= thr) {
-                const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
-                cval[pos] = x;
-                ckey[pos] = ((uint32_t)cp << 8) | (uint32_t)v;  // orders like cp * V + v
-                cbinl[pos] = (uint16_t)bn;
-              }
+          for (int i = 0; i < TBK; ++i) cm |= (bins[i] <= take_bin ? 1u : 0u) << i;
+          while (cm) {
+            const int i = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const int v = cv0 + i;
+            const double add = (i == tk_sidx) ? gsel : (((bbits >> i) & 1u) ? b_on : b_off);
+            const double x = xadd(xadd(sp, drow[v]), add);
+            if (sure || x >= thr) {
+              const int bn = min(__double2int_rz(xmul(xsub(U, x), ibw)), NBINS - 1);
+              const int pos = hcum[bn] + atomicAdd(&hfill[bn], 1);
+              cval[pos] = x;
+              ckey[pos] = ((uint32_t)cp << 8) | (uint32_t)v;  // orders like cp * V + v
+              cbinl[pos] = (uint16_t)bn;
             }
           }
           LB_ARR(2);
@@ -2147,9 +2147,6 @@ __global__ void __launch_bounds__(small::NT, 2)
           const uint64_t regm = ~(((uint64_t)bm1 << 32) | bm0) & (n >= 64 ? ~0ull : ((1ull << n) - 1));
           int G = 1;
           while (G < 32 && 2 * G * n <= NC) G <<= 1;
-#ifdef LB_G4R
-          if (G < 4 && n <= NC / 4) G = 4;
-#endif
           const int groups = NC / G, g = tid / G, r = tid & (G - 1);
           for (int i0 = 0; i0 < n; i0 += groups) {
             const int i = i0 + g;
@@ -2211,6 +2208,7 @@ __global__ void __launch_bounds__(small::NT, 2)
         LB_ARR(6);
         bar_sync(1, NC);  // S6
         LB_REL(6);
+        const unsigned kp0 = keep[0], kp1 = keep[1];
         LB_PHASE(7);
 
         // ---- scatter in rank order; boundary entries built from the chosen pairs;
@@ -2219,21 +2217,18 @@ __global__ void __launch_bounds__(small::NT, 2)
           hist[i] = 0;
           hfill[i] = 0;
         }
-        const int newK = __popc(keep[0]) + __popc(keep[1]);
+        const int newK = __popc(kp0) + __popc(kp1);
         {
           int G = 1;
           while (G < 32 && 2 * G * nsel <= NC) G <<= 1;
-#ifdef LB_G4S
-          if (G < 4 && nsel <= NC / 4) G = 4;
-#endif
           const int groups = NC / G, g = tid / G, r = tid & (G - 1);
           for (int i0 = 0; i0 < nsel; i0 += groups) {
             const int i = i0 + g;
             if (i >= nsel) continue;
             const int rk = rankv[i];
-            if (!((keep[rk >> 5] >> (rk & 31)) & 1u)) continue;
-            const int pos = __popc(keep[rk >> 5] & ((1u << (rk & 31)) - 1u)) +
-                            (rk >= 32 ? __popc(keep[0]) : 0);
+            const unsigned kw = rk >= 32 ? kp1 : kp0;
+            if (!((kw >> (rk & 31)) & 1u)) continue;
+            const int pos = __popc(kw & ((1u << (rk & 31)) - 1u)) + (rk >= 32 ? __popc(kp0) : 0);
             const int4 bs = bsel[i];
             Ent* dst = X_ENTS + pos * OC;
             int cnt;
