@@ -116,7 +116,7 @@ struct BatchDev {
   // speculative n-gram pair budget of frames_small_kernel per frame (<= its shared-memory cap)
   int32_t spec_cap;
 };
-constexpr int NPHASE = 20;
+constexpr int NPHASE = 26;
 constexpr int NBAR_EV = 10;  // frames_small_kernel TIMING: barrier events per frame
 
 // Byte layout of the per-CTA working set; each region lives in shared memory or, when the

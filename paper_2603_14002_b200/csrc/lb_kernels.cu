@@ -473,6 +473,12 @@ __device__ __forceinline__ void sort_entries(Ent* e, int n) {
   }
 }
 
+// 32-bit fingerprint of a beam's two prefix-hash lanes (equal lanes -> equal fingerprints)
+__device__ __forceinline__ uint32_t hash_fp(uint64_t a1, uint64_t a2) {
+  const uint64_t x = a1 ^ (a2 * 0x9E3779B97F4A7C15ull);
+  return (uint32_t)(x >> 32) ^ (uint32_t)x;
+}
+
 // order-preserving 64-bit key of an fp64 (after canonicalising -0.0)
 __device__ __forceinline__ uint64_t ord64(double x) {
   uint64_t u = (uint64_t)__double_as_longlong(xadd(x, 0.0));
@@ -1360,7 +1366,7 @@ constexpr int KC = 64, OC = 3, VC = 48, VPC = 56, VPDC = 50;
 // at 160 -> 7.13 ms; the n-gram warps are the critical path up to S3 and the uncovered parents'
 // few selected boundary beams take the warp path); LC 280 and 4-frame D chunks keep two CTAs
 // inside the 132 KB shared-memory carve-out (124 KB of L1 for the lexicon / n-gram probes)
-constexpr int LC = 280, PC = 80, TSC = 128, SCHUNK = 4;
+constexpr int LC = 280, PC = 80, SCHUNK = 4;
 constexpr int NC = 256, NWC = NC / 32, NT = NC + NGT;
 constexpr int TBK = VC / 4;  // candidate tokens per thread: 4 threads per parent
 static_assert(KC * 4 == NC && TBK % 4 == 0, "candidate mapping: one parent per 4 threads");
@@ -1388,10 +1394,8 @@ constexpr int O_BSEL = O_BLIST + KC * 4;
 constexpr int O_KEEP = O_BSEL + KC * 16;
 constexpr int O_POFF = O_KEEP + 16;
 constexpr int O_PRES = O_POFF + ((KC + 1) * 4 + 15) / 16 * 16;
-constexpr int O_SLOTB = O_PRES + PC * (int)sizeof(PairRes);
-constexpr int O_SLOTM = O_SLOTB + TSC * 4;
-constexpr int O_MYSLOT = O_SLOTM + TSC * 4;
-constexpr int O_QINFO = O_MYSLOT + KC * 4;  // int4 per speculative pair: (entry, word, surface, -)
+constexpr int O_NFP = O_PRES + PC * (int)sizeof(PairRes);
+constexpr int O_QINFO = O_NFP + KC * 4;  // int4 per speculative pair: (entry, word, surface, -)
 constexpr int TOTAL = O_QINFO + PC * 16;
 static_assert(O_BEAM % 16 == 0 && O_CVAL % 16 == 0 && O_PRES % 16 == 0 && BEAM_BYTES % 16 == 0,
               "16-byte alignment");
@@ -1562,9 +1566,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   uint32_t* keep = reinterpret_cast<uint32_t*>(sm + O_KEEP);
   int32_t* ppoff = reinterpret_cast<int32_t*>(sm + O_POFF);
   PairRes* pres = reinterpret_cast<PairRes*>(sm + O_PRES);
-  int32_t* slotb = reinterpret_cast<int32_t*>(sm + O_SLOTB);
-  int32_t* slotm = reinterpret_cast<int32_t*>(sm + O_SLOTM);
-  int32_t* myslot = reinterpret_cast<int32_t*>(sm + O_MYSLOT);
+  uint32_t* nfp = reinterpret_cast<uint32_t*>(sm + O_NFP);  // hash-lane fingerprints (recombination)
   Ent* gbents = reinterpret_cast<Ent*>(gs + G_BENTS);
   WarpScratch* wsc = reinterpret_cast<WarpScratch*>(gs + G_WARP);
 
@@ -1587,7 +1589,6 @@ __global__ void __launch_bounds__(small::NT, 2)
 #define X_ENTS ((Ent*)(BUF(par ^ 1) + B_ENTS))
 
   const int V = m.V, VP = m.VP, VPD = b.VPD, O = c.O, KC_ = b.K;
-  const int TS = TSC;
   const double ibw = c.inv_binw;
   const double b_on = c.beta, b_off = xmul(c.beta, 0.0);
   const double g_on = c.gamma, g_off = xmul(c.gamma, 0.0);
@@ -1640,6 +1641,8 @@ __global__ void __launch_bounds__(small::NT, 2)
     s_K = K;
     s_tbase = (unsigned)clock();
     for (int e = 0; e < NBAR_EV; ++e) s_tarr[e] = 0;
+    if (TIMING)
+      for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
     mbar_init(&dbar[0], 1);
     mbar_init(&dbar[1], 1);
     fence_mbar_init();
@@ -1672,9 +1675,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   // TIMING: critical-path accounting per barrier event e (SM clock, 32-bit wrap-safe): every
   // arriving warp records its arrival (atomicMax), thread 0 after the release adds
   // work[e] = last arrival - previous release and sync[e] = release - last arrival.
-  const bool timing = TIMING && b.phase_cycles != nullptr;
-  if (timing && tid == 0)
-    for (int i = 0; i < NPHASE; ++i) ph[i] = 0;
+  const bool timing = TIMING && b.phase_cycles != nullptr;  // ph[] zeroed before the first barrier
   unsigned trel = timing ? (unsigned)clock() : 0u, tfs = trel;
 #define LB_ARR(e)                                              \
   if (timing && lane == 0) atomicMax(&s_tarr[e], (unsigned)clock() - s_tbase);
@@ -1698,6 +1699,8 @@ __global__ void __launch_bounds__(small::NT, 2)
     if (warp >= NWC) {
       // ================== speculative n-gram warps (as in frames_kernel) ==================
       const int gt = tid - NC, ngw = warp - NWC;
+      const bool ngtim = timing && gt == 0;
+      unsigned tg = ngtim ? (unsigned)clock() : 0u;
       int carry = 0;
       for (int base = 0; base < K; base += NGT) {
         const int p = base + gt;
@@ -1726,6 +1729,11 @@ __global__ void __launch_bounds__(small::NT, 2)
         if (carry <= SCAP) s_ngcov = carry;
       }
       const int P = carry;
+      if (ngtim) {
+        const unsigned tn = (unsigned)clock();
+        ph[20] += tn - tg;
+        tg = tn;
+      }
       {
         // pair table: each parent writes its own (entry, surface) pairs -- no search.  Parents
         // are in score order; when the pairs exceed PC only the leading parents whose pairs all
@@ -1761,6 +1769,12 @@ __global__ void __launch_bounds__(small::NT, 2)
         bar_sync(3, NGT);
         const int PCOV = s_ngcov;
         constexpr int NQ = NGT / 4;
+        if (ngtim) {
+          const unsigned tn = (unsigned)clock();
+          ph[21] += tn - tg;
+          ph[23] += 1000u * (unsigned)((PCOV + NQ - 1) / NQ);
+          tg = tn;
+        }
         const int grp = gt >> 2, sub = lane & 3;
         for (int q0 = 0; q0 < PCOV; q0 += NQ) {
           const int q = q0 + grp;
@@ -1788,8 +1802,8 @@ __global__ void __launch_bounds__(small::NT, 2)
             pres[q] = pr;
           }
         }
+        if (ngtim) ph[22] += (unsigned)clock() - tg;
       }
-      LB_ARR(3);
       LB_ARR(8);
       bar_arrive(2, NT);
     } else {
@@ -1852,10 +1866,6 @@ __global__ void __launch_bounds__(small::NT, 2)
       if (lane == 0) wmax[warp] = wm;
       if (tid == 0) s_nb = 0;
       if (tid < 2) keep[tid] = 0;
-      for (int i = tid; i < TS; i += NC) {
-        slotb[i] = -1;
-        slotm[i] = 0x7FFFFFFF;
-      }
       LB_ARR(0);
       bar_sync(1, NC);  // S1
       LB_REL(0);
@@ -1973,30 +1983,19 @@ __global__ void __launch_bounds__(small::NT, 2)
           }
         } else {
           ++st_fallback;
-          nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, VP, thr, blank, space, sink, rows, C_LAST, C_SCORE,
-                                       drow, hist, cval, ckey, sval, skey, &s_inr, &s_cnt2);
+          nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, VP, thr, blank, space, sink,
+                                       rows, C_LAST, C_SCORE, drow, hist, cval, ckey, sval, skey,
+                                       &s_inr, &s_cnt2);
         }
       }
       LB_ARR(3);
-      LB_ARR(9);
-      bar_sync(2, NT);  // S3: selection done + speculative n-gram results ready
-      if (timing && tid == 0) {  // n-gram warps' and compute warps' arrival since frame start
-        ph[17] += s_tarr[8] + s_tbase - tfs;
-        ph[18] += s_tarr[9] + s_tbase - tfs;
-        s_tarr[8] = 0;
-        s_tarr[9] = 0;
-      }
+      bar_sync(1, NC);  // S3: the selection is visible to every compute warp
       LB_REL(3);
       LB_PHASE(3);
-
+      // ---- F1: materialise survivors (no n-gram results needed yet: the speculative n-gram
+      // warps may still be probing).  Selected beams spread over all compute warps
+      // (j = lane * NWC + warp); word-boundary beams are listed for F2 with their acoustic score.
       if (!dead) {
-        const int ncov = s_ngcov;
-        const bool ngover = ncov < s_ngP;  // some parents' pairs were not speculated
-        if (timing && tid == 0 && ngover) ph[16] += 1000;  // permille of frames past the speculative pair cap
-        LB_PHASE(13);
-        // ---- F: materialise survivors; new word boundaries pick their top-o pairs
-        // selected beams spread over all compute warps (j = lane * NWC + warp), so the few
-        // word-boundary merges run in parallel instead of serialising inside one warp
         for (int j = lane * NWC + warp; j < nsel; j += NC) {
           const double x = sval[j];
           const uint32_t f = skey[j];
@@ -2019,11 +2018,44 @@ __global__ void __launch_bounds__(small::NT, 2)
             if ((((uintptr_t)r1 >> 7) - ((uintptr_t)r0 >> 7)) > 1)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(r0 + 128));
           }
+          if (emit && tok == space) blist[atomicAdd(&s_nb, 1)] = j;
+          nscore[j] = x;
+          nh1[j] = a1;
+          nh2[j] = a2;
+          nfp[j] = hash_fp(a1, a2);
+          nlast[j] = (tok == blank) ? lp : tok;
+          npre[j] = np;
+          npar[j] = p;
+          bsel[j] = make_int4(-1, 0, 0, 0);
+        }
+      }
+      LB_ARR(9);
+      bar_sync(2, NT);  // S3b: speculative n-gram results ready (+ F1 visible)
+      if (timing && tid == 0) {  // n-gram warps' and compute warps' arrival since frame start
+        const unsigned tnow = (unsigned)clock();
+        ph[17] += s_tarr[8] + s_tbase - tfs;
+        ph[18] += s_tarr[9] + s_tbase - tfs;
+        ph[24] += s_tarr[9] + s_tbase - trel;  // F1 (compute warps)
+        ph[25] += tnow - (s_tarr[9] + s_tbase);  // waiting for the n-gram warps + release
+        trel = tnow;
+        s_tarr[8] = 0;
+        s_tarr[9] = 0;
+      }
+
+      if (!dead) {
+        const int ncov = s_ngcov;
+        const bool ngover = ncov < s_ngP;  // some parents' pairs were not speculated
+        if (timing && tid == 0 && ngover) ph[16] += 1000;  // permille of frames past the speculative pair cap
+        LB_PHASE(13);
+        // ---- F2: new word boundaries pick their top-o pairs (decoder.py:182-235)
+        const int nb0 = s_nb;
+        for (int bi = lane * NWC + warp; bi < nb0; bi += NC) {
+          const int j = blist[bi];
+          const int p = npar[j];
+          const double x = nscore[j];
           double sc = x;
           int4 bs = make_int4(-1, 0, 0, 0);
-          LB_PHASE(14);
-          if (emit && tok == space) {
-            blist[atomicAdd(&s_nb, 1)] = j;
+          {
             pairs_l += (unsigned)(ppoff[p + 1] - ppoff[p]);
             if (ppoff[p + 1] > ncov) {
               bs.x = -2;
@@ -2095,11 +2127,6 @@ __global__ void __launch_bounds__(small::NT, 2)
             }
           }
           nscore[j] = sc;
-          nh1[j] = a1;
-          nh2[j] = a2;
-          nlast[j] = (tok == blank) ? lp : tok;
-          npre[j] = np;
-          npar[j] = p;
           bsel[j] = bs;
         }
         LB_PHASE(12);
@@ -2129,85 +2156,42 @@ __global__ void __launch_bounds__(small::NT, 2)
         }
         LB_PHASE(5);
 
-        // ---- H1: recombination ranking; regular beams are already in (score desc, j asc)
-        // order, only the nb boundary beams need comparisons; hash groups via a smem table
+        // ---- H: recombination (decoder.py:297-312) in one pass.  rank(i) = #{j : (s_j, -j) >
+        // (s_i, -i)} over the selection, and beam i survives iff no live j with the same prefix
+        // hash lanes ranks ahead of it (the first-ranked beam of each prefix keeps it).  All
+        // pairs, four threads per beam: no hash table, no second barrier.
         {
+          static_assert(KC * 4 == NC, "recombination: four threads per selected beam");
           const int n = nsel;
-          // beams outside blist are "regular": their score is sval[j], and sval is sorted
-          // (score desc, j asc), so a boundary beam counts the regular beams ahead of it by two
-          // binary searches over sval and a popcount of the regular mask (built per warp)
-          unsigned bm0 = 0, bm1 = 0;
-          for (int k2 = lane; k2 < nb; k2 += 32) {
-            const int j = blist[k2];
-            if (j < 32) bm0 |= 1u << j;
-            else bm1 |= 1u << (j - 32);
+          const int i = tid >> 2, r = tid & 3;
+          const bool act = i < n;
+          const double si = act ? nscore[i] : 0.0;
+          const uint64_t a1 = act ? nh1[i] : 0ull, a2 = act ? nh2[i] : 0ull;
+          // a 32-bit fingerprint of the hash lanes filters the exact 128-bit comparison
+          const uint32_t fi = act ? nfp[i] : 0u;
+          int cnt = 0, dup = 0;
+#pragma unroll
+          for (int it = 0; it < KC / 4; ++it) {
+            const int j = r + 4 * it;
+            const double sj = nscore[j];
+            const uint32_t fj = nfp[j];
+            const bool ahead = (j < n) & ((sj > si) | ((sj == si) & (j < i)));
+            cnt += ahead ? 1 : 0;
+            if (ahead & (fj == fi)) dup |= (nh1[j] == a1) & (nh2[j] == a2) ? 1 : 0;
           }
-          bm0 = __reduce_or_sync(FULLMASK, bm0);
-          bm1 = __reduce_or_sync(FULLMASK, bm1);
-          const uint64_t regm = ~(((uint64_t)bm1 << 32) | bm0) & (n >= 64 ? ~0ull : ((1ull << n) - 1));
-          int G = 1;
-          while (G < 32 && 2 * G * n <= NC) G <<= 1;
-          const int groups = NC / G, g = tid / G, r = tid & (G - 1);
-          for (int i0 = 0; i0 < n; i0 += groups) {
-            const int i = i0 + g;
-            const bool act = i < n;
-            const double si = act ? nscore[i] : 0.0;
-            const bool ib = act && !((regm >> i) & 1ull);
-            int cnt = 0;
-            if (act) {
-              for (int k2 = r; k2 < nb; k2 += G) {
-                const int j = blist[k2];
-                const double sj = nscore[j];
-                cnt += (sj > si) || (sj == si && j < i);
-                if (!ib) cnt -= (j < i);
-              }
-              if (ib && r == 0) {
-                int lo = 0, hi = n;  // first j with sval[j] <= si
-                while (lo < hi) {
-                  const int mid = (lo + hi) >> 1;
-                  if (sval[mid] > si) lo = mid + 1;
-                  else hi = mid;
-                }
-                const int a = lo;
-                hi = n;  // first j with sval[j] < si
-                while (lo < hi) {
-                  const int mid = (lo + hi) >> 1;
-                  if (sval[mid] >= si) lo = mid + 1;
-                  else hi = mid;
-                }
-                const int e = max(a, min(lo, i));
-                cnt += __popcll(regm & (e >= 64 ? ~0ull : ((1ull << e) - 1)));
-              }
-            }
-            for (int o = G >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULLMASK, cnt, o);
-            if (act && r == 0) {
-              if (!ib) cnt += i;
-              rankv[i] = cnt;
-              if (si > GUARD) {
-                const uint64_t a1 = nh1[i], a2 = nh2[i];
-                int h = (int)((a1 ^ (a2 * 0x9E3779B97F4A7C15ull)) >> 20) & (TS - 1);
-                for (;;) {
-                  const int owner = atomicCAS(&slotb[h], -1, i);
-                  if (owner == -1 || (nh1[owner] == a1 && nh2[owner] == a2)) break;
-                  h = (h + 1) & (TS - 1);
-                }
-                myslot[i] = h;
-                atomicMin(&slotm[h], cnt);
-              }
-            }
+          cnt += __shfl_xor_sync(FULLMASK, cnt, 1);
+          dup |= __shfl_xor_sync(FULLMASK, dup, 1);
+          cnt += __shfl_xor_sync(FULLMASK, cnt, 2);
+          dup |= __shfl_xor_sync(FULLMASK, dup, 2);
+          if (act && r == 0) {
+            rankv[i] = cnt;
+            if (si > GUARD && !dup) atomicOr(&keep[cnt >> 5], 1u << (cnt & 31));
           }
         }
         LB_ARR(5);
         bar_sync(1, NC);  // S5
         LB_REL(5);
         LB_PHASE(6);
-        for (int i = tid; i < nsel; i += NC) {
-          if (nscore[i] > GUARD && slotm[myslot[i]] == rankv[i])
-            atomicOr(&keep[rankv[i] >> 5], 1u << (rankv[i] & 31));
-        }
-        LB_ARR(6);
-        bar_sync(1, NC);  // S6
-        LB_REL(6);
         const unsigned kp0 = keep[0], kp1 = keep[1];
         LB_PHASE(7);
 

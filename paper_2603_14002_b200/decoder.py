@@ -423,7 +423,8 @@ class DeviceBatch:
     PHASES = ("A_work", "S1_sync", "scan_work", "hcum_sync", "collect_work", "S2_sync",
               "rank_work", "S3_sync", "F_work", "S4_sync", "recomb_work", "S5_sync",
               "keep_work", "S6_sync", "scatter_work", "frame_sync", "spec_overflow_permille",
-              "ngram_warps_to_S3", "compute_to_S3", "ngover_work")
+              "ngram_warps_to_S3", "compute_to_S3", "ngover_work", "ng_scan", "ng_table",
+              "ng_score", "ng_rounds_permille", "F1_work", "S3b_wait")
 
     def enable_phase_timing(self, on: bool = True):
         N.check(N.lib().lb_batch_enable_phase_timing(self.h, int(on)))
