@@ -77,6 +77,32 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
       "l"(src), "r"(bytes), "r"(b)
       : "memory");
 }
+// the same with an L2 evict-first hint: streamed log-prob rows must not push the lexicon and
+// n-gram images (re-read every frame) out of L2
+__device__ __forceinline__ void tma_bulk_g2s_stream(void* dst, const void* src, unsigned bytes,
+                                                    uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+#ifdef LB_NO_L2HINT
+  tma_bulk_g2s(dst, src, bytes, bar);
+  return;
+#endif
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;\n" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b), "l"(pol)
+      : "memory");
+}
+// word-history nodes are written once per frame and read back only after the search
+__device__ __forceinline__ void st_stream(uint32_t* p, uint32_t v) {
+#ifdef LB_NO_L2HINT
+  *p = v;
+#else
+  __stcs(p, v);
+#endif
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   unsigned s = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile(
@@ -442,8 +468,8 @@ __device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const Batch
         for (int i = 0; i < kept; ++i) {
           const NgCand& cd = ws->top[i];
           const uint32_t node = (uint32_t)(base + i);
-          b.nparent[nb + node] = cd.node;
-          b.nsurf[nb + node] = cd.surf;
+          st_stream(b.nparent + nb + node, cd.node);
+          st_stream(b.nsurf + nb + node, cd.surf);
           WordScore sw;
           sw.slen = (int)cd.hlen;
           for (int t = 0; t < MAXH; ++t) {
@@ -1664,8 +1690,8 @@ __global__ void __launch_bounds__(small::NT, 2)
     const int nf = min(SCHUNK, te - f0);
     const unsigned bytes = (unsigned)(nf * VPD * sizeof(double));
     mbar_expect_tx(&dbar[ci & 1], bytes);
-    tma_bulk_g2s(dbuf + (size_t)(ci & 1) * SCHUNK * VPDC, Dtrial + (size_t)f0 * VPD, bytes,
-                 &dbar[ci & 1]);
+    tma_bulk_g2s_stream(dbuf + (size_t)(ci & 1) * SCHUNK * VPDC, Dtrial + (size_t)f0 * VPD,
+                        bytes, &dbar[ci & 1]);
   };
   if (tid == 0) issue_chunk(0);
 
@@ -1701,57 +1727,47 @@ __global__ void __launch_bounds__(small::NT, 2)
       const int gt = tid - NC, ngw = warp - NWC;
       const bool ngtim = timing && gt == 0;
       unsigned tg = ngtim ? (unsigned)clock() : 0u;
-      int carry = 0;
-      for (int base = 0; base < K; base += NGT) {
-        const int p = base + gt;
-        int np = 0;
-        if (p < K) {
-          const int32_t* row = rows + p * VP;
-          if (row[V] > 0 && C_LAST[p] != space) np = C_NENT[p] * row[V];
-        }
-        int incl = np;
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(FULLMASK, incl, o);
-          if (lane >= o) incl += y;
-        }
-        if (lane == 31) ngtot[ngw] = incl;
-        bar_sync(3, NGT);
-        const int woff = ngw ? ngtot[0] : 0;
-        const int tot = ngtot[0] + ngtot[1];
-        if (p < K) ppoff[p] = carry + woff + incl - np;
-        carry += tot;
-        bar_sync(3, NGT);
+      // one parent per n-gram thread: pair offsets by a warp scan + one cross-warp barrier
+      static_assert(KC <= NGT, "one parent per speculative n-gram thread");
+      const int p = gt;
+      int np = 0, ns = 0, nent = 0;
+      if (p < K) {
+        ns = rows[p * VP + V];
+        nent = C_NENT[p];
+        if (ns > 0 && C_LAST[p] != space) np = nent * ns;
       }
+      int incl = np;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULLMASK, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) ngtot[ngw] = incl;
+      bar_sync(3, NGT);
+      const int q0 = (ngw ? ngtot[0] : 0) + incl - np, q1 = q0 + np;
+      const int P = ngtot[0] + ngtot[1];
       const int SCAP = min(PC, b.spec_cap);
+      if (p < K) ppoff[p] = q0;
       if (gt == 0) {
-        ppoff[K] = carry;
-        s_ngP = carry;
-        if (carry <= SCAP) s_ngcov = carry;
+        ppoff[K] = P;
+        s_ngP = P;
+        if (P <= SCAP) s_ngcov = P;
       }
-      const int P = carry;
       if (ngtim) {
         const unsigned tn = (unsigned)clock();
         ph[20] += tn - tg;
         tg = tn;
       }
       {
-        // pair table: each parent writes its own (entry, surface) pairs -- no search.  Parents
-        // are in score order; when the pairs exceed PC only the leading parents whose pairs all
-        // fit are speculated (s_ngcov = their pair count), the rest take the warp path after S4
+        // pair table: each parent writes its own (entry, surface) pairs in creation order
+        // q = q0 + e * ns + s.  Parents are in score order; when the pairs exceed PC only the
+        // leading parents whose pairs all fit are speculated (s_ngcov = their pair count), the
+        // rest take the warp path after S4
         int4* qinfo = reinterpret_cast<int4*>(sm + O_QINFO);
-        for (int p = gt; p < K; p += NGT) {
-          // ppoff[K] is written by thread 0 without a barrier: use the scan total instead
-          const int q0 = ppoff[p], q1 = p + 1 < K ? ppoff[p + 1] : P;
-          if (q1 > SCAP) {
-            if (q0 <= SCAP) s_ngcov = q0;  // the first parent that does not fit (unique)
-            continue;
-          }
-          if (q0 == q1) continue;
+        if (q1 > SCAP) {
+          if (q0 <= SCAP) s_ngcov = q0;  // the first parent that does not fit (unique)
+        } else if (np > 0) {
           const CompHdr ch = comp_hdr(rows + p * VP, V);
-          for (int q = q0; q < q1; ++q) {
-            const int local = q - q0;
-            const int e = local / ch.ns;
-            const int sidx = local - e * ch.ns;
+          for (int sidx = 0; sidx < ns; ++sidx) {
             int w, surf;
             if (sidx == 0) {
               w = ch.l0;
@@ -1763,7 +1779,7 @@ __global__ void __launch_bounds__(small::NT, 2)
               w = __ldg(m.comp_lm + ch.off + sidx);
               surf = __ldg(m.comp_surf + ch.off + sidx);
             }
-            qinfo[q] = make_int4(p * OC + e, w, surf, 0);
+            for (int e = 0; e < nent; ++e) qinfo[q0 + e * ns + sidx] = make_int4(p * OC + e, w, surf, 0);
           }
         }
         bar_sync(3, NGT);
@@ -2106,16 +2122,16 @@ __global__ void __launch_bounds__(small::NT, 2)
                 } else {
                   const size_t nbase = (size_t)trial * b.ncap;
                   if (kept > 0) {
-                    b.nparent[nbase + base] = pres[t0].node;
-                    b.nsurf[nbase + base] = pres[t0].surf;
+                    st_stream(b.nparent + nbase + base, pres[t0].node);
+                    st_stream(b.nsurf + nbase + base, pres[t0].surf);
                   }
                   if (kept > 1) {
-                    b.nparent[nbase + base + 1] = pres[t1].node;
-                    b.nsurf[nbase + base + 1] = pres[t1].surf;
+                    st_stream(b.nparent + nbase + base + 1, pres[t1].node);
+                    st_stream(b.nsurf + nbase + base + 1, pres[t1].surf);
                   }
                   if (kept > 2) {
-                    b.nparent[nbase + base + 2] = pres[t2].node;
-                    b.nsurf[nbase + base + 2] = pres[t2].surf;
+                    st_stream(b.nparent + nbase + base + 2, pres[t2].node);
+                    st_stream(b.nsurf + nbase + base + 2, pres[t2].surf);
                   }
                   bs.x = kept;
                   bs.y = base;
