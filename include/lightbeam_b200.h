@@ -123,6 +123,9 @@ int lb_model_create(const lb_table_desc* table, const lb_ngram_desc* ngram, int3
 int lb_model_destroy(lb_model* m);
 /* bytes of device memory held by the model images */
 int lb_model_footprint(const lb_model* m, int64_t* bytes);
+/* 1 when the table is a breadth-first trie (successors of a state are consecutive ids, space ->
+   root) and the frame kernel derives successors arithmetically; 0 = successor-list lookups */
+int lb_model_lex_contiguous(const lb_model* m, int32_t* out);
 
 /* stream: a cudaStream_t (NULL = legacy default stream). */
 int lb_batch_create(lb_model* m, const lb_config* cfg, int32_t max_trials, int32_t max_frames,

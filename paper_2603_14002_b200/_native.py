@@ -197,6 +197,7 @@ _SIGS = {
     "lb_model_create": (C.c_int, [C.POINTER(LbTableDesc), C.POINTER(LbNgramDesc), _I32, _P]),
     "lb_model_destroy": (C.c_int, [_P]),
     "lb_model_footprint": (C.c_int, [_P, _P]),
+    "lb_model_lex_contiguous": (C.c_int, [_P, _P]),
     "lb_batch_create": (C.c_int, [_P, C.POINTER(LbConfig), _I32, _I32, _P, _P]),
     "lb_batch_destroy": (C.c_int, [_P]),
     "lb_batch_layout": (C.c_int, [_P, _P, _P, _P]),

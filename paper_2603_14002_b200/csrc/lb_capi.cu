@@ -137,6 +137,59 @@ int lb_model_create(const lb_table_desc* td, const lb_ngram_desc* nd, int32_t de
   CK(lbk::pad_table(m->d_table, tmp, S, V, VP, m->d_comp_off, m->d_comp_surf, m->d_comp_lm, 0));
   CK(cudaDeviceSynchronize());
   CK(cudaFree(tmp));
+  // compact lexicon image (LexRec per state + successor list), built on the host
+  int64_t n_next = 0;
+  int32_t contig = 1;
+  {
+    std::vector<lbd::LexRec> lex((size_t)S);
+    std::vector<int32_t> nexts;
+    nexts.reserve((size_t)S * 2);
+    for (int32_t s = 0; s < S; ++s) {
+      const int32_t* row = td->table + (size_t)s * V;
+      lbd::LexRec& r = lex[(size_t)s];
+      r.mask = 0ull;
+      r.base = (int32_t)nexts.size();
+      for (int32_t v = 0; v < V; ++v)
+        if (row[v] != td->sink) {
+          r.mask |= 1ull << v;
+          nexts.push_back(row[v]);
+        }
+      const int32_t off = td->comp_offsets[s], n = td->comp_offsets[s + 1] - off;
+      r.ns = n;
+      r.s0 = n > 0 ? td->comp_surface[off] : -1;
+      r.l0 = n > 0 ? td->comp_lmword[off] : -1;
+      r.s1 = n > 1 ? td->comp_surface[off + 1] : -1;
+      r.l1 = n > 1 ? td->comp_lmword[off + 1] : -1;
+    }
+    n_next = (int64_t)nexts.size();
+    // breadth-first tries: successors of each state (space excluded) are consecutive ids
+    for (int32_t s = 0; s < S && contig; ++s) {
+      const int32_t* row = td->table + (size_t)s * V;
+      int32_t expect = -1;
+      for (int32_t v = 0; v < V && contig; ++v) {
+        if (row[v] == td->sink) continue;
+        if (v == td->space_id) {
+          if (row[v] != 0) contig = 0;
+        } else if (v == td->blank_id) {
+          contig = 0;
+        } else {
+          if (expect >= 0 && row[v] != expect) contig = 0;
+          expect = row[v] + 1;
+        }
+      }
+    }
+    if (contig)
+      for (int32_t s = 0; s < S; ++s) {
+        lbd::LexRec& r = lex[(size_t)s];
+        const unsigned long long ms = r.mask & ~(1ull << td->space_id);
+        r.base = ms ? td->table[(size_t)s * V + __builtin_ctzll(ms)] : 0;
+      }
+    CK(dalloc(&m->d_lex, (size_t)S));
+    CK(cudaMemcpy(m->d_lex, lex.data(), (size_t)S * sizeof(lbd::LexRec), cudaMemcpyHostToDevice));
+    CK(dalloc(&m->d_lex_next, (size_t)std::max<int64_t>(n_next, 1)));
+    if (n_next > 0)
+      CK(cudaMemcpy(m->d_lex_next, nexts.data(), (size_t)n_next * 4, cudaMemcpyHostToDevice));
+  }
   // n-gram image: bucketized cuckoo table (4 records per 128-byte bucket, 2 candidate buckets)
   // built on the host -- deterministic and a few hundred ms for 1M grams
   std::vector<NgRec> tab;
@@ -151,9 +204,12 @@ int lb_model_create(const lb_table_desc* td, const lb_ngram_desc* nd, int32_t de
   CK(cudaMemcpy(m->d_ng, tab.data(), tab.size() * sizeof(NgRec), cudaMemcpyHostToDevice));
   const int64_t cap = m->ng_cap;
   m->bytes = (int64_t)S * VP * 4 + ((int64_t)S + 1) * 4 + (int64_t)td->n_comp * 8 +
-             cap * (int64_t)sizeof(NgRec);
+             cap * (int64_t)sizeof(NgRec) + (int64_t)S * (int64_t)sizeof(lbd::LexRec) + n_next * 4;
   ModelDev& d = m->dev;
   d.table = m->d_table;
+  d.lex = m->d_lex;
+  d.lex_next = m->d_lex_next;
+  d.lex_contig = contig;
   d.S = S;
   d.V = V;
   d.VP = VP;
@@ -184,8 +240,16 @@ int lb_model_destroy(lb_model* m) {
   cudaFree(m->d_comp_off);
   cudaFree(m->d_comp_surf);
   cudaFree(m->d_comp_lm);
+  cudaFree(m->d_lex);
+  cudaFree(m->d_lex_next);
   cudaFree(m->d_ng);
   delete m;
+  return LB_OK;
+}
+
+int lb_model_lex_contiguous(const lb_model* m, int32_t* out) {
+  if (!m || !out) return fail(LB_ERR_ARG, "null argument");
+  *out = m->dev.lex_contig;
   return LB_OK;
 }
 

@@ -57,8 +57,26 @@ static_assert(sizeof(Ent) == 64, "Ent must be 64 bytes");
 //   row[V+0] = number of distinct completing surfaces, row[V+1] = CSR offset,
 //   row[V+2], row[V+3] = (surface, LM word) of the first, row[V+4], row[V+5] of the second.
 constexpr int ROW_HDR = 6;
+
+// Compact lexicon record (the k <= 64 frames kernel): one 32-byte sector per state instead of a
+// 192-byte padded row.  mask bit v <=> table[s][v] != sink; the successors of the set bits, in
+// token order, are lex_next[base ...] (next state of token v = lex_next[base + popc(mask & ((1 <<
+// v) - 1))]); then the completion header: count of distinct surfaces and the first two
+// (surface, LM word) pairs (the rest through comp_off / comp_surf / comp_lm).
+struct __align__(16) LexRec {
+  unsigned long long mask;
+  int32_t base, ns, s0, l0, s1, l1;
+};
+static_assert(sizeof(LexRec) == 32, "LexRec is one 32-byte sector");
+
 struct ModelDev {
   const int32_t* table;
+  const LexRec* lex;        // [S] compact records
+  const int32_t* lex_next;  // successors of the valid transitions, per state in token order
+  // 1 when every state's non-space successors are consecutive ids in token order and a valid
+  // space transition leads to the root (breadth-first tries, lexicon.py:149-209): then
+  // LexRec.base is the first child and next(s, v) = base + rank, with no successor load
+  int32_t lex_contig;
   int32_t S, V, VP;  // VP: int32 row pitch (multiple of 4)
   int32_t sink, blank, space;
   const int32_t* comp_off;

@@ -372,6 +372,11 @@ __device__ __forceinline__ CompHdr comp_hdr(const int32_t* row, int V) {
   return CompHdr{row[V], row[V + 1], row[V + 2], row[V + 3], row[V + 4], row[V + 5]};
 }
 
+// The same header from a compact lexicon record (the CSR offset is read only for >2 surfaces).
+__device__ __forceinline__ CompHdr lex_hdr(const ModelDev& m, const LexRec& r, int state) {
+  return CompHdr{r.ns, r.ns > 2 ? __ldg(m.comp_off + state) : 0, r.s0, r.l0, r.s1, r.l1};
+}
+
 // apply_ngram (decoder.py:182-235) for one beam, one full warp.  Candidates are the
 // (entry, distinct surface) pairs in creation order; the running top-O list is ordered by
 // (-total, seq) -- candidates arrive in increasing seq, so strict '>' keeps ties stable.
@@ -1387,7 +1392,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
 // and word-boundary entries are built straight from the speculative pair results.
 // =====================================================================================
 namespace small {
-constexpr int KC = 64, OC = 3, VC = 48, VPC = 56, VPDC = 50;
+constexpr int KC = 64, OC = 3, VC = 48, VPDC = 50;
 // PC: speculative (entry, surface) pairs per frame -- 64..80 measured best at config 2 (7.23 ms
 // at 160 -> 7.13 ms; the n-gram warps are the critical path up to S3 and the uncovered parents'
 // few selected boundary beams take the warp path); LC 280 and 4-frame D chunks keep two CTAs
@@ -1402,7 +1407,7 @@ constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8
 constexpr int BEAM_BYTES = B_ENTS + KC * OC * (int)sizeof(Ent);
 constexpr int O_DBUF = 0;
 constexpr int O_ROWS = O_DBUF + 2 * SCHUNK * VPDC * 8;
-constexpr int O_BEAM = O_ROWS + KC * VPC * 4;
+constexpr int O_BEAM = O_ROWS + KC * (int)sizeof(LexRec);  // one compact lexicon record per beam
 constexpr int O_CVAL = O_BEAM + 2 * BEAM_BYTES;
 constexpr int O_CKEY = O_CVAL + LC * 8;
 constexpr int O_CBINL = O_CKEY + LC * 4;
@@ -1440,8 +1445,8 @@ constexpr int GTOTAL = G_WARP + NWC * (int)sizeof(WarpScratch);
 // out of line so its ~1300 instructions stay out of the frame loop's instruction-cache footprint.
 // Called by all NC compute threads; returns nsel with sval/skey in (value desc, index asc) order.
 __device__ LB_COLD int small_fallback_select(const int ck, const double cbeta, const double cgamma,
-                                             int K, int V, int VP, double thr,
-                                             int blank, int space, int sink, const int32_t* rows,
+                                             int K, int V, double thr,
+                                             int blank, int space, const LexRec* lrow,
                                              const int32_t* C_LAST, const double* C_SCORE,
                                              const double* drow, unsigned* hist, double* cval,
                                              uint32_t* ckey, double* sval, uint32_t* skey,
@@ -1453,8 +1458,7 @@ __device__ LB_COLD int small_fallback_select(const int ck, const double cbeta, c
   auto cval_at = [&](int f) -> double {
     const int p = f / V, v = f - (f / V) * V;
     const int lp = C_LAST[p];
-    const int nx = rows[p * VP + v];
-    if (!((nx != sink) || (v == blank) || (v == lp))) return -DBL_MAX;
+    if (!(((lrow[p].mask >> v) & 1ull) || (v == blank) || (v == lp))) return -DBL_MAX;
     const double x = cand_value(C_SCORE[p], drow[v], v, lp,
                                 FrameConsts{cbeta, cgamma, blank, space});
     return x > GUARD ? x : -DBL_MAX;
@@ -1574,7 +1578,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   char* gs = b.gscratch + (int64_t)trial * b.gscratch_stride;
 
   double* dbuf = reinterpret_cast<double*>(sm + O_DBUF);
-  int32_t* rows = reinterpret_cast<int32_t*>(sm + O_ROWS);
+  LexRec* lrow = reinterpret_cast<LexRec*>(sm + O_ROWS);  // lexicon record of each beam's prefix
   double* cval = reinterpret_cast<double*>(sm + O_CVAL);
   uint32_t* ckey = reinterpret_cast<uint32_t*>(sm + O_CKEY);
   uint16_t* cbinl = reinterpret_cast<uint16_t*>(sm + O_CBINL);
@@ -1614,11 +1618,11 @@ __global__ void __launch_bounds__(small::NT, 2)
 #define X_NENT ((int32_t*)(BUF(par ^ 1) + B_NENT))
 #define X_ENTS ((Ent*)(BUF(par ^ 1) + B_ENTS))
 
-  const int V = m.V, VP = m.VP, VPD = b.VPD, O = c.O, KC_ = b.K;
+  const int V = m.V, VPD = b.VPD, O = c.O, KC_ = b.K;
   const double ibw = c.inv_binw;
   const double b_on = c.beta, b_off = xmul(c.beta, 0.0);
   const double g_on = c.gamma, g_off = xmul(c.gamma, 0.0);
-  const int blank = m.blank, space = m.space, sink = m.sink;
+  const int blank = m.blank, space = m.space;
   // candidate mapping: thread -> parent cp = tid / 4 and its token block of TBK tokens, with
   // the block's static token classes as bit masks (bit i = token cv0 + i)
   const int cp = tid >> 2, cv0 = (tid & 3) * TBK;
@@ -1644,8 +1648,9 @@ __global__ void __launch_bounds__(small::NT, 2)
       C_LAST[i] = b.last[hb + i];
       C_PRE[i] = b.prefix[hb + i];
       C_NENT[i] = b.nent[hb + i];
-      const int32_t* src = m.table + (size_t)b.prefix[hb + i] * VP;
-      for (int q = 0; q < VP; q += 4) cp_async16(rows + i * VP + q, src + q);
+      const LexRec* src = m.lex + b.prefix[hb + i];
+      cp_async16(&lrow[i], src);
+      cp_async16(reinterpret_cast<char*>(&lrow[i]) + 16, reinterpret_cast<const char*>(src) + 16);
     }
     cp_async_commit();
     for (int i = tid; i < K * O; i += NT) {
@@ -1732,7 +1737,7 @@ __global__ void __launch_bounds__(small::NT, 2)
       const int p = gt;
       int np = 0, ns = 0, nent = 0;
       if (p < K) {
-        ns = rows[p * VP + V];
+        ns = lrow[p].ns;
         nent = C_NENT[p];
         if (ns > 0 && C_LAST[p] != space) np = nent * ns;
       }
@@ -1766,7 +1771,7 @@ __global__ void __launch_bounds__(small::NT, 2)
         if (q1 > SCAP) {
           if (q0 <= SCAP) s_ngcov = q0;  // the first parent that does not fit (unique)
         } else if (np > 0) {
-          const CompHdr ch = comp_hdr(rows + p * VP, V);
+          const CompHdr ch = lex_hdr(m, lrow[p], C_PRE[p]);
           for (int sidx = 0; sidx < ns; ++sidx) {
             int w, surf;
             if (sidx == 0) {
@@ -1855,23 +1860,17 @@ __global__ void __launch_bounds__(small::NT, 2)
       uint16_t bins[TBK];
       double wm = -DBL_MAX;
       if (__any_sync(FULLMASK, pin)) {
-        const int4* rseg = reinterpret_cast<const int4*>(rows + pcl * VP + cv0);
+        // allowed tokens (lexicon.py:124-137): a valid transition, the blank, or the repeat
+        const unsigned albits = ((unsigned)(lrow[pcl].mask >> cv0) & tk_inv) | abits;
 #pragma unroll
-        for (int q = 0; q < TBK / 4; ++q) {
-          const int4 n4 = rseg[q];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = 4 * q + u;
-            const int nx = u == 0 ? n4.x : u == 1 ? n4.y : u == 2 ? n4.z : n4.w;
-            const double add = (i == tk_sidx) ? gsel : (((bbits >> i) & 1u) ? b_on : b_off);
-            const double x = xadd(xadd(sp, drow[cv0 + i]), add);
-            const bool al = (nx != sink) ? ((tk_inv >> i) & 1u) : ((abits >> i) & 1u);
-            const bool ok = pin && al && (x > GUARD);
-            const int bn = min(__double2int_rz(xmul(xsub(U, x), ibw)), NBINS - 1);
-            bins[i] = ok ? (uint16_t)bn : (uint16_t)0xFFFF;
-            atomicAdd(&hist[ok ? bn : NBINS], 1u);
-            wm = (ok && x > wm) ? x : wm;
-          }
+        for (int i = 0; i < TBK; ++i) {
+          const double add = (i == tk_sidx) ? gsel : (((bbits >> i) & 1u) ? b_on : b_off);
+          const double x = xadd(xadd(sp, drow[cv0 + i]), add);
+          const bool ok = pin && ((albits >> i) & 1u) && (x > GUARD);
+          const int bn = min(__double2int_rz(xmul(xsub(U, x), ibw)), NBINS - 1);
+          bins[i] = ok ? (uint16_t)bn : (uint16_t)0xFFFF;
+          atomicAdd(&hist[ok ? bn : NBINS], 1u);
+          wm = (ok && x > wm) ? x : wm;
         }
       } else {
 #pragma unroll
@@ -1999,9 +1998,9 @@ __global__ void __launch_bounds__(small::NT, 2)
           }
         } else {
           ++st_fallback;
-          nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, VP, thr, blank, space, sink,
-                                       rows, C_LAST, C_SCORE, drow, hist, cval, ckey, sval, skey,
-                                       &s_inr, &s_cnt2);
+          nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, thr, blank, space, lrow, C_LAST,
+                                       C_SCORE, drow, hist, cval, ckey, sval, skey, &s_inr,
+                                       &s_cnt2);
         }
       }
       LB_ARR(3);
@@ -2024,16 +2023,16 @@ __global__ void __launch_bounds__(small::NT, 2)
           if (emit) {
             a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
             a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
-            np = rows[p * VP + tok];
+            const LexRec& lr = lrow[p];
+            if (m.lex_contig) {  // breadth-first trie: first child + rank, space -> root
+              const unsigned long long ms = lr.mask & ~(1ull << space);
+              np = tok == space ? 0 : lr.base + __popcll(ms & ((1ull << tok) - 1ull));
+            } else {
+              np = __ldg(m.lex_next + lr.base + __popcll(lr.mask & ((1ull << tok) - 1ull)));
+            }
           }
-          {  // warm L1 with the next frame's lexicon row (gathered by cp.async.ca at the scatter)
-            const char* r0 = reinterpret_cast<const char*>(m.table + (size_t)np * VP);
-            const char* r1 = r0 + VP * 4 - 1;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(r0));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(r1));
-            if ((((uintptr_t)r1 >> 7) - ((uintptr_t)r0 >> 7)) > 1)
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(r0 + 128));
-          }
+          // warm L1 with the next frame's lexicon record (gathered by cp.async.ca at the scatter)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(m.lex + np));
           if (emit && tok == space) blist[atomicAdd(&s_nb, 1)] = j;
           nscore[j] = x;
           nh1[j] = a1;
@@ -2159,7 +2158,7 @@ __global__ void __launch_bounds__(small::NT, 2)
             const int p = npar[j];
             int outn = -1;
             double sc = nscore[j];
-            warp_apply_ngram(m, c, b, trial, C_ENTS + p * OC, C_NENT[p], comp_hdr(rows + p * VP, V),
+            warp_apply_ngram(m, c, b, trial, C_ENTS + p * OC, C_NENT[p], lex_hdr(m, lrow[p], C_PRE[p]),
                              &wsc[warp], gbents + (size_t)j * OC, &outn, &sc, &s_ncount, &s_fail,
                              calls_l, probes_l);
             if (lane == 0) {
@@ -2276,8 +2275,9 @@ __global__ void __launch_bounds__(small::NT, 2)
                 b.dump_score[di] = nscore[i];
               }
             }
-            const int32_t* srow = m.table + (size_t)npre[i] * VP;
-            for (int u = r; u < (VP >> 2); u += G) cp_async16_ca(rows + pos * VP + u * 4, srow + u * 4);
+            if (r < 2)
+              cp_async16_ca(reinterpret_cast<char*>(&lrow[pos]) + 16 * r,
+                            reinterpret_cast<const char*>(m.lex + npre[i]) + 16 * r);
           }
           cp_async_commit();
           cp_async_wait_all();

@@ -17,6 +17,8 @@ struct lb_model {
   int32_t* d_comp_off = nullptr;
   int32_t* d_comp_surf = nullptr;
   int32_t* d_comp_lm = nullptr;
+  lbd::LexRec* d_lex = nullptr;
+  int32_t* d_lex_next = nullptr;
   lbd::NgRec* d_ng = nullptr;
   int64_t ng_cap = 0;
   int max_probe = 0;

@@ -149,6 +149,14 @@ class DeviceModel:
             N.lib(False).lb_model_destroy(self.handle)
             self.handle = None
 
+    @property
+    def lex_contiguous(self) -> bool:
+        """Whether the frame kernel derives lexicon successors arithmetically (breadth-first
+        trie) or looks them up in the compact image's successor list."""
+        out = C.c_int32()
+        N.check(N.lib().lb_model_lex_contiguous(self.handle, C.byref(out)))
+        return bool(out.value)
+
     def footprint(self) -> int:
         out = C.c_int64()
         N.check(N.lib().lb_model_footprint(self.handle, C.byref(out)))

@@ -456,3 +456,33 @@ def test_run_search_many_interleaves_host_fusion_batches():
     for b, wv in zip(batches, want):
         got = [(r.text, r.score, r.nbest) for r in _collect(b, cfg, False, 0.0)]
         assert got == wv
+
+
+def test_relabelled_table_general_successor_path():
+    """A transition table whose states are not breadth-first numbered (ids shuffled) takes the
+    compact image's general successor-list path (LexRec.base into lex_next) instead of the
+    first-child + rank arithmetic; results equal the oracle's on the same relabelled table."""
+    from paper_2603_14002_b200.lexicon import TransitionTable
+
+    w = synth.toy_world(n_words=1500, seed=11)
+    tt = w.table
+    S = tt.num_states
+    rng = np.random.default_rng(5)
+    perm = np.arange(S)
+    perm[1:S - 1] = 1 + rng.permutation(S - 2)  # root 0 and sink S-1 keep their ids
+    table = np.empty_like(tt.table)
+    table[perm] = perm[tt.table]
+    comps = {int(perm[s]): tt.completions_at(s) for s in tt.completion_states()}
+    rt = TransitionTable(table, tt.sink, comps, tt.entries, tt.blank_id, tt.space_id)
+    cfg = PROFILES["b2t25"].replace(beam_size=64)
+    raws = synth.make_logits(12, 200, 41, base_seed=606)
+    ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
+    scale = cfg.ngram_weight / cfg.llm_weight
+    for table_ in (rt, tt):
+        got = decode_batch(ds, cfg, table_, w.model, DeviceNgramScorer(w.model, scale))
+        for i, d in enumerate(ds):
+            want = O.decode(d, cfg, table_, w.model, StubScorer(ngram_model=w.model, scale=scale))
+            assert (got[i].text, got[i].score, got[i].nbest, got[i].llm_events) == (
+                want.text, want.score, want.nbest, want.llm_events), i
+    assert device_model(rt, w.model).lex_contiguous is False
+    assert device_model(tt, w.model).lex_contiguous is True
