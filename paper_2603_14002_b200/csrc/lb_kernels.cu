@@ -1558,7 +1558,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   using namespace small;
   extern __shared__ __align__(128) char sm[];
   __shared__ __align__(8) uint64_t dbar[2];
-  __shared__ unsigned hist[NBINS + 1];  // + a spare bin for rejected candidates (never read)
+  __shared__ unsigned hist[NBINS + 32];  // + one spare bin per lane for rejected candidates
   __shared__ int hcum[NBINS];  // exclusive prefix of hist (published by warp 0)
   __shared__ int hfill[NBINS];
   __shared__ double wmax[NWC];
@@ -1856,7 +1856,7 @@ __global__ void __launch_bounds__(small::NT, 2)
       // (decoder.py:252-256) adds beta*0 = +-0.0 to the space column, an exact identity.  The
       // bin is trunc((U - x) / binw) clamped to NBINS-1: x <= U (U rounds up), so no lower
       // clamp; monotone in x, identical to the clamped double form.  Rejected candidates count
-      // into the spare bin NBINS (never scanned).
+      // into a per-lane spare bin NBINS + lane (never scanned; no same-address conflicts).
       uint16_t bins[TBK];
       double wm = -DBL_MAX;
       if (__any_sync(FULLMASK, pin)) {
@@ -1869,7 +1869,7 @@ __global__ void __launch_bounds__(small::NT, 2)
           const bool ok = pin && ((albits >> i) & 1u) && (x > GUARD);
           const int bn = min(__double2int_rz(xmul(xsub(U, x), ibw)), NBINS - 1);
           bins[i] = ok ? (uint16_t)bn : (uint16_t)0xFFFF;
-          atomicAdd(&hist[ok ? bn : NBINS], 1u);
+          atomicAdd(&hist[ok ? bn : NBINS + lane], 1u);  // rejected: no intra-warp conflict
           wm = (ok && x > wm) ? x : wm;
         }
       } else {
