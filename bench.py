@@ -650,7 +650,7 @@ def llm_core(dev, world, cfg, raws, llm, precision, steps, warmup, world_n=1, su
     # GEMM twice over (hi + lo activation halves), reported separately as `executed_tf`
     flops = rows * scorer.cfg.flops_per_token()
     achieved_tf = flops / (llm_ms / 1e3) / 1e12 if llm_ms > 0 else 0.0
-    executed_tf = achieved_tf * (2 if scorer.split else 1)
+    executed_tf = achieved_tf * scorer.executed_flops_per_token() / scorer.cfg.flops_per_token()
     peaks = {}
     pp = ROOT / "MEASURED_PEAKS.json"
     if pp.exists():
@@ -743,7 +743,7 @@ def llm_core_interleaved(dev, world, cfg, raws, llm, precision, steps, warmup, w
     flops = rows * scorer.cfg.flops_per_token()
     # event time of the two overlapped streams summed: a conservative (low) achieved rate
     achieved_tf = flops / (llm_ms / 1e3) / 1e12 if llm_ms > 0 else 0.0
-    executed_tf = achieved_tf * (2 if scorer.split else 1)
+    executed_tf = achieved_tf * scorer.executed_flops_per_token() / scorer.cfg.flops_per_token()
     peaks = {}
     pp = ROOT / "MEASURED_PEAKS.json"
     if pp.exists():
@@ -903,7 +903,7 @@ def run_llm(args):
                          "achieved_basis": "algorithmic: 2 x params per forward row (no bf16x2 doubling)",
                          "executed": core["executed_tf"],
                          "executed_frac": core["executed_tf"] / peak_tf,
-                         "executed_flops_per_row": scorer.cfg.flops_per_token() * (2 if scorer.split else 1),
+                         "executed_flops_per_row": scorer.executed_flops_per_token(),
                          "precision": args.precision,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"
                          if pp.exists() else "fallback 1400 TFLOP/s"},

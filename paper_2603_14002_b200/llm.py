@@ -351,12 +351,18 @@ class LlamaScorer:
     def __init__(self, config="tiny", seed: int = 0, device: int = 0, max_slots: int | None = None,
                  max_depth: int = 1023, row_chunk: int = 16384, lm_chunk: int = 2048,
                  precision: str = "bf16x2", lm_head: str = "fused", fused_swiglu: bool = False,
-                 fused_swiglu_min_rows: int = 4096, graphs: bool | None = None):
+                 fused_swiglu_min_rows: int = 4096, graphs: bool | None = None,
+                 lse_split: bool = False):
         """precision: "bf16x2" (default) feeds every body GEMM the activation as a hi+lo pair of
         bf16 values against duplicated bf16 weights -- fp32-equivalent activations on the bf16
         tensor cores, scores within ~1e-3 of an fp32 forward even for 40-token texts -- and keeps
         q/K/V in fp32; "bf16" is one bf16 operand per activation (half the body FLOPs; measured
-        per-text error vs fp32 grows to ~0.1 at 40 tokens on the random-init 1B model)."""
+        per-text error vs fp32 grows to ~0.1 at 40 tokens on the random-init 1B model).
+        lse_split: in bf16x2, also run the LM-head log-sum-exp GEMM on hi|lo activations.  Off by
+        default: a token's log-prob is h.E[token] with the fp32 final hidden state (lp kernel)
+        minus the row's LSE, and the LSE -- a softmax-weighted average of logits -- barely feels
+        the hi-only rounding (tools/prec_lse.py: 39-token text error max 1.1e-3 on the 1B model,
+        2.1e-3 on the 8B one, against 5.6e-4 / 1.7e-3 with hi|lo), for half the head FLOPs."""
         import torch
 
         if not torch.cuda.is_available():
@@ -390,6 +396,7 @@ class LlamaScorer:
         self.lm_head = lm_head
         self.precision = precision
         self.split = precision == "bf16x2"
+        self.lse_split = bool(lse_split) and self.split
         # gate/up rows interleaved in 128-row blocks for the tcgen05 GEMM with the SwiGLU epilogue
         # (opt-in, for waves of >= fused_swiglu_min_rows rows).  On the 13.4k-row final wave of
         # config 3 its 128x256 tiles keep the tensor pipe ~81% busy and the gate/up product never
@@ -407,7 +414,8 @@ class LlamaScorer:
                 for k in ("wqkv", "wo", "wgu", "wgui", "wfc", "wd"):
                     if k in L:
                         L[k + "2"] = torch.cat([L[k], L[k]], 1).contiguous()
-            self.emb2 = torch.cat([self.weights.emb, self.weights.emb], 1).contiguous()
+            if self.lse_split or lm_head == "cublas":
+                self.emb2 = torch.cat([self.weights.emb, self.weights.emb], 1).contiguous()
         self.device_llm_scorer = self  # the GPU decoder drives this scorer on the device
         # graph mode: whole decodes replay as one CUDA graph (events padded to a fixed row
         # capacity, no host round trip per event) -- for small models, where an event is
@@ -418,6 +426,16 @@ class LlamaScorer:
         torch.cuda.synchronize(device)
 
     # ---- reference protocol (host strings, one full forward per text, no KV reuse)
+    def executed_flops_per_token(self) -> float:
+        """FLOPs the tensor cores execute per forwarded token: bf16x2 runs every body GEMM on
+        hi|lo activations (twice the algorithmic work) and the LM head once (or twice with
+        lse_split)."""
+        c = self.cfg
+        head = 2.0 * c.vocab_size * c.hidden
+        body = c.flops_per_token() - head
+        k = 2 if self.split else 1
+        return k * body + (2 if self.lse_split else 1) * head
+
     def next_request_id(self) -> int:
         return next(self._ids)
 
@@ -865,7 +883,8 @@ class DeviceLlmSession:
         sfx = "2" if self.scorer.split else ""
         f32 = torch.float32
         if self.scorer.lm_head == "fused":  # K6 on tcgen05: logits never leave TMEM
-            E = self.scorer.emb2 if sfx else W.emb
+            # bf16x2: the LSE GEMM reads only the hi half of hn (first H columns) unless lse_split
+            E = self.scorer.emb2 if (sfx and self.scorer.lse_split) else W.emb
             nt = (E.shape[0] + 255) // 256
             partial = torch.empty((n, nt, 2), dtype=torch.float32, device=hn.device)
             N.check(lib.lb_llm_lmhead_lse(self.h, hn.data_ptr(), n, hn.stride(0), E.shape[1],

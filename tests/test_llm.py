@@ -242,26 +242,32 @@ def test_llm_device_kernels_peaky_model_vs_oracle(precision):
     weights): the hand-written kernels add no error beyond bf16 operands."""
     from paper_2603_14002_b200 import LlamaScorer
 
-    sc = LlamaScorer(_peaky_tiny(), seed=5, precision=precision)
+    # lse_split: every GEMM on the same operands as the dense path (the default hi-only LSE is
+    # checked against the fp32 oracle at the end)
+    sc = LlamaScorer(_peaky_tiny(), seed=5, precision=precision, lse_split=True)
     w, cfg = _world_cfg()
     raws = synth.make_logits(3, 120, 41, base_seed=17)
-    _, got, sess = _decode_with_session(sc, raws, cfg, w)
-    ex = sess.export()
-    first = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._cap)}
-    mid = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._low)}
     oracle = LO.OracleLlmScorer(sc.cfg, sc.weights.hf_state_dict())
-    texts, devs = [], []
-    for s in range(1, len(ex["parent"])):
-        if ex["parent"][s] < 0 or not ex["state"][s] & 2:
-            continue
-        words, cur = [], s
-        while cur != 0:
-            words.append(int(ex["token"][cur]))
-            cur = int(ex["parent"][cur])
-        words.reverse()
-        text = " ".join([first[words[0]]] + [mid[t] for t in words[1:]])
-        texts.append(text)
-        devs.append(ex["cum"][s])
+
+    def scored_texts(scorer):
+        _, got, sess = _decode_with_session(scorer, raws, cfg, w)
+        ex = sess.export()
+        first = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._cap)}
+        mid = {int(t): s for s, t in zip(sess.batch.dm.surfaces, sess._low)}
+        texts, devs = [], []
+        for s in range(1, len(ex["parent"])):
+            if ex["parent"][s] < 0 or not ex["state"][s] & 2:
+                continue
+            words, cur = [], s
+            while cur != 0:
+                words.append(int(ex["token"][cur]))
+                cur = int(ex["parent"][cur])
+            words.reverse()
+            texts.append(" ".join([first[words[0]]] + [mid[t] for t in words[1:]]))
+            devs.append(ex["cum"][s])
+        return texts, devs
+
+    texts, devs = scored_texts(sc)
     assert len(texts) > 20
     want = [oracle.score(t) for t in texts]
     dense = sc.score_texts_dense(texts)
@@ -275,6 +281,11 @@ def test_llm_device_kernels_peaky_model_vs_oracle(precision):
     assert max(e_dev) <= 2.0 * max(e_dense) + 1e-4
     if precision == "bf16x2":  # fp32-equivalent activations: the north-star 1e-2 per text holds
         assert max(abs(a - b) for a, b in zip(devs, want)) <= TOL
+        # the default scorer: LM-head log-sum-exp from the bf16 hi half of the final hidden state
+        texts2, devs2 = scored_texts(LlamaScorer(_peaky_tiny(), seed=5, precision=precision))
+        err2 = [abs(d - oracle.score(t)) for t, d in zip(texts2, devs2)]
+        print("hi-only LSE: text error max %.2e mean %.2e" % (max(err2), np.mean(err2)))
+        assert max(err2) <= TOL
 
 
 @pytest.mark.gpu
@@ -377,7 +388,10 @@ def test_fused_lmhead_lse_matches_cublas_path(precision):
     raws = synth.make_logits(3, 100, 41, base_seed=41)
     outs = []
     for mode in ("cublas", "fused"):  # fused: tcgen05 LM head + LSE
-        sc = LlamaScorer("tiny", seed=6, precision=precision, lm_head=mode, fused_swiglu=False)
+        # lse_split: the fused head on the same hi|lo operands as the cuBLAS path (the default
+        # hi-only LSE is checked against the fp32 oracle elsewhere)
+        sc = LlamaScorer("tiny", seed=6, precision=precision, lm_head=mode, fused_swiglu=False,
+                         lse_split=True)
         _, got, sess = _decode_with_session(sc, raws, cfg, w)
         outs.append((sess.export(), [(g.text, g.score) for g in got]))
     (a, ga), (b, gb) = outs
@@ -413,7 +427,7 @@ def test_fused_lmhead_1b_shapes():
     raws = synth.make_logits(2, 60, 41, base_seed=3)
     res = []
     for mode in ("cublas", "fused"):
-        sc = LlamaScorer("llama-3.2-1b", seed=2, lm_head=mode)
+        sc = LlamaScorer("llama-3.2-1b", seed=2, lm_head=mode, lse_split=True)
         _, got, sess = _decode_with_session(sc, raws, cfg, w)
         ex = sess.export()
         res.append(ex)
