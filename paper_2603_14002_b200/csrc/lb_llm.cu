@@ -997,6 +997,293 @@ __global__ void __launch_bounds__(256) chain_attn_mma_kernel(LlmDev l, int layer
   }
 }
 
+// ---------------------------------------------------------------- sibling-grouped attention
+// Rows of one forward chunk that share a parent slot are siblings: same depth d, same ancestor
+// chain (positions 0 .. d-1), different own position d.  In the final event of a config-3 batch
+// ~6 rows share each parent (every leaf text is forwarded for its punctuation), elsewhere ~1.3.
+// Siblings are grouped SIB = 16 / G per tile so one CTA gathers the shared chain once and the
+// G x SIB query rows fill the M = 16 rows of the MMAs (the per-row kernel uses G of them).
+struct GrpDev {
+  int32_t* cnt;     // [cap] siblings per parent slot in this chunk (reset after the build)
+  int32_t* base;    // [cap] first tile of a parent's siblings
+  int32_t* row_k;   // [rows] sibling index of a row within its parent
+  int32_t* tiles;   // [rows][SIB] rows of each tile
+  int32_t* tile_n;  // [rows] rows in each tile
+  int32_t* ntiles;  // [1]
+};
+
+__global__ void grp_count_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    g.row_k[r] = pos[r] > 0 ? atomicAdd(g.cnt + l.s_parent[slots[r]], 1) : 0;
+}
+
+__global__ void grp_base_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n,
+                                int SIB) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (pos[r] == 0) {  // the BOS row: no chain to share, a tile of its own
+      const int t = atomicAdd(g.ntiles, 1);
+      g.tiles[(size_t)t * SIB] = r;
+      g.tile_n[t] = 1;
+    } else if (g.row_k[r] == 0) {
+      const int p = l.s_parent[slots[r]];
+      g.base[p] = atomicAdd(g.ntiles, (g.cnt[p] + SIB - 1) / SIB);
+    }
+  }
+}
+
+__global__ void grp_fill_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n,
+                                int SIB) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (pos[r] == 0) continue;
+    const int p = l.s_parent[slots[r]], k = g.row_k[r];
+    const int t = g.base[p] + k / SIB;
+    g.tiles[(size_t)t * SIB + k % SIB] = r;
+    if (k % SIB == 0) g.tile_n[t] = min(SIB, g.cnt[p] - (k / SIB) * SIB);
+  }
+}
+
+__global__ void grp_reset_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    if (pos[r] > 0) g.cnt[l.s_parent[slots[r]]] = 0;
+}
+
+// One CTA per sibling tile, one warp per kv head.  M row m = sib * G + head-in-group.  The tile
+// walks a virtual sequence in 16-position chunks: the shared chain (positions 0 .. d-1, visible to
+// every row) followed by the siblings' own K/V rows (position d + i = sibling i, visible only to
+// sibling i's rows) -- for a single row exactly chain_attn_mma_kernel's positions 0 .. d.
+// grid = (tiles, kv-head groups).
+template <int HD, bool SPLIT, int nstages>
+__global__ void __launch_bounds__(128, 3) chain_attn_grp_kernel(LlmDev l, int layer, const void* qv,
+                                                             const int32_t* chains,
+                                                             const int32_t* pos, GrpDev gd,
+                                                             int SIB, float scale, bf16* out) {
+  pdl_wait();
+  const int tile = blockIdx.x;
+  constexpr int KK = HD / 16;
+  constexpr int NT = HD / 8;
+  extern __shared__ __align__(128) unsigned char attn_smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(attn_smem);
+  unsigned char* stages = attn_smem + 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, qd = lane & 3;
+  // blockIdx.y: a group of KH = blockDim.x / 32 kv heads (its slice of each cache row is staged)
+  const int NKV = l.NKV, KH = blockDim.x >> 5, h0 = blockIdx.y * KH, kvh = h0 + warp;
+  const int G = l.NH / NKV;
+  const int cnt = gd.tile_n[tile];
+  const int32_t* trow = gd.tiles + (size_t)tile * SIB;
+  const int d = pos[trow[0]];
+  const int pitchc = l.max_depth + 1;
+  const int32_t* ch = chains + (size_t)trow[0] * pitchc;  // shared chain: ch[0 .. d-1]
+  const int ghalf = NKV * HD * 2;                // bytes of one bf16 half of a cache row
+  const int grow = ghalf * (SPLIT ? 2 : 1);       // cache row: [hi] or [hi | lo], all kv heads
+  const int halfb = KH * HD * 2;                  // staged half: this CTA's kv heads
+  const int rowb = halfb * (SPLIT ? 2 : 1);
+  const int pitch = rowb + 16;
+  const int stage_bytes = 2 * MMA_CH * pitch;
+  const int nv = d + cnt;  // virtual positions: chain, then one own row per sibling
+  const int nch = (nv + MMA_CH - 1) / MMA_CH;
+  const unsigned char* kbase = reinterpret_cast<const unsigned char*>(l.kc) + (size_t)layer * l.cap * grow + h0 * HD * 2;
+  const unsigned char* vbase = reinterpret_cast<const unsigned char*>(l.vc) + (size_t)layer * l.cap * grow + h0 * HD * 2;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto chunk_n = [&](int c) { return min(MMA_CH, nv - c * MMA_CH); };
+  auto issue = [&](int c) {  // warp 0
+    const int st = c % nstages, cn = chunk_n(c);
+    unsigned char* kd = stages + (size_t)st * stage_bytes;
+    unsigned char* vd = kd + (size_t)MMA_CH * pitch;
+    if (lane == 0) mbar_expect_tx(&bars[st], (unsigned)(2 * cn * rowb));
+    __syncwarp();
+    if (lane < cn) {
+      const int v = c * MMA_CH + lane;
+      const size_t sl = v < d ? (size_t)ch[v] : (size_t)chains[(size_t)trow[v - d] * pitchc + d];
+      tma_bulk_g2s(kd + (size_t)lane * pitch, kbase + sl * grow, halfb, &bars[st]);
+      tma_bulk_g2s(vd + (size_t)lane * pitch, vbase + sl * grow, halfb, &bars[st]);
+      if (SPLIT) {
+        tma_bulk_g2s(kd + (size_t)lane * pitch + halfb, kbase + sl * grow + ghalf, halfb, &bars[st]);
+        tma_bulk_g2s(vd + (size_t)lane * pitch + halfb, vbase + sl * grow + ghalf, halfb, &bars[st]);
+      }
+    }
+  };
+  if (warp == 0) issue(0);
+  // Q fragments: A rows grp (a0, a2) and grp + 8 (a1, a3); row m -> sibling m / G, head m % G.
+  // Rows of missing siblings keep q = 0 (finite scores, never written).
+  uint32_t qa[KK][4], ql[SPLIT ? KK : 1][4];
+  int rsib[2];
+#pragma unroll
+  for (int hr = 0; hr < 2; ++hr) {
+    const int mrow = grp + 8 * hr;
+    const int sib = mrow / G;
+    rsib[hr] = sib;
+    const bool valid = sib < cnt;
+    const size_t qoff = valid ? ((size_t)trow[sib] * l.NH + (size_t)(kvh * G + mrow % G)) * HD : 0;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        const int col = kk * 16 + hlf * 8 + qd * 2;
+        uint32_t hi = 0u, lo = 0u;
+        if (valid) {
+          if (SPLIT) {
+            const float2 f = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(qv) + qoff + col);
+            const __nv_bfloat162 h = __floats2bfloat162_rn(f.x, f.y);
+            const float2 hf = __bfloat1622float2(h);
+            hi = *reinterpret_cast<const uint32_t*>(&h);
+            lo = pack_bf16(f.x - hf.x, f.y - hf.y);
+          } else {
+            hi = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const bf16*>(qv) + qoff + col);
+          }
+        }
+        qa[kk][hlf * 2 + hr] = hi;
+        if (SPLIT) ql[kk][hlf * 2 + hr] = lo;
+      }
+  }
+  float o[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  float mrun[2] = {-INFINITY, -INFINITY}, den[2] = {0.f, 0.f};
+  const int hoff = warp * HD * 2;
+  for (int c = 0; c < nch; ++c) {
+    if (nstages == 2 && warp == 0 && c + 1 < nch) issue(c + 1);
+    const int cn = chunk_n(c);
+    const int vown = d - c * MMA_CH;  // chunk index of sibling 0's own position
+    const int st = c % nstages;
+    unsigned char* ks = stages + (size_t)st * stage_bytes;
+    unsigned char* vs = ks + (size_t)MMA_CH * pitch;
+    if (cn < MMA_CH) {  // zero this warp's slices of the unused V rows (0 * stale NaN = NaN)
+      constexpr int U = HD / 4;
+      for (int i = lane; i < (MMA_CH - cn) * U; i += 32) {
+        unsigned char* rp = vs + (size_t)(cn + i / U) * pitch + hoff;
+        reinterpret_cast<uint2*>(rp)[i % U] = make_uint2(0u, 0u);
+        if (SPLIT) reinterpret_cast<uint2*>(rp + halfb)[i % U] = make_uint2(0u, 0u);
+      }
+    }
+    mbar_wait(&bars[st], (unsigned)((c / nstages) & 1));
+    __syncwarp();
+    float sc[2][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+      const unsigned char* kr = ks + (size_t)(t * 8 + grp) * pitch + hoff;
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk) {
+        uint32_t kb2[2];
+        kb2[0] = *reinterpret_cast<const uint32_t*>(kr + (kk * 16 + qd * 2) * 2);
+        kb2[1] = *reinterpret_cast<const uint32_t*>(kr + (kk * 16 + 8 + qd * 2) * 2);
+        mma_bf16_16816(sc[t], qa[kk], kb2);
+        if (SPLIT) {
+          uint32_t kl2[2];
+          kl2[0] = *reinterpret_cast<const uint32_t*>(kr + halfb + (kk * 16 + qd * 2) * 2);
+          kl2[1] = *reinterpret_cast<const uint32_t*>(kr + halfb + (kk * 16 + 8 + qd * 2) * 2);
+          mma_bf16_16816(sc[t], ql[kk], kb2);
+          mma_bf16_16816(sc[t], qa[kk], kl2);
+        }
+      }
+    }
+    // online softmax per row (hr 0: row grp, hr 1: row grp + 8)
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = t * 8 + qd * 2 + (e & 1), hr = e >> 1;
+        // chain positions are shared; position vown + i is sibling i's own row (rows of missing
+        // siblings see everything, finite and never written)
+        const bool vis = j < cn && (j < vown || rsib[hr] >= cnt || j == vown + rsib[hr]);
+        sc[t][e] = vis ? sc[t][e] * scale : -INFINITY;
+        mx[hr] = fmaxf(mx[hr], sc[t][e]);
+      }
+    float corr[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(FULLMASK, mx[hr], 1));
+      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(FULLMASK, mx[hr], 2));
+      const float mnew = fmaxf(mrun[hr], mx[hr]);
+      corr[hr] = __expf(mrun[hr] - mnew);
+      mrun[hr] = mnew;
+    }
+    float ps[2] = {0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        sc[t][e] = __expf(sc[t][e] - mrun[e >> 1]);
+        ps[e >> 1] += sc[t][e];
+      }
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      ps[hr] += __shfl_xor_sync(FULLMASK, ps[hr], 1);
+      ps[hr] += __shfl_xor_sync(FULLMASK, ps[hr], 2);
+      den[hr] = den[hr] * corr[hr] + ps[hr];
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      o[t][0] *= corr[0];
+      o[t][1] *= corr[0];
+      o[t][2] *= corr[1];
+      o[t][3] *= corr[1];
+    }
+    // P (A operand, 16 rows x 16 positions) from the S fragments (+ its lo part when split)
+    uint32_t pa[4], pl[4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(sc[t][2 * hr], sc[t][2 * hr + 1]);
+        pa[t * 2 + hr] = *reinterpret_cast<const uint32_t*>(&h);
+        if (SPLIT) {
+          const float2 hf = __bfloat1622float2(h);
+          pl[t * 2 + hr] = pack_bf16(sc[t][2 * hr] - hf.x, sc[t][2 * hr + 1] - hf.y);
+        }
+      }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < NT; t += 2) {
+      const int mi = lane >> 3, r = lane & 7;
+      const unsigned char* addr = vs + (size_t)((mi & 1) * 8 + r) * pitch + hoff + ((t + (mi >> 1)) * 8) * 2;
+      uint32_t vb4[4];
+      ldsm_x4_trans(vb4, addr);
+      const uint32_t b0[2] = {vb4[0], vb4[1]};
+      const uint32_t b1[2] = {vb4[2], vb4[3]};
+      mma_bf16_16816(o[t], pa, b0);
+      mma_bf16_16816(o[t + 1], pa, b1);
+      if (SPLIT) {
+        uint32_t vl4[4];
+        ldsm_x4_trans(vl4, addr + halfb);
+        const uint32_t c0[2] = {vl4[0], vl4[1]};
+        const uint32_t c1[2] = {vl4[2], vl4[3]};
+        mma_bf16_16816(o[t], pl, b0);
+        mma_bf16_16816(o[t + 1], pl, b1);
+        mma_bf16_16816(o[t], pa, c0);
+        mma_bf16_16816(o[t + 1], pa, c1);
+      }
+    }
+    __syncthreads();  // every warp is done with this stage before it is refilled
+    if (nstages == 1 && warp == 0 && c + 1 < nch) issue(c + 1);
+  }
+  const int W = l.NH * HD;
+#pragma unroll
+  for (int hr = 0; hr < 2; ++hr) {
+    const int mrow = grp + 8 * hr, sib = rsib[hr];
+    if (sib >= cnt) continue;
+    const float inv = 1.f / den[hr];
+    bf16* orow = out + (size_t)trow[sib] * W * (SPLIT ? 2 : 1) + (size_t)(kvh * G + mrow % G) * HD;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const float a = o[t][2 * hr] * inv, b = o[t][2 * hr + 1] * inv;
+      const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+      *reinterpret_cast<__nv_bfloat162*>(orow + t * 8 + qd * 2) = h;
+      if (SPLIT) {
+        const float2 hf = __bfloat1622float2(h);
+        *reinterpret_cast<__nv_bfloat162*>(orow + W + t * 8 + qd * 2) = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+      }
+    }
+  }
+}
+
 // gu[M][2F] = [gate | up] (bf16, or fp32 in split precision) -> out[M][F] = bf16(silu(gate) * up)
 // (split: hi|lo pairs [M][2F]); 8 columns per thread
 template <typename TI>
@@ -1574,6 +1861,12 @@ struct lb_llm {
   int64_t events = 0, waves = 0, rows = 0, cum = 0, max_wave_rows = 0;
   int32_t cur_nwaves = 0;
   std::vector<int64_t> wave_off, wave_rows;
+  // sibling tiles of the last eager forward chunk (lb_llm_wave_rows -> lb_llm_attention)
+  GrpDev grp{};
+  int64_t grp_cap = 0;  // rows the tile buffers hold
+  int32_t grp_rows = -1;
+  int32_t grp_tiles = 0;
+  const int32_t* grp_pos = nullptr;
 };
 
 #define CKL(expr)                                                                        \
@@ -1625,6 +1918,15 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     int _rc = launched(launch_pdl(__VA_ARGS__)); \
     if (_rc) return _rc;                      \
   } while (0)
+
+// LB_ATT_GROUP=0: per-row chain attention only (A/B switch)
+static bool att_group_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LB_ATT_GROUP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 static int check_err_flags(lb_llm* l) {
   int32_t err = 0;
@@ -1747,7 +2049,9 @@ int lb_llm_destroy(lb_llm* l) {
   void* ptrs[] = {x.s_parent, x.s_token, x.s_depth, x.s_fwd, x.s_cum, x.s_pun, x.s_lp, x.s_cumv,
                   x.s_plp, x.s_lse, x.s_h, x.kc, x.vc, x.htab, x.ctr, x.node_slot, x.nlist,
                   x.nlist_depth, x.fwd_list, x.cum_list, x.wave_slots, x.blk,
-                  l->d_tok_low, l->d_tok_cap, l->d_tok_low_off, l->d_tok_cap_off};
+                  l->d_tok_low, l->d_tok_cap, l->d_tok_low_off, l->d_tok_cap_off,
+                  l->grp.cnt, l->grp.base, l->grp.row_k, l->grp.tiles, l->grp.tile_n,
+                  l->grp.ntiles};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete l;
@@ -1849,6 +2153,7 @@ int lb_llm_wave_rows_async(lb_llm* l, int32_t rows_cap, int32_t* tokens, int32_t
   if (!l || !tokens || !positions || !slots || !chains) return lbh::set_error(LB_ERR_ARG, "null argument");
   if (rows_cap < 1) return lbh::set_error(LB_ERR_ARG, "rows_cap must be >= 1");
   const int grid = std::min(4 * 148, (rows_cap + 127) / 128);
+  l->grp_rows = -1;  // graph mode: per-row attention (the tile count is not known on the host)
   LAUNCH(wave_rows_async_kernel<<<grid, 128, 0, l->b->st>>>(l->dev, rows_cap, tokens, positions,
                                                             slots, chains));
   return LB_OK;
@@ -1870,8 +2175,47 @@ int lb_llm_wave_rows(lb_llm* l, int32_t wave, int64_t row0, int32_t n, int32_t* 
   if (row0 < 0 || n < 0 || row0 + n > l->wave_rows[wave]) return lbh::set_error(LB_ERR_ARG, "rows out of range");
   if (n == 0) return LB_OK;
   const int grid = std::min(4 * 148, (n + 127) / 128);
-  LAUNCH(wave_rows_kernel<<<grid, 128, 0, l->b->st>>>(l->dev, l->wave_off[wave] + row0, n, tokens,
-                                                      positions, slots, chains));
+  cudaStream_t st = l->b->st;
+  LAUNCH(wave_rows_kernel<<<grid, 128, 0, st>>>(l->dev, l->wave_off[wave] + row0, n, tokens,
+                                                positions, slots, chains));
+  l->grp_rows = -1;
+  if (!att_group_enabled()) return LB_OK;
+  // sibling tiles of this chunk for the grouped attention kernel
+  LlmDev& x = l->dev;
+  const int SIB = 16 / (x.NH / x.NKV);
+  GrpDev& g = l->grp;
+  if (!g.cnt) {
+    CKL(dalloc(&g.cnt, (size_t)x.cap));
+    CKL(dalloc(&g.base, (size_t)x.cap));
+    CKL(dalloc(&g.ntiles, 1));
+    CKL(cudaMemsetAsync(g.cnt, 0, (size_t)x.cap * 4, st));
+  }
+  if (l->grp_cap < n) {
+    cudaFree(g.row_k);
+    cudaFree(g.tiles);
+    cudaFree(g.tile_n);
+    g.row_k = g.tiles = g.tile_n = nullptr;
+    const int64_t want = std::max<int64_t>(n, 2 * l->grp_cap);
+    CKL(dalloc(&g.row_k, (size_t)want));
+    CKL(dalloc(&g.tiles, (size_t)want * SIB));
+    CKL(dalloc(&g.tile_n, (size_t)want));
+    l->grp_cap = want;
+  }
+  CKL(cudaMemsetAsync(g.ntiles, 0, 4, st));
+  LAUNCH(grp_count_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n));
+  LAUNCH(grp_base_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n, SIB));
+  LAUNCH(grp_fill_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n, SIB));
+  LAUNCH(grp_reset_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n));
+  // the tile count decides the kernel: grouping pays only when siblings share tiles (the
+  // final event of a batch: ~6 rows per parent); one small copy + sync per forward chunk
+  int32_t nt = 0;
+  CKL(cudaMemcpyAsync(&nt, g.ntiles, 4, cudaMemcpyDeviceToHost, st));
+  CKL(cudaStreamSynchronize(st));
+  l->grp_tiles = nt;
+  if ((int64_t)nt * 4 <= (int64_t)n * 3) {
+    l->grp_rows = n;
+    l->grp_pos = positions;
+  }
   return LB_OK;
 }
 
@@ -1981,6 +2325,36 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
     if (nst == 2) MMA_ATT_N(HDV, SV, 2); \
     else MMA_ATT_N(HDV, SV, 1);        \
   } while (0)
+    const bool grouped = l->grp_rows == M && l->grp_pos == pos;
+    if (grouped) {  // sibling tiles built by lb_llm_wave_rows for this chunk
+      const int SIB = 16 / G;
+      // kv heads per CTA: the largest group whose double-buffered stage fits ~70 KB, so three
+      // CTAs share an SM and the next chunk's gather overlaps this one's MMAs
+      int KH = x.NKV;
+      auto gstage = [&](int kh) { return 2 * MMA_CH * (kh * x.HD * 2 * (x.split ? 2 : 1) + 16); };
+      while (KH > 4 || (KH > 1 && 128 + 2 * gstage(KH) > 70 * 1024)) KH /= 2;  // <= 128 threads
+      if (const char* e = std::getenv("LB_ATT_KH")) KH = std::max(1, std::min(KH, atoi(e)));
+      const int gnst = 128 + 2 * gstage(KH) <= 100 * 1024 ? 2 : 1;
+      const int gsmem = 128 + gnst * gstage(KH);
+#define GRP_ATT_N(HDV, SV, NS)                                                                      \
+  do {                                                                                              \
+    CKL(cudaFuncSetAttribute(chain_attn_grp_kernel<HDV, SV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem)); \
+    LAUNCH_PDL((chain_attn_grp_kernel<HDV, SV, NS>), dim3(l->grp_tiles, x.NKV / KH), dim3(32 * KH), gsmem, st, x, layer, q, chains, pos, l->grp, SIB, scale, oo); \
+  } while (0)
+#define GRP_ATT(HDV, SV)               \
+  do {                                 \
+    if (gnst == 2) GRP_ATT_N(HDV, SV, 2); \
+    else GRP_ATT_N(HDV, SV, 1);        \
+  } while (0)
+      if (x.HD == 64) {
+        if (x.split) GRP_ATT(64, true); else GRP_ATT(64, false);
+      } else {
+        if (x.split) GRP_ATT(128, true); else GRP_ATT(128, false);
+      }
+#undef GRP_ATT
+#undef GRP_ATT_N
+      return LB_OK;
+    }
     if (x.HD == 64) {
       if (x.split) MMA_ATT(64, true); else MMA_ATT(64, false);
     } else {
