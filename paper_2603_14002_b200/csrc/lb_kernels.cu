@@ -52,6 +52,10 @@ __device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -372,9 +376,9 @@ __device__ __forceinline__ CompHdr comp_hdr(const int32_t* row, int V) {
   return CompHdr{row[V], row[V + 1], row[V + 2], row[V + 3], row[V + 4], row[V + 5]};
 }
 
-// The same header from a compact lexicon record (the CSR offset is read only for >2 surfaces).
-__device__ __forceinline__ CompHdr lex_hdr(const ModelDev& m, const LexRec& r, int state) {
-  return CompHdr{r.ns, r.ns > 2 ? __ldg(m.comp_off + state) : 0, r.s0, r.l0, r.s1, r.l1};
+// The same header from a compact lexicon record and the beam's staged CSR offset.
+__device__ __forceinline__ CompHdr small_hdr(const LexRec& r, int off) {
+  return CompHdr{r.ns, off, r.s0, r.l0, r.s1, r.l1};
 }
 
 // apply_ngram (decoder.py:182-235) for one beam, one full warp.  Candidates are the
@@ -1426,7 +1430,8 @@ constexpr int O_KEEP = O_BSEL + KC * 16;
 constexpr int O_POFF = O_KEEP + 16;
 constexpr int O_PRES = O_POFF + ((KC + 1) * 4 + 15) / 16 * 16;
 constexpr int O_NFP = O_PRES + PC * (int)sizeof(PairRes);
-constexpr int O_QINFO = O_NFP + KC * 4;  // int4 per speculative pair: (entry, word, surface, -)
+constexpr int O_LOFF = O_NFP + KC * 4;  // completion CSR offset of each beam's prefix state
+constexpr int O_QINFO = O_LOFF + KC * 4;  // int4 per speculative pair: (entry, word, surface, -)
 constexpr int TOTAL = O_QINFO + PC * 16;
 static_assert(O_BEAM % 16 == 0 && O_CVAL % 16 == 0 && O_PRES % 16 == 0 && BEAM_BYTES % 16 == 0,
               "16-byte alignment");
@@ -1597,6 +1602,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   int32_t* ppoff = reinterpret_cast<int32_t*>(sm + O_POFF);
   PairRes* pres = reinterpret_cast<PairRes*>(sm + O_PRES);
   uint32_t* nfp = reinterpret_cast<uint32_t*>(sm + O_NFP);  // hash-lane fingerprints (recombination)
+  int32_t* loff = reinterpret_cast<int32_t*>(sm + O_LOFF);   // comp_off[prefix] per beam
   Ent* gbents = reinterpret_cast<Ent*>(gs + G_BENTS);
   WarpScratch* wsc = reinterpret_cast<WarpScratch*>(gs + G_WARP);
 
@@ -1649,6 +1655,7 @@ __global__ void __launch_bounds__(small::NT, 2)
       C_PRE[i] = b.prefix[hb + i];
       C_NENT[i] = b.nent[hb + i];
       const LexRec* src = m.lex + b.prefix[hb + i];
+      cp_async4(&loff[i], m.comp_off + b.prefix[hb + i]);
       cp_async16(&lrow[i], src);
       cp_async16(reinterpret_cast<char*>(&lrow[i]) + 16, reinterpret_cast<const char*>(src) + 16);
     }
@@ -1763,29 +1770,37 @@ __global__ void __launch_bounds__(small::NT, 2)
         tg = tn;
       }
       {
-        // pair table: each parent writes its own (entry, surface) pairs in creation order
-        // q = q0 + e * ns + s.  Parents are in score order; when the pairs exceed PC only the
-        // leading parents whose pairs all fit are speculated (s_ngcov = their pair count), the
-        // rest take the warp path after S4
+        // pair table, one pair per thread (balanced: a parent may carry dozens of homophone
+        // pairs): pair q of parent p = (entry e, surface s) with q = ppoff[p] + e * ns + s, the
+        // creation order.  Parents are in score order; when the pairs exceed PC only the leading
+        // parents whose pairs all fit are speculated (s_ngcov = their pair count), the rest take
+        // the warp path after S4
         int4* qinfo = reinterpret_cast<int4*>(sm + O_QINFO);
-        if (q1 > SCAP) {
-          if (q0 <= SCAP) s_ngcov = q0;  // the first parent that does not fit (unique)
-        } else if (np > 0) {
-          const CompHdr ch = lex_hdr(m, lrow[p], C_PRE[p]);
-          for (int sidx = 0; sidx < ns; ++sidx) {
-            int w, surf;
-            if (sidx == 0) {
-              w = ch.l0;
-              surf = ch.s0;
-            } else if (sidx == 1) {
-              w = ch.l1;
-              surf = ch.s1;
-            } else {
-              w = __ldg(m.comp_lm + ch.off + sidx);
-              surf = __ldg(m.comp_surf + ch.off + sidx);
-            }
-            for (int e = 0; e < nent; ++e) qinfo[q0 + e * ns + sidx] = make_int4(p * OC + e, w, surf, 0);
+        if (q1 > SCAP && q0 <= SCAP) s_ngcov = q0;  // the first parent that does not fit (unique)
+        bar_sync(3, NGT);
+        const int PC0 = s_ngcov;
+        for (int q = gt; q < PC0; q += NGT) {
+          int lo = 0, hi = K - 1;  // the parent: last p with ppoff[p] <= q
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (ppoff[mid] <= q) lo = mid;
+            else hi = mid - 1;
           }
+          const LexRec& lr = lrow[lo];
+          const int local = q - ppoff[lo];
+          const int e = local / lr.ns, sidx = local - e * lr.ns;
+          int w, surf;
+          if (sidx == 0) {
+            w = lr.l0;
+            surf = lr.s0;
+          } else if (sidx == 1) {
+            w = lr.l1;
+            surf = lr.s1;
+          } else {
+            w = __ldg(m.comp_lm + loff[lo] + sidx);
+            surf = __ldg(m.comp_surf + loff[lo] + sidx);
+          }
+          qinfo[q] = make_int4(lo * OC + e, w, surf, 0);
         }
         bar_sync(3, NGT);
         const int PCOV = s_ngcov;
@@ -2158,7 +2173,7 @@ __global__ void __launch_bounds__(small::NT, 2)
             const int p = npar[j];
             int outn = -1;
             double sc = nscore[j];
-            warp_apply_ngram(m, c, b, trial, C_ENTS + p * OC, C_NENT[p], lex_hdr(m, lrow[p], C_PRE[p]),
+            warp_apply_ngram(m, c, b, trial, C_ENTS + p * OC, C_NENT[p], small_hdr(lrow[p], loff[p]),
                              &wsc[warp], gbents + (size_t)j * OC, &outn, &sc, &s_ncount, &s_fail,
                              calls_l, probes_l);
             if (lane == 0) {
@@ -2278,6 +2293,7 @@ __global__ void __launch_bounds__(small::NT, 2)
             if (r < 2)
               cp_async16_ca(reinterpret_cast<char*>(&lrow[pos]) + 16 * r,
                             reinterpret_cast<const char*>(m.lex + npre[i]) + 16 * r);
+            if (r == G - 1) cp_async4(&loff[pos], m.comp_off + npre[i]);
           }
           cp_async_commit();
           cp_async_wait_all();
