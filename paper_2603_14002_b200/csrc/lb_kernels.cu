@@ -1862,6 +1862,39 @@ __global__ void __launch_bounds__(small::NT, 2)
       const unsigned lpb = (unsigned)(lp - cv0) < (unsigned)TBK ? 1u << (lp - cv0) : 0u;
       const unsigned bbits = tk_phon & ~lpb;
       const unsigned abits = tk_blank | (lpb & tk_inv);
+      // F1 (materialise selected beam j from its (value, key)): hash lanes, last token, next
+      // prefix state (and an L1 prefetch of its lexicon record), word-boundary list.  No
+      // n-gram results are needed, so it runs while the speculative n-gram warps still probe.
+      auto materialise = [&](int j, double x, uint32_t f) {
+        const int p = (int)(f >> 8);
+        const int tok = (int)(f & 0xFFu);
+        const int lp = C_LAST[p], pp = C_PRE[p];
+        const bool emit = (tok != blank) && (tok != lp);
+        uint64_t a1 = C_H1[p], a2 = C_H2[p];
+        int np = pp;
+        if (emit) {
+          a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
+          a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
+          const LexRec& lr = lrow[p];
+          if (m.lex_contig) {  // breadth-first trie: first child + rank, space -> root
+            const unsigned long long ms = lr.mask & ~(1ull << space);
+            np = tok == space ? 0 : lr.base + __popcll(ms & ((1ull << tok) - 1ull));
+          } else {
+            np = __ldg(m.lex_next + lr.base + __popcll(lr.mask & ((1ull << tok) - 1ull)));
+          }
+        }
+        // warm L1 with the next frame's lexicon record (gathered by cp.async.ca at the scatter)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(m.lex + np));
+        if (emit && tok == space) blist[atomicAdd(&s_nb, 1)] = j;
+        nscore[j] = x;
+        nh1[j] = a1;
+        nh2[j] = a2;
+        nfp[j] = hash_fp(a1, a2);
+        nlast[j] = (tok == blank) ? lp : tok;
+        npre[j] = np;
+        npar[j] = p;
+        bsel[j] = make_int4(-1, 0, 0, 0);
+      };
       LB_PHASE(0);
 
       // ---- A: candidates of parent cp for its TBK tokens; bins kept in registers.  Branch-free
@@ -2006,66 +2039,25 @@ __global__ void __launch_bounds__(small::NT, 2)
               const double vq = cval[q];
               r += (vq > va) || (vq == va && ckey[q] < ka);
             }
-            if (r < nsel) {
-              sval[r] = va;
-              skey[r] = ka;
-            }
+            if (r < nsel) materialise(r, va, ka);  // F1 fused into the ranking
           }
         } else {
           ++st_fallback;
           nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, thr, blank, space, lrow, C_LAST,
                                        C_SCORE, drow, hist, cval, ckey, sval, skey, &s_inr,
                                        &s_cnt2);
+          bar_sync(1, NC);  // the exact selection is visible to every compute warp
+          for (int j = lane * NWC + warp; j < nsel; j += NC) materialise(j, sval[j], skey[j]);
         }
       }
-      LB_ARR(3);
-      bar_sync(1, NC);  // S3: the selection is visible to every compute warp
-      LB_REL(3);
       LB_PHASE(3);
-      // ---- F1: materialise survivors (no n-gram results needed yet: the speculative n-gram
-      // warps may still be probing).  Selected beams spread over all compute warps
-      // (j = lane * NWC + warp); word-boundary beams are listed for F2 with their acoustic score.
-      if (!dead) {
-        for (int j = lane * NWC + warp; j < nsel; j += NC) {
-          const double x = sval[j];
-          const uint32_t f = skey[j];
-          const int p = (int)(f >> 8);
-          const int tok = (int)(f & 0xFFu);
-          const int lp = C_LAST[p], pp = C_PRE[p];
-          const bool emit = (tok != blank) && (tok != lp);
-          uint64_t a1 = C_H1[p], a2 = C_H2[p];
-          int np = pp;
-          if (emit) {
-            a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
-            a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
-            const LexRec& lr = lrow[p];
-            if (m.lex_contig) {  // breadth-first trie: first child + rank, space -> root
-              const unsigned long long ms = lr.mask & ~(1ull << space);
-              np = tok == space ? 0 : lr.base + __popcll(ms & ((1ull << tok) - 1ull));
-            } else {
-              np = __ldg(m.lex_next + lr.base + __popcll(lr.mask & ((1ull << tok) - 1ull)));
-            }
-          }
-          // warm L1 with the next frame's lexicon record (gathered by cp.async.ca at the scatter)
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(m.lex + np));
-          if (emit && tok == space) blist[atomicAdd(&s_nb, 1)] = j;
-          nscore[j] = x;
-          nh1[j] = a1;
-          nh2[j] = a2;
-          nfp[j] = hash_fp(a1, a2);
-          nlast[j] = (tok == blank) ? lp : tok;
-          npre[j] = np;
-          npar[j] = p;
-          bsel[j] = make_int4(-1, 0, 0, 0);
-        }
-      }
       LB_ARR(9);
       bar_sync(2, NT);  // S3b: speculative n-gram results ready (+ F1 visible)
       if (timing && tid == 0) {  // n-gram warps' and compute warps' arrival since frame start
         const unsigned tnow = (unsigned)clock();
         ph[17] += s_tarr[8] + s_tbase - tfs;
         ph[18] += s_tarr[9] + s_tbase - tfs;
-        ph[24] += s_tarr[9] + s_tbase - trel;  // F1 (compute warps)
+        ph[24] += s_tarr[9] + s_tbase - trel;  // ranking + F1 (compute warps)
         ph[25] += tnow - (s_tarr[9] + s_tbase);  // waiting for the n-gram warps + release
         trel = tnow;
         s_tarr[8] = 0;
