@@ -48,10 +48,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -1405,24 +1401,25 @@ constexpr int LC = 280, PC = 80, SCHUNK = 4;
 constexpr int NC = 256, NWC = NC / 32, NT = NC + NGT;
 constexpr int TBK = VC / 4;  // candidate tokens per thread: 4 threads per parent
 static_assert(KC * 4 == NC && TBK % 4 == 0, "candidate mapping: one parent per 4 threads");
+// Beam state by slot (double-buffered by frame parity): beams live in the slot their selection
+// gave them (slot j = rank j of the frame's top-k selection); JMAP lists the slots of the kept
+// beams in post-fusion score order, so parent p of the next frame is slot JMAP[p] -- no beam is
+// moved at the end of a frame.  LROW / LOFF: the lexicon record and completion-CSR offset of a
+// beam's prefix state, gathered by cp.async as soon as the beam is materialised.
 constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8,
               B_PRE = 3 * KC * 8 + KC * 4, B_NENT = 3 * KC * 8 + 2 * KC * 4,
-              B_ENTS = 3 * KC * 8 + 3 * KC * 4;
+              B_JMAP = 3 * KC * 8 + 3 * KC * 4, B_LOFF = B_JMAP + KC * 4, B_LROW = B_LOFF + KC * 4,
+              B_ENTS = B_LROW + KC * (int)sizeof(LexRec);
+static_assert(B_LROW % 16 == 0 && B_ENTS % 16 == 0, "16-byte aligned beam arrays");
 constexpr int BEAM_BYTES = B_ENTS + KC * OC * (int)sizeof(Ent);
 constexpr int O_DBUF = 0;
-constexpr int O_ROWS = O_DBUF + 2 * SCHUNK * VPDC * 8;
-constexpr int O_BEAM = O_ROWS + KC * (int)sizeof(LexRec);  // one compact lexicon record per beam
+constexpr int O_BEAM = O_DBUF + 2 * SCHUNK * VPDC * 8;
 constexpr int O_CVAL = O_BEAM + 2 * BEAM_BYTES;
 constexpr int O_CKEY = O_CVAL + LC * 8;
 constexpr int O_CBINL = O_CKEY + LC * 4;
 constexpr int O_SVAL = O_CBINL + LC * 2;
 constexpr int O_SKEY = O_SVAL + KC * 8;
-constexpr int O_NSCORE = O_SKEY + KC * 4;
-constexpr int O_NH1 = O_NSCORE + KC * 8;
-constexpr int O_NH2 = O_NH1 + KC * 8;
-constexpr int O_NLAST = O_NH2 + KC * 8;
-constexpr int O_NPRE = O_NLAST + KC * 4;
-constexpr int O_NPAR = O_NPRE + KC * 4;
+constexpr int O_NPAR = O_SKEY + KC * 4;
 constexpr int O_RANK = O_NPAR + KC * 4;
 constexpr int O_BLIST = O_RANK + KC * 4;
 constexpr int O_BSEL = O_BLIST + KC * 4;
@@ -1430,14 +1427,12 @@ constexpr int O_KEEP = O_BSEL + KC * 16;
 constexpr int O_POFF = O_KEEP + 16;
 constexpr int O_PRES = O_POFF + ((KC + 1) * 4 + 15) / 16 * 16;
 constexpr int O_NFP = O_PRES + PC * (int)sizeof(PairRes);
-constexpr int O_LOFF = O_NFP + KC * 4;  // completion CSR offset of each beam's prefix state
-constexpr int O_QINFO = O_LOFF + KC * 4;  // int4 per speculative pair: (entry, word, surface, -)
+constexpr int O_QINFO = O_NFP + KC * 4;  // int4 per speculative pair: (entry slot, word, surface, -)
 constexpr int TOTAL = O_QINFO + PC * 16;
 static_assert(O_BEAM % 16 == 0 && O_CVAL % 16 == 0 && O_PRES % 16 == 0 && BEAM_BYTES % 16 == 0,
               "16-byte alignment");
-// global scratch per trial: entries of boundary beams on the rare overflow path + warp scratch
-constexpr int G_BENTS = 0;
-constexpr int G_WARP = KC * OC * (int)sizeof(Ent);
+// global scratch per trial: the warp path's top-o lists
+constexpr int G_WARP = 0;
 constexpr int GTOTAL = G_WARP + NWC * (int)sizeof(WarpScratch);
 }  // namespace small
 
@@ -1451,7 +1446,8 @@ constexpr int GTOTAL = G_WARP + NWC * (int)sizeof(WarpScratch);
 // Called by all NC compute threads; returns nsel with sval/skey in (value desc, index asc) order.
 __device__ LB_COLD int small_fallback_select(const int ck, const double cbeta, const double cgamma,
                                              int K, int V, double thr,
-                                             int blank, int space, const LexRec* lrow,
+                                             int blank, int space, const int32_t* jmap,
+                                             const LexRec* lrow,
                                              const int32_t* C_LAST, const double* C_SCORE,
                                              const double* drow, unsigned* hist, double* cval,
                                              uint32_t* ckey, double* sval, uint32_t* skey,
@@ -1462,9 +1458,10 @@ __device__ LB_COLD int small_fallback_select(const int ck, const double cbeta, c
   // ---- fallback: exact radix select on the 96-bit key (ord64(value), ~flat index)
   auto cval_at = [&](int f) -> double {
     const int p = f / V, v = f - (f / V) * V;
-    const int lp = C_LAST[p];
-    if (!(((lrow[p].mask >> v) & 1ull) || (v == blank) || (v == lp))) return -DBL_MAX;
-    const double x = cand_value(C_SCORE[p], drow[v], v, lp,
+    const int jp = jmap[p];
+    const int lp = C_LAST[jp];
+    if (!(((lrow[jp].mask >> v) & 1ull) || (v == blank) || (v == lp))) return -DBL_MAX;
+    const double x = cand_value(C_SCORE[jp], drow[v], v, lp,
                                 FrameConsts{cbeta, cgamma, blank, space});
     return x > GUARD ? x : -DBL_MAX;
   };
@@ -1583,27 +1580,21 @@ __global__ void __launch_bounds__(small::NT, 2)
   char* gs = b.gscratch + (int64_t)trial * b.gscratch_stride;
 
   double* dbuf = reinterpret_cast<double*>(sm + O_DBUF);
-  LexRec* lrow = reinterpret_cast<LexRec*>(sm + O_ROWS);  // lexicon record of each beam's prefix
   double* cval = reinterpret_cast<double*>(sm + O_CVAL);
   uint32_t* ckey = reinterpret_cast<uint32_t*>(sm + O_CKEY);
   uint16_t* cbinl = reinterpret_cast<uint16_t*>(sm + O_CBINL);
   double* sval = reinterpret_cast<double*>(sm + O_SVAL);
   uint32_t* skey = reinterpret_cast<uint32_t*>(sm + O_SKEY);
-  double* nscore = reinterpret_cast<double*>(sm + O_NSCORE);
-  uint64_t* nh1 = reinterpret_cast<uint64_t*>(sm + O_NH1);
-  uint64_t* nh2 = reinterpret_cast<uint64_t*>(sm + O_NH2);
-  int32_t* nlast = reinterpret_cast<int32_t*>(sm + O_NLAST);
-  int32_t* npre = reinterpret_cast<int32_t*>(sm + O_NPRE);
   int32_t* npar = reinterpret_cast<int32_t*>(sm + O_NPAR);
   int32_t* rankv = reinterpret_cast<int32_t*>(sm + O_RANK);
   int32_t* blist = reinterpret_cast<int32_t*>(sm + O_BLIST);
-  int4* bsel = reinterpret_cast<int4*>(sm + O_BSEL);  // {kept|-1|-2, node base, top01, top23}
+  // per slot: {kept pairs | -1 inherit | -2 warp path pending | -3 entries built, node base,
+  // top01, top23}
+  int4* bsel = reinterpret_cast<int4*>(sm + O_BSEL);
   uint32_t* keep = reinterpret_cast<uint32_t*>(sm + O_KEEP);
   int32_t* ppoff = reinterpret_cast<int32_t*>(sm + O_POFF);
   PairRes* pres = reinterpret_cast<PairRes*>(sm + O_PRES);
   uint32_t* nfp = reinterpret_cast<uint32_t*>(sm + O_NFP);  // hash-lane fingerprints (recombination)
-  int32_t* loff = reinterpret_cast<int32_t*>(sm + O_LOFF);   // comp_off[prefix] per beam
-  Ent* gbents = reinterpret_cast<Ent*>(gs + G_BENTS);
   WarpScratch* wsc = reinterpret_cast<WarpScratch*>(gs + G_WARP);
 
   // beam buffers selected by parity: cur = buffer `par`, nxt = buffer `par ^ 1`
@@ -1623,6 +1614,12 @@ __global__ void __launch_bounds__(small::NT, 2)
 #define X_PRE ((int32_t*)(BUF(par ^ 1) + B_PRE))
 #define X_NENT ((int32_t*)(BUF(par ^ 1) + B_NENT))
 #define X_ENTS ((Ent*)(BUF(par ^ 1) + B_ENTS))
+#define C_JMAP ((int32_t*)(BUF(par) + B_JMAP))
+#define C_LOFF ((int32_t*)(BUF(par) + B_LOFF))
+#define C_LROW ((LexRec*)(BUF(par) + B_LROW))
+#define X_JMAP ((int32_t*)(BUF(par ^ 1) + B_JMAP))
+#define X_LOFF ((int32_t*)(BUF(par ^ 1) + B_LOFF))
+#define X_LROW ((LexRec*)(BUF(par ^ 1) + B_LROW))
 
   const int V = m.V, VPD = b.VPD, O = c.O, KC_ = b.K;
   const double ibw = c.inv_binw;
@@ -1654,10 +1651,11 @@ __global__ void __launch_bounds__(small::NT, 2)
       C_LAST[i] = b.last[hb + i];
       C_PRE[i] = b.prefix[hb + i];
       C_NENT[i] = b.nent[hb + i];
+      C_JMAP[i] = i;
       const LexRec* src = m.lex + b.prefix[hb + i];
-      cp_async4(&loff[i], m.comp_off + b.prefix[hb + i]);
-      cp_async16(&lrow[i], src);
-      cp_async16(reinterpret_cast<char*>(&lrow[i]) + 16, reinterpret_cast<const char*>(src) + 16);
+      cp_async4(&C_LOFF[i], m.comp_off + b.prefix[hb + i]);
+      cp_async16(&C_LROW[i], src);
+      cp_async16(reinterpret_cast<char*>(&C_LROW[i]) + 16, reinterpret_cast<const char*>(src) + 16);
     }
     cp_async_commit();
     for (int i = tid; i < K * O; i += NT) {
@@ -1744,9 +1742,10 @@ __global__ void __launch_bounds__(small::NT, 2)
       const int p = gt;
       int np = 0, ns = 0, nent = 0;
       if (p < K) {
-        ns = lrow[p].ns;
-        nent = C_NENT[p];
-        if (ns > 0 && C_LAST[p] != space) np = nent * ns;
+        const int jp = C_JMAP[p];
+        ns = C_LROW[jp].ns;
+        nent = C_NENT[jp];
+        if (ns > 0 && C_LAST[jp] != space) np = nent * ns;
       }
       int incl = np;
       for (int o = 1; o < 32; o <<= 1) {
@@ -1786,7 +1785,8 @@ __global__ void __launch_bounds__(small::NT, 2)
             if (ppoff[mid] <= q) lo = mid;
             else hi = mid - 1;
           }
-          const LexRec& lr = lrow[lo];
+          const int jlo = C_JMAP[lo];
+          const LexRec& lr = C_LROW[jlo];
           const int local = q - ppoff[lo];
           const int e = local / lr.ns, sidx = local - e * lr.ns;
           int w, surf;
@@ -1797,10 +1797,10 @@ __global__ void __launch_bounds__(small::NT, 2)
             w = lr.l1;
             surf = lr.s1;
           } else {
-            w = __ldg(m.comp_lm + loff[lo] + sidx);
-            surf = __ldg(m.comp_surf + loff[lo] + sidx);
+            w = __ldg(m.comp_lm + C_LOFF[jlo] + sidx);
+            surf = __ldg(m.comp_surf + C_LOFF[jlo] + sidx);
           }
-          qinfo[q] = make_int4(lo * OC + e, w, surf, 0);
+          qinfo[q] = make_int4(jlo * OC + e, w, surf, 0);
         }
         bar_sync(3, NGT);
         const int PCOV = s_ngcov;
@@ -1854,8 +1854,9 @@ __global__ void __launch_bounds__(small::NT, 2)
       // per-thread parent constants (thread -> parent cp, tokens cv0 .. cv0 + TBK - 1)
       const bool pin = cp < K;
       const int pcl = pin ? cp : 0;
-      const int lp = C_LAST[pcl];
-      const double sp = C_SCORE[pcl];
+      const int jcl = C_JMAP[pcl];
+      const int lp = C_LAST[jcl];
+      const double sp = C_SCORE[jcl];
       const double gsel = lp != space ? g_on : g_off;
       // token classes of this frame: bonus bits (phoneme, not a repeat of lp) and the tokens
       // that are always allowed (blank, the repeat of lp; lexicon.py:124-137)
@@ -1868,14 +1869,15 @@ __global__ void __launch_bounds__(small::NT, 2)
       auto materialise = [&](int j, double x, uint32_t f) {
         const int p = (int)(f >> 8);
         const int tok = (int)(f & 0xFFu);
-        const int lp = C_LAST[p], pp = C_PRE[p];
+        const int jp = C_JMAP[p];
+        const int lp = C_LAST[jp], pp = C_PRE[jp];
         const bool emit = (tok != blank) && (tok != lp);
-        uint64_t a1 = C_H1[p], a2 = C_H2[p];
+        uint64_t a1 = C_H1[jp], a2 = C_H2[jp];
         int np = pp;
         if (emit) {
           a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
           a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
-          const LexRec& lr = lrow[p];
+          const LexRec& lr = C_LROW[jp];
           if (m.lex_contig) {  // breadth-first trie: first child + rank, space -> root
             const unsigned long long ms = lr.mask & ~(1ull << space);
             np = tok == space ? 0 : lr.base + __popcll(ms & ((1ull << tok) - 1ull));
@@ -1883,15 +1885,19 @@ __global__ void __launch_bounds__(small::NT, 2)
             np = __ldg(m.lex_next + lr.base + __popcll(lr.mask & ((1ull << tok) - 1ull)));
           }
         }
-        // warm L1 with the next frame's lexicon record (gathered by cp.async.ca at the scatter)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(m.lex + np));
+        // the next frame's lexicon record and completion-CSR offset of slot j (waited for at
+        // the end of the frame)
+        cp_async16(&X_LROW[j], m.lex + np);
+        cp_async16(reinterpret_cast<char*>(&X_LROW[j]) + 16, reinterpret_cast<const char*>(m.lex + np) + 16);
+        cp_async4(&X_LOFF[j], m.comp_off + np);
+        cp_async_commit();
         if (emit && tok == space) blist[atomicAdd(&s_nb, 1)] = j;
-        nscore[j] = x;
-        nh1[j] = a1;
-        nh2[j] = a2;
+        X_SCORE[j] = x;
+        X_H1[j] = a1;
+        X_H2[j] = a2;
         nfp[j] = hash_fp(a1, a2);
-        nlast[j] = (tok == blank) ? lp : tok;
-        npre[j] = np;
+        X_LAST[j] = (tok == blank) ? lp : tok;
+        X_PRE[j] = np;
         npar[j] = p;
         bsel[j] = make_int4(-1, 0, 0, 0);
       };
@@ -1909,7 +1915,7 @@ __global__ void __launch_bounds__(small::NT, 2)
       double wm = -DBL_MAX;
       if (__any_sync(FULLMASK, pin)) {
         // allowed tokens (lexicon.py:124-137): a valid transition, the blank, or the repeat
-        const unsigned albits = ((unsigned)(lrow[pcl].mask >> cv0) & tk_inv) | abits;
+        const unsigned albits = ((unsigned)(C_LROW[jcl].mask >> cv0) & tk_inv) | abits;
 #pragma unroll
         for (int i = 0; i < TBK; ++i) {
           const double add = (i == tk_sidx) ? gsel : (((bbits >> i) & 1u) ? b_on : b_off);
@@ -2043,7 +2049,7 @@ __global__ void __launch_bounds__(small::NT, 2)
           }
         } else {
           ++st_fallback;
-          nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, thr, blank, space, lrow, C_LAST,
+          nsel = small_fallback_select(c.k, c.beta, c.gamma, K, V, thr, blank, space, C_JMAP, C_LROW, C_LAST,
                                        C_SCORE, drow, hist, cval, ckey, sval, skey, &s_inr,
                                        &s_cnt2);
           bar_sync(1, NC);  // the exact selection is visible to every compute warp
@@ -2074,7 +2080,7 @@ __global__ void __launch_bounds__(small::NT, 2)
         for (int bi = lane * NWC + warp; bi < nb0; bi += NC) {
           const int j = blist[bi];
           const int p = npar[j];
-          const double x = nscore[j];
+          const double x = X_SCORE[j];
           double sc = x;
           int4 bs = make_int4(-1, 0, 0, 0);
           {
@@ -2143,12 +2149,12 @@ __global__ void __launch_bounds__(small::NT, 2)
                   bs.y = base;
                   bs.z = (t0 & 0xFFFF) | ((kept > 1 ? t1 : 0) << 16);
                   bs.w = kept > 2 ? t2 : 0;
-                  sc = xadd(x, xsub(best, C_ENTS[p * OC].total));
+                  sc = xadd(x, xsub(best, C_ENTS[C_JMAP[p] * OC].total));
                 }
               }
             }
           }
-          nscore[j] = sc;
+          X_SCORE[j] = sc;
           bsel[j] = bs;
         }
         LB_PHASE(12);
@@ -2162,15 +2168,16 @@ __global__ void __launch_bounds__(small::NT, 2)
           for (int bi = warp; bi < nb; bi += NWC) {
             const int j = blist[bi];
             if (bsel[j].x != -2) continue;  // speculated parent
-            const int p = npar[j];
+            const int jp = C_JMAP[npar[j]];
             int outn = -1;
-            double sc = nscore[j];
-            warp_apply_ngram(m, c, b, trial, C_ENTS + p * OC, C_NENT[p], small_hdr(lrow[p], loff[p]),
-                             &wsc[warp], gbents + (size_t)j * OC, &outn, &sc, &s_ncount, &s_fail,
-                             calls_l, probes_l);
+            double sc = X_SCORE[j];
+            warp_apply_ngram(m, c, b, trial, C_ENTS + jp * OC, C_NENT[jp],
+                             small_hdr(C_LROW[jp], C_LOFF[jp]), &wsc[warp], X_ENTS + j * OC, &outn,
+                             &sc, &s_ncount, &s_fail, calls_l, probes_l);
             if (lane == 0) {
-              nscore[j] = sc;
-              bsel[j] = make_int4(outn >= 0 ? -2 - outn : -1, 0, 0, 0);  // -2-n: n entries in gbents
+              X_SCORE[j] = sc;
+              X_NENT[j] = max(outn, 0);
+              bsel[j] = make_int4(-3, 0, 0, 0);  // entries built in the slot
             }
           }
           if (timing && tid == 0) ph[19] += (unsigned)clock() - trel;
@@ -2187,19 +2194,19 @@ __global__ void __launch_bounds__(small::NT, 2)
           const int n = nsel;
           const int i = tid >> 2, r = tid & 3;
           const bool act = i < n;
-          const double si = act ? nscore[i] : 0.0;
-          const uint64_t a1 = act ? nh1[i] : 0ull, a2 = act ? nh2[i] : 0ull;
+          const double si = act ? X_SCORE[i] : 0.0;
+          const uint64_t a1 = act ? X_H1[i] : 0ull, a2 = act ? X_H2[i] : 0ull;
           // a 32-bit fingerprint of the hash lanes filters the exact 128-bit comparison
           const uint32_t fi = act ? nfp[i] : 0u;
           int cnt = 0, dup = 0;
 #pragma unroll
           for (int it = 0; it < KC / 4; ++it) {
             const int j = r + 4 * it;
-            const double sj = nscore[j];
+            const double sj = X_SCORE[j];
             const uint32_t fj = nfp[j];
             const bool ahead = (j < n) & ((sj > si) | ((sj == si) & (j < i)));
             cnt += ahead ? 1 : 0;
-            if (ahead & (fj == fi)) dup |= (nh1[j] == a1) & (nh2[j] == a2) ? 1 : 0;
+            if (ahead & (fj == fi)) dup |= (X_H1[j] == a1) & (X_H2[j] == a2) ? 1 : 0;
           }
           cnt += __shfl_xor_sync(FULLMASK, cnt, 1);
           dup |= __shfl_xor_sync(FULLMASK, dup, 1);
@@ -2209,40 +2216,14 @@ __global__ void __launch_bounds__(small::NT, 2)
             rankv[i] = cnt;
             if (si > GUARD && !dup) atomicOr(&keep[cnt >> 5], 1u << (cnt & 31));
           }
-        }
-        LB_ARR(5);
-        bar_sync(1, NC);  // S5
-        LB_REL(5);
-        LB_PHASE(6);
-        const unsigned kp0 = keep[0], kp1 = keep[1];
-        LB_PHASE(7);
-
-        // ---- scatter in rank order; boundary entries built from the chosen pairs;
-        // next frame's lexicon rows prefetched with cp.async
-        for (int i = tid; i < NBINS; i += NC) {
-          hist[i] = 0;
-          hfill[i] = 0;
-        }
-        const int newK = __popc(kp0) + __popc(kp1);
-        {
-          int G = 1;
-          while (G < 32 && 2 * G * nsel <= NC) G <<= 1;
-          const int groups = NC / G, g = tid / G, r = tid & (G - 1);
-          for (int i0 = 0; i0 < nsel; i0 += groups) {
-            const int i = i0 + g;
-            if (i >= nsel) continue;
-            const int rk = rankv[i];
-            const unsigned kw = rk >= 32 ? kp1 : kp0;
-            if (!((kw >> (rk & 31)) & 1u)) continue;
-            const int pos = __popc(kw & ((1u << (rk & 31)) - 1u)) + (rk >= 32 ? __popc(kp0) : 0);
+          // entries of live beam i into its slot (four threads): fresh word boundaries from the
+          // chosen speculative pairs, the rest inherit their parent's
+          if (act && si > GUARD) {
             const int4 bs = bsel[i];
-            Ent* dst = X_ENTS + pos * OC;
-            int cnt;
-            if (bs.x >= 0) {  // fresh word boundary: entries from the chosen pairs
-              cnt = bs.x;
-              for (int e = r; e < cnt; e += G) {
-                const int q = e == 0 ? (bs.z & 0xFFFF) : e == 1 ? (bs.z >> 16)
-                                                       : e == 2 ? (bs.w & 0xFFFF) : (bs.w >> 16);
+            Ent* dst = X_ENTS + i * OC;
+            if (bs.x >= 0) {
+              for (int e = r; e < bs.x; e += 4) {
+                const int q = e == 0 ? (bs.z & 0xFFFF) : e == 1 ? (bs.z >> 16) : (bs.w & 0xFFFF);
                 const PairRes& pr = pres[q];
                 WordScore sw;
                 sw.slen = pr.hlen;
@@ -2253,43 +2234,48 @@ __global__ void __launch_bounds__(small::NT, 2)
                 new_entry(dst[e], pr.total, pr.cum, sw, (uint32_t)(bs.y + e),
                           (uint32_t)(q - ppoff[npar[i]]), pr.depth);
               }
-            } else if (bs.x <= -2) {  // overflow path: entries in global scratch
-              cnt = -2 - bs.x;
-              const uint4* su = reinterpret_cast<const uint4*>(gbents + (size_t)i * OC);
+              if (r == 0) X_NENT[i] = bs.x;
+            } else if (bs.x == -1) {
+              const int jp = C_JMAP[npar[i]];
+              const int cnt_e = C_NENT[jp];
+              const uint4* su = reinterpret_cast<const uint4*>(C_ENTS + jp * OC);
               uint4* du = reinterpret_cast<uint4*>(dst);
-              for (int u = r; u < cnt * ENT_U4; u += G) du[u] = su[u];
-            } else {  // inherit the parent's entries
-              const int p = npar[i];
-              cnt = C_NENT[p];
-              const uint4* su = reinterpret_cast<const uint4*>(C_ENTS + p * OC);
-              uint4* du = reinterpret_cast<uint4*>(dst);
-              for (int u = r; u < cnt * ENT_U4; u += G) du[u] = su[u];
+              for (int u = r; u < cnt_e * ENT_U4; u += 4) du[u] = su[u];
+              if (r == 0) X_NENT[i] = cnt_e;
             }
-            if (r == 0) {
-              if (pos == 0) s_maxs = nscore[i];
-              X_SCORE[pos] = nscore[i];
-              X_H1[pos] = nh1[i];
-              X_H2[pos] = nh2[i];
-              X_LAST[pos] = nlast[i];
-              X_PRE[pos] = npre[i];
-              X_NENT[pos] = cnt;
-              if (b.dump_k) {
-                const size_t di = ((size_t)trial * b.Tmax + t) * KC_ + pos;
-                b.dump_h1[di] = nh1[i];
-                b.dump_h2[di] = nh2[i];
-                b.dump_pre[di] = npre[i];
-                b.dump_last[di] = nlast[i];
-                b.dump_score[di] = nscore[i];
-              }
-            }
-            if (r < 2)
-              cp_async16_ca(reinterpret_cast<char*>(&lrow[pos]) + 16 * r,
-                            reinterpret_cast<const char*>(m.lex + npre[i]) + 16 * r);
-            if (r == G - 1) cp_async4(&loff[pos], m.comp_off + npre[i]);
           }
-          cp_async_commit();
-          cp_async_wait_all();
         }
+        LB_ARR(5);
+        bar_sync(1, NC);  // S5
+        LB_REL(5);
+        LB_PHASE(6);
+        const unsigned kp0 = keep[0], kp1 = keep[1];
+        LB_PHASE(7);
+
+        // ---- order: the kept beams' slots in rank order become the next frame's parents (no
+        // beam moves); then this frame's lexicon-record gathers must have landed
+        for (int i = tid; i < NBINS; i += NC) {
+          hist[i] = 0;
+          hfill[i] = 0;
+        }
+        const int newK = __popc(kp0) + __popc(kp1);
+        for (int i = tid; i < nsel; i += NC) {
+          const int rk = rankv[i];
+          const unsigned kw = rk >= 32 ? kp1 : kp0;
+          if (!((kw >> (rk & 31)) & 1u)) continue;
+          const int pos = __popc(kw & ((1u << (rk & 31)) - 1u)) + (rk >= 32 ? __popc(kp0) : 0);
+          X_JMAP[pos] = i;
+          if (pos == 0) s_maxs = X_SCORE[i];
+          if (b.dump_k) {
+            const size_t di = ((size_t)trial * b.Tmax + t) * KC_ + pos;
+            b.dump_h1[di] = X_H1[i];
+            b.dump_h2[di] = X_H2[i];
+            b.dump_pre[di] = X_PRE[i];
+            b.dump_last[di] = X_LAST[i];
+            b.dump_score[di] = X_SCORE[i];
+          }
+        }
+        cp_async_wait_all();
         if (b.dump_k && tid == 0) b.dump_k[(size_t)trial * b.Tmax + t] = newK;
         if (tid == 0) {
           s_K = newK;
@@ -2312,8 +2298,9 @@ __global__ void __launch_bounds__(small::NT, 2)
     // ---- optional interval fusion of the device n-gram scorer (decoder.py:428-430)
     if (fusion_mode == 1 && t > 0 && (t % c.r) == 0) {
       for (int i = tid; i < K; i += NT) {
-        Ent* e = C_ENTS + i * OC;
-        const int n = C_NENT[i];
+        const int ji = C_JMAP[i];
+        Ent* e = C_ENTS + ji * OC;
+        const int n = C_NENT[ji];
         const double prev = e[0].total;
         for (int q = 0; q < n; ++q) {
           if (e[q].node == 0) {
@@ -2324,12 +2311,12 @@ __global__ void __launch_bounds__(small::NT, 2)
           }
         }
         sort_entries(e, n);
-        C_SCORE[i] = xadd(C_SCORE[i], xsub(e[0].total, prev));
+        C_SCORE[ji] = xadd(C_SCORE[ji], xsub(e[0].total, prev));
       }
       __syncthreads();
       if (warp == 0) {
         double ms = -DBL_MAX;
-        for (int i = lane; i < K; i += 32) ms = fmax(ms, C_SCORE[i]);
+        for (int i = lane; i < K; i += 32) ms = fmax(ms, C_SCORE[C_JMAP[i]]);
         ms = warp_max(ms);
         if (lane == 0) s_maxs = ms;
       }
@@ -2358,16 +2345,18 @@ __global__ void __launch_bounds__(small::NT, 2)
   if (status == 0 || status == 4) {
     const size_t hb = (size_t)trial * KC_;
     for (int i = tid; i < K; i += NT) {
-      b.score[hb + i] = C_SCORE[i];
-      b.h1[hb + i] = C_H1[i];
-      b.h2[hb + i] = C_H2[i];
-      b.last[hb + i] = C_LAST[i];
-      b.prefix[hb + i] = C_PRE[i];
-      b.nent[hb + i] = C_NENT[i];
+      const int ji = C_JMAP[i];
+      b.score[hb + i] = C_SCORE[ji];
+      b.h1[hb + i] = C_H1[ji];
+      b.h2[hb + i] = C_H2[ji];
+      b.last[hb + i] = C_LAST[ji];
+      b.prefix[hb + i] = C_PRE[ji];
+      b.nent[hb + i] = C_NENT[ji];
     }
     for (int i = tid; i < K * O; i += NT) {
       const int bi = i / O, e = i - bi * O;
-      if (e < C_NENT[bi]) b.ents[hb * O + i] = C_ENTS[bi * OC + e];
+      const int jb = C_JMAP[bi];
+      if (e < C_NENT[jb]) b.ents[hb * O + i] = C_ENTS[jb * OC + e];
     }
   }
   atomicAdd(&s_calls, calls_l);
@@ -2400,6 +2389,12 @@ __global__ void __launch_bounds__(small::NT, 2)
 #undef X_PRE
 #undef X_NENT
 #undef X_ENTS
+#undef C_JMAP
+#undef C_LOFF
+#undef C_LROW
+#undef X_JMAP
+#undef X_LOFF
+#undef X_LROW
 }
 
 // =====================================================================================
