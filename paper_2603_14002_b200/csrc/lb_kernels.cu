@@ -1427,8 +1427,10 @@ constexpr int O_KEEP = O_BSEL + KC * 16;
 constexpr int O_POFF = O_KEEP + 16;
 constexpr int O_PRES = O_POFF + ((KC + 1) * 4 + 15) / 16 * 16;
 constexpr int O_NFP = O_PRES + PC * (int)sizeof(PairRes);
-constexpr int O_QINFO = O_NFP + KC * 4;  // int4 per speculative pair: (entry slot, word, surface, -)
-constexpr int TOTAL = O_QINFO + PC * 16;
+constexpr int O_QINFO = O_NFP + KC * 4;  // int4 per speculative pair: (entry slot, word, surface, parent)
+constexpr int O_PTOP = O_QINFO + PC * 16;  // int4 per parent: its top-o speculated pairs (-1: none)
+constexpr int O_PVAL = O_PTOP + KC * 16;   // per speculative pair: its new total, or -inf if killed
+constexpr int TOTAL = O_PVAL + PC * 8;
 static_assert(O_BEAM % 16 == 0 && O_CVAL % 16 == 0 && O_PRES % 16 == 0 && BEAM_BYTES % 16 == 0,
               "16-byte alignment");
 // global scratch per trial: the warp path's top-o lists
@@ -1800,7 +1802,7 @@ __global__ void __launch_bounds__(small::NT, 2)
             w = __ldg(m.comp_lm + C_LOFF[jlo] + sidx);
             surf = __ldg(m.comp_surf + C_LOFF[jlo] + sidx);
           }
-          qinfo[q] = make_int4(jlo * OC + e, w, surf, 0);
+          qinfo[q] = make_int4(jlo * OC + e, w, surf, lo);
         }
         bar_sync(3, NGT);
         const int PCOV = s_ngcov;
@@ -1836,7 +1838,25 @@ __global__ void __launch_bounds__(small::NT, 2)
             pr.depth = (uint16_t)(E.depth + 1);
             pr.hlen = (uint8_t)sw.slen;
             pres[q] = pr;
+            reinterpret_cast<double*>(sm + O_PVAL)[q] = pr.valid ? pr.total : -INFINITY;
           }
+        }
+        // each parent's top-o pairs (total desc, creation order asc: decoder.py:221-227), one
+        // pair per thread ranking itself among its parent's pairs, so F2 does no pair loop
+        int4* ptop = reinterpret_cast<int4*>(sm + O_PTOP);
+        if (p < K) ptop[p] = make_int4(-1, -1, -1, -1);
+        bar_sync(3, NGT);
+        const double* pval = reinterpret_cast<const double*>(sm + O_PVAL);
+        for (int q = gt; q < PCOV; q += NGT) {
+          const double tq = pval[q];
+          if (tq == -INFINITY) continue;  // killed pair (OOV without <unk>)
+          const int pp = qinfo[q].w, a0 = ppoff[pp], a1 = ppoff[pp + 1];
+          int rk = 0;
+          for (int q2 = a0; q2 < a1; ++q2) {
+            const double t2 = pval[q2];
+            rk += (t2 > tq || (t2 == tq && q2 < q)) ? 1 : 0;
+          }
+          if (rk < O) reinterpret_cast<int*>(&ptop[pp])[rk] = q;  // ortho_beams <= 3
         }
         if (ngtim) ph[22] += (unsigned)clock() - tg;
       }
@@ -2088,32 +2108,9 @@ __global__ void __launch_bounds__(small::NT, 2)
             if (ppoff[p + 1] > ncov) {
               bs.x = -2;
             } else {
-              const int q0 = ppoff[p], q1 = ppoff[p + 1];
-              // running top-O pair list (total desc, q asc) in three registers (OC == 3)
-              static_assert(OC == 3, "top-O registers");
-              int t0 = 0, t1 = 0, t2 = 0;
-              int ntop = 0;
-              for (int q = q0; q < q1; ++q) {
-                if (!pres[q].valid) continue;
-                const double tq = pres[q].total;
-                int pos = 0;
-                if (ntop > 0 && !(tq > pres[t0].total)) {
-                  pos = 1;
-                  if (ntop > 1 && !(tq > pres[t1].total)) pos = (ntop > 2 && !(tq > pres[t2].total)) ? 3 : 2;
-                }
-                if (pos >= O) continue;
-                if (pos == 0) {
-                  t2 = t1;
-                  t1 = t0;
-                  t0 = q;
-                } else if (pos == 1) {
-                  t2 = t1;
-                  t1 = q;
-                } else {
-                  t2 = q;
-                }
-                ntop = min(ntop + 1, O);
-              }
+              const int4 pt = reinterpret_cast<const int4*>(sm + O_PTOP)[p];
+              const int t0 = pt.x, t1 = pt.y, t2 = pt.z;
+              const int ntop = t0 < 0 ? 0 : t1 < 0 ? 1 : t2 < 0 ? 2 : 3;
               if (ntop == 0) {
                 sc = NEG_INF;  // decoder.py:223-225
               } else {
