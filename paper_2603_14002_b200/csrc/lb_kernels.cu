@@ -1567,7 +1567,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   __shared__ int hfill[NBINS];
   __shared__ double wmax[NWC];
   __shared__ double s_maxs;
-  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov, s_inr, s_cnt2;
+  __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov, s_inr, s_cnt2, s_nsel;
   __shared__ int ngtot[2];
   __shared__ unsigned s_calls, s_probes, s_pairs;
   __shared__ unsigned s_tarr[NBAR_EV], s_tbase;  // TIMING only
@@ -1862,6 +1862,21 @@ __global__ void __launch_bounds__(small::NT, 2)
       }
       LB_ARR(8);
       bar_arrive(2, NT);
+      // then, while the compute warps rank and recombine, copy the inherited entries of every
+      // live non-boundary beam into its slot (four threads per beam)
+      bar_sync(4, NT);  // F2 done
+      if (s_status == 0) {
+        const int nsl = s_nsel, r4 = gt & 3;
+        for (int i = gt >> 2; i < nsl; i += NGT / 4) {
+          if (bsel[i].x != -1 || !(X_SCORE[i] > GUARD)) continue;
+          const int jp = C_JMAP[npar[i]];
+          const int cnt_e = C_NENT[jp];
+          const uint4* su = reinterpret_cast<const uint4*>(C_ENTS + jp * OC);
+          uint4* du = reinterpret_cast<uint4*>(X_ENTS + i * OC);
+          for (int u = r4; u < cnt_e * ENT_U4; u += 4) du[u] = su[u];
+          if (r4 == 0) X_NENT[i] = cnt_e;
+        }
+      }
     } else {
       // ============================== compute warps ==============================
       if (cr == 0) {
@@ -2077,6 +2092,7 @@ __global__ void __launch_bounds__(small::NT, 2)
         }
       }
       LB_PHASE(3);
+      if (tid == 0) s_nsel = nsel;
       LB_ARR(9);
       bar_sync(2, NT);  // S3b: speculative n-gram results ready (+ F1 visible)
       if (timing && tid == 0) {  // n-gram warps' and compute warps' arrival since frame start
@@ -2090,6 +2106,7 @@ __global__ void __launch_bounds__(small::NT, 2)
         s_tarr[9] = 0;
       }
 
+      if (dead) bar_arrive(4, NT);
       if (!dead) {
         const int ncov = s_ngcov;
         const bool ngover = ncov < s_ngP;  // some parents' pairs were not speculated
@@ -2155,6 +2172,7 @@ __global__ void __launch_bounds__(small::NT, 2)
           bsel[j] = bs;
         }
         LB_PHASE(12);
+        bar_arrive(4, NT);  // the n-gram warps may copy inherited entries now
         LB_ARR(4);
         bar_sync(1, NC);  // S4
         LB_REL(4);
@@ -2213,8 +2231,8 @@ __global__ void __launch_bounds__(small::NT, 2)
             rankv[i] = cnt;
             if (si > GUARD && !dup) atomicOr(&keep[cnt >> 5], 1u << (cnt & 31));
           }
-          // entries of live beam i into its slot (four threads): fresh word boundaries from the
-          // chosen speculative pairs, the rest inherit their parent's
+          // entries of a fresh word boundary i into its slot (four threads) from the chosen
+          // speculative pairs; inherited entries are copied by the n-gram warps meanwhile
           if (act && si > GUARD) {
             const int4 bs = bsel[i];
             Ent* dst = X_ENTS + i * OC;
@@ -2232,13 +2250,6 @@ __global__ void __launch_bounds__(small::NT, 2)
                           (uint32_t)(q - ppoff[npar[i]]), pr.depth);
               }
               if (r == 0) X_NENT[i] = bs.x;
-            } else if (bs.x == -1) {
-              const int jp = C_JMAP[npar[i]];
-              const int cnt_e = C_NENT[jp];
-              const uint4* su = reinterpret_cast<const uint4*>(C_ENTS + jp * OC);
-              uint4* du = reinterpret_cast<uint4*>(dst);
-              for (int u = r; u < cnt_e * ENT_U4; u += 4) du[u] = su[u];
-              if (r == 0) X_NENT[i] = cnt_e;
             }
           }
         }
