@@ -1012,39 +1012,53 @@ struct GrpDev {
   int32_t* ntiles;  // [1]
 };
 
-__global__ void grp_count_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
-    g.row_k[r] = pos[r] > 0 ? atomicAdd(g.cnt + l.s_parent[slots[r]], 1) : 0;
+// rows r < n of a forward chunk: slots[r]; n from the host (nh >= 0) or the device's forward-set
+// count (nh < 0: planning, before the host knows it)
+__device__ __forceinline__ int grp_rows(const LlmDev& l, int nh) {
+  return nh >= 0 ? nh : (int)min((int64_t)l.ctr[C_NFWD], l.cap);
 }
 
-__global__ void grp_base_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n,
-                                int SIB) {
+__global__ void grp_count_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh) {
+  const int n = grp_rows(l, nh);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    if (pos[r] == 0) {  // the BOS row: no chain to share, a tile of its own
+    const int s = slots[r];
+    g.row_k[r] = l.s_depth[s] > 0 ? atomicAdd(g.cnt + l.s_parent[s], 1) : 0;
+  }
+}
+
+__global__ void grp_base_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int SIB) {
+  const int n = grp_rows(l, nh);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int s = slots[r];
+    if (l.s_depth[s] == 0) {  // the BOS row: no chain to share, a tile of its own
       const int t = atomicAdd(g.ntiles, 1);
       g.tiles[(size_t)t * SIB] = r;
       g.tile_n[t] = 1;
     } else if (g.row_k[r] == 0) {
-      const int p = l.s_parent[slots[r]];
+      const int p = l.s_parent[s];
       g.base[p] = atomicAdd(g.ntiles, (g.cnt[p] + SIB - 1) / SIB);
     }
   }
 }
 
-__global__ void grp_fill_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n,
-                                int SIB) {
+__global__ void grp_fill_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int SIB) {
+  const int n = grp_rows(l, nh);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    if (pos[r] == 0) continue;
-    const int p = l.s_parent[slots[r]], k = g.row_k[r];
+    const int s = slots[r];
+    if (l.s_depth[s] == 0) continue;
+    const int p = l.s_parent[s], k = g.row_k[r];
     const int t = g.base[p] + k / SIB;
     g.tiles[(size_t)t * SIB + k % SIB] = r;
     if (k % SIB == 0) g.tile_n[t] = min(SIB, g.cnt[p] - (k / SIB) * SIB);
   }
 }
 
-__global__ void grp_reset_kernel(LlmDev l, GrpDev g, const int32_t* slots, const int32_t* pos, int n) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
-    if (pos[r] > 0) g.cnt[l.s_parent[slots[r]]] = 0;
+__global__ void grp_reset_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh) {
+  const int n = grp_rows(l, nh);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int s = slots[r];
+    if (l.s_depth[s] > 0) g.cnt[l.s_parent[s]] = 0;
+  }
 }
 
 // One CTA per sibling tile, one warp per kv head.  M row m = sib * G + head-in-group.  The tile
@@ -1866,6 +1880,7 @@ struct lb_llm {
   int64_t grp_cap = 0;  // rows the tile buffers hold
   int32_t grp_rows = -1;
   int32_t grp_tiles = 0;
+  int32_t plan_tiles = -1;  // tiles of the current wave built during planning (-1: none)
   const int32_t* grp_pos = nullptr;
 };
 
@@ -1926,6 +1941,39 @@ static bool att_group_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+// Sibling tiles (see chain_attn_grp_kernel) of rows r < n of slots[]: n >= 0 from the host, or
+// n < 0 = the device's forward-set count (during planning).  Buffers hold cap_rows rows.
+static int grp_build(lb_llm* l, const int32_t* slots, int n, int64_t cap_rows) {
+  LlmDev& x = l->dev;
+  cudaStream_t st = l->b->st;
+  const int SIB = 16 / (x.NH / x.NKV);
+  GrpDev& g = l->grp;
+  if (!g.cnt) {
+    CKL(dalloc(&g.cnt, (size_t)x.cap));
+    CKL(dalloc(&g.base, (size_t)x.cap));
+    CKL(dalloc(&g.ntiles, 1));
+    CKL(cudaMemsetAsync(g.cnt, 0, (size_t)x.cap * 4, st));
+  }
+  if (l->grp_cap < cap_rows) {
+    cudaFree(g.row_k);
+    cudaFree(g.tiles);
+    cudaFree(g.tile_n);
+    g.row_k = g.tiles = g.tile_n = nullptr;
+    const int64_t want = std::max<int64_t>(cap_rows, 2 * l->grp_cap);
+    CKL(dalloc(&g.row_k, (size_t)want));
+    CKL(dalloc(&g.tiles, (size_t)want * SIB));
+    CKL(dalloc(&g.tile_n, (size_t)want));
+    l->grp_cap = want;
+  }
+  const int grid = n >= 0 ? std::max(1, std::min(4 * 148, (n + 127) / 128)) : 4 * 148;
+  CKL(cudaMemsetAsync(g.ntiles, 0, 4, st));
+  LAUNCH(grp_count_kernel<<<grid, 128, 0, st>>>(x, g, slots, n));
+  LAUNCH(grp_base_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, SIB));
+  LAUNCH(grp_fill_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, SIB));
+  LAUNCH(grp_reset_kernel<<<grid, 128, 0, st>>>(x, g, slots, n));
+  return LB_OK;
 }
 
 static int check_err_flags(lb_llm* l) {
@@ -2102,10 +2150,18 @@ int lb_llm_plan(lb_llm* l, int32_t final_, int32_t min_frames, int32_t* n_waves,
   LAUNCH(flag_count_kernel<<<nblk, CB, 0, st>>>(x, x.blk));
   LAUNCH(blk_scan_kernel<<<1, CB, 0, st>>>(x.blk, nblk));
   LAUNCH(compact_kernel<<<nblk, CB, 0, st>>>(x, x.blk));
+  // sibling tiles of the whole wave, built before the one synchronisation of the plan
+  int32_t ntiles = -1;
+  if (att_group_enabled()) {
+    int rc = grp_build(l, x.wave_slots, -1, x.cap);
+    if (rc) return rc;
+    CKL(cudaMemcpyAsync(&ntiles, l->grp.ntiles, 4, cudaMemcpyDeviceToHost, st));
+  }
   int32_t nfc[2] = {0, 0};  // C_NFWD, C_NCUM
   CKL(cudaMemcpyAsync(nfc, x.ctr + C_NFWD, 8, cudaMemcpyDeviceToHost, st));
   int rc = check_err_flags(l);  // synchronises
   if (rc) return rc;
+  l->plan_tiles = ntiles;
   l->wave_off.clear();
   l->wave_rows.clear();
   // One wave per event (see compact_kernel): inside a layer the K/V of all rows are written
@@ -2145,6 +2201,7 @@ int lb_llm_plan_async(lb_llm* l, int32_t final_, int32_t min_frames, int32_t row
   LAUNCH(blk_scan_kernel<<<1, CB, 0, st>>>(x.blk, nblk));
   LAUNCH(compact_kernel<<<nblk, CB, 0, st>>>(x, x.blk));
   LAUNCH(plan_async_kernel<<<1, 32, 0, st>>>(x, rows_cap));
+  l->plan_tiles = -1;
   return LB_OK;
 }
 
@@ -2180,36 +2237,20 @@ int lb_llm_wave_rows(lb_llm* l, int32_t wave, int64_t row0, int32_t n, int32_t* 
                                                 positions, slots, chains));
   l->grp_rows = -1;
   if (!att_group_enabled()) return LB_OK;
-  // sibling tiles of this chunk for the grouped attention kernel
-  LlmDev& x = l->dev;
-  const int SIB = 16 / (x.NH / x.NKV);
-  GrpDev& g = l->grp;
-  if (!g.cnt) {
-    CKL(dalloc(&g.cnt, (size_t)x.cap));
-    CKL(dalloc(&g.base, (size_t)x.cap));
-    CKL(dalloc(&g.ntiles, 1));
-    CKL(cudaMemsetAsync(g.cnt, 0, (size_t)x.cap * 4, st));
+  if (row0 == 0 && n == l->wave_rows[wave] && l->plan_tiles >= 0) {
+    // the whole wave in one chunk: the tiles built during planning apply (row r = wave row r)
+    if ((int64_t)l->plan_tiles * 4 <= (int64_t)n * 3) {
+      l->grp_tiles = l->plan_tiles;
+      l->grp_rows = n;
+      l->grp_pos = positions;
+    }
+    return LB_OK;
   }
-  if (l->grp_cap < n) {
-    cudaFree(g.row_k);
-    cudaFree(g.tiles);
-    cudaFree(g.tile_n);
-    g.row_k = g.tiles = g.tile_n = nullptr;
-    const int64_t want = std::max<int64_t>(n, 2 * l->grp_cap);
-    CKL(dalloc(&g.row_k, (size_t)want));
-    CKL(dalloc(&g.tiles, (size_t)want * SIB));
-    CKL(dalloc(&g.tile_n, (size_t)want));
-    l->grp_cap = want;
-  }
-  CKL(cudaMemsetAsync(g.ntiles, 0, 4, st));
-  LAUNCH(grp_count_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n));
-  LAUNCH(grp_base_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n, SIB));
-  LAUNCH(grp_fill_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n, SIB));
-  LAUNCH(grp_reset_kernel<<<grid, 128, 0, st>>>(x, g, slots, positions, n));
-  // the tile count decides the kernel: grouping pays only when siblings share tiles (the
-  // final event of a batch: ~6 rows per parent); one small copy + sync per forward chunk
+  // a partial chunk: tiles of its own rows (one small copy + sync)
+  int rc = grp_build(l, slots, n, n);
+  if (rc) return rc;
   int32_t nt = 0;
-  CKL(cudaMemcpyAsync(&nt, g.ntiles, 4, cudaMemcpyDeviceToHost, st));
+  CKL(cudaMemcpyAsync(&nt, l->grp.ntiles, 4, cudaMemcpyDeviceToHost, st));
   CKL(cudaStreamSynchronize(st));
   l->grp_tiles = nt;
   if ((int64_t)nt * 4 <= (int64_t)n * 3) {
