@@ -275,7 +275,7 @@ void plan_layout(lb_batch* b) {
   const int64_t lcap = std::max<int64_t>(2 * K, K + 256);
   int64_t sz[N_REGIONS] = {};
   sz[R_DBUF] = 2 * CHUNK * VPD * 8;
-  sz[R_ROWS] = K * VP * 4;
+  sz[R_ROWS] = K * (int64_t)sizeof(LexRec);  // compact lexicon record per beam
   const int64_t beam[7] = {K * 8, K * 8, K * 8, K * 4, K * 4, K * 4, K * O * (int64_t)sizeof(Ent)};
   for (int i = 0; i < 7; ++i) {
     sz[R_CUR_SCORE + i] = beam[i];

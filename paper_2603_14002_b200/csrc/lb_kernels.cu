@@ -372,6 +372,19 @@ __device__ __forceinline__ CompHdr comp_hdr(const int32_t* row, int V) {
   return CompHdr{row[V], row[V + 1], row[V + 2], row[V + 3], row[V + 4], row[V + 5]};
 }
 
+// Successor of prefix state `lr` on token `tok` (a valid transition): breadth-first tries give
+// first child + rank (space -> root), any other table a successor-list lookup.
+__device__ __forceinline__ int lex_succ(const ModelDev& m, const LexRec& lr, int tok) {
+  if (m.lex_contig) {
+    const unsigned long long ms = lr.mask & ~(1ull << m.space);
+    return tok == m.space ? 0 : lr.base + __popcll(ms & ((1ull << tok) - 1ull));
+  }
+  return __ldg(m.lex_next + lr.base + __popcll(lr.mask & ((1ull << tok) - 1ull)));
+}
+// Completion header from a compact lexicon record (CSR offset read only for > 2 surfaces).
+__device__ __forceinline__ CompHdr lex_hdr_g(const ModelDev& m, const LexRec& r, int state) {
+  return CompHdr{r.ns, r.ns > 2 ? __ldg(m.comp_off + state) : 0, r.s0, r.l0, r.s1, r.l1};
+}
 // The same header from a compact lexicon record and the beam's staged CSR offset.
 __device__ __forceinline__ CompHdr small_hdr(const LexRec& r, int off) {
   return CompHdr{r.ns, off, r.s0, r.l0, r.s1, r.l1};
@@ -579,7 +592,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
     return L.in_smem[r] ? smem + L.off[r] : gs + L.off[r];
   };
   double* dbuf = reinterpret_cast<double*>(R(R_DBUF));
-  int32_t* rows = reinterpret_cast<int32_t*>(R(R_ROWS));
+  LexRec* lrows = reinterpret_cast<LexRec*>(R(R_ROWS));  // staged lexicon records (when they fit)
   BeamPtrs cur{(double*)R(R_CUR_SCORE), (uint64_t*)R(R_CUR_H1), (uint64_t*)R(R_CUR_H2),
                (int32_t*)R(R_CUR_LAST), (int32_t*)R(R_CUR_PRE), (int32_t*)R(R_CUR_NENT),
                (Ent*)R(R_CUR_ENTS)};
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
   int32_t* slotm = reinterpret_cast<int32_t*>(R(R_SLOTM));   // [tslots]
   int32_t* myslot = reinterpret_cast<int32_t*>(R(R_MYSLOT)); // [K]
 
-  const int V = m.V, VP = m.VP, VPD = b.VPD, O = c.O, KC = b.K;
+  const int V = m.V, VPD = b.VPD, O = c.O, KC = b.K;
   const int nkw = (c.k + 31) >> 5;
   const int TS = L.tslots;
   const float invV = 1.0f / (float)V;
@@ -629,8 +642,9 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
       cur.pre[i] = b.prefix[hb + i];
       cur.nent[i] = b.nent[hb + i];
       if (L.stage_rows) {
-        const int32_t* src = m.table + (size_t)b.prefix[hb + i] * VP;
-        for (int q = 0; q < VP; q += 4) cp_async16(rows + i * VP + q, src + q);
+        const LexRec* src = m.lex + b.prefix[hb + i];
+        cp_async16(&lrows[i], src);
+        cp_async16(reinterpret_cast<char*>(&lrows[i]) + 16, reinterpret_cast<const char*>(src) + 16);
       }
     }
     if (L.stage_rows) cp_async_commit();
@@ -694,9 +708,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
     ph[i] += (unsigned long long)(tnow - tprev);   \
     tprev = tnow;                                  \
   }
-  auto rowp = [&](int p) -> const int32_t* {
-    return L.stage_rows ? rows + p * VP : m.table + (size_t)cur.pre[p] * VP;
-  };
+  auto lrec = [&](int p) -> const LexRec& { return L.stage_rows ? lrows[p] : m.lex[cur.pre[p]]; };
 
   for (int t = tb; t < te; ++t) {
     const int rel = t - tb;
@@ -713,8 +725,8 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
         const int p = base + gt;
         int np = 0;
         if (p < K) {
-          const int32_t* row = rowp(p);
-          if (row[V] > 0 && cur.last[p] != m.space) np = cur.nent[p] * row[V];
+          const int ns = lrec(p).ns;
+          if (ns > 0 && cur.last[p] != m.space) np = cur.nent[p] * ns;
         }
         int incl = np;
         for (int o = 1; o < 32; o <<= 1) {
@@ -759,7 +771,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
               else hi = mid - 1;
             }
             p = lo;
-            const CompHdr ch = comp_hdr(rowp(p), V);
+            const CompHdr ch = lex_hdr_g(m, lrec(p), cur.pre[p]);
             const int local = q - ppoff[p];
             e = local / ch.ns;
             const int sidx = local - e * ch.ns;
@@ -816,9 +828,8 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
         const int p = (int)(((float)f + 0.5f) * invV);
         const int v = f - p * V;
         const int lp = cur.last[p];
-        const int nx = rowp(p)[v];
         uint16_t bin = 0xFFFF;
-        if ((nx != m.sink) || (v == m.blank) || (v == lp)) {
+        if (((lrec(p).mask >> v) & 1ull) || (v == m.blank) || (v == lp)) {
           double x = xadd(cur.score[p], drow[v]);
           const bool ph2 = (v != m.blank) & (v != m.space);
           x = xadd(x, (ph2 && v != lp) ? b_on : b_off);
@@ -1063,7 +1074,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
           if (emit) {
             a1 = a1 * H_MULT1 + (uint64_t)(tok + 1);
             a2 = a2 * H_MULT2 + (uint64_t)(tok + 1);
-            np = rowp(p)[tok];
+            np = lex_succ(m, lrec(p), tok);
           }
           double sc = x;
           int bn = -1;
@@ -1155,7 +1166,7 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
             int outn = -1;
             double sc = nscore[j];
             warp_apply_ngram(m, c, b, trial, cur.ents + (size_t)p * O, cur.nent[p],
-                             comp_hdr(rowp(p), V), &wsc[warp], bents + (size_t)j * O, &outn, &sc,
+                             lex_hdr_g(m, lrec(p), cur.pre[p]), &wsc[warp], bents + (size_t)j * O, &outn, &sc,
                              &s_ncount, &s_fail, calls_l, probes_l);
             if (lane == 0) {
               nscore[j] = sc;
@@ -1279,10 +1290,9 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
         const uint4* su = reinterpret_cast<const uint4*>(srcE);
         uint4* du = reinterpret_cast<uint4*>(nxt.ents + (size_t)pos * O);
         for (int u = r; u < cnt * ENT_U4; u += G) du[u] = su[u];
-        if (L.stage_rows) {
-          const int32_t* srow = m.table + (size_t)npre[i] * VP;
-          for (int u = r; u < (VP >> 2); u += G) cp_async16(rows + pos * VP + u * 4, srow + u * 4);
-        }
+        if (L.stage_rows && r < 2)
+          cp_async16(reinterpret_cast<char*>(&lrows[pos]) + 16 * r,
+                     reinterpret_cast<const char*>(m.lex + npre[i]) + 16 * r);
       }
       if (L.stage_rows) {
         cp_async_commit();
