@@ -307,11 +307,12 @@ void plan_layout(lb_batch* b) {
   for (int i = 0; i < N_REGIONS; ++i) in_smem[i] = 1;
   in_smem[R_WARP] = 0;  // scratch of the rare warp-per-beam n-gram path: global (L1-cached)
   // bulkiest / least latency-critical first; a beam of several hundred (the b2t25 profile's
-  // 900) keeps only the log-prob stage and the small per-frame arrays in shared memory
-  const int spill_order[] = {R_BENTS, R_NXT_ENTS, R_CUR_ENTS, R_ROWS, R_CV, R_CVAL, R_CKEY,
+  // 900) keeps the log-prob stage, the 32-B lexicon record per beam (read by every candidate)
+  // and the small per-frame arrays in shared memory
+  const int spill_order[] = {R_BENTS, R_NXT_ENTS, R_CUR_ENTS, R_CV, R_CVAL, R_CKEY,
                              R_NXT_H1, R_NXT_H2, R_CUR_H1, R_CUR_H2, R_NH1, R_NH2,
                              R_PAIRS, R_CBIN, R_SLOTB, R_SLOTM, R_NSCORE, R_SVAL, R_SKEY,
-                             R_NLAST, R_NPRE, R_NPAR, R_BNENT, R_MYSLOT, R_BLIST, R_RANK,
+                             R_NLAST, R_NPRE, R_NPAR, R_BNENT, R_MYSLOT, R_BLIST, R_RANK, R_ROWS,
                              R_NXT_LAST, R_NXT_PRE, R_NXT_NENT, R_CUR_LAST, R_CUR_PRE,
                              R_CUR_NENT, R_NXT_SCORE, R_CUR_SCORE, R_POFF, R_KEEP};
   auto total = [&]() {
