@@ -1290,9 +1290,10 @@ __global__ void __launch_bounds__(NC + NGT, (NC <= 256 ? 2 : 1))
         const uint4* su = reinterpret_cast<const uint4*>(srcE);
         uint4* du = reinterpret_cast<uint4*>(nxt.ents + (size_t)pos * O);
         for (int u = r; u < cnt * ENT_U4; u += G) du[u] = su[u];
-        if (L.stage_rows && r < 2)
-          cp_async16(reinterpret_cast<char*>(&lrows[pos]) + 16 * r,
-                     reinterpret_cast<const char*>(m.lex + npre[i]) + 16 * r);
+        if (L.stage_rows)
+          for (int u = r; u < 2; u += G)  // the record's two 16-B halves (G may be 1)
+            cp_async16(reinterpret_cast<char*>(&lrows[pos]) + 16 * u,
+                       reinterpret_cast<const char*>(m.lex + npre[i]) + 16 * u);
       }
       if (L.stage_rows) {
         cp_async_commit();
