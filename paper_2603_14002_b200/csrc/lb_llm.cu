@@ -1018,46 +1018,53 @@ __device__ __forceinline__ int grp_rows(const LlmDev& l, int nh) {
   return nh >= 0 ? nh : (int)min((int64_t)l.ctr[C_NFWD], l.cap);
 }
 
-__global__ void grp_count_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh) {
+// the tile key of a row: its ancestor GAP = 1 << gsh levels up (-1: too shallow, a tile alone)
+__device__ __forceinline__ int grp_key(const LlmDev& l, int s, int gsh) {
+  if (l.s_depth[s] < (1 << gsh)) return -1;
+  for (int k = 0; k < (1 << gsh); ++k) s = l.s_parent[s];
+  return s;
+}
+
+__global__ void grp_count_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int gsh) {
   const int n = grp_rows(l, nh);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const int s = slots[r];
-    g.row_k[r] = l.s_depth[s] > 0 ? atomicAdd(g.cnt + l.s_parent[s], 1) : 0;
+    const int key = grp_key(l, slots[r], gsh);
+    g.row_k[r] = key >= 0 ? atomicAdd(g.cnt + key, 1) : 0;
   }
 }
 
-__global__ void grp_base_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int SIB) {
+__global__ void grp_base_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int SIB,
+                                int gsh) {
   const int n = grp_rows(l, nh);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const int s = slots[r];
-    if (l.s_depth[s] == 0) {  // the BOS row: no chain to share, a tile of its own
+    const int key = grp_key(l, slots[r], gsh);
+    if (key < 0) {  // too shallow (the BOS row, ...): a tile of its own
       const int t = atomicAdd(g.ntiles, 1);
       g.tiles[(size_t)t * SIB] = r;
       g.tile_n[t] = 1;
     } else if (g.row_k[r] == 0) {
-      const int p = l.s_parent[s];
-      g.base[p] = atomicAdd(g.ntiles, (g.cnt[p] + SIB - 1) / SIB);
+      g.base[key] = atomicAdd(g.ntiles, (g.cnt[key] + SIB - 1) / SIB);
     }
   }
 }
 
-__global__ void grp_fill_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int SIB) {
+__global__ void grp_fill_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int SIB,
+                                int gsh) {
   const int n = grp_rows(l, nh);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const int s = slots[r];
-    if (l.s_depth[s] == 0) continue;
-    const int p = l.s_parent[s], k = g.row_k[r];
+    const int p = grp_key(l, slots[r], gsh), k = g.row_k[r];
+    if (p < 0) continue;
     const int t = g.base[p] + k / SIB;
     g.tiles[(size_t)t * SIB + k % SIB] = r;
     if (k % SIB == 0) g.tile_n[t] = min(SIB, g.cnt[p] - (k / SIB) * SIB);
   }
 }
 
-__global__ void grp_reset_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh) {
+__global__ void grp_reset_kernel(LlmDev l, GrpDev g, const int32_t* slots, int nh, int gsh) {
   const int n = grp_rows(l, nh);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const int s = slots[r];
-    if (l.s_depth[s] > 0) g.cnt[l.s_parent[s]] = 0;
+    const int key = grp_key(l, slots[r], gsh);
+    if (key >= 0) g.cnt[key] = 0;
   }
 }
 
@@ -1070,7 +1077,8 @@ template <int HD, bool SPLIT, int nstages>
 __global__ void __launch_bounds__(128, 3) chain_attn_grp_kernel(LlmDev l, int layer, const void* qv,
                                                              const int32_t* chains,
                                                              const int32_t* pos, GrpDev gd,
-                                                             int SIB, float scale, bf16* out) {
+                                                             int SIB, int gsh, float scale,
+                                                             bf16* out) {
   pdl_wait();
   const int tile = blockIdx.x;
   constexpr int KK = HD / 16;
@@ -1087,14 +1095,17 @@ __global__ void __launch_bounds__(128, 3) chain_attn_grp_kernel(LlmDev l, int la
   const int32_t* trow = gd.tiles + (size_t)tile * SIB;
   const int d = pos[trow[0]];
   const int pitchc = l.max_depth + 1;
-  const int32_t* ch = chains + (size_t)trow[0] * pitchc;  // shared chain: ch[0 .. d-1]
+  // rows of a tile share their ancestors up to depth d - GAP (GAP = 1 << gsh private positions
+  // per row: GAP = 1 siblings, 2 cousins): shared chain ch[0 .. nsh-1]
+  const int GAP = 1 << gsh, nsh = d - GAP + 1;
+  const int32_t* ch = chains + (size_t)trow[0] * pitchc;
   const int ghalf = NKV * HD * 2;                // bytes of one bf16 half of a cache row
   const int grow = ghalf * (SPLIT ? 2 : 1);       // cache row: [hi] or [hi | lo], all kv heads
   const int halfb = KH * HD * 2;                  // staged half: this CTA's kv heads
   const int rowb = halfb * (SPLIT ? 2 : 1);
   const int pitch = rowb + 16;
   const int stage_bytes = 2 * MMA_CH * pitch;
-  const int nv = d + cnt;  // virtual positions: chain, then one own row per sibling
+  const int nv = nsh + (cnt << gsh);  // virtual positions: shared chain, then GAP per row
   const int nch = (nv + MMA_CH - 1) / MMA_CH;
   const unsigned char* kbase = reinterpret_cast<const unsigned char*>(l.kc) + (size_t)layer * l.cap * grow + h0 * HD * 2;
   const unsigned char* vbase = reinterpret_cast<const unsigned char*>(l.vc) + (size_t)layer * l.cap * grow + h0 * HD * 2;
@@ -1113,7 +1124,9 @@ __global__ void __launch_bounds__(128, 3) chain_attn_grp_kernel(LlmDev l, int la
     __syncwarp();
     if (lane < cn) {
       const int v = c * MMA_CH + lane;
-      const size_t sl = v < d ? (size_t)ch[v] : (size_t)chains[(size_t)trow[v - d] * pitchc + d];
+      const size_t sl = v < nsh ? (size_t)ch[v]
+                                : (size_t)chains[(size_t)trow[(v - nsh) >> gsh] * pitchc + nsh +
+                                                 ((v - nsh) & (GAP - 1))];
       tma_bulk_g2s(kd + (size_t)lane * pitch, kbase + sl * grow, halfb, &bars[st]);
       tma_bulk_g2s(vd + (size_t)lane * pitch, vbase + sl * grow, halfb, &bars[st]);
       if (SPLIT) {
@@ -1163,7 +1176,7 @@ __global__ void __launch_bounds__(128, 3) chain_attn_grp_kernel(LlmDev l, int la
   for (int c = 0; c < nch; ++c) {
     if (nstages == 2 && warp == 0 && c + 1 < nch) issue(c + 1);
     const int cn = chunk_n(c);
-    const int vown = d - c * MMA_CH;  // chunk index of sibling 0's own position
+    const int vown = nsh - c * MMA_CH;  // chunk index of row 0's first private position
     const int st = c % nstages;
     unsigned char* ks = stages + (size_t)st * stage_bytes;
     unsigned char* vs = ks + (size_t)MMA_CH * pitch;
@@ -1206,7 +1219,7 @@ __global__ void __launch_bounds__(128, 3) chain_attn_grp_kernel(LlmDev l, int la
         const int j = t * 8 + qd * 2 + (e & 1), hr = e >> 1;
         // chain positions are shared; position vown + i is sibling i's own row (rows of missing
         // siblings see everything, finite and never written)
-        const bool vis = j < cn && (j < vown || rsib[hr] >= cnt || j == vown + rsib[hr]);
+        const bool vis = j < cn && (j < vown || rsib[hr] >= cnt || ((j - vown) >> gsh) == rsib[hr]);
         sc[t][e] = vis ? sc[t][e] * scale : -INFINITY;
         mx[hr] = fmaxf(mx[hr], sc[t][e]);
       }
@@ -1935,6 +1948,15 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   } while (0)
 
 // LB_ATT_GROUP=0: per-row chain attention only (A/B switch)
+// LB_ATT_GAP = 1 (siblings: rows sharing a parent) or 2 (cousins: rows sharing a grandparent,
+// two private positions each)
+static int att_group_shift() {
+  static const int v = [] {
+    const char* e = std::getenv("LB_ATT_GAP");
+    return (e && e[0] == '2') ? 1 : 0;
+  }();
+  return v;
+}
 static bool att_group_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("LB_ATT_GROUP");
@@ -1969,10 +1991,11 @@ static int grp_build(lb_llm* l, const int32_t* slots, int n, int64_t cap_rows) {
   }
   const int grid = n >= 0 ? std::max(1, std::min(4 * 148, (n + 127) / 128)) : 4 * 148;
   CKL(cudaMemsetAsync(g.ntiles, 0, 4, st));
-  LAUNCH(grp_count_kernel<<<grid, 128, 0, st>>>(x, g, slots, n));
-  LAUNCH(grp_base_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, SIB));
-  LAUNCH(grp_fill_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, SIB));
-  LAUNCH(grp_reset_kernel<<<grid, 128, 0, st>>>(x, g, slots, n));
+  const int gsh = att_group_shift();
+  LAUNCH(grp_count_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, gsh));
+  LAUNCH(grp_base_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, SIB, gsh));
+  LAUNCH(grp_fill_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, SIB, gsh));
+  LAUNCH(grp_reset_kernel<<<grid, 128, 0, st>>>(x, g, slots, n, gsh));
   return LB_OK;
 }
 
@@ -2380,7 +2403,7 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
 #define GRP_ATT_N(HDV, SV, NS)                                                                      \
   do {                                                                                              \
     CKL(cudaFuncSetAttribute(chain_attn_grp_kernel<HDV, SV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem)); \
-    LAUNCH_PDL((chain_attn_grp_kernel<HDV, SV, NS>), dim3(l->grp_tiles, x.NKV / KH), dim3(32 * KH), gsmem, st, x, layer, q, chains, pos, l->grp, SIB, scale, oo); \
+    LAUNCH_PDL((chain_attn_grp_kernel<HDV, SV, NS>), dim3(l->grp_tiles, x.NKV / KH), dim3(32 * KH), gsmem, st, x, layer, q, chains, pos, l->grp, SIB, att_group_shift(), scale, oo); \
   } while (0)
 #define GRP_ATT(HDV, SV)               \
   do {                                 \
