@@ -684,12 +684,13 @@ class DeviceLlmSession:
             max_slots = int(scorer.max_slots)
         else:
             # measured on the synthetic B2T worlds: slots per utterance ~ T k (1 + 20/r) / 96
-            # (T=500: 743 at k=64 r=20, 3725 at k=256 r=10); sized 2x that, capped by memory
+            # (T=500: 743 at k=64 r=20, 3725 at k=256 r=10); sized 2x that, capped at half the
+            # free memory (the 1B model's T=2000 k=256 r=10 sweep point needs ~1.1M slots)
             c = batch.cfg
             per_trial = batch.max_frames * c.beam_size * (1 + 20 / c.llm_rescore_interval) / 48
             want = max(1 << 16, int(batch.max_trials * per_trial))
             free, _ = torch.cuda.mem_get_info(scorer.device)
-            max_slots = int(min(want, 0.4 * free / per_slot, 1 << 26))
+            max_slots = int(min(want, 0.5 * free / per_slot, 1 << 26))
         self.max_slots = max_slots
         self.pitch = scorer.max_depth + 1
         d = N.LbLlmDesc()

@@ -85,6 +85,11 @@ def main():
                     ok += int(res[i] is not None and res[i][0] == want.text and res[i][1] == want.score)
                 point["parity"] = f"{ok}/{args.check}"
                 point["check_s"] = time.perf_counter() - t0
+                sess = getattr(batch, "_llm_session", None)
+                if sess is not None:  # free this point's prefix cache before the next point sizes its own
+                    sess.destroy()
+                    batch._llm_session = None
+                    torch.cuda.empty_cache()
                 print(json.dumps(point), flush=True)
                 results.append(point)
     if args.out:
