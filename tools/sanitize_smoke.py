@@ -24,5 +24,7 @@ for k in (16, 64, 96, 300) + ((900,) if os.environ.get("SAN_WIDE") else ()):
 cfg = PROFILES["b2t25"].replace(beam_size=16, llm_rescore_interval=20)
 ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
 for prec in ("bf16", "bf16x2"):
-    decode_batch(ds, cfg, w.table, w.model, LlamaScorer("tiny", seed=1, precision=prec, max_slots=4096))
-    print("llm ok", prec, flush=True)
+    for graphs in (True, False):  # eager: sibling-tile attention + planning-time tiles
+        decode_batch(ds, cfg, w.table, w.model,
+                     LlamaScorer("tiny", seed=1, precision=prec, max_slots=4096, graphs=graphs))
+        print("llm ok", prec, "graphs" if graphs else "eager", flush=True)
