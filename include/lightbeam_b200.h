@@ -363,7 +363,7 @@ int lb_llm_lmhead_lse(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t 
 int lb_llm_gateup_swiglu(lb_llm* l, const void* h, int32_t M, int64_t ldh, int32_t K,
                          const void* wgu_interleaved, int64_t ldw, int32_t ffn, void* act);
 /* out[8]: slots, events, waves, forwarded rows, widest wave, device bytes, scores computed
- * (next-token log-probs), 0 */
+ * (next-token log-probs), attention launches that used sibling tiles */
 int lb_llm_stats(lb_llm* l, int64_t* out);
 /* Parity/debug: the slot table.  *n = slots in use; the first min(*n, max_n) rows are copied
  * into the host buffers (NULL skips a field).  state bits:

@@ -1886,6 +1886,7 @@ struct lb_llm {
   int64_t bytes = 0;
   // stats
   int64_t events = 0, waves = 0, rows = 0, cum = 0, max_wave_rows = 0;
+  int64_t grouped_launches = 0;  // attention launches that used sibling tiles
   int32_t cur_nwaves = 0;
   std::vector<int64_t> wave_off, wave_rows;
   // sibling tiles of the last eager forward chunk (lb_llm_wave_rows -> lb_llm_attention)
@@ -2155,6 +2156,7 @@ int lb_llm_reset_device(lb_llm* l) {
 int lb_llm_reset_stats(lb_llm* l) {
   if (!l) return lbh::set_error(LB_ERR_ARG, "null argument");
   l->events = l->waves = l->rows = l->cum = l->max_wave_rows = 0;
+  l->grouped_launches = 0;
   return LB_OK;
 }
 
@@ -2415,6 +2417,7 @@ int lb_llm_attention(lb_llm* l, int32_t layer, const void* q, int32_t M, const i
       } else {
         if (x.split) GRP_ATT(128, true); else GRP_ATT(128, false);
       }
+      ++l->grouped_launches;
 #undef GRP_ATT
 #undef GRP_ATT_N
       return LB_OK;
@@ -2571,7 +2574,7 @@ int lb_llm_stats(lb_llm* l, int64_t* out) {
   out[4] = std::max<int64_t>(l->max_wave_rows, dev[2]);
   out[5] = l->bytes;
   out[6] = l->cum;
-  out[7] = 0;
+  out[7] = l->grouped_launches;
   return LB_OK;
 }
 

@@ -971,7 +971,7 @@ class DeviceLlmSession:
         N.check(N.lib().lb_llm_stats(self.h, N.ptr(out)))
         return {"slots": int(out[0]), "events": int(out[1]), "waves": int(out[2]),
                 "forward_rows": int(out[3]), "max_wave_rows": int(out[4]), "cache_bytes": int(out[5]),
-                "scores": int(out[6])}
+                "scores": int(out[6]), "grouped_attention_launches": int(out[7])}
 
     def export(self) -> dict:
         """Slot table for parity checks: parent, token, depth, state bits, score, punct lps."""

@@ -536,3 +536,30 @@ def test_llm_stream_api_matches_batch_api(tiny_scorer):
     got = list(decode_stream_raw(iter(batches), cfg, w.table, w.model, tiny_scorer))
     for gb, wb in zip(got, want):
         assert [(r.text, r.score, r.nbest) for r in gb] == [(r.text, r.score, r.nbest) for r in wb]
+
+
+@pytest.mark.gpu
+def test_sibling_tile_attention_matches_per_row():
+    """The sibling-tile attention kernel (rows sharing a parent slot grouped per CTA, their own
+    positions masked per row) against the per-row kernel on the same decode: it is used, and
+    every scored text agrees within float rounding (the two kernels chunk the positions alike
+    for single rows; tiles only change which rows share a CTA)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    probe = os.path.join(os.path.dirname(__file__), "_att_probe.py")
+    out = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, LB_ATT_GROUP=mode)
+        r = subprocess.run([sys.executable, probe], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["1"]["stats"]["grouped_attention_launches"] > 0
+    assert out["0"]["stats"]["grouped_attention_launches"] == 0
+    a, b = out["1"]["scores"], out["0"]["scores"]
+    common = a.keys() & b.keys()
+    assert len(common) > 50
+    assert max(abs(a[k] - b[k]) for k in common) < 2e-3
