@@ -1415,7 +1415,9 @@ static_assert(KC * 4 == NC && TBK % 4 == 0, "candidate mapping: one parent per 4
 // Beam state by slot (double-buffered by frame parity): beams live in the slot their selection
 // gave them (slot j = rank j of the frame's top-k selection); JMAP lists the slots of the kept
 // beams in post-fusion score order, so parent p of the next frame is slot JMAP[p] -- no beam is
-// moved at the end of a frame.  LROW / LOFF: the lexicon record and completion-CSR offset of a
+// moved at the end of a frame.  JMAP is indexed by the rank among all selected beams, with -1
+// holes for the ones recombination dropped (ranks are monotone in the compacted positions, so
+// every (parent, token) tie-break is unchanged) -- no compaction pass per frame.  LROW / LOFF: the lexicon record and completion-CSR offset of a
 // beam's prefix state, gathered by cp.async as soon as the beam is materialised.
 constexpr int B_SCORE = 0, B_H1 = KC * 8, B_H2 = 2 * KC * 8, B_LAST = 3 * KC * 8,
               B_PRE = 3 * KC * 8 + KC * 4, B_NENT = 3 * KC * 8 + 2 * KC * 4,
@@ -1472,6 +1474,7 @@ __device__ LB_COLD int small_fallback_select(const int ck, const double cbeta, c
   auto cval_at = [&](int f) -> double {
     const int p = f / V, v = f - (f / V) * V;
     const int jp = jmap[p];
+    if (jp < 0) return -DBL_MAX;  // a dropped rank (hole)
     const int lp = C_LAST[jp];
     if (!(((lrow[jp].mask >> v) & 1ull) || (v == blank) || (v == lp))) return -DBL_MAX;
     const double x = cand_value(C_SCORE[jp], drow[v], v, lp,
@@ -1579,6 +1582,7 @@ __global__ void __launch_bounds__(small::NT, 2)
   __shared__ double wmax[NWC];
   __shared__ double s_maxs;
   __shared__ int s_nb, s_ncount, s_fail, s_status, s_K, s_ngP, s_ngcov, s_inr, s_cnt2, s_nsel;
+  __shared__ int s_live[2];  // surviving beams of a frame, by frame parity
   __shared__ int ngtot[2];
   __shared__ unsigned s_calls, s_probes, s_pairs;
   __shared__ unsigned s_tarr[NBAR_EV], s_tbase;  // TIMING only
@@ -1654,7 +1658,8 @@ __global__ void __launch_bounds__(small::NT, 2)
   }
 
   // ---- load the home beam state and gather the first frame's lexicon rows
-  int K = b.nbeam[trial];
+  int K = b.nbeam[trial];  // parents of the frame (ranks incl. holes)
+  int Klive = K;            // surviving beams among them
   {
     const size_t hb = (size_t)trial * KC_;
     for (int i = tid; i < K; i += NT) {
@@ -1681,6 +1686,7 @@ __global__ void __launch_bounds__(small::NT, 2)
     hfill[i] = 0;
   }
   if (tid == 0) {
+    s_live[0] = s_live[1] = 0;
     s_ncount = b.ncount[trial];
     s_fail = 0;
     s_status = 0;
@@ -1743,7 +1749,7 @@ __global__ void __launch_bounds__(small::NT, 2)
     const int rel = t - tb;
     const int ci = rel / SCHUNK;
     const int cr = rel - ci * SCHUNK;
-    st_beams_in += K;
+    st_beams_in += Klive;
 
     if (warp >= NWC) {
       // ================== speculative n-gram warps (as in frames_kernel) ==================
@@ -1754,11 +1760,11 @@ __global__ void __launch_bounds__(small::NT, 2)
       static_assert(KC <= NGT, "one parent per speculative n-gram thread");
       const int p = gt;
       int np = 0, ns = 0, nent = 0;
-      if (p < K) {
-        const int jp = C_JMAP[p];
-        ns = C_LROW[jp].ns;
-        nent = C_NENT[jp];
-        if (ns > 0 && C_LAST[jp] != space) np = nent * ns;
+      const int jp0 = p < K ? C_JMAP[p] : -1;
+      if (jp0 >= 0) {
+        ns = C_LROW[jp0].ns;
+        nent = C_NENT[jp0];
+        if (ns > 0 && C_LAST[jp0] != space) np = nent * ns;
       }
       int incl = np;
       for (int o = 1; o < 32; o <<= 1) {
@@ -1898,9 +1904,9 @@ __global__ void __launch_bounds__(small::NT, 2)
       const double U = __dadd_ru(__dadd_ru(__dadd_ru(s_maxs, drow[V]), fmax(c.beta, 0.0)),
                                  fmax(c.gamma, 0.0));
       // per-thread parent constants (thread -> parent cp, tokens cv0 .. cv0 + TBK - 1)
-      const bool pin = cp < K;
-      const int pcl = pin ? cp : 0;
-      const int jcl = C_JMAP[pcl];
+      const int jraw = cp < K ? C_JMAP[cp] : -1;
+      const bool pin = jraw >= 0;  // a live parent (not beyond K, not a dropped rank)
+      const int jcl = pin ? jraw : 0;
       const int lp = C_LAST[jcl];
       const double sp = C_SCORE[jcl];
       const double gsel = lp != space ? g_on : g_off;
@@ -2118,6 +2124,9 @@ __global__ void __launch_bounds__(small::NT, 2)
       }
 
       if (dead) bar_arrive(4, NT);
+      // the previous frame's survivor count was read by every thread right after that frame's
+      // end barrier; after this hand-off (all warps) its buffer serves the next frame
+      if (tid == 0) s_live[(rel + 1) & 1] = 0;
       if (!dead) {
         const int ncov = s_ngcov;
         const bool ngover = ncov < s_ngP;  // some parents' pairs were not speculated
@@ -2240,7 +2249,13 @@ __global__ void __launch_bounds__(small::NT, 2)
           dup |= __shfl_xor_sync(FULLMASK, dup, 2);
           if (act && r == 0) {
             rankv[i] = cnt;
-            if (si > GUARD && !dup) atomicOr(&keep[cnt >> 5], 1u << (cnt & 31));
+            const bool kept = si > GUARD && !dup;
+            X_JMAP[cnt] = kept ? i : -1;  // the next frame's parent of rank cnt (or a hole)
+            if (kept) {
+              atomicOr(&keep[cnt >> 5], 1u << (cnt & 31));
+              atomicAdd(&s_live[rel & 1], 1);
+              if (cnt == 0) s_maxs = si;  // rank 0: the best survivor
+            }
           }
           // entries of a fresh word boundary i into its slot (four threads) from the chosen
           // speculative pairs; inherited entries are copied by the n-gram warps meanwhile
@@ -2264,28 +2279,20 @@ __global__ void __launch_bounds__(small::NT, 2)
             }
           }
         }
-        LB_ARR(5);
-        bar_sync(1, NC);  // S5
-        LB_REL(5);
-        LB_PHASE(6);
-        const unsigned kp0 = keep[0], kp1 = keep[1];
-        LB_PHASE(7);
-
-        // ---- order: the kept beams' slots in rank order become the next frame's parents (no
-        // beam moves); then this frame's lexicon-record gathers must have landed
+        // histogram bins free again for the next frame; this frame's lexicon-record gathers
         for (int i = tid; i < NBINS; i += NC) {
           hist[i] = 0;
           hfill[i] = 0;
         }
-        const int newK = __popc(kp0) + __popc(kp1);
-        for (int i = tid; i < nsel; i += NC) {
-          const int rk = rankv[i];
-          const unsigned kw = rk >= 32 ? kp1 : kp0;
-          if (!((kw >> (rk & 31)) & 1u)) continue;
-          const int pos = __popc(kw & ((1u << (rk & 31)) - 1u)) + (rk >= 32 ? __popc(kp0) : 0);
-          X_JMAP[pos] = i;
-          if (pos == 0) s_maxs = X_SCORE[i];
-          if (b.dump_k) {
+        cp_async_wait_all();
+        if (b.dump_k) {  // debug traces: the survivors in compacted rank order
+          bar_sync(1, NC);
+          const unsigned kp0 = keep[0], kp1 = keep[1];
+          for (int i = tid; i < nsel; i += NC) {
+            const int rk = rankv[i];
+            const unsigned kw = rk >= 32 ? kp1 : kp0;
+            if (!((kw >> (rk & 31)) & 1u)) continue;
+            const int pos = __popc(kw & ((1u << (rk & 31)) - 1u)) + (rk >= 32 ? __popc(kp0) : 0);
             const size_t di = ((size_t)trial * b.Tmax + t) * KC_ + pos;
             b.dump_h1[di] = X_H1[i];
             b.dump_h2[di] = X_H2[i];
@@ -2293,15 +2300,9 @@ __global__ void __launch_bounds__(small::NT, 2)
             b.dump_last[di] = X_LAST[i];
             b.dump_score[di] = X_SCORE[i];
           }
+          if (tid == 0) b.dump_k[(size_t)trial * b.Tmax + t] = __popc(kp0) + __popc(kp1);
         }
-        cp_async_wait_all();
-        if (b.dump_k && tid == 0) b.dump_k[(size_t)trial * b.Tmax + t] = newK;
-        if (tid == 0) {
-          s_K = newK;
-          if (s_fail) s_status = 4;
-          else if (newK == 0) s_status = 2;  // decoder.py:314-315
-        }
-        if (s_fail || newK == 0) fail_t = t;
+        if (tid == 0) s_K = nsel;
       }  // !dead
     }  // compute warps
     LB_ARR(7);
@@ -2311,13 +2312,20 @@ __global__ void __launch_bounds__(small::NT, 2)
     LB_PHASE(8);
     par ^= 1;
     K = s_K;
-    st_beams_out += K;
+    Klive = s_live[rel & 1];
+    st_beams_out += Klive;
+    if (s_status == 0 && (s_fail || Klive == 0)) {  // decoder.py:314-315 / arena exhausted
+      if (tid == 0) s_status = s_fail ? 4 : 2;
+      fail_t = t;
+      break;
+    }
     if (s_status != 0) break;
 
     // ---- optional interval fusion of the device n-gram scorer (decoder.py:428-430)
     if (fusion_mode == 1 && t > 0 && (t % c.r) == 0) {
       for (int i = tid; i < K; i += NT) {
         const int ji = C_JMAP[i];
+        if (ji < 0) continue;
         Ent* e = C_ENTS + ji * OC;
         const int n = C_NENT[ji];
         const double prev = e[0].total;
@@ -2335,7 +2343,8 @@ __global__ void __launch_bounds__(small::NT, 2)
       __syncthreads();
       if (warp == 0) {
         double ms = -DBL_MAX;
-        for (int i = lane; i < K; i += 32) ms = fmax(ms, C_SCORE[C_JMAP[i]]);
+        for (int i = lane; i < K; i += 32)
+          if (C_JMAP[i] >= 0) ms = fmax(ms, C_SCORE[C_JMAP[i]]);
         ms = warp_max(ms);
         if (lane == 0) s_maxs = ms;
       }
@@ -2358,13 +2367,26 @@ __global__ void __launch_bounds__(small::NT, 2)
       b.status[trial] = status;
       b.fail_frame[trial] = fail_t;
     }
-    b.nbeam[trial] = K;
+    b.nbeam[trial] = Klive;
     b.ncount[trial] = s_ncount;
   }
   if (status == 0 || status == 4) {
+    // the home state is compact: the survivors' slots in rank order (holes squeezed out)
+    int32_t* cslot = rankv;  // free now: compacted position -> slot
+    if (warp == 0) {
+      int base = 0;
+      for (int i0 = 0; i0 < K; i0 += 32) {
+        const int i = i0 + lane;
+        const int ji = i < K ? C_JMAP[i] : -1;
+        const unsigned bl = __ballot_sync(FULLMASK, ji >= 0);
+        if (ji >= 0) cslot[base + __popc(bl & ((1u << lane) - 1u))] = ji;
+        base += __popc(bl);
+      }
+    }
+    __syncthreads();
     const size_t hb = (size_t)trial * KC_;
-    for (int i = tid; i < K; i += NT) {
-      const int ji = C_JMAP[i];
+    for (int i = tid; i < Klive; i += NT) {
+      const int ji = cslot[i];
       b.score[hb + i] = C_SCORE[ji];
       b.h1[hb + i] = C_H1[ji];
       b.h2[hb + i] = C_H2[ji];
@@ -2372,9 +2394,9 @@ __global__ void __launch_bounds__(small::NT, 2)
       b.prefix[hb + i] = C_PRE[ji];
       b.nent[hb + i] = C_NENT[ji];
     }
-    for (int i = tid; i < K * O; i += NT) {
+    for (int i = tid; i < Klive * O; i += NT) {
       const int bi = i / O, e = i - bi * O;
-      const int jb = C_JMAP[bi];
+      const int jb = cslot[bi];
       if (e < C_NENT[jb]) b.ents[hb * O + i] = C_ENTS[jb * OC + e];
     }
   }
