@@ -25,6 +25,7 @@ kernel reads the scores from the cache.
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import threading
 import time
 import weakref
@@ -664,6 +665,17 @@ def _graph_search(batch: DeviceBatch, cfg, sess, final_llm_only: bool, t_max: in
 def _collect(batch: DeviceBatch, cfg, final_llm_only: bool, wall: float):
     st, ff = batch.status()
     res = batch.results()
+    gc_on = gc.isenabled()
+    if gc_on:  # ~256 result objects over ~15k fresh n-best objects: no collection in between
+        gc.disable()
+    try:
+        return _collect_items(batch, cfg, final_llm_only, wall, st, ff, res)
+    finally:
+        if gc_on:
+            gc.enable()
+
+
+def _collect_items(batch, cfg, final_llm_only, wall, st, ff, res):
     out = []
     for i in range(batch.n):
         if batch.frames[i] == 0:  # decoder.py:421-422 (per item, so one bad item keeps the batch)
