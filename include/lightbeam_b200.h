@@ -245,6 +245,11 @@ int lb_launch_count(uint64_t* out);
 int lb_batch_mark_begin(lb_batch* b);
 int lb_batch_mark_end(lb_batch* b, float* ms, int64_t* launches);
 int lb_batch_sync(lb_batch* b);
+/* Order `b`'s stream after everything enqueued on `prev`'s stream so far (event record + stream
+ * wait; no host synchronisation).  decode_stream_raw uses it so two pipelined batches' search
+ * kernels run back to back instead of sharing the SMs, while the next batch's H2D copy and
+ * prologue, and the host's result assembly, still overlap the running search. */
+int lb_batch_after(lb_batch* b, lb_batch* prev);
 
 /* Standalone acoustic prologue (logits.py:119-130) on device `device`: host in/out. */
 int lb_log_softmax_host(const float* x, int64_t rows, int32_t cols, double alpha,

@@ -225,6 +225,7 @@ _SIGS = {
     "lb_batch_mark_begin": (C.c_int, [_P]),
     "lb_batch_mark_end": (C.c_int, [_P, _P, _P]),
     "lb_batch_sync": (C.c_int, [_P]),
+    "lb_batch_after": (C.c_int, [_P, _P]),
     "lb_stream_create": (C.c_int, [_I32, _P]),
     "lb_stream_destroy": (C.c_int, [_P]),
     "lb_host_alloc": (C.c_int, [_I64, _P]),

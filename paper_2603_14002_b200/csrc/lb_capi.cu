@@ -454,6 +454,7 @@ static int batch_alloc(lb_batch* b, int32_t max_trials, int32_t max_frames) {
   d.D = b->d_D;
   CK(cudaEventCreate(&b->ev0));
   CK(cudaEventCreate(&b->ev1));
+  CK(cudaEventCreateWithFlags(&b->evd, cudaEventDisableTiming));
   b->T_host.assign(B, 0);
   return LB_OK;
 }
@@ -486,6 +487,7 @@ int lb_batch_destroy(lb_batch* b) {
     if (p) cudaFreeHost(p);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
+  if (b->evd) cudaEventDestroy(b->evd);
   delete b;
   return LB_OK;
 }
@@ -1142,6 +1144,14 @@ int lb_batch_mark_end(lb_batch* b, float* ms, int64_t* launches) {
   CK(cudaEventElapsedTime(&t, b->ev0, b->ev1));
   if (ms) *ms = t;
   if (launches) *launches = (int64_t)(lbk::g_launches - b->launch_mark);
+  return LB_OK;
+}
+
+int lb_batch_after(lb_batch* b, lb_batch* prev) {
+  if (!b || !prev) return fail(LB_ERR_ARG, "null argument");
+  if (b == prev || b->st == prev->st) return LB_OK;  // one stream is already ordered
+  CK(cudaEventRecord(prev->evd, prev->st));
+  CK(cudaStreamWaitEvent(b->st, prev->evd, 0));
   return LB_OK;
 }
 

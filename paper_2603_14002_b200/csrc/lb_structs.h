@@ -73,6 +73,7 @@ struct lb_batch {
   int injective = -1;  // texts_injective(m), computed on first use
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evd = nullptr;  // lb_batch_after: end of this batch's enqueued work
   unsigned long long launch_mark = 0;
 };
 namespace lbh {

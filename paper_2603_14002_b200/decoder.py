@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import gc
+import os
 import threading
 import time
 import weakref
@@ -485,6 +486,10 @@ class DeviceBatch:
     def sync(self):
         N.check(N.lib().lb_batch_sync(self.h))
 
+    def after(self, prev: "DeviceBatch"):
+        """Order this batch's later launches after everything already enqueued on `prev`."""
+        N.check(N.lib().lb_batch_after(self.h, prev.h))
+
     def results(self):
         """[(text, score, nbest)] per trial (None for failed trials).  The library ranks and
         dedupes on the host (lb_batch_results_size); the CPython binding `_lb_results` builds the
@@ -751,6 +756,9 @@ def _raw_array(raws):
     return _stack([np.asarray(getattr(r, "frames", r), dtype=np.float32) for r in raws], np.float32)
 
 
+_SERIAL_SEARCH = os.environ.get("LB_STREAM_OVERLAP", "0") != "1"
+
+
 def decode_stream_raw(batches, config, tt, lm, scorer, final_llm_only: bool = False,
                       device: int = 0):
     """Generator over many batches of raw logits (each a RawLogits list or `(array, frames)`):
@@ -779,6 +787,11 @@ def decode_stream_raw(batches, config, tt, lm, scorer, final_llm_only: bool = Fa
         batch = dm.pipeline_batch(cfg, slot, arr.shape[0], max(arr.shape[1], 1))
         t0 = time.perf_counter()
         batch.load_logits(arr, frames)
+        if _SERIAL_SEARCH and pending and pending[-1][2] is None:
+            # the previous batch's launches are all issued: this batch's H2D copy and prologue
+            # overlap its search, the search kernels themselves run back to back (two
+            # persistent searches sharing the SMs and the L2 took ~20% longer per batch)
+            batch.after(pending[-1][0])
         item = [batch, t0, _search_steps(batch, cfg, scorer, model, final_llm_only)]
         pending.append(item)
         try:  # launch right away (up to its first fusion event): the GPU never waits on the host
