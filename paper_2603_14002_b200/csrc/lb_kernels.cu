@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <cstdint>
 
 #include "lb_device.cuh"
@@ -3000,6 +3001,39 @@ cudaError_t rowmax(double* d, int64_t rows, int32_t V, int32_t pitch, cudaStream
   return cudaGetLastError();
 }
 
+// Bulk L2 prefetch of the read-only search images (cuckoo n-gram buckets, compact lexicon
+// records) at the start of a decode: fire-and-forget `cp.async.bulk.prefetch.L2` in 32 KB
+// pieces, so the image lines are L2-resident before the frame loop's probes reach them instead
+// of missing to HBM one dependent probe round at a time during the first frames.  Opt-in
+// (LB_L2_PREFETCH=1): measured 4.746 vs 4.763 ms per config-2 step without/with it -- the
+// n-gram probe rounds cost the same with the images already L2-resident.
+__device__ __forceinline__ void l2_prefetch_range(const void* base, size_t bytes, int gtid,
+                                                  int gthreads) {
+  constexpr size_t PIECE = 32768;
+  const char* p = reinterpret_cast<const char*>(base);
+  const size_t n = (bytes + PIECE - 1) / PIECE;
+  for (size_t i = gtid; i < n; i += gthreads) {
+    const size_t off = i * PIECE;
+    const unsigned len = (unsigned)((min(PIECE, bytes - off) + 15) & ~(size_t)15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(len)
+                 : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(128) l2_prefetch_kernel(ModelDev m) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x, n = gridDim.x * blockDim.x;
+  l2_prefetch_range(m.ng, (size_t)m.ng_nb * NG_WAYS * sizeof(NgRec), g, n);
+  l2_prefetch_range(m.lex, (size_t)m.S * sizeof(LexRec), g, n);
+}
+
+static int l2_prefetch_enabled() {
+  static const int on = [] {
+    const char* e = getenv("LB_L2_PREFETCH");
+    return e ? atoi(e) : 0;
+  }();
+  return on;
+}
+
 cudaError_t reset(const ModelDev& m, const BatchDev& b, cudaStream_t st) {
   reset_kernel<<<(b.B + 127) / 128, 128, 0, st>>>(m, b);
   ++g_launches;
@@ -3009,6 +3043,10 @@ cudaError_t reset(const ModelDev& m, const BatchDev& b, cudaStream_t st) {
 cudaError_t frames(const ModelDev& m, const CfgDev& c, const BatchDev& b, const Layout& L, int t0,
                    int t1, int fusion_mode, double scale, cudaStream_t st) {
   const size_t sm = (size_t)L.smem_bytes;
+  if (t0 == 0 && l2_prefetch_enabled() && m.ng != nullptr && m.lex != nullptr) {
+    l2_prefetch_kernel<<<16, 128, 0, st>>>(m);  // first frame range of a decode
+    ++g_launches;
+  }
   if (L.small) {
     // the phase-timer build is a separate instantiation: the production kernel carries no
     // timer state (it would cost registers at the 96-register cap)
