@@ -2444,8 +2444,14 @@ __global__ void __launch_bounds__(small::NT, 2)
 // =====================================================================================
 __device__ int64_t block_excl_scan(int64_t v, int64_t* out_excl);
 
-constexpr int CLOSE_NT = 512;  // 16 warps: the open beams' closures are independent
-__global__ void __launch_bounds__(CLOSE_NT) close_kernel(ModelDev m, CfgDev c, BatchDev b) {
+#ifndef LB_CLOSE_NT
+#define LB_CLOSE_NT 512
+#endif
+#ifndef LB_CLOSE_MINB
+#define LB_CLOSE_MINB 1
+#endif
+constexpr int CLOSE_NT = LB_CLOSE_NT;  // 16 warps: the open beams' closures are independent
+__global__ void __launch_bounds__(CLOSE_NT, LB_CLOSE_MINB) close_kernel(ModelDev m, CfgDev c, BatchDev b) {
   constexpr int NT = CLOSE_NT, NW = NT / 32;
   __shared__ WarpScratch wsc[NW];
   __shared__ int s_ncount, s_fail;
@@ -2883,6 +2889,66 @@ __global__ void log_softmax_kernel(const float* x, int64_t rows, int32_t V, int3
   if (out_pitch > V && lane == 0) orow[V] = mx2;
 }
 
+// K1, row-per-thread form (the production launch): a CTA stages LSM_ROWS rows of fp32 logits
+// in shared memory with coalesced loads, every thread runs one row's log-softmax with the same
+// operations in the same order as log_softmax_kernel (max, exp(x - max), numpy's 8-accumulator
+// pairwise sum + sequential tail, log), and the fp64 rows leave through a shared staging buffer
+// with coalesced stores.  One warp per row left 23 of 64 lane slots idle and serialised the sum
+// on one lane; here the 41 exps of a row are independent instructions of one thread.
+constexpr int LSM_ROWS = 64;
+__global__ void __launch_bounds__(LSM_ROWS) log_softmax_rows_kernel(
+    const float* __restrict__ x, int64_t rows, int32_t V, int32_t in_pitch, double alpha,
+    double* __restrict__ out, int32_t out_pitch) {
+  extern __shared__ __align__(16) char lsm[];
+  const int W = out_pitch > V ? V + 1 : V;  // columns written per row (slot V: the row max)
+  const int SW = W | 1;                      // odd staging stride: conflict-free row access
+  double* ob = reinterpret_cast<double*>(lsm);
+  float* xin = reinterpret_cast<float*>(ob + LSM_ROWS * SW);
+  const int64_t r0 = (int64_t)blockIdx.x * LSM_ROWS;
+  const int nr = (int)(rows - r0 < LSM_ROWS ? rows - r0 : (int64_t)LSM_ROWS);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < nr * V; i += LSM_ROWS) {
+    const int r = i / V, c = i - r * V;
+    xin[r * V + c] = __ldcs(x + (r0 + r) * in_pitch + c);
+  }
+  __syncthreads();
+  if (tid < nr) {
+    const float* xr = xin + tid * V;
+    double* e = ob + tid * SW;
+    double mx = -DBL_MAX;
+    for (int i = 0; i < V; ++i) mx = fmax(mx, (double)xr[i]);
+    for (int i = 0; i < V; ++i) e[i] = exp(xsub((double)xr[i], mx));
+    double res = 0.0;
+    if (V < 8) {
+      for (int i = 0; i < V; ++i) res = xadd(res, e[i]);
+    } else {
+      const int full = V - (V % 8);
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = e[j];
+      for (int i = 8; i < full; i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = xadd(r[j], e[i + j]);
+      }
+      res = xadd(xadd(xadd(r[0], r[1]), xadd(r[2], r[3])), xadd(xadd(r[4], r[5]), xadd(r[6], r[7])));
+      for (int i = full; i < V; ++i) res = xadd(res, e[i]);
+    }
+    const double lse = xadd(mx, log(res));
+    double m2 = -DBL_MAX;
+    for (int i = 0; i < V; ++i) {
+      const double o = xmul(alpha, xsub((double)xr[i], lse));
+      e[i] = o;
+      m2 = fmax(m2, o);
+    }
+    if (W > V) e[V] = m2;
+  }
+  __syncthreads();
+  for (int i = tid; i < nr * W; i += LSM_ROWS) {
+    const int r = i / W, c = i - r * W;
+    out[(r0 + r) * out_pitch + c] = ob[r * SW + c];
+  }
+}
+
 // row maximum into slot V of a padded log-prob matrix that was uploaded as is
 __global__ void rowmax_kernel(double* d, int64_t rows, int32_t V, int32_t pitch) {
   const int lane = threadIdx.x & 31;
@@ -2985,11 +3051,32 @@ cudaError_t pad_table(int32_t* dst, const int32_t* src, int32_t S, int32_t V, in
   return cudaGetLastError();
 }
 
+static int lsm_rows_enabled() {  // LB_LSM_ROWS=0: the warp-per-row K1 (A/B)
+  static const int on = [] {
+    const char* e = getenv("LB_LSM_ROWS");
+    return e ? atoi(e) : 1;
+  }();
+  return on;
+}
+
 cudaError_t log_softmax(const float* x, int64_t rows, int32_t V, int32_t in_pitch, double alpha,
                         double* out, int32_t out_pitch, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  log_softmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(x, rows, V, in_pitch, alpha, out,
-                                                                 out_pitch);
+  if (lsm_rows_enabled()) {
+    const int W = out_pitch > V ? V + 1 : V;
+    const size_t smem = (size_t)LSM_ROWS * ((W | 1) * sizeof(double) + V * sizeof(float));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(log_softmax_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           LSM_ROWS * (65 * 8 + 64 * 4));
+      attr = true;
+    }
+    log_softmax_rows_kernel<<<(unsigned)((rows + LSM_ROWS - 1) / LSM_ROWS), LSM_ROWS, smem, st>>>(
+        x, rows, V, in_pitch, alpha, out, out_pitch);
+  } else {
+    log_softmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(x, rows, V, in_pitch, alpha,
+                                                                   out, out_pitch);
+  }
   ++g_launches;
   return cudaGetLastError();
 }

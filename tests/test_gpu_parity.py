@@ -2,6 +2,9 @@
 golden fixtures.  Bar: bit-exact texts, fp64 scores, n-best lists, event counts, per-frame
 ordered beams (hash lanes, prefix ids, last token, score) and error messages."""
 
+import os
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -23,6 +26,37 @@ def test_prologue_kernel_vs_numpy():
         want = np.asarray(case["d"])
         # numpy's SIMD exp is not libm-exact: allow a few ulps (north star: "within a few ulps")
         np.testing.assert_allclose(got, want, rtol=8 * np.finfo(np.float64).eps, atol=1e-15)
+
+
+def test_prologue_row_kernel_equals_warp_kernel(tmp_path):
+    """K1's row-per-thread form (default) and the warp-per-row form (LB_LSM_ROWS=0, run in a
+    child process: the switch is read once per process) give bit-identical rows and row maxima,
+    for every width 1..64, ragged row counts and a padded output pitch."""
+    import subprocess
+    import sys
+
+    from paper_2603_14002_b200 import _native
+
+    rng = np.random.default_rng(5)
+    cases = [(rng.normal(0, 3, size=(int(n), v)).astype(np.float32), 0.7 + v / 100)
+             for v, n in zip(range(1, 65), rng.integers(1, 300, size=64))]
+    np.savez(tmp_path / "in.npz", *[c[0] for c in cases])
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "from paper_2603_14002_b200 import _native\n"
+        "z = np.load(%r); out = {}\n"
+        "for i in range(64):\n"
+        "    x = z['arr_%%d' %% i]; out['o%%d' %% i] = _native.log_softmax_host(x, 0.7 + x.shape[1] / 100)\n"
+        "np.savez(%r, **out)\n" % (str(Path(__file__).resolve().parents[1]),
+                                     str(tmp_path / "in.npz"), str(tmp_path / "warp.npz")))
+    env = dict(os.environ, LB_LSM_ROWS="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+    warp = np.load(tmp_path / "warp.npz")
+    for i, (x, alpha) in enumerate(cases):
+        got = _native.log_softmax_host(x, alpha)
+        assert got.tobytes() == warp["o%d" % i].tobytes(), (i, x.shape)
+    # the padded batch layout (slot V = row max) through a device batch is covered by the
+    # raw-logit full-size tests (tests/test_full_size.py)
 
 
 def test_device_score_word_hand_cases():
