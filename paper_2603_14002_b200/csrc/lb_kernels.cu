@@ -396,15 +396,20 @@ __device__ __forceinline__ CompHdr small_hdr(const LexRec& r, int off) {
 // (-total, seq) -- candidates arrive in increasing seq, so strict '>' keeps ties stable.
 // On return (lane 0 authoritative): *outn = kept entries (written to outents), or -1 when no
 // candidate survived (beam killed: *score = NEG_INF, decoder.py:223-225).
-__device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const BatchDev& b, int trial,
-                                 const Ent* pents, int pn, const CompHdr ch, WarpScratch* ws,
-                                 Ent* outents, int* outn, double* score, int* node_counter,
-                                 int* fail, unsigned& calls, unsigned& probes) {
-  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+// NP = pairs per warp round: 4 (8 lanes per pair, one cuckoo bucket per lane) or 8 (4 lanes per
+// pair probing both buckets, quad_score_word); the candidates reach the top-O list in the same
+// order either way, so both give identical results.
+template <int NP, class Scratch>
+__device__ void warp_apply_ngram_t(const ModelDev& m, const CfgDev& c, const BatchDev& b, int trial,
+                                   const Ent* pents, int pn, const CompHdr ch, Scratch* ws,
+                                   Ent* outents, int* outn, double* score, int* node_counter,
+                                   int* fail, unsigned& calls, unsigned& probes) {
+  static_assert(NP == 4 || NP == 8, "4 or 8 pairs per round");
+  const int lane = threadIdx.x & 31, sub = lane & (32 / NP - 1), grp = lane / (32 / NP);
   const int ns = ch.ns;
   const int npairs = pn * ns;
   int ntop = 0;
-  for (int base = 0; base < npairs; base += 4) {
+  for (int base = 0; base < npairs; base += NP) {
     const int pi = base + grp;
     const bool act = pi < npairs;
     int e = 0, s = 0, w = -1, surf = -1;
@@ -426,7 +431,8 @@ __device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const Batch
     uint32_t hh[MAXH] = {E.h[0], E.h[1], E.h[2]};
     double hb[MAXH] = {E.bo[0], E.bo[1], E.bo[2]};
     WordScore sw;
-    group_score_word(m, act, hh, E.hlen, hb, w, sw, probes);
+    if (NP == 4) group_score_word(m, act, hh, E.hlen, hb, w, sw, probes);
+    else quad_score_word(m, act, hh, E.hlen, hb, w, sw, probes);
     if (sub == 0) {
       NgCand& pc = ws->pending[grp];
       pc.valid = 0;
@@ -450,7 +456,7 @@ __device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const Batch
     }
     __syncwarp();
     if (lane == 0) {
-      for (int g = 0; g < 4; ++g) {
+      for (int g = 0; g < NP; ++g) {
         const NgCand& cd = ws->pending[g];
         if (!cd.valid) continue;
         int pos = ntop;
@@ -503,6 +509,16 @@ __device__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c, const Batch
     }
   }
   __syncwarp();
+}
+
+__device__ __forceinline__ void warp_apply_ngram(const ModelDev& m, const CfgDev& c,
+                                                 const BatchDev& b, int trial, const Ent* pents,
+                                                 int pn, const CompHdr ch, WarpScratch* ws,
+                                                 Ent* outents, int* outn, double* score,
+                                                 int* node_counter, int* fail, unsigned& calls,
+                                                 unsigned& probes) {
+  warp_apply_ngram_t<4>(m, c, b, trial, pents, pn, ch, ws, outents, outn, score, node_counter,
+                        fail, calls, probes);
 }
 
 // insertion sort of <= OMAX entries by (-total, seq) (decoder.py:369)
@@ -2453,7 +2469,16 @@ __device__ int64_t block_excl_scan(int64_t v, int64_t* out_excl);
 constexpr int CLOSE_NT = LB_CLOSE_NT;  // 16 warps: the open beams' closures are independent
 __global__ void __launch_bounds__(CLOSE_NT, LB_CLOSE_MINB) close_kernel(ModelDev m, CfgDev c, BatchDev b) {
   constexpr int NT = CLOSE_NT, NW = NT / 32;
-  __shared__ WarpScratch wsc[NW];
+#ifdef LB_CLOSE_NP4
+  constexpr int CNP = 4;
+#else
+  constexpr int CNP = 8;
+#endif
+  struct CloseScratch {
+    NgCand top[OMAX];
+    NgCand pending[CNP];
+  };
+  __shared__ CloseScratch wsc[NW];
   __shared__ int s_ncount, s_fail;
   __shared__ unsigned s_calls, s_probes;
   extern __shared__ __align__(16) Ent close_tmp[];
@@ -2475,7 +2500,9 @@ __global__ void __launch_bounds__(CLOSE_NT, LB_CLOSE_MINB) close_kernel(ModelDev
   for (int i = warp; i < K; i += NW) {
     const int st = b.prefix[hb + i];
     if (st == 0) continue;  // root: nothing pending
-    const CompHdr ch = comp_hdr(m.table + (size_t)st * m.VP, m.V);
+    // completion header from the compact record (L2-resident after the frame loop; the padded
+    // table row it replaces is not touched by the frame kernels)
+    const CompHdr ch = lex_hdr_g(m, m.lex[st], st);
     if (ch.ns == 0) {
       if (lane == 0) b.score[hb + i] = NEG_INF;
       continue;
@@ -2483,8 +2510,8 @@ __global__ void __launch_bounds__(CLOSE_NT, LB_CLOSE_MINB) close_kernel(ModelDev
     double sc = b.score[hb + i];
     int outn = -1;
     Ent* pe = b.ents + (hb + i) * O;
-    warp_apply_ngram(m, c, b, trial, pe, b.nent[hb + i], ch, &wsc[warp], tmp, &outn, &sc,
-                     &s_ncount, &s_fail, calls, probes);
+    warp_apply_ngram_t<CNP>(m, c, b, trial, pe, b.nent[hb + i], ch, &wsc[warp], tmp, &outn, &sc,
+                            &s_ncount, &s_fail, calls, probes);
     if (lane == 0) {
       b.score[hb + i] = sc;
       if (outn >= 0) {
