@@ -2479,7 +2479,7 @@ __global__ void __launch_bounds__(CLOSE_NT, LB_CLOSE_MINB) close_kernel(ModelDev
     NgCand pending[CNP];
   };
   __shared__ CloseScratch wsc[NW];
-  __shared__ int s_ncount, s_fail;
+  __shared__ int s_ncount, s_fail, s_next;
   __shared__ unsigned s_calls, s_probes;
   extern __shared__ __align__(16) Ent close_tmp[];
   const int trial = blockIdx.x;
@@ -2494,33 +2494,47 @@ __global__ void __launch_bounds__(CLOSE_NT, LB_CLOSE_MINB) close_kernel(ModelDev
     s_fail = 0;
     s_calls = 0;
     s_probes = 0;
+    s_next = NW;
   }
   __syncthreads();
   unsigned calls = 0, probes = 0;
-  for (int i = warp; i < K; i += NW) {
-    const int st = b.prefix[hb + i];
-    if (st == 0) continue;  // root: nothing pending
-    // completion header from the compact record (L2-resident after the frame loop; the padded
-    // table row it replaces is not touched by the frame kernels)
-    const CompHdr ch = lex_hdr_g(m, m.lex[st], st);
-    if (ch.ns == 0) {
-      if (lane == 0) b.score[hb + i] = NEG_INF;
-      continue;
-    }
-    double sc = b.score[hb + i];
-    int outn = -1;
-    Ent* pe = b.ents + (hb + i) * O;
-    warp_apply_ngram_t<CNP>(m, c, b, trial, pe, b.nent[hb + i], ch, &wsc[warp], tmp, &outn, &sc,
-                            &s_ncount, &s_fail, calls, probes);
-    if (lane == 0) {
-      b.score[hb + i] = sc;
-      if (outn >= 0) {
-        b.nent[hb + i] = outn;
-        for (int q = 0; q < outn; ++q) pe[q] = tmp[q];
+  // beams handed out dynamically (first NW statically): closures differ in cost (root beams
+  // are free, homophone-heavy states take several probe rounds), so a fixed round-robin left
+  // most warps waiting at the compaction barrier for the slowest one
+  for (int i = warp; i < K;) {
+    do {
+      const int st = b.prefix[hb + i];
+      if (st == 0) continue;  // root: nothing pending
+      // completion header from the compact record (L2-resident after the frame loop; the padded
+      // table row it replaces is not touched by the frame kernels)
+      const CompHdr ch = lex_hdr_g(m, m.lex[st], st);
+      if (ch.ns == 0) {
+        if (lane == 0) b.score[hb + i] = NEG_INF;
+        continue;
       }
-      b.prefix[hb + i] = 0;
-    }
-    __syncwarp();
+      double sc = b.score[hb + i];
+      int outn = -1;
+      Ent* pe = b.ents + (hb + i) * O;
+      warp_apply_ngram_t<CNP>(m, c, b, trial, pe, b.nent[hb + i], ch, &wsc[warp], tmp, &outn, &sc,
+                              &s_ncount, &s_fail, calls, probes);
+      outn = __shfl_sync(FULLMASK, outn, 0);  // lane 0 is authoritative
+      if (lane == 0) {
+        b.score[hb + i] = sc;
+        if (outn >= 0) b.nent[hb + i] = outn;
+        b.prefix[hb + i] = 0;
+      }
+      static_assert(sizeof(Ent) % 8 == 0, "Ent copies as 8-byte words");
+      if (outn > 0) {  // the kept entries (lane 0 built them in shared memory): whole warp copies
+        const int nw = outn * (int)(sizeof(Ent) / 8);
+        const uint2* src = reinterpret_cast<const uint2*>(tmp);
+        uint2* dst = reinterpret_cast<uint2*>(pe);
+        for (int q = lane; q < nw; q += 32) dst[q] = src[q];
+      }
+      __syncwarp();
+    } while (0);
+    int nx = 0;
+    if (lane == 0) nx = atomicAdd(&s_next, 1);
+    i = __shfl_sync(FULLMASK, nx, 0);
   }
   atomicAdd(&s_calls, calls);
   atomicAdd(&s_probes, probes);
