@@ -2930,64 +2930,72 @@ __global__ void log_softmax_kernel(const float* x, int64_t rows, int32_t V, int3
   if (out_pitch > V && lane == 0) orow[V] = mx2;
 }
 
-// K1, row-per-thread form (the production launch): a CTA stages LSM_ROWS rows of fp32 logits
-// in shared memory with coalesced loads, every thread runs one row's log-softmax with the same
-// operations in the same order as log_softmax_kernel (max, exp(x - max), numpy's 8-accumulator
-// pairwise sum + sequential tail, log), and the fp64 rows leave through a shared staging buffer
-// with coalesced stores.  One warp per row left 23 of 64 lane slots idle and serialised the sum
-// on one lane; here the 41 exps of a row are independent instructions of one thread.
-constexpr int LSM_ROWS = 64;
-__global__ void __launch_bounds__(LSM_ROWS) log_softmax_rows_kernel(
+// K1, eight lanes per row (the production launch): lane t of a row's 8-lane group owns the
+// columns i = t (mod 8), so it holds numpy's pairwise accumulator r[t] (columns below
+// V - V % 8, in order) plus at most one tail column; the accumulators combine by xor shuffles
+// in numpy's order ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and the tail columns are then added
+// one by one, exactly as log_softmax_kernel does with one warp per row.  No shared memory and
+// few registers: ~60 resident warps per SM hide the fp64 exp latency the warp-per-row form
+// (41 of 64 lane slots busy, the sum serialised on lane 0) and a row-per-thread form (smem-
+// limited to 12 warps per SM) could not.
+__global__ void __launch_bounds__(256) log_softmax_oct_kernel(
     const float* __restrict__ x, int64_t rows, int32_t V, int32_t in_pitch, double alpha,
     double* __restrict__ out, int32_t out_pitch) {
-  extern __shared__ __align__(16) char lsm[];
-  const int W = out_pitch > V ? V + 1 : V;  // columns written per row (slot V: the row max)
-  const int SW = W | 1;                      // odd staging stride: conflict-free row access
-  double* ob = reinterpret_cast<double*>(lsm);
-  float* xin = reinterpret_cast<float*>(ob + LSM_ROWS * SW);
-  const int64_t r0 = (int64_t)blockIdx.x * LSM_ROWS;
-  const int nr = (int)(rows - r0 < LSM_ROWS ? rows - r0 : (int64_t)LSM_ROWS);
-  const int tid = threadIdx.x;
-  for (int i = tid; i < nr * V; i += LSM_ROWS) {
-    const int r = i / V, c = i - r * V;
-    xin[r * V + c] = __ldcs(x + (r0 + r) * in_pitch + c);
+  const int lane = threadIdx.x & 31, t = lane & 7, gbase = lane & ~7;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const bool live = row < rows;  // whole 8-lane groups are live or not; shuffles stay uniform
+  const float* xr = x + (live ? row : 0) * in_pitch;
+  const int full = V >= 8 ? V - (V % 8) : 0;
+  double xv[8], e[8];
+  double mx = -DBL_MAX;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = t + 8 * k;
+    xv[k] = (live && i < V) ? (double)__ldcs(xr + i) : -DBL_MAX;
+    mx = fmax(mx, xv[k]);
   }
-  __syncthreads();
-  if (tid < nr) {
-    const float* xr = xin + tid * V;
-    double* e = ob + tid * SW;
-    double mx = -DBL_MAX;
-    for (int i = 0; i < V; ++i) mx = fmax(mx, (double)xr[i]);
-    for (int i = 0; i < V; ++i) e[i] = exp(xsub((double)xr[i], mx));
-    double res = 0.0;
-    if (V < 8) {
-      for (int i = 0; i < V; ++i) res = xadd(res, e[i]);
-    } else {
-      const int full = V - (V % 8);
-      double r[8];
+  mx = fmax(mx, __shfl_xor_sync(FULLMASK, mx, 1));
+  mx = fmax(mx, __shfl_xor_sync(FULLMASK, mx, 2));
+  mx = fmax(mx, __shfl_xor_sync(FULLMASK, mx, 4));
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = e[j];
-      for (int i = 8; i < full; i += 8) {
+  for (int k = 0; k < 8; ++k) e[k] = (t + 8 * k < V) ? exp(xsub(xv[k], mx)) : 0.0;
+  double res = 0.0;
+  if (V < 8) {
+    for (int k = 0; k < V; ++k) res = xadd(res, __shfl_sync(FULLMASK, e[0], gbase + k));
+  } else {
+    double r = e[0];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = xadd(r[j], e[i + j]);
-      }
-      res = xadd(xadd(xadd(r[0], r[1]), xadd(r[2], r[3])), xadd(xadd(r[4], r[5]), xadd(r[6], r[7])));
-      for (int i = full; i < V; ++i) res = xadd(res, e[i]);
-    }
-    const double lse = xadd(mx, log(res));
-    double m2 = -DBL_MAX;
-    for (int i = 0; i < V; ++i) {
-      const double o = xmul(alpha, xsub((double)xr[i], lse));
-      e[i] = o;
+    for (int k = 1; k < 8; ++k)
+      if (t + 8 * k < full) r = xadd(r, e[k]);
+    const double r1 = __shfl_xor_sync(FULLMASK, r, 1);
+    const double s01 = (t & 1) ? xadd(r1, r) : xadd(r, r1);
+    const double t1 = __shfl_xor_sync(FULLMASK, s01, 2);
+    const double s03 = (t & 2) ? xadd(t1, s01) : xadd(s01, t1);
+    const double t2 = __shfl_xor_sync(FULLMASK, s03, 4);
+    res = (t & 4) ? xadd(t2, s03) : xadd(s03, t2);
+    // tail column full + k lives in lane k's element full / 8
+    double tail = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (8 * k == full) tail = e[k];
+    for (int k = 0; k < V - full; ++k) res = xadd(res, __shfl_sync(FULLMASK, tail, gbase + k));
+  }
+  const double lse = xadd(mx, log(res));
+  double m2 = -DBL_MAX;
+  double* orow = out + (live ? row : 0) * out_pitch;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = t + 8 * k;
+    if (i < V) {
+      const double o = xmul(alpha, xsub(xv[k], lse));
       m2 = fmax(m2, o);
+      if (live) orow[i] = o;
     }
-    if (W > V) e[V] = m2;
   }
-  __syncthreads();
-  for (int i = tid; i < nr * W; i += LSM_ROWS) {
-    const int r = i / W, c = i - r * W;
-    out[(r0 + r) * out_pitch + c] = ob[r * SW + c];
-  }
+  m2 = fmax(m2, __shfl_xor_sync(FULLMASK, m2, 1));
+  m2 = fmax(m2, __shfl_xor_sync(FULLMASK, m2, 2));
+  m2 = fmax(m2, __shfl_xor_sync(FULLMASK, m2, 4));
+  if (live && t == 0 && out_pitch > V) orow[V] = m2;  // padded layout: slot V = row max
 }
 
 // row maximum into slot V of a padded log-prob matrix that was uploaded as is
@@ -3092,7 +3100,7 @@ cudaError_t pad_table(int32_t* dst, const int32_t* src, int32_t S, int32_t V, in
   return cudaGetLastError();
 }
 
-static int lsm_rows_enabled() {  // LB_LSM_ROWS=0: the warp-per-row K1 (A/B)
+static int lsm_rows_enabled() {  // LB_LSM_ROWS=0: the warp-per-row K1 (A/B, parity test)
   static const int on = [] {
     const char* e = getenv("LB_LSM_ROWS");
     return e ? atoi(e) : 1;
@@ -3104,15 +3112,8 @@ cudaError_t log_softmax(const float* x, int64_t rows, int32_t V, int32_t in_pitc
                         double* out, int32_t out_pitch, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
   if (lsm_rows_enabled()) {
-    const int W = out_pitch > V ? V + 1 : V;
-    const size_t smem = (size_t)LSM_ROWS * ((W | 1) * sizeof(double) + V * sizeof(float));
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(log_softmax_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           LSM_ROWS * (65 * 8 + 64 * 4));
-      attr = true;
-    }
-    log_softmax_rows_kernel<<<(unsigned)((rows + LSM_ROWS - 1) / LSM_ROWS), LSM_ROWS, smem, st>>>(
+    const int64_t threads = rows * 8;
+    log_softmax_oct_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
         x, rows, V, in_pitch, alpha, out, out_pitch);
   } else {
     log_softmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(x, rows, V, in_pitch, alpha,
