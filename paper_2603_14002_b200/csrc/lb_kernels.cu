@@ -2622,10 +2622,15 @@ __global__ void __launch_bounds__(CLOSE_NT, LB_CLOSE_MINB) close_kernel(ModelDev
 // =====================================================================================
 // device n-gram scorer fusion (apply_llm with StubScorer(ngram_model, scale) semantics)
 // =====================================================================================
-__global__ void __launch_bounds__(256) device_fusion_kernel(ModelDev m, CfgDev c, BatchDev b,
-                                                            int final_, double scale,
-                                                            int min_frames) {
-  constexpr int NT = 256, NW = NT / 32;
+#ifndef LB_FUSION_NT
+#define LB_FUSION_NT 512
+#endif
+constexpr int FUSION_NT = LB_FUSION_NT;  // 16 warps, two CTAs per SM: every utterance in one wave
+__global__ void __launch_bounds__(FUSION_NT, 2) device_fusion_kernel(ModelDev m, CfgDev c,
+                                                                     BatchDev b, int final_,
+                                                                     double scale,
+                                                                     int min_frames) {
+  constexpr int NT = FUSION_NT, NW = NT / 32;
   __shared__ unsigned s_probes;
   const int trial = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -3221,7 +3226,7 @@ cudaError_t close(const ModelDev& m, const CfgDev& c, const BatchDev& b, cudaStr
 
 cudaError_t device_ngram_fusion(const ModelDev& m, const CfgDev& c, const BatchDev& b, int final_,
                                 double scale, int min_frames, cudaStream_t st) {
-  device_fusion_kernel<<<b.B, 256, 0, st>>>(m, c, b, final_, scale, min_frames);
+  device_fusion_kernel<<<b.B, FUSION_NT, 0, st>>>(m, c, b, final_, scale, min_frames);
   ++g_launches;
   return cudaGetLastError();
 }
