@@ -2951,38 +2951,40 @@ __global__ void __launch_bounds__(256) log_softmax_oct_kernel(
   const bool live = row < rows;  // whole 8-lane groups are live or not; shuffles stay uniform
   const float* xr = x + (live ? row : 0) * in_pitch;
   const int full = V >= 8 ? V - (V % 8) : 0;
-  double xv[8], e[8];
+  float xf[8];  // the row's columns t, t+8, ... as read (fp32: 8 registers, no fp64 copies)
   double mx = -DBL_MAX;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int i = t + 8 * k;
-    xv[k] = (live && i < V) ? (double)__ldcs(xr + i) : -DBL_MAX;
-    mx = fmax(mx, xv[k]);
+    xf[k] = (live && i < V) ? __ldcs(xr + i) : 0.f;
+    if (i < V) mx = fmax(mx, (double)xf[k]);
   }
   mx = fmax(mx, __shfl_xor_sync(FULLMASK, mx, 1));
   mx = fmax(mx, __shfl_xor_sync(FULLMASK, mx, 2));
   mx = fmax(mx, __shfl_xor_sync(FULLMASK, mx, 4));
+  // exps consumed as produced: r = numpy's accumulator r[t] over the columns below `full`
+  // (in column order), e0 = this lane's first exp (V < 8), tail = its column full + t
+  double r = 0.0, e0 = 0.0, tail = 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) e[k] = (t + 8 * k < V) ? exp(xsub(xv[k], mx)) : 0.0;
+  for (int k = 0; k < 8; ++k) {
+    const int i = t + 8 * k;
+    if (i < V) {
+      const double ek = exp(xsub((double)xf[k], mx));
+      if (k == 0) e0 = ek;
+      if (i < full) r = k == 0 ? ek : xadd(r, ek);
+      else tail = ek;  // i >= full: the (only) tail column of this lane
+    }
+  }
   double res = 0.0;
   if (V < 8) {
-    for (int k = 0; k < V; ++k) res = xadd(res, __shfl_sync(FULLMASK, e[0], gbase + k));
+    for (int k = 0; k < V; ++k) res = xadd(res, __shfl_sync(FULLMASK, e0, gbase + k));
   } else {
-    double r = e[0];
-#pragma unroll
-    for (int k = 1; k < 8; ++k)
-      if (t + 8 * k < full) r = xadd(r, e[k]);
     const double r1 = __shfl_xor_sync(FULLMASK, r, 1);
     const double s01 = (t & 1) ? xadd(r1, r) : xadd(r, r1);
     const double t1 = __shfl_xor_sync(FULLMASK, s01, 2);
     const double s03 = (t & 2) ? xadd(t1, s01) : xadd(s01, t1);
     const double t2 = __shfl_xor_sync(FULLMASK, s03, 4);
     res = (t & 4) ? xadd(t2, s03) : xadd(s03, t2);
-    // tail column full + k lives in lane k's element full / 8
-    double tail = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (8 * k == full) tail = e[k];
     for (int k = 0; k < V - full; ++k) res = xadd(res, __shfl_sync(FULLMASK, tail, gbase + k));
   }
   const double lse = xadd(mx, log(res));
@@ -2992,7 +2994,7 @@ __global__ void __launch_bounds__(256) log_softmax_oct_kernel(
   for (int k = 0; k < 8; ++k) {
     const int i = t + 8 * k;
     if (i < V) {
-      const double o = xmul(alpha, xsub(xv[k], lse));
+      const double o = xmul(alpha, xsub((double)xf[k], lse));
       m2 = fmax(m2, o);
       if (live) orow[i] = o;
     }
