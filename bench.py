@@ -548,8 +548,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "frames_kernel (K2)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": _profile_traffic("r2g_frames_ncu.json"),
-                         "traffic_source": "profiles/r2g_frames_ncu.json (ncu --set full, same launch)",
+                         "traffic": _profile_traffic("r2h_frames_ncu.json"),
+                         "traffic_source": "profiles/r2h_frames_ncu.json (ncu --set full, same launch)",
                          "kernel_ms": k_ms, "algorithmic_bytes": alg,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pp.exists() else "fallback 6650 GB/s"},
             "cpu_baseline": cpu,
