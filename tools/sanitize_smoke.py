@@ -8,7 +8,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from oracle import lightbeam_oracle as O  # noqa: E402
 from paper_2603_14002_b200 import (PROFILES, DeviceNgramScorer, LlamaScorer, StubScorer,  # noqa: E402
-                                   decode_batch, synth)
+                                   decode_batch, decode_batch_raw, synth)
 
 w = synth.toy_world(n_words=2000, seed=7)
 raws = synth.make_logits(3, 60, 41, base_seed=11)
@@ -20,6 +20,8 @@ for k in (16, 64, 96, 300) + ((900,) if os.environ.get("SAN_WIDE") else ()):
     scale = cfg.ngram_weight / cfg.llm_weight
     decode_batch(ds, cfg, w.table, w.model, DeviceNgramScorer(w.model, scale))
     decode_batch(ds, cfg, w.table, w.model, StubScorer(table={}))
+    # raw fp32 logits: the K1 prologue (eight lanes per row) feeds the search
+    decode_batch_raw(list(raws), cfg, w.table, w.model, DeviceNgramScorer(w.model, scale))
     print("frames ok k", k, flush=True)
 cfg = PROFILES["b2t25"].replace(beam_size=16, llm_rescore_interval=20)
 ds = [O.log_softmax_scaled(r, cfg.acoustic_scale) for r in raws]
